@@ -1,0 +1,177 @@
+"""Generate the golden fixtures in tests/golden/ by running the LIVE reference.
+
+Run in the build container (the only place /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/make_golden.py
+
+Inputs (theta0, quadrature points, probe vectors, Omega seeds) are seeded and
+reproducible by ``oracle.ngd_oracle``; the *outputs* stored here come from the
+unmodified reference package (``nystromngd``), so the fixtures pin both the
+oracle and the CUDA path.  The N-D Poisson problems of BASELINE C3/C5 do not
+exist in the reference; they are defined here by subclassing the
+reference's ``Poisson1D`` exactly as SURVEY 7.1 step 0 prescribes, and the
+interior-only microbench (C4) uses the reference's ``GramianOperator.from_stack``.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from nystromngd import gramian, krylov, model, optim, problems, sketch  # noqa: E402
+from nystromngd import autodiff as ad  # noqa: E402
+
+from oracle import ngd_oracle as O  # noqa: E402  (inputs only: points, boundary sampler)
+
+
+class PoissonND(problems.Poisson1D):
+    """Reference-side N-D Poisson (subclass of problems.Poisson1D)."""
+
+    def __init__(self, topology, kind):
+        self.input_dim = topology.input_dim
+        self.kind = kind
+        self._o = O.PoissonProblem(topology.widths, kind=kind)
+        super().__init__(topology)
+
+    def exact(self, x):
+        return self._o.exact(x)
+
+    def exact_grad(self, x):
+        return self._o.exact_grad(x)
+
+    def exact_laplacian(self, x):
+        return -self._o.source(x)
+
+    def source(self, x):
+        return self._o.source(x)
+
+    def dirichlet(self, x):
+        return self._o.exact(x)
+
+    def sample_quadrature(self, n_interior, n_boundary, seed):
+        q = self._o.sample_quadrature(n_interior, n_boundary, seed)
+        return problems.QuadratureSet(q.interior_points, q.interior_weights, q.boundary_points, q.boundary_weights)
+
+
+def _basic(prob, theta, quad, v):
+    gop = gramian.GramianOperator.from_problem(prob, theta, quad)
+    frozen = ad.freeze(theta)
+    return {
+        "loss": np.array(prob.loss_value(theta, quad)),
+        "grad": prob.loss_grad(theta, quad),
+        "metric": np.asarray(ad.primal_value(prob.metric_stack(theta, frozen, quad))),
+        "v": v,
+        "gv": gop.matvec(v),
+    }
+
+
+def case_c1():
+    widths = (2, 32, 32, 1)
+    prob = problems.make_problem("poisson2d", topology=model.MlpTopology(widths))
+    quad = prob.sample_quadrature(900, 120, 0)
+    theta = model.init(prob.topology, 0).values
+    p = theta.shape[0]
+    out = _basic(prob, theta, quad, np.random.default_rng(1).standard_normal(p))
+    out["theta0"] = theta
+    gop = gramian.GramianOperator.from_problem(prob, theta, quad)
+    # sketch block on a fixed post-QR Omega (compare Y on the same Omega)
+    omega, _ = np.linalg.qr(np.random.default_rng(123).standard_normal((p, 8)), mode="reduced")
+    out["omega8"] = omega
+    out["y8"] = gop.matmat(omega)
+    # full Nystrom factor at rank 100, preconditioner, PCG at a fixed iteration count
+    factor = sketch.nystrom_approximate(gop, 100, seed=7)
+    mu = 1e-4
+    pre = sketch.NystromPreconditioner(factor, mu)
+    out["eig100"] = factor.eigenvalues
+    out["mu"] = np.array(mu)
+    out["pinv_v"] = pre.apply(out["v"])
+    g = out["grad"]
+    for k in (1, 5, 20):
+        rep = krylov.pcg(gramian.ShiftedOperator(gop, mu), g, 1e-300, k, precond=pre)
+        out[f"pcg{k}_x"] = rep.solution
+        out[f"pcg{k}_meta"] = np.array([rep.iterations, rep.matvecs, rep.relative_residual, rep.converged, rep.breakdown], dtype=float)
+    # 20-step NGD loss trajectory, fixed rank 100
+    cfg = optim.NystromNgdConfig(ell0=100, ell_max=100, cg_maxit=20, kappa=1e-300,
+                                 mu_floor_mode="grad-power", mu_floor_coeff=1e-6,
+                                 mu_floor_exponent=1.0, iterations=20, seed=0)
+    saved = optim.adapt_rank
+    optim.adapt_rank = lambda eigenvalues, mu, ell, ell_max, ratio=10.0: ell
+    try:
+        t0 = time.time()
+        theta_f, recs = optim.nystrom_ngd_run(prob, theta, cfg, quad)
+        print(f"  c1 20 NGD steps in {time.time() - t0:.1f}s")
+    finally:
+        optim.adapt_rank = saved
+    out["traj_loss"] = np.array([r.loss for r in recs])
+    out["traj_mu"] = np.array([r.mu for r in recs])
+    out["traj_pcg"] = np.array([r.pcg_iters for r in recs])
+    out["traj_matvecs"] = np.array([r.matvecs for r in recs])
+    out["traj_theta"] = theta_f
+    # adaptive-rank trajectory (default policy), 8 steps, small ell0
+    cfg2 = optim.NystromNgdConfig(ell0=10, ell_max=100, cg_maxit=20, iterations=8, seed=3)
+    _, recs2 = optim.nystrom_ngd_run(prob, theta, cfg2, quad)
+    out["adapt_loss"] = np.array([r.loss for r in recs2])
+    out["adapt_ell"] = np.array([r.ell for r in recs2])
+    out["adapt_mu"] = np.array([r.mu for r in recs2])
+    out["adapt_pcg"] = np.array([r.pcg_iters for r in recs2])
+    out["adapt_matvecs"] = np.array([r.matvecs for r in recs2])
+    return out
+
+
+def case_c2():
+    widths = (2, 64, 64, 64, 1)
+    prob = problems.make_problem("poisson2d", topology=model.MlpTopology(widths))
+    quad = prob.sample_quadrature(4096, 512, 0)
+    theta = model.init(prob.topology, 0).values
+    out = _basic(prob, theta, quad, np.random.default_rng(1).standard_normal(theta.shape[0]))
+    return out
+
+
+def case_nd(widths, kind, n_int, n_bnd):
+    top = model.MlpTopology(widths)
+    prob = PoissonND(top, kind)
+    quad = prob.sample_quadrature(n_int, n_bnd, 0)
+    theta = model.init(top, 0).values
+    return _basic(prob, theta, quad, np.random.default_rng(1).standard_normal(theta.shape[0]))
+
+
+def case_c4(n):
+    widths = (2, 256, 256, 256, 1)
+    top = model.MlpTopology(widths)
+    x = np.random.default_rng(0).random((n, 2))
+    w = np.full(n, 1.0 / n)
+    theta = model.init(top, 0).values
+    stack = lambda th: model.input_derivatives(top, th, x)[2]
+    gop = gramian.GramianOperator.from_stack(stack, theta, w)
+    v = np.random.default_rng(1).standard_normal(theta.shape[0])
+    return {"x": x, "v": v, "gv": gop.matvec(v)}
+
+
+def main():
+    cases = {
+        "c1": case_c1,
+        "c2": case_c2,
+        "c3_sub": lambda: case_nd((5, 128, 128, 128, 1), "sinsum", 256, 64),
+        "c5_sub": lambda: case_nd((10, 256, 256, 256, 256, 1), "gauss", 24, 8),
+        "c4_sub": lambda: case_c4(96),
+    }
+    only = sys.argv[1:]
+    for name, fn in cases.items():
+        if only and name not in only:
+            continue
+        t0 = time.time()
+        data = fn()
+        path = os.path.join(HERE, f"{name}.npz")
+        np.savez_compressed(path, **data)
+        print(f"{name}: {time.time() - t0:.1f}s -> {path} ({os.path.getsize(path) / 1e6:.2f} MB)")
+
+
+if __name__ == "__main__":
+    main()
