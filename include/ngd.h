@@ -1,0 +1,121 @@
+/*
+ * ngd.h -- C-ABI of the B200-native NystromNGD inner solve (libngd_b200.so).
+ *
+ * The reference (nystromngd, pure Python/numpy) has no FFI: its boundary is a
+ * duck-typed Python protocol.  Each entry point below backs one
+ * piece of that protocol; the Python host layer (paper_2505_11638_b200/*.py)
+ * binds them with ctypes exactly as INTEGRATION.md shows.
+ *
+ * Conventions
+ *   - every pointer argument named d_* is a DEVICE pointer (fp64 unless noted);
+ *     h_* are host pointers.  Work is stream-ordered on the context's stream.
+ *   - p x ell matrices crossing the ABI are COLUMN-major (each column a
+ *     contiguous p-vector) unless the name says _rowmajor.
+ *   - parameter vectors use the reference's flat layout: per layer W (n_out x n_in)
+ *     row-major, then b (model.py:41-51).
+ *   - return value: NGD_OK or one of the NGD_E_* codes; ngd_last_error() gives text.
+ *     Python maps NGD_E_SHAPE -> ValueError, NGD_E_NONFINITE -> NonFiniteError,
+ *     NGD_E_CHOL -> retry / SketchFailure, NGD_E_CUDA/NCCL -> RuntimeError.
+ */
+#ifndef NGD_B200_H_
+#define NGD_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NGD_OK 0
+#define NGD_E_SHAPE 1
+#define NGD_E_NONFINITE 2
+#define NGD_E_CHOL 3
+#define NGD_E_CUDA 4
+#define NGD_E_NCCL 5
+#define NGD_E_STATE 6
+
+typedef struct ngd_ctx ngd_ctx;
+
+/* SolveReport (krylov.py:12-21) */
+typedef struct ngd_solve_report {
+  int32_t iterations;
+  int32_t matvecs;
+  int32_t converged;
+  int32_t breakdown;
+  double relative_residual;
+} ngd_solve_report;
+
+const char* ngd_last_error(void);
+int ngd_version(void);
+
+/* ---- context: MlpTopology (model.py:12-51) + device workspace ---------- */
+int ngd_ctx_create(const int32_t* widths, int32_t n_widths, int32_t device, ngd_ctx** out);
+int ngd_ctx_destroy(ngd_ctx* ctx);
+int ngd_ctx_set_stream(ngd_ctx* ctx, void* cuda_stream);
+int64_t ngd_param_count(const ngd_ctx* ctx);
+
+/* ---- multi-GPU: point shards + NCCL all-reduce -------------- */
+int ngd_nccl_unique_id(uint8_t* h_id_out /* 128 bytes */);
+int ngd_ctx_set_comm(ngd_ctx* ctx, const uint8_t* h_id /* 128 bytes */, int32_t rank, int32_t nranks);
+
+/* ---- quadrature: QuadratureSet + data offsets (problems.py:34-48,161-177)
+ * x_* row-major (n, d); w_* quadrature weights; off_* residual offsets
+ * (source f on interior points, -g on boundary points) so that
+ * residual = metric + off.  Device pointers, copied into the context. */
+int ngd_set_points(ngd_ctx* ctx, int64_t n_int, const double* d_x_int, const double* d_w_int,
+                   const double* d_off_int, int64_t n_bnd, const double* d_x_bnd, const double* d_w_bnd,
+                   const double* d_off_bnd);
+
+/* ---- loss (PdeProblem.loss_value, problems.py:92-99); all-reduced ------- */
+int ngd_loss(ngd_ctx* ctx, const double* d_theta, double* h_loss);
+/* loss at theta - alpha * dir (backtracking_linesearch candidate, optim.py:137) */
+int ngd_loss_at(ngd_ctx* ctx, const double* d_theta, double alpha, const double* d_dir, double* h_loss);
+
+/* ---- linearisation (GramianOperator.from_problem, gramian.py:33-41) -----
+ * caches jets + adjoints at theta; also returns the loss (may be NULL) and,
+ * if d_metric != NULL, the metric stack values [Lap u]_int ++ [u]_bnd. */
+int ngd_linearize(ngd_ctx* ctx, const double* d_theta, double* h_loss, double* d_metric);
+/* gradient J^T (w o r) at the current linearisation (PdeProblem.loss_grad, problems.py:101-102) */
+int ngd_loss_grad(ngd_ctx* ctx, double* d_grad);
+/* metric-stack JVP / VJP at the current linearisation (LinearizedMap.jvp/vjp, autodiff.py:605-609) */
+int ngd_jvp(ngd_ctx* ctx, const double* d_v, double* d_out /* n_int + n_bnd */);
+int ngd_vjp(ngd_ctx* ctx, const double* d_cot /* n_int + n_bnd */, double* d_out /* p */);
+
+/* ---- Gramian (GramianOperator.matvec/matmat, ShiftedOperator; gramian.py:48-61,123-135) */
+int ngd_gram_matvec(ngd_ctx* ctx, const double* d_v, double mu, double* d_out);
+int ngd_gram_matmat(ngd_ctx* ctx, const double* d_V, int64_t ell, int64_t ldv, double* d_Y, int64_t ldy);
+
+/* ---- randomized Nystrom (nystrom_approximate, sketch.py:58-90) ----------
+ * prepare: orthonormalise Omega in place (p x ell, col-major).
+ * finish : given Y = G Omega, produce U (p x ell ROW-major) and eigenvalues
+ *          (descending, >= 0); returns NGD_E_CHOL when Omega^T Y_nu is not PD. */
+int ngd_fill_gaussian(ngd_ctx* ctx, uint64_t seed, double* d_out, int64_t n);
+int ngd_nystrom_prepare(ngd_ctx* ctx, double* d_omega, int64_t p, int32_t ell);
+int ngd_nystrom_finish(ngd_ctx* ctx, const double* d_omega, double* d_Y, int64_t p, int32_t ell,
+                       double* d_U_rowmajor, double* d_eig, double* h_shift);
+/* dense operator helper (DenseOperator.matmat, gramian.py:101-120): Y = G V */
+int ngd_dense_matmat(ngd_ctx* ctx, const double* d_G, int64_t p, const double* d_V, int64_t ell, double* d_Y);
+
+/* ---- preconditioner (NystromPreconditioner.apply, sketch.py:101-112) ---- */
+int ngd_precond_apply(ngd_ctx* ctx, const double* d_U_rowmajor, const double* d_eig, int32_t ell, double mu,
+                      const double* d_v, double* d_out, int64_t p);
+
+/* ---- PCG (krylov.py:24-88) on (G + mu I) at the current linearisation, or on
+ * a dense SPD matrix d_dense (p x p) when non-NULL.  U/eig may be NULL (no precond). */
+int ngd_pcg(ngd_ctx* ctx, const double* d_dense, int64_t p, const double* d_b, double mu,
+            const double* d_U_rowmajor, const double* d_eig, int32_t ell, double precond_mu, double rel_tol,
+            int32_t maxit, int32_t recompute_every, double* d_x, ngd_solve_report* h_report);
+
+/* ---- vector helpers used by the host policy ------------------------------
+ * ngd_dot: h_out = x . y (deterministic reduction, synchronises);
+ * ngd_axpy: out = a - alpha * b (theta update / line-search candidate, optim.py:137,252) */
+int ngd_dot(ngd_ctx* ctx, const double* d_x, const double* d_y, int64_t n, double* h_out);
+int ngd_axpy(ngd_ctx* ctx, const double* d_a, double alpha, const double* d_b, double* d_out, int64_t n);
+
+/* ---- timing support for bench.py: kernel events on the context stream --- */
+int ngd_stream_sync(ngd_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NGD_B200_H_ */

@@ -1,0 +1,877 @@
+// C-ABI of the B200 NystromNGD inner solve (include/ngd.h).
+//
+// Host orchestration of the CUDA kernels in ngd_jet.cu / ngd_vec.cu plus the
+// small dense factorizations (cuBLAS / cuSOLVER) of the Nystrom sketch and the
+// NCCL all-reduces of the point-sharded multi-GPU path.  Every entry point is
+// stream-ordered on the context's stream; only scalars the host policy needs
+// (loss values, PCG report, Cholesky status) are copied back.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ngd.h"
+#include "ngd_kernels.h"
+
+using namespace ngd;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) return fail(NGD_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+  } while (0)
+#define CKB(x)                                                                                   \
+  do {                                                                                           \
+    cublasStatus_t s_ = (x);                                                                     \
+    if (s_ != CUBLAS_STATUS_SUCCESS) return fail(NGD_E_CUDA, "%s:%d %s: cublas status %d", __FILE__, __LINE__, #x, (int)s_); \
+  } while (0)
+#define CKS(x)                                                                                   \
+  do {                                                                                           \
+    cusolverStatus_t s_ = (x);                                                                   \
+    if (s_ != CUSOLVER_STATUS_SUCCESS) return fail(NGD_E_CUDA, "%s:%d %s: cusolver status %d", __FILE__, __LINE__, #x, (int)s_); \
+  } while (0)
+#define CKN(x)                                                                                   \
+  do {                                                                                           \
+    ncclResult_t r_ = (x);                                                                       \
+    if (r_ != ncclSuccess) return fail(NGD_E_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #x, ncclGetErrorString(r_)); \
+  } while (0)
+#define TRY(x)                 \
+  do {                         \
+    int rc_ = (x);             \
+    if (rc_ != NGD_OK) return rc_; \
+  } while (0)
+
+inline int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// grow-only device buffer
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  double* d() const { return static_cast<double*>(p); }
+};
+
+}  // namespace
+
+struct ngd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t sol = nullptr;
+  gesvdjInfo_t svdj = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+
+  std::vector<int> w;  // widths
+  int NL = 0, d = 0, C = 0;
+  int64_t p = 0;
+  std::vector<int64_t> woff, boff;
+  std::vector<int> Mp_f, Kp_f, Mp_r, Kp_r, mtiles;
+  std::vector<int> rowbase;  // phase-A partial rows per layer
+  int rows_A = 0;
+
+  // packed operands
+  std::vector<Buf> apf, apr, vp;
+  // point data
+  bool have_points = false;
+  Geom gm{};
+  int G = 1, kps = 1;  // phase-B splits
+  Buf w_pad, off_pad, w_c, F, cot_grad, cot, metric_tmp;
+  std::vector<Buf> zin, dbuf;  // per layer
+  Buf dseed, pre_last, zs0, zs1;
+  Buf partA, partB;
+  Buf redp;         // reduction partials
+  Buf counters;     // unsigned counters
+  Buf scal;         // device scalars
+  Buf pcgs;         // PcgState
+  Buf pr, pz, pd, pad, ptmp;  // PCG vectors
+  Buf ppart, pcprime;         // precond scratch
+  Buf jt, smat;               // sketch scratch
+  Buf fj_tab;                 // FormJ device tables
+  Buf nys_m, nys_tau, nys_r, nys_ur, nys_v, nys_s, nys_work, nys_info;
+  double* h_pin = nullptr;    // pinned host scalars
+  bool lin_valid = false;
+
+  double* S(int i) { return scal.d() + i; }
+  unsigned* counter(int i) { return static_cast<unsigned*>(counters.p) + i; }
+};
+
+enum Scalar { SC_LOSS = 0, SC_FRO2 = 1, SC_SHIFT = 2, SC_TMP = 3, SC_N = 8 };
+
+static int bind(ngd_ctx* c) {
+  CK(cudaSetDevice(c->device));
+  return NGD_OK;
+}
+
+static int allreduce(ngd_ctx* c, double* buf, size_t n) {
+  if (c->nranks <= 1 || !c->comm) return NGD_OK;
+  CKN(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, c->comm, c->stream));
+  return NGD_OK;
+}
+
+// ------------------------------- forward sweep -------------------------------
+// FWD over all layers.  store=true: linearisation buffers (zin/dbuf/pre_last);
+// store=false: ping-pong scratch, only the output-layer pre-activations kept.
+static int forward(ngd_ctx* c, bool store) {
+  const Geom& gm = c->gm;
+  for (int l = 0; l < c->NL; ++l) {
+    const bool last = (l == c->NL - 1);
+    JetArgs a{};
+    a.A = c->apf[l].d();
+    a.Kp = c->Kp_f[l];
+    a.M = c->w[l + 1];
+    a.s_pad = gm.s_pad;
+    a.bias = nullptr;  // theta bias added through the packed bias vector below
+    a.n_pts_pad = gm.n_pts_pad();
+    const double* src;
+    double* zout;
+    double* pre;
+    if (store) {
+      src = c->zin[l].d();
+      zout = last ? nullptr : c->zin[l + 1].d();
+      pre = last ? c->pre_last.d() : c->dbuf[l].d();
+    } else {
+      src = (l == 0) ? c->zin[0].d() : ((l & 1) ? c->zs0.d() : c->zs1.d());
+      zout = last ? nullptr : ((l & 1) ? c->zs1.d() : c->zs0.d());
+      pre = last ? c->pre_last.d() : nullptr;
+    }
+    a.B = src;
+    a.z_out = zout;
+    a.pre_out = pre;
+    a.bias = c->apf[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l];  // packed bias follows the packed W
+    for (int seg = 0; seg < 2; ++seg) {
+      const int CC = seg == 0 ? gm.C : 1;
+      a.col0 = seg == 0 ? 0 : gm.int_cols();
+      a.pt0 = seg == 0 ? 0 : gm.nib * PB;
+      const int nblk = seg == 0 ? gm.nib : gm.nbb;
+      CK(jet_gemm(CC, FWD, a, nblk, c->mtiles[l], c->stream));
+    }
+  }
+  return NGD_OK;
+}
+
+static int pack_theta(ngd_ctx* c, const double* theta, bool rev) {
+  for (int l = 0; l < c->NL; ++l) {
+    pack(c->apf[l].d(), c->Mp_f[l], c->Kp_f[l], theta, c->woff[l], c->w[l + 1], c->w[l], 0, nullptr, c->stream);
+    // bias row appended after the packed matrix (length Mp_f)
+    pack(c->apf[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l], 1, c->Mp_f[l], theta, c->boff[l], 1, c->w[l + 1], 0,
+         nullptr, c->stream);
+    if (rev && l + 1 < c->NL)
+      pack(c->apr[l].d(), c->Mp_r[l], c->Kp_r[l], theta, c->woff[l + 1], c->w[l + 2], c->w[l + 1], 1, nullptr,
+           c->stream);
+  }
+  CK(cudaGetLastError());
+  return NGD_OK;
+}
+
+static int loss_finish(ngd_ctx* c, double* h_loss, double* F, double* cot) {
+  const Geom& gm = c->gm;
+  residual_loss(c->pre_last.d(), gm, c->w_pad.d(), c->off_pad.d(), F, cot, c->redp.d(), c->counter(0),
+                c->S(SC_LOSS), c->stream);
+  TRY(allreduce(c, c->S(SC_LOSS), 1));
+  if (h_loss) {
+    CK(cudaMemcpyAsync(c->h_pin, c->S(SC_LOSS), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *h_loss = 0.5 * c->h_pin[0];
+    if (!std::isfinite(*h_loss)) return fail(NGD_E_NONFINITE, "non-finite loss");
+  }
+  return NGD_OK;
+}
+
+// ------------------------------ phase A / B ---------------------------------
+static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double* cot_out, const int* skip) {
+  const Geom& gm = c->gm;
+  for (int l = 0; l < c->NL; ++l) {
+    pack(c->vp[l].d(), c->Mp_f[l], c->Kp_f[l], v, c->woff[l], c->w[l + 1], c->w[l], 0, skip, c->stream);
+    pack(c->vp[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l], 1, c->Mp_f[l], v, c->boff[l], 1, c->w[l + 1], 0, skip,
+         c->stream);
+  }
+  for (int l = 0; l < c->NL; ++l) {
+    JetArgs a{};
+    a.A = c->vp[l].d();
+    a.Kp = c->Kp_f[l];
+    a.M = c->w[l + 1];
+    a.B = c->zin[l].d();
+    a.s_pad = gm.s_pad;
+    a.bias = c->vp[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l];
+    a.Dk = (l == c->NL - 1) ? c->dseed.d() : c->dbuf[l].d();
+    a.partA = c->partA.d() + (int64_t)c->rowbase[l] * gm.n_pts_pad();
+    a.n_pts_pad = gm.n_pts_pad();
+    a.skip = skip;
+    for (int seg = 0; seg < 2; ++seg) {
+      const int CC = seg == 0 ? gm.C : 1;
+      a.col0 = seg == 0 ? 0 : gm.int_cols();
+      a.pt0 = seg == 0 ? 0 : gm.nib * PB;
+      const int nblk = seg == 0 ? gm.nib : gm.nbb;
+      CK(jet_gemm(CC, PHA, a, nblk, c->mtiles[l], c->stream));
+    }
+  }
+  reduce_pha(c->partA.d(), c->rows_A, gm.n_pts_pad(), w_or_null, cot_out, skip, c->stream);
+  CK(cudaGetLastError());
+  return NGD_OK;
+}
+
+// out = J^T cot (+ mu v), all-reduced over ranks
+static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* v, double* out, const int* skip) {
+  const Geom& gm = c->gm;
+  for (int l = 0; l < c->NL; ++l) {
+    PhbArgs a{};
+    a.D = (l == c->NL - 1) ? c->dseed.d() : c->dbuf[l].d();
+    a.Z = c->zin[l].d();
+    a.cvec = cot;
+    a.M = c->w[l + 1];
+    a.N = c->w[l];
+    a.s_pad = gm.s_pad;
+    a.int_cols = gm.int_cols();
+    a.C = gm.C;
+    a.nib = gm.nib;
+    a.ktiles_total = (int)(gm.s_pad / 16);
+    a.ktiles_per_split = c->kps;
+    a.off = c->woff[l];
+    a.part = c->partB.d();
+    a.p = c->p;
+    a.skip = skip;
+    CK(phase_b(a, c->G, c->stream));
+  }
+  if (c->nranks > 1) {
+    reduce_splits(c->partB.d(), c->G, c->p, 0.0, nullptr, out, skip, c->stream);
+    TRY(allreduce(c, out, c->p));
+    if (v && mu != 0.0) add_scaled(out, mu, v, c->p, skip, c->stream);
+  } else {
+    reduce_splits(c->partB.d(), c->G, c->p, mu, (v && mu != 0.0) ? v : nullptr, out, skip, c->stream);
+  }
+  CK(cudaGetLastError());
+  return NGD_OK;
+}
+
+static int gram_mv(ngd_ctx* c, const double* v, double mu, double* out, const int* skip) {
+  TRY(phase_a(c, v, c->w_pad.d(), c->cot.d(), skip));
+  TRY(phase_b_all(c, c->cot.d(), mu, v, out, skip));
+  return NGD_OK;
+}
+
+static int need_lin(ngd_ctx* c) {
+  if (!c->have_points) return fail(NGD_E_STATE, "ngd_set_points has not been called");
+  if (!c->lin_valid) return fail(NGD_E_STATE, "no linearisation: call ngd_linearize first");
+  return NGD_OK;
+}
+
+extern "C" {
+
+const char* ngd_last_error(void) { return g_err.c_str(); }
+int ngd_version(void) { return 1; }
+
+int ngd_ctx_create(const int32_t* widths, int32_t n_widths, int32_t device, ngd_ctx** out) {
+  if (!widths || n_widths < 2 || !out) return fail(NGD_E_SHAPE, "need at least input and output widths");
+  for (int i = 0; i < n_widths; ++i)
+    if (widths[i] < 1) return fail(NGD_E_SHAPE, "layer widths must be >= 1");
+  if (widths[n_widths - 1] != 1) return fail(NGD_E_SHAPE, "scalar-output networks only (metric stack is scalar)");
+  if (widths[0] > 10) return fail(NGD_E_SHAPE, "input dimension %d > 10 not compiled", widths[0]);
+  auto* c = new ngd_ctx();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete c;
+    return fail(NGD_E_CUDA, "cudaSetDevice(%d) failed", device);
+  }
+  c->w.assign(widths, widths + n_widths);
+  c->NL = n_widths - 1;
+  c->d = widths[0];
+  c->C = c->d + 2;
+  int64_t off = 0;
+  c->rows_A = 0;
+  for (int l = 0; l < c->NL; ++l) {
+    const int nin = c->w[l], nout = c->w[l + 1];
+    c->woff.push_back(off);
+    off += (int64_t)nin * nout;
+    c->boff.push_back(off);
+    off += nout;
+    c->Mp_f.push_back((int)rup(nout, 64));
+    c->Kp_f.push_back((int)rup(nin, 16));
+    c->mtiles.push_back((int)rup(nout, 64) / 64);
+    c->rowbase.push_back(c->rows_A);
+    c->rows_A += c->mtiles.back();
+    if (l + 1 < c->NL) {
+      c->Mp_r.push_back((int)rup(nout, 64));
+      c->Kp_r.push_back((int)rup(c->w[l + 2], 16));
+    } else {
+      c->Mp_r.push_back(0);
+      c->Kp_r.push_back(0);
+    }
+  }
+  c->p = off;
+  c->apf.resize(c->NL);
+  c->apr.resize(c->NL);
+  c->vp.resize(c->NL);
+  c->zin.resize(c->NL);
+  c->dbuf.resize(c->NL);
+  int rc = NGD_OK;
+  auto ck = [&](cudaError_t e) {
+    if (e != cudaSuccess && rc == NGD_OK) rc = fail(NGD_E_CUDA, "allocation failed: %s", cudaGetErrorString(e));
+  };
+  for (int l = 0; l < c->NL; ++l) {
+    const size_t nf = sizeof(double) * ((size_t)c->Mp_f[l] * c->Kp_f[l] + c->Mp_f[l]);
+    ck(c->apf[l].ensure(nf));
+    ck(c->vp[l].ensure(nf));
+    if (l + 1 < c->NL) ck(c->apr[l].ensure(sizeof(double) * (size_t)c->Mp_r[l] * c->Kp_r[l]));
+  }
+  ck(c->redp.ensure(sizeof(double) * 4096));
+  ck(c->counters.ensure(sizeof(unsigned) * 64));
+  ck(c->scal.ensure(sizeof(double) * SC_N));
+  ck(c->pcgs.ensure(sizeof(PcgState)));
+  if (rc == NGD_OK) {
+    cudaMemset(c->counters.p, 0, c->counters.bytes);
+    cudaMemset(c->scal.p, 0, c->scal.bytes);
+    if (cudaMallocHost(&c->h_pin, 64 * sizeof(double)) != cudaSuccess) rc = fail(NGD_E_CUDA, "pinned alloc failed");
+  }
+  if (rc == NGD_OK && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) rc = fail(NGD_E_CUDA, "cublasCreate failed");
+  if (rc == NGD_OK && cusolverDnCreate(&c->sol) != CUSOLVER_STATUS_SUCCESS)
+    rc = fail(NGD_E_CUDA, "cusolverDnCreate failed");
+  if (rc == NGD_OK && cusolverDnCreateGesvdjInfo(&c->svdj) != CUSOLVER_STATUS_SUCCESS)
+    rc = fail(NGD_E_CUDA, "gesvdj info failed");
+  if (rc != NGD_OK) {
+    ngd_ctx_destroy(c);
+    return rc;
+  }
+  cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
+  *out = c;
+  return NGD_OK;
+}
+
+int ngd_ctx_destroy(ngd_ctx* c) {
+  if (!c) return NGD_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  cudaDeviceSynchronize();
+  for (auto* v : {&c->apf, &c->apr, &c->vp, &c->zin, &c->dbuf})
+    for (auto& b : *v) b.release();
+  for (Buf* b : {&c->w_pad, &c->off_pad, &c->w_c, &c->F, &c->cot_grad, &c->cot, &c->metric_tmp, &c->dseed,
+                 &c->pre_last, &c->zs0, &c->zs1, &c->partA, &c->partB, &c->redp, &c->counters, &c->scal, &c->pcgs,
+                 &c->pr, &c->pz, &c->pd, &c->pad, &c->ptmp, &c->ppart, &c->pcprime, &c->jt, &c->smat, &c->fj_tab,
+                 &c->nys_m, &c->nys_tau, &c->nys_r, &c->nys_ur, &c->nys_v, &c->nys_s, &c->nys_work, &c->nys_info})
+    b->release();
+  if (c->h_pin) cudaFreeHost(c->h_pin);
+  if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
+  if (c->sol) cusolverDnDestroy(c->sol);
+  if (c->blas) cublasDestroy(c->blas);
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  return NGD_OK;
+}
+
+int ngd_ctx_set_stream(ngd_ctx* c, void* stream) {
+  TRY(bind(c));
+  c->stream = static_cast<cudaStream_t>(stream);
+  CKB(cublasSetStream(c->blas, c->stream));
+  CKS(cusolverDnSetStream(c->sol, c->stream));
+  return NGD_OK;
+}
+
+int64_t ngd_param_count(const ngd_ctx* c) { return c ? c->p : -1; }
+
+int ngd_nccl_unique_id(uint8_t* h_id) {
+  ncclUniqueId id;
+  CKN(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "nccl id size");
+  memcpy(h_id, &id, sizeof(id));
+  return NGD_OK;
+}
+
+int ngd_ctx_set_comm(ngd_ctx* c, const uint8_t* h_id, int32_t rank, int32_t nranks) {
+  TRY(bind(c));
+  if (nranks <= 1) {
+    c->rank = 0;
+    c->nranks = 1;
+    return NGD_OK;
+  }
+  ncclUniqueId id;
+  memcpy(&id, h_id, sizeof(id));
+  CKN(ncclCommInitRank(&c->comm, nranks, id, rank));
+  c->rank = rank;
+  c->nranks = nranks;
+  return NGD_OK;
+}
+
+int ngd_set_points(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w_int, const double* off_int,
+                   int64_t n_bnd, const double* x_bnd, const double* w_bnd, const double* off_bnd) {
+  TRY(bind(c));
+  if (n_int < 0 || n_bnd < 0 || n_int + n_bnd == 0) return fail(NGD_E_SHAPE, "need at least one point");
+  if (n_int + n_bnd > (int64_t)1 << 30) return fail(NGD_E_SHAPE, "too many points");
+  Geom gm{};
+  gm.d = c->d;
+  gm.C = c->C;
+  gm.n_int = (int)n_int;
+  gm.n_bnd = (int)n_bnd;
+  gm.nib = (int)((n_int + PB - 1) / PB);
+  gm.nbb = (int)((n_bnd + PB - 1) / PB);
+  gm.s_pad = (int64_t)gm.nib * PB * gm.C + (int64_t)gm.nbb * PB;
+  c->gm = gm;
+  const int npp = gm.n_pts_pad();
+  const size_t col_b = sizeof(double) * gm.s_pad;
+  int maxw = 16;
+  for (int l = 0; l < c->NL; ++l) {
+    CK(c->zin[l].ensure(col_b * rup(c->w[l], 16)));
+    CK(cudaMemsetAsync(c->zin[l].p, 0, col_b * rup(c->w[l], 16), c->stream));
+    if (l + 1 < c->NL) {
+      CK(c->dbuf[l].ensure(col_b * rup(c->w[l + 1], 16)));
+      CK(cudaMemsetAsync(c->dbuf[l].p, 0, col_b * rup(c->w[l + 1], 16), c->stream));
+      maxw = std::max<int>(maxw, (int)rup(c->w[l + 1], 16));
+    }
+  }
+  CK(c->dseed.ensure(col_b * 16));
+  CK(cudaMemsetAsync(c->dseed.p, 0, col_b * 16, c->stream));
+  CK(c->pre_last.ensure(col_b * 16));
+  CK(c->zs0.ensure(col_b * maxw));
+  CK(c->zs1.ensure(col_b * maxw));
+  CK(cudaMemsetAsync(c->zs0.p, 0, col_b * maxw, c->stream));
+  CK(cudaMemsetAsync(c->zs1.p, 0, col_b * maxw, c->stream));
+  for (Buf* b : {&c->w_pad, &c->off_pad, &c->F, &c->cot_grad, &c->cot}) {
+    CK(b->ensure(sizeof(double) * npp));
+    CK(cudaMemsetAsync(b->p, 0, sizeof(double) * npp, c->stream));
+  }
+  CK(c->w_c.ensure(sizeof(double) * (n_int + n_bnd)));
+  CK(c->metric_tmp.ensure(sizeof(double) * npp));
+  // weights / offsets into padded point order
+  if (n_int) {
+    CK(cudaMemcpyAsync(c->w_pad.d(), w_int, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->off_pad.d(), off_int, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->w_c.d(), w_int, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  if (n_bnd) {
+    CK(cudaMemcpyAsync(c->w_pad.d() + (int64_t)gm.nib * PB, w_bnd, sizeof(double) * n_bnd, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(c->off_pad.d() + (int64_t)gm.nib * PB, off_bnd, sizeof(double) * n_bnd,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->w_c.d() + n_int, w_bnd, sizeof(double) * n_bnd, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  init_point_data(c->zin[0].d(), c->dseed.d(), gm, x_int, x_bnd, c->stream);
+  CK(cudaGetLastError());
+  // phase-A partial rows and phase-B split plan
+  CK(c->partA.ensure(sizeof(double) * (size_t)c->rows_A * npp));
+  int tiles = 1;
+  for (int l = 0; l < c->NL; ++l) tiles = std::max(tiles, ((c->w[l] + 63) / 64) * ((c->w[l + 1] + 63) / 64));
+  const int kt = (int)(gm.s_pad / 16);
+  int G = std::max(1, std::min(kt, (2 * 148 + tiles - 1) / tiles));
+  G = std::max(1, std::min(G, kt / 4 > 0 ? kt / 4 : 1));  // at least 4 k-tiles per split
+  c->kps = (kt + G - 1) / G;
+  c->G = (kt + c->kps - 1) / c->kps;
+  CK(c->partB.ensure(sizeof(double) * (size_t)c->G * c->p));
+  c->have_points = true;
+  c->lin_valid = false;
+  return NGD_OK;
+}
+
+int ngd_loss(ngd_ctx* c, const double* theta, double* h_loss) {
+  TRY(bind(c));
+  if (!c->have_points) return fail(NGD_E_STATE, "ngd_set_points has not been called");
+  TRY(pack_theta(c, theta, false));
+  TRY(forward(c, false));
+  return loss_finish(c, h_loss, nullptr, nullptr);
+}
+
+int ngd_loss_at(ngd_ctx* c, const double* theta, double alpha, const double* dir, double* h_loss) {
+  TRY(bind(c));
+  CK(c->ptmp.ensure(sizeof(double) * c->p));
+  theta_minus(theta, alpha, dir, c->ptmp.d(), c->p, c->stream);
+  return ngd_loss(c, c->ptmp.d(), h_loss);
+}
+
+int ngd_linearize(ngd_ctx* c, const double* theta, double* h_loss, double* d_metric) {
+  TRY(bind(c));
+  if (!c->have_points) return fail(NGD_E_STATE, "ngd_set_points has not been called");
+  c->lin_valid = false;
+  TRY(pack_theta(c, theta, true));
+  TRY(forward(c, true));
+  TRY(loss_finish(c, h_loss, c->F.d(), c->cot_grad.d()));
+  // reverse sweep over the jets: D_l from D_{l+1}
+  const Geom& gm = c->gm;
+  for (int l = c->NL - 2; l >= 0; --l) {
+    JetArgs a{};
+    a.A = c->apr[l].d();
+    a.Kp = c->Kp_r[l];
+    a.M = c->w[l + 1];
+    a.B = (l + 1 == c->NL - 1) ? c->dseed.d() : c->dbuf[l + 1].d();
+    a.s_pad = gm.s_pad;
+    a.dbuf = c->dbuf[l].d();
+    a.n_pts_pad = gm.n_pts_pad();
+    for (int seg = 0; seg < 2; ++seg) {
+      const int CC = seg == 0 ? gm.C : 1;
+      a.col0 = seg == 0 ? 0 : gm.int_cols();
+      a.pt0 = seg == 0 ? 0 : gm.nib * PB;
+      const int nblk = seg == 0 ? gm.nib : gm.nbb;
+      CK(jet_gemm(CC, REV, a, nblk, c->mtiles[l], c->stream));
+    }
+  }
+  if (d_metric) gather_points(c->F.d(), d_metric, gm, c->stream);
+  CK(cudaGetLastError());
+  c->lin_valid = true;
+  return NGD_OK;
+}
+
+int ngd_loss_grad(ngd_ctx* c, double* d_grad) {
+  TRY(bind(c));
+  TRY(need_lin(c));
+  return phase_b_all(c, c->cot_grad.d(), 0.0, nullptr, d_grad, nullptr);
+}
+
+int ngd_jvp(ngd_ctx* c, const double* v, double* out) {
+  TRY(bind(c));
+  TRY(need_lin(c));
+  TRY(phase_a(c, v, nullptr, c->cot.d(), nullptr));
+  gather_points(c->cot.d(), out, c->gm, c->stream);
+  CK(cudaGetLastError());
+  return NGD_OK;
+}
+
+int ngd_vjp(ngd_ctx* c, const double* cot, double* out) {
+  TRY(bind(c));
+  TRY(need_lin(c));
+  scatter_points(cot, c->cot.d(), c->gm, c->stream);
+  return phase_b_all(c, c->cot.d(), 0.0, nullptr, out, nullptr);
+}
+
+int ngd_gram_matvec(ngd_ctx* c, const double* v, double mu, double* out) {
+  TRY(bind(c));
+  TRY(need_lin(c));
+  return gram_mv(c, v, mu, out, nullptr);
+}
+
+// Y = G V by the J-chunk formulation: per point chunk, explicit Jacobian rows
+// Jt (R x p), S = Jt V, Y += Jt^T (w o S)  -- two DGEMMs on FP64 tensor cores.
+int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, double* Y, int64_t ldy) {
+  TRY(bind(c));
+  TRY(need_lin(c));
+  if (ell < 1 || ldv < c->p || ldy < c->p) return fail(NGD_E_SHAPE, "bad matmat shape");
+  const Geom& gm = c->gm;
+  const int nq = gm.n_int + gm.n_bnd;
+  const size_t budget = (size_t)8 << 30;  // bytes for one Jacobian chunk
+  int64_t R = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(budget / (sizeof(double) * c->p))));
+  CK(c->jt.ensure(sizeof(double) * (size_t)R * c->p));
+  CK(c->smat.ensure(sizeof(double) * (size_t)R * ell));
+  // device tables for FormJ
+  const int NL = c->NL;
+  const size_t tab_bytes = NL * (2 * sizeof(double*) + 2 * sizeof(int) + sizeof(int64_t)) + 64;
+  CK(c->fj_tab.ensure(tab_bytes));
+  std::vector<char> h(tab_bytes, 0);
+  auto** hz = reinterpret_cast<const double**>(h.data());
+  auto** hd = hz + NL;
+  auto* hoff = reinterpret_cast<int64_t*>(hd + NL);
+  auto* hin = reinterpret_cast<int*>(hoff + NL);
+  auto* hout = hin + NL;
+  for (int l = 0; l < NL; ++l) {
+    hz[l] = c->zin[l].d();
+    hd[l] = (l == NL - 1) ? c->dseed.d() : c->dbuf[l].d();
+    hoff[l] = c->woff[l];
+    hin[l] = c->w[l];
+    hout[l] = c->w[l + 1];
+  }
+  CK(cudaMemcpyAsync(c->fj_tab.p, h.data(), tab_bytes, cudaMemcpyHostToDevice, c->stream));
+  char* db = static_cast<char*>(c->fj_tab.p);
+  FormJArgs fa{};
+  fa.Z = reinterpret_cast<const double* const*>(db);
+  fa.D = reinterpret_cast<const double* const*>(db + NL * sizeof(double*));
+  fa.off = reinterpret_cast<const int64_t*>(db + 2 * NL * sizeof(double*));
+  fa.n_in = reinterpret_cast<const int*>(db + 2 * NL * sizeof(double*) + NL * sizeof(int64_t));
+  fa.n_out = fa.n_in + NL;
+  fa.s_pad = gm.s_pad;
+  fa.int_cols = gm.int_cols();
+  fa.C = gm.C;
+  fa.nib = gm.nib;
+  fa.n_int = gm.n_int;
+  fa.Jt = c->jt.d();
+  fa.ldj = c->p;
+  const double one = 1.0, zero = 0.0;
+  for (int64_t q0 = 0; q0 < nq; q0 += R) {
+    const int64_t r = std::min<int64_t>(R, nq - q0);
+    fa.q0 = (int)q0;
+    CK(form_j(fa, (int)r, NL, c->stream));
+    // S (r x ell) = Jt_chunk (r x p) * V  -> col-major: S = Jt^T(p x r)^T V
+    CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)r, (int)ell, (int)c->p, &one, c->jt.d(), (int)c->p, V,
+                    (int)ldv, &zero, c->smat.d(), (int)r));
+    scale_rows(c->smat.d(), r, (int)ell, c->w_c.d() + q0, c->stream);
+    const double beta = (q0 == 0) ? 0.0 : 1.0;
+    CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)c->p, (int)ell, (int)r, &one, c->jt.d(), (int)c->p,
+                    c->smat.d(), (int)r, &beta, Y, (int)ldy));
+  }
+  if (c->nranks > 1) {
+    if (ldy != c->p) return fail(NGD_E_SHAPE, "multi-rank matmat needs ldy == p");
+    TRY(allreduce(c, Y, (size_t)c->p * ell));
+  }
+  CK(cudaGetLastError());
+  return NGD_OK;
+}
+
+int ngd_fill_gaussian(ngd_ctx* c, uint64_t seed, double* out, int64_t n) {
+  TRY(bind(c));
+  fill_gaussian(out, n, seed, c->stream);
+  CK(cudaGetLastError());
+  return NGD_OK;
+}
+
+// Cholesky-QR2 of Omega in place: Omega <- Omega R^{-1}, twice.  Gives the same
+// orthonormal basis as the reference's Householder QR (sketch.py:75) up to column signs.
+int ngd_nystrom_prepare(ngd_ctx* c, double* omega, int64_t p, int32_t ell) {
+  TRY(bind(c));
+  if (ell < 1 || ell > p) return fail(NGD_E_SHAPE, "rank must be in [1, %lld], got %d", (long long)p, ell);
+  CK(c->nys_m.ensure(sizeof(double) * (size_t)ell * ell));
+  CK(c->nys_info.ensure(sizeof(int) * 4));
+  int lwork = 0;
+  CKS(cusolverDnDpotrf_bufferSize(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, &lwork));
+  CK(c->nys_work.ensure(sizeof(double) * std::max(lwork, 1)));
+  const double one = 1.0, zero = 0.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, omega, (int)p, &zero,
+                    c->nys_m.d(), ell));
+    CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, c->nys_work.d(), lwork,
+                         static_cast<int*>(c->nys_info.p)));
+    CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p,
+                    ell, &one, c->nys_m.d(), ell, omega, (int)p));
+  }
+  int info = 0;
+  CK(cudaMemcpyAsync(&c->h_pin[8], c->nys_info.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  memcpy(&info, &c->h_pin[8], sizeof(int));
+  if (info != 0) return fail(NGD_E_CHOL, "test matrix is numerically rank deficient (potrf info %d)", info);
+  return NGD_OK;
+}
+
+// sketch.py:77-86: shift, Cholesky of Omega^T Y_nu, B = Y_nu C^{-1}, thin SVD of B
+// (Householder QR of B, Jacobi SVD of R, U = Q U_R), eigenvalues max(s^2 - nu, 0).
+int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, int32_t ell, double* U_row,
+                       double* eig, double* h_shift) {
+  TRY(bind(c));
+  if (ell < 1 || ell > p) return fail(NGD_E_SHAPE, "rank must be in [1, %lld], got %d", (long long)p, ell);
+  const int64_t n = p * ell;
+  CK(c->nys_m.ensure(sizeof(double) * (size_t)ell * ell));
+  CK(c->nys_r.ensure(sizeof(double) * (size_t)ell * ell));
+  CK(c->nys_ur.ensure(sizeof(double) * (size_t)ell * ell));
+  CK(c->nys_v.ensure(sizeof(double) * (size_t)ell * ell));
+  CK(c->nys_s.ensure(sizeof(double) * ell));
+  CK(c->nys_tau.ensure(sizeof(double) * ell));
+  CK(c->nys_info.ensure(sizeof(int) * 4));
+  // 1. nu = eps ||Y||_F ; Y_nu = Y + nu Omega
+  dot(Y, Y, n, c->redp.d(), c->counter(1), c->S(SC_FRO2), nullptr, c->stream);
+  add_shift(Y, omega, n, c->S(SC_FRO2), c->S(SC_SHIFT), c->stream);
+  // 2. M = Omega^T Y_nu ; upper Cholesky
+  const double one = 1.0, zero = 0.0;
+  CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, (int)p, &one, omega, (int)p, Y, (int)p, &zero,
+                  c->nys_m.d(), ell));
+  int lw_potrf = 0, lw_geqrf = 0, lw_orgqr = 0, lw_svd = 0;
+  CKS(cusolverDnDpotrf_bufferSize(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, &lw_potrf));
+  CKS(cusolverDnDgeqrf_bufferSize(c->sol, (int)p, ell, Y, (int)p, &lw_geqrf));
+  CKS(cusolverDnDorgqr_bufferSize(c->sol, (int)p, ell, ell, Y, (int)p, c->nys_tau.d(), &lw_orgqr));
+  CKS(cusolverDnDgesvdj_bufferSize(c->sol, CUSOLVER_EIG_MODE_VECTOR, 0, ell, ell, c->nys_r.d(), ell, c->nys_s.d(),
+                                   c->nys_ur.d(), ell, c->nys_v.d(), ell, &lw_svd, c->svdj));
+  const int lw = std::max(std::max(lw_potrf, lw_geqrf), std::max(lw_orgqr, lw_svd));
+  CK(c->nys_work.ensure(sizeof(double) * std::max(lw, 1)));
+  int* info = static_cast<int*>(c->nys_info.p);
+  CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, c->nys_work.d(), lw_potrf, info));
+  CK(cudaMemcpyAsync(&c->h_pin[8], info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int hinfo = 0;
+  memcpy(&hinfo, &c->h_pin[8], sizeof(int));
+  if (hinfo != 0) return fail(NGD_E_CHOL, "sketch Cholesky failed (potrf info %d)", hinfo);
+  // 3. B = Y_nu C^{-1}
+  CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p, ell,
+                  &one, c->nys_m.d(), ell, Y, (int)p));
+  // 4. B = Q R
+  CKS(cusolverDnDgeqrf(c->sol, (int)p, ell, Y, (int)p, c->nys_tau.d(), c->nys_work.d(), lw_geqrf, info));
+  CK(cudaMemcpy2DAsync(c->nys_r.d(), sizeof(double) * ell, Y, sizeof(double) * p, sizeof(double) * ell, ell,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  triu(c->nys_r.d(), ell, ell, c->stream);
+  // 5. R = U_R diag(s) V^T (Jacobi, descending)
+  CKS(cusolverDnDgesvdj(c->sol, CUSOLVER_EIG_MODE_VECTOR, 0, ell, ell, c->nys_r.d(), ell, c->nys_s.d(), c->nys_ur.d(),
+                        ell, c->nys_v.d(), ell, c->nys_work.d(), lw_svd, info, c->svdj));
+  // 6. Q explicitly, U^T = U_R^T Q^T  (row-major p x ell output)
+  CKS(cusolverDnDorgqr(c->sol, (int)p, ell, ell, Y, (int)p, c->nys_tau.d(), c->nys_work.d(), lw_orgqr, info));
+  CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_T, ell, (int)p, ell, &one, c->nys_ur.d(), ell, Y, (int)p, &zero,
+                  U_row, ell));
+  eig_from_sv(c->nys_s.d(), ell, c->S(SC_SHIFT), eig, c->stream);
+  CK(cudaMemcpyAsync(&c->h_pin[0], c->S(SC_SHIFT), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (h_shift) *h_shift = c->h_pin[0];
+  CK(cudaGetLastError());
+  return NGD_OK;
+}
+
+int ngd_dense_matmat(ngd_ctx* c, const double* G, int64_t p, const double* V, int64_t ell, double* Y) {
+  TRY(bind(c));
+  const double one = 1.0, zero = 0.0;
+  // G is a C-order (row-major) p x p matrix: in column-major terms it is G^T.
+  CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)p, (int)ell, (int)p, &one, G, (int)p, V, (int)p, &zero, Y,
+                  (int)p));
+  return NGD_OK;
+}
+
+int ngd_precond_apply(ngd_ctx* c, const double* U, const double* eig, int32_t ell, double mu, const double* v,
+                      double* out, int64_t p) {
+  TRY(bind(c));
+  CK(c->ppart.ensure(sizeof(double) * (size_t)precond_blocks(p) * ell));
+  CK(c->pcprime.ensure(sizeof(double) * ell));
+  CK(precond_apply(U, p, ell, eig, nullptr, mu, v, out, c->ppart.d(), c->pcprime.d(), nullptr, c->stream));
+  return NGD_OK;
+}
+
+int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double mu, const double* U,
+            const double* eig, int32_t ell, double precond_mu, double rel_tol, int32_t maxit,
+            int32_t recompute_every, double* x, ngd_solve_report* rep) {
+  TRY(bind(c));
+  if (!(rel_tol > 0.0 && rel_tol < 1.0)) return fail(NGD_E_SHAPE, "rel_tol must be in (0, 1), got %g", rel_tol);
+  if (maxit < 1) return fail(NGD_E_SHAPE, "maxit must be >= 1");
+  if (recompute_every < 1) recompute_every = 1 << 30;
+  if (!dense) {
+    TRY(need_lin(c));
+    if (p != c->p) return fail(NGD_E_SHAPE, "expected vector of length %lld, got %lld", (long long)c->p, (long long)p);
+  }
+  if (p < 1) return fail(NGD_E_SHAPE, "empty system");
+  for (Buf* bf : {&c->pr, &c->pz, &c->pd, &c->pad, &c->ptmp}) CK(bf->ensure(sizeof(double) * p));
+  if (U) {
+    CK(c->ppart.ensure(sizeof(double) * (size_t)precond_blocks(p) * ell));
+    CK(c->pcprime.ensure(sizeof(double) * ell));
+  }
+  auto* st = static_cast<PcgState*>(c->pcgs.p);
+  const int* done = &st->done;
+  double* r = c->pr.d();
+  double* z = c->pz.d();
+  double* dvec = c->pd.d();
+  double* ad = c->pad.d();
+  double* tmp = c->ptmp.d();
+  const double one = 1.0, zero = 0.0;
+  auto apply_A = [&](const double* in, double* outv, const int* skip) -> int {
+    if (dense) {
+      CKB(cublasDgemv(c->blas, CUBLAS_OP_T, (int)p, (int)p, &one, dense, (int)p, in, 1, &zero, outv, 1));
+      if (mu != 0.0) add_scaled(outv, mu, in, p, skip, c->stream);
+      return NGD_OK;
+    }
+    return gram_mv(c, in, mu, outv, skip);
+  };
+  auto apply_P = [&](const double* in, double* outv, const int* skip) -> int {
+    if (!U) {
+      CK(cudaMemcpyAsync(outv, in, sizeof(double) * p, cudaMemcpyDeviceToDevice, c->stream));
+      return NGD_OK;
+    }
+    CK(precond_apply(U, p, ell, eig, nullptr, precond_mu, in, outv, c->ppart.d(), c->pcprime.d(), skip, c->stream));
+    return NGD_OK;
+  };
+  PcgState* sp = st;
+  // ||b||
+  dot(b, b, p, c->redp.d(), c->counter(2), &sp->bb, nullptr, c->stream);
+  pcg_init(sp, rel_tol, c->stream);
+  pcg_start(b, x, r, p, c->stream);
+  TRY(apply_P(r, z, done));
+  dot(r, z, p, c->redp.d(), c->counter(3), &sp->rz_new, done, c->stream);
+  pcg_first_dir(z, dvec, p, sp, c->stream);
+  for (int it = 1; it <= maxit; ++it) {
+    TRY(apply_A(dvec, ad, done));
+    dot(dvec, ad, p, c->redp.d(), c->counter(4), &sp->dad, done, c->stream);
+    pcg_alpha(sp, it, c->stream);
+    const int rec = (it % recompute_every == 0);
+    pcg_update(x, r, dvec, ad, p, sp, rec, c->stream);
+    if (rec) {
+      TRY(apply_A(x, tmp, done));
+      pcg_true_res(b, tmp, r, p, sp, 1, 0, c->stream);
+    }
+    dot(r, r, p, c->redp.d(), c->counter(5), &sp->rr, done, c->stream);
+    pcg_check(sp, c->stream);
+    TRY(apply_P(r, z, done));
+    dot(r, z, p, c->redp.d(), c->counter(6), &sp->rz_new, done, c->stream);
+    pcg_dir(z, dvec, p, sp, c->stream);
+    if ((it & 7) == 0 && it < maxit) {
+      // cheap host poll so long solves stop issuing work after convergence
+      CK(cudaMemcpyAsync(&c->h_pin[16], &sp->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      int dn = 0;
+      memcpy(&dn, &c->h_pin[16], sizeof(int));
+      if (dn) break;
+    }
+  }
+  // final true residual (krylov.py:83-88)
+  CK(cudaMemcpyAsync(&c->h_pin[16], &sp->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int dn = 0;
+  memcpy(&dn, &c->h_pin[16], sizeof(int));
+  if (dn != 2) {
+    TRY(apply_A(x, tmp, nullptr));
+    pcg_true_res(b, tmp, r, p, sp, 0, 1, c->stream);
+    dot(r, r, p, c->redp.d(), c->counter(5), &sp->rr, nullptr, c->stream);
+  }
+  pcg_final(sp, c->stream);
+  PcgState hs;
+  CK(cudaMemcpyAsync(c->h_pin + 20, sp, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  memcpy(&hs, c->h_pin + 20, sizeof(PcgState));
+  CK(cudaGetLastError());
+  if (rep) {
+    if (dn == 2) {
+      rep->iterations = 0;
+      rep->matvecs = 0;
+      rep->relative_residual = 0.0;
+      rep->converged = 1;
+      rep->breakdown = 0;
+    } else {
+      rep->iterations = hs.iterations;
+      rep->matvecs = hs.matvecs;
+      rep->relative_residual = hs.rel;
+      rep->converged = hs.converged;
+      rep->breakdown = hs.breakdown;
+    }
+  }
+  return NGD_OK;
+}
+
+int ngd_dot(ngd_ctx* c, const double* x, const double* y, int64_t n, double* h_out) {
+  TRY(bind(c));
+  dot(x, y, n, c->redp.d(), c->counter(7), c->S(SC_TMP), nullptr, c->stream);
+  CK(cudaMemcpyAsync(&c->h_pin[24 + 16], c->S(SC_TMP), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *h_out = c->h_pin[24 + 16];
+  return NGD_OK;
+}
+
+int ngd_axpy(ngd_ctx* c, const double* a, double alpha, const double* b, double* out, int64_t n) {
+  TRY(bind(c));
+  theta_minus(a, alpha, b, out, n, c->stream);
+  CK(cudaGetLastError());
+  return NGD_OK;
+}
+
+int ngd_stream_sync(ngd_ctx* c) {
+  TRY(bind(c));
+  CK(cudaStreamSynchronize(c->stream));
+  return NGD_OK;
+}
+
+}  // extern "C"

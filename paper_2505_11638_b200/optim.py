@@ -1,0 +1,242 @@
+"""NystromNGD outer loop on the GPU (mirror of nystromngd/optim.py:19-270).
+
+The host keeps only the scalar policy of the reference -- ``adapt_mu``,
+``adapt_rank``, the Armijo backtracking control flow, the rng that seeds each
+sketch -- restated here with the same names and semantics.  theta, the
+gradient, the sketch, the Nystrom factor and the PCG iterates stay on the
+device; the host reads back the scalars the policy needs (loss, ||g||, top
+eigenvalue, g.d, PCG report, candidate losses).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .gramian import GramianOperator, ShiftedOperator
+from .krylov import pcg
+from .sketch import NystromPreconditioner, nystrom_approximate
+
+EPS_MACH = np.finfo(float).eps  # optim.py:19
+
+__all__ = ["NystromNgdConfig", "RunRecord", "adapt_mu", "adapt_rank", "backtracking_linesearch", "nystrom_ngd_run"]
+
+
+@dataclass(frozen=True)
+class NystromNgdConfig:
+    """optim.py:40-69, plus two build-specific knobs:
+    ``fixed_rank`` pins ell = ell0 (benchmark configs) and
+    ``omega_source`` picks host-numpy ("host", bit-identical to the reference)
+    or on-device Philox ("device") Gaussian test matrices."""
+
+    ell0: int = 10
+    ell_max: int | None = None
+    gamma: float | None = None
+    cg_maxit: int = 20
+    kappa: float = 0.1
+    rank_ratio: float = 10.0
+    mu_floor_mode: str = "loss-power"
+    mu_floor_coeff: float = 1e-4
+    mu_floor_exponent: float = 2.0
+    ls_shrink: float = 0.5
+    ls_max_backtracks: int = 30
+    ls_sufficient_decrease: float = 1e-4
+    iterations: int = 300
+    seed: int = 0
+    fixed_rank: bool = False
+    omega_source: str = "host"
+
+    def __post_init__(self):
+        if self.ell0 < 1:
+            raise ValueError("need ell0 >= 1")
+        if self.ell_max is not None and self.ell0 > self.ell_max:
+            raise ValueError("need 1 <= ell0 <= ell_max")
+        if self.gamma is not None and self.gamma <= 0:
+            raise ValueError("gamma must be positive")
+        if not 0.0 < self.kappa < 1.0:
+            raise ValueError("kappa must be in (0, 1)")
+        if self.mu_floor_mode not in ("loss-power", "grad-power", "constant"):
+            raise ValueError(f"unknown mu floor mode {self.mu_floor_mode!r}")
+        if self.omega_source not in ("host", "device"):
+            raise ValueError(f"unknown omega source {self.omega_source!r}")
+
+
+@dataclass(frozen=True)
+class RunRecord:
+    """One optimizer iteration in the trace (optim.py:72-83)."""
+
+    iteration: int
+    loss: float
+    h1_rel_error: float
+    mu: float
+    ell: int
+    pcg_iters: int
+    matvecs: int
+    seconds: float
+
+
+def adapt_mu(lam1, gamma, loss, grad_norm, mode, coeff, exponent):
+    """mu = max(gamma * eps * lam1, floor) (optim.py:86-103)."""
+    if lam1 < 0 or gamma <= 0:
+        raise ValueError("need lam1 >= 0 and gamma > 0")
+    base = gamma * EPS_MACH * lam1
+    if mode == "loss-power":
+        floor = coeff * abs(loss) ** exponent
+    elif mode == "grad-power":
+        floor = coeff * grad_norm**exponent
+    elif mode == "constant":
+        floor = coeff
+    else:
+        raise ValueError(f"unknown mu floor mode {mode!r}")
+    return max(base, floor)
+
+
+def adapt_rank(eigenvalues, mu, ell, ell_max, ratio=10.0):
+    """Next sketch rank from the estimated spectrum (optim.py:106-118)."""
+    eigenvalues = np.asarray(eigenvalues, dtype=float)
+    threshold = ratio * mu
+    if eigenvalues[-1] > threshold:
+        return min(2 * ell, ell_max)
+    first_below = int(np.argmax(eigenvalues < threshold)) + 1
+    return min(first_below + 1, ell_max)
+
+
+def backtracking_linesearch(theta, direction, loss_fn, grad_dot_dir, shrink=0.5, max_backtracks=30,
+                            sufficient_decrease=1e-4, loss0=None):
+    """Armijo backtracking along theta - alpha * direction (optim.py:121-146).
+
+    ``loss_fn(theta, alpha, direction)`` evaluates the loss at the candidate
+    (on the device); ``loss0`` may be supplied when the caller already holds
+    the (bitwise identical, deterministic) loss at theta."""
+    if loss0 is None:
+        loss0 = loss_fn(theta, 0.0, direction)
+    alpha = 1.0
+    for _ in range(max_backtracks + 1):
+        try:
+            loss_new = loss_fn(theta, alpha, direction)
+        except _lib.NonFiniteError:
+            loss_new = np.inf
+        if loss_new <= loss0 - sufficient_decrease * alpha * grad_dot_dir:
+            return alpha, loss_new
+        alpha *= shrink
+    return 0.0, loss0
+
+
+def _resolve_gamma(config, p):
+    return float(config.gamma) if config.gamma is not None else float(p)
+
+
+def _resolve_ell_max(config, p):  # optim.py:169-174
+    if config.ell_max is not None:
+        return min(config.ell_max, p)
+    return max(min(500, p // 2), min(config.ell0, p))
+
+
+def _cg_rel_tol(kappa, grad_norm):  # optim.py:183-185
+    return min(max(min(kappa, grad_norm), 1e-300), 1.0 - 1e-16)
+
+
+class _StepTimer:
+    """Optional per-phase CUDA-event timing (bench.py)."""
+
+    def __init__(self, enabled):
+        self.enabled = enabled
+        self.events = []
+
+    def mark(self, name):
+        if self.enabled:
+            torch = _lib.torch_mod()
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.events.append((name, e))
+
+
+def nystrom_ngd_run(problem, theta0, config, quad, quad_eval=None, h1_stop=None, step_hook=None, timer=None):
+    """Natural gradient descent with a randomized Nystrom preconditioner (optim.py:188-270).
+
+    Returns (theta_final, [RunRecord, ...]); theta_final is a CUDA tensor if
+    theta0 was one, else a numpy array."""
+    torch = _lib.torch_mod()
+    theta = _lib.to_device(theta0).clone()
+    p = theta.shape[0]
+    gamma = _resolve_gamma(config, p)
+    ell_max = _resolve_ell_max(config, p)
+    ell = min(config.ell0, ell_max)
+    rng = np.random.default_rng(config.seed)
+    ctx = problem.context(quad)
+    if ctx.p != p:
+        raise ValueError(f"expected {ctx.p} parameters, got {p}")
+    cand = torch.empty_like(theta)
+
+    def loss_at(th, alpha, direction):
+        out = _lib.ctypes.c_double()
+        ctx.call("ngd_loss_at", _lib.ptr(th), float(alpha), _lib.ptr(direction), _lib.ctypes.byref(out))
+        return float(out.value)
+
+    def dot(a, b):
+        out = _lib.ctypes.c_double()
+        ctx.call("ngd_dot", _lib.ptr(a), _lib.ptr(b), p, _lib.ctypes.byref(out))
+        return float(out.value)
+
+    records = []
+    total_matvecs = 0
+    floor_boost = 1.0
+    grad = torch.empty_like(theta)
+    for k in range(config.iterations):
+        tic = time.perf_counter()
+        if timer:
+            timer.mark("start")
+        gop = GramianOperator.from_problem(problem, theta, quad)  # linearise once: loss, jets, adjoints
+        loss = gop.loss
+        if not np.isfinite(loss):
+            raise _lib.NonFiniteError(f"non-finite loss at iteration {k}")
+        ctx.call("ngd_loss_grad", _lib.ptr(grad))
+        grad_norm = float(np.sqrt(dot(grad, grad)))
+        if timer:
+            timer.mark("linearize+grad")
+        factor = nystrom_approximate(gop, ell, seed=int(rng.integers(2**63)), omega_source=config.omega_source)
+        if timer:
+            timer.mark("sketch")
+        mu = adapt_mu(factor.eig_host[0], gamma, loss, grad_norm, config.mu_floor_mode,
+                      config.mu_floor_coeff * floor_boost, config.mu_floor_exponent)
+        if mu <= 0.0:
+            mu = gamma * EPS_MACH
+        precond = NystromPreconditioner(factor, mu)
+        report = pcg(ShiftedOperator(gop, mu), grad, _cg_rel_tol(config.kappa, grad_norm), config.cg_maxit,
+                     precond=precond)
+        if timer:
+            timer.mark("pcg")
+        d = report.solution
+        alpha, _ = backtracking_linesearch(theta, d, loss_at, dot(grad, d), shrink=config.ls_shrink,
+                                           max_backtracks=config.ls_max_backtracks,
+                                           sufficient_decrease=config.ls_sufficient_decrease, loss0=loss)
+        if step_hook is not None:
+            step_hook(k, {"theta": theta.clone(), "grad": grad.clone(), "direction": d.clone(), "alpha": alpha,
+                          "eigenvalues": factor.eig_host, "mu": mu, "report": report})
+        if alpha == 0.0:
+            floor_boost *= 10.0
+        else:
+            ctx.call("ngd_axpy", _lib.ptr(theta), float(alpha), _lib.ptr(d), _lib.ptr(cand), p)
+            theta, cand = cand, theta
+            floor_boost = 1.0
+        if timer:
+            timer.mark("linesearch")
+        total_matvecs += gop.matvec_count
+        h1 = float("nan")
+        if quad_eval is not None:
+            h1 = h1_relative_error(problem, theta, quad_eval)
+        records.append(RunRecord(k, loss, h1, mu, ell, report.iterations, total_matvecs, time.perf_counter() - tic))
+        if not config.fixed_rank:
+            ell = adapt_rank(factor.eig_host, mu, ell, ell_max, ratio=config.rank_ratio)
+        if h1_stop is not None and records[-1].h1_rel_error <= h1_stop:
+            break
+    return _lib.like_input(theta, theta0), records
+
+
+def h1_relative_error(problem, theta, quad):
+    """Relative H1 error (problems.py:104-119).  Not yet a device kernel: evaluated
+    from device jets when available; raises otherwise."""
+    raise NotImplementedError("h1_relative_error on the device is not implemented yet")
