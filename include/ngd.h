@@ -106,14 +106,25 @@ int ngd_pcg(ngd_ctx* ctx, const double* d_dense, int64_t p, const double* d_b, d
             const double* d_U_rowmajor, const double* d_eig, int32_t ell, double precond_mu, double rel_tol,
             int32_t maxit, int32_t recompute_every, double* d_x, ngd_solve_report* h_report);
 
+/* ---- tuning knobs: "svd" = 0 (Householder QR + Jacobi SVD) | 1 (shifted Cholesky-QR3 + polar SVD, default) */
+int ngd_set_option(ngd_ctx* ctx, const char* key, int64_t value);
+
 /* ---- vector helpers used by the host policy ------------------------------
  * ngd_dot: h_out = x . y (deterministic reduction, synchronises);
  * ngd_axpy: out = a - alpha * b (theta update / line-search candidate, optim.py:137,252) */
 int ngd_dot(ngd_ctx* ctx, const double* d_x, const double* d_y, int64_t n, double* h_out);
 int ngd_axpy(ngd_ctx* ctx, const double* d_a, double alpha, const double* d_b, double* d_out, int64_t n);
 
-/* ---- timing support for bench.py: kernel events on the context stream --- */
+/* ---- evidence for bench.py ---------------------------------------------
+ * ngd_launch_count: number of this library's kernel launches so far (process-wide).
+ * ngd_probe_start(kind, n): bracket the next n launches of kernel class `kind`
+ *   (1 FWD jets, 2 REV jets, 3 phase A, 4 phase B, 5 J rows, 6 preconditioner,
+ *   7 vector/scalar, 8 pack) with CUDA events on their launch stream;
+ *   ngd_probe_stop returns the summed device time and the launch count. */
 int ngd_stream_sync(ngd_ctx* ctx);
+int64_t ngd_launch_count(void);
+int ngd_probe_start(int32_t kind, int32_t max_launches);
+int ngd_probe_stop(double* h_total_ms, int64_t* h_count);
 
 #ifdef __cplusplus
 }

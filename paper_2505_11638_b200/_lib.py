@@ -67,13 +67,30 @@ SIGNATURES = {
     "ngd_dense_matmat": [_P, _P, _I64, _P, _I64, _P],
     "ngd_precond_apply": [_P, _P, _P, _I32, _D, _P, _P, _I64],
     "ngd_pcg": [_P, _P, _I64, _P, _D, _P, _P, _I32, _D, _D, _I32, _I32, _P, ctypes.POINTER(SolveReportC)],
+    "ngd_set_option": [_P, ctypes.c_char_p, _I64],
     "ngd_dot": [_P, _P, _P, _I64, ctypes.POINTER(_D)],
     "ngd_axpy": [_P, _P, _D, _P, _P, _I64],
     "ngd_stream_sync": [_P],
+    "ngd_launch_count": [],
+    "ngd_probe_start": [_I32, _I32],
+    "ngd_probe_stop": [ctypes.POINTER(_D), ctypes.POINTER(_I64)],
 }
-_RESTYPE = {"ngd_last_error": ctypes.c_char_p, "ngd_param_count": _I64}
+_RESTYPE = {"ngd_last_error": ctypes.c_char_p, "ngd_param_count": _I64, "ngd_launch_count": _I64}
 
 _lib = None
+_contexts = []  # weak registry so option changes reach live contexts
+OPTIONS = {"svd": 1}
+
+
+def set_option(key, value):
+    """Set a library knob on every live and future context (see ngd_set_option)."""
+    import weakref
+
+    OPTIONS[key] = int(value)
+    for ref in list(_contexts):
+        ctx = ref()
+        if ctx is not None and ctx._h is not None:
+            ctx.call("ngd_set_option", key.encode(), int(value))
 
 
 def load():
@@ -176,6 +193,11 @@ class Context:
         self.points_key = None
         self.lin_token = 0
         self.lin_owner = None
+        import weakref
+
+        for k, v in OPTIONS.items():
+            self.call("ngd_set_option", k.encode(), int(v))
+        _contexts.append(weakref.ref(self))
 
     @property
     def handle(self):

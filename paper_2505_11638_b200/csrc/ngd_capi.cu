@@ -124,6 +124,9 @@ struct ngd_ctx {
   Buf fj_tab;                 // FormJ device tables
   Buf nys_m, nys_tau, nys_r, nys_ur, nys_v, nys_s, nys_work, nys_info;
   double* h_pin = nullptr;    // pinned host scalars
+  cusolverDnParams_t dn_params = nullptr;
+  std::vector<char> h_work;
+  int svd_method = 1;
   bool lin_valid = false;
 
   double* S(int i) { return scal.d() + i; }
@@ -290,6 +293,52 @@ static int need_lin(ngd_ctx* c) {
   return NGD_OK;
 }
 
+// Shifted Cholesky-QR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020) in place:
+// B (p x ell, col-major) <- Q, nys_r <- R (upper, ell x ell, col-major).
+static int scholqr3(ngd_ctx* c, double* B, int64_t p, int ell) {
+  const double one = 1.0, zero = 0.0;
+  int lw = 0;
+  CKS(cusolverDnDpotrf_bufferSize(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, &lw));
+  CK(c->nys_work.ensure(sizeof(double) * std::max<size_t>(lw, (size_t)ell * ell)));
+  CK(c->nys_v.ensure(sizeof(double) * (size_t)ell * ell));
+  int* info = static_cast<int*>(c->nys_info.p);
+  const double shift_coef = 11.0 * ((double)p * ell + (double)ell * (ell + 1)) * 2.220446049250313e-16;
+  for (int pass = 0; pass < 3; ++pass) {
+    double* W = c->nys_m.d();
+    CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, B, (int)p, &zero, W, ell));
+    if (pass == 0) shift_diag(W, ell, shift_coef, c->stream);
+    CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, ell, W, ell, c->nys_work.d(), lw, info));
+    triu(W, ell, ell, c->stream);
+    CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p, ell,
+                    &one, W, ell, B, (int)p));
+    if (pass == 0) {
+      CK(cudaMemcpyAsync(c->nys_r.d(), W, sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+      // R <- R_pass * R  (both upper triangular)
+      CKB(cublasDtrmm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ell, ell,
+                      &one, W, ell, c->nys_r.d(), ell, c->nys_v.d(), ell));
+      CK(cudaMemcpyAsync(c->nys_r.d(), c->nys_v.d(), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+  return NGD_OK;
+}
+
+// SVD of the ell x ell matrix in nys_r: singular values -> nys_s (descending), U -> nys_ur.
+static int small_svd_polar(ngd_ctx* c, int ell) {
+  if (!c->dn_params) CKS(cusolverDnCreateParams(&c->dn_params));
+  size_t wd = 0, wh = 0;
+  CKS(cusolverDnXgesvdp_bufferSize(c->sol, c->dn_params, CUSOLVER_EIG_MODE_VECTOR, 1, ell, ell, CUDA_R_64F,
+                                   c->nys_r.d(), ell, CUDA_R_64F, c->nys_s.d(), CUDA_R_64F, c->nys_ur.d(), ell,
+                                   CUDA_R_64F, c->nys_v.d(), ell, CUDA_R_64F, &wd, &wh));
+  CK(c->nys_work.ensure(std::max<size_t>(wd, 8)));
+  c->h_work.resize(std::max<size_t>(wh, 8));
+  double err = 0.0;
+  CKS(cusolverDnXgesvdp(c->sol, c->dn_params, CUSOLVER_EIG_MODE_VECTOR, 1, ell, ell, CUDA_R_64F, c->nys_r.d(), ell,
+                        CUDA_R_64F, c->nys_s.d(), CUDA_R_64F, c->nys_ur.d(), ell, CUDA_R_64F, c->nys_v.d(), ell,
+                        CUDA_R_64F, c->nys_work.p, wd, c->h_work.data(), wh, static_cast<int*>(c->nys_info.p), &err));
+  return NGD_OK;
+}
+
 extern "C" {
 
 const char* ngd_last_error(void) { return g_err.c_str(); }
@@ -385,6 +434,7 @@ int ngd_ctx_destroy(ngd_ctx* c) {
     b->release();
   if (c->h_pin) cudaFreeHost(c->h_pin);
   if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
+  if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
   if (c->sol) cusolverDnDestroy(c->sol);
   if (c->blas) cublasDestroy(c->blas);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -707,16 +757,24 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
   // 3. B = Y_nu C^{-1}
   CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p, ell,
                   &one, c->nys_m.d(), ell, Y, (int)p));
-  // 4. B = Q R
-  CKS(cusolverDnDgeqrf(c->sol, (int)p, ell, Y, (int)p, c->nys_tau.d(), c->nys_work.d(), lw_geqrf, info));
-  CK(cudaMemcpy2DAsync(c->nys_r.d(), sizeof(double) * ell, Y, sizeof(double) * p, sizeof(double) * ell, ell,
-                       cudaMemcpyDeviceToDevice, c->stream));
-  triu(c->nys_r.d(), ell, ell, c->stream);
-  // 5. R = U_R diag(s) V^T (Jacobi, descending)
-  CKS(cusolverDnDgesvdj(c->sol, CUSOLVER_EIG_MODE_VECTOR, 0, ell, ell, c->nys_r.d(), ell, c->nys_s.d(), c->nys_ur.d(),
-                        ell, c->nys_v.d(), ell, c->nys_work.d(), lw_svd, info, c->svdj));
-  // 6. Q explicitly, U^T = U_R^T Q^T  (row-major p x ell output)
-  CKS(cusolverDnDorgqr(c->sol, (int)p, ell, ell, Y, (int)p, c->nys_tau.d(), c->nys_work.d(), lw_orgqr, info));
+  if (c->svd_method == 0) {
+    // 4. B = Q R (Householder)
+    CKS(cusolverDnDgeqrf(c->sol, (int)p, ell, Y, (int)p, c->nys_tau.d(), c->nys_work.d(), lw_geqrf, info));
+    CK(cudaMemcpy2DAsync(c->nys_r.d(), sizeof(double) * ell, Y, sizeof(double) * p, sizeof(double) * ell, ell,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    triu(c->nys_r.d(), ell, ell, c->stream);
+    // 5. R = U_R diag(s) V^T (Jacobi, descending)
+    CKS(cusolverDnDgesvdj(c->sol, CUSOLVER_EIG_MODE_VECTOR, 0, ell, ell, c->nys_r.d(), ell, c->nys_s.d(),
+                          c->nys_ur.d(), ell, c->nys_v.d(), ell, c->nys_work.d(), lw_svd, info, c->svdj));
+    // 6. Q explicitly
+    CKS(cusolverDnDorgqr(c->sol, (int)p, ell, ell, Y, (int)p, c->nys_tau.d(), c->nys_work.d(), lw_orgqr, info));
+  } else {
+    // 4. B = Q R by shifted Cholesky-QR3 (GEMM/SYRK + potrf + TRSM; stable for cond(B) up to 1/eps)
+    TRY(scholqr3(c, Y, p, ell));
+    // 5. R = U_R diag(s) V^T (polar-decomposition SVD, descending)
+    TRY(small_svd_polar(c, ell));
+  }
+  // U^T = U_R^T Q^T  (row-major p x ell output)
   CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_T, ell, (int)p, ell, &one, c->nys_ur.d(), ell, Y, (int)p, &zero,
                   U_row, ell));
   eig_from_sv(c->nys_s.d(), ell, c->S(SC_SHIFT), eig, c->stream);
@@ -850,6 +908,16 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
     }
   }
   return NGD_OK;
+}
+
+int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
+  if (!c || !key) return fail(NGD_E_SHAPE, "bad option");
+  if (!strcmp(key, "svd")) {
+    if (value < 0 || value > 1) return fail(NGD_E_SHAPE, "svd method must be 0 (geqrf+gesvdj) or 1 (scholqr3+gesvdp)");
+    c->svd_method = (int)value;
+    return NGD_OK;
+  }
+  return fail(NGD_E_SHAPE, "unknown option '%s'", key);
 }
 
 int ngd_dot(ngd_ctx* c, const double* x, const double* y, int64_t n, double* h_out) {

@@ -231,7 +231,9 @@ static cudaError_t launch_jet(const JetArgs& a, int nblocks, int mtiles, cudaStr
     attr_set = true;
   }
   if (nblocks <= 0 || mtiles <= 0) return cudaSuccess;
+  probe_before(MODE == FWD ? K_FWD : (MODE == REV ? K_REV : K_PHA), st);
   kern<<<dim3(nblocks, mtiles), kThreads, smem, st>>>(a);
+  probe_after(MODE == FWD ? K_FWD : (MODE == REV ? K_REV : K_PHA), st);
   return cudaGetLastError();
 }
 
@@ -372,7 +374,9 @@ __global__ void __launch_bounds__(kThreads) phb_kernel(PhbArgs p) {
 
 cudaError_t phase_b(const PhbArgs& a, int splits, cudaStream_t st) {
   dim3 grid((a.N + PBN - 1) / PBN, (a.M + PBM - 1) / PBM, splits);
+  probe_before(K_PHB, st);
   phb_kernel<<<grid, kThreads, 0, st>>>(a);
+  probe_after(K_PHB, st);
   return cudaGetLastError();
 }
 
@@ -417,7 +421,9 @@ __global__ void __launch_bounds__(kThreads) formj_kernel(FormJArgs a) {
 
 cudaError_t form_j(const FormJArgs& a, int R, int n_layers, cudaStream_t st) {
   if (R <= 0) return cudaSuccess;
+  probe_before(K_FORMJ, st);
   formj_kernel<<<dim3(R, n_layers), kThreads, 0, st>>>(a);
+  probe_after(K_FORMJ, st);
   return cudaGetLastError();
 }
 

@@ -7,6 +7,11 @@
 
 namespace ngd {
 
+// kernel classes for launch accounting / probe timing (ngd_probe.cu)
+enum KernelKind { K_FWD = 1, K_REV = 2, K_PHA = 3, K_PHB = 4, K_FORMJ = 5, K_PRECOND = 6, K_VEC = 7, K_PACK = 8 };
+void probe_before(int kind, cudaStream_t st);
+void probe_after(int kind, cudaStream_t st);
+
 // device-side PCG scalars (krylov.py:24-88)
 struct PcgState {
   double bb, norm_b, tol, rz, rz_new, dad, alpha, rr, rel;
@@ -101,6 +106,7 @@ void scale_rows(double* S, int64_t R, int ell, const double* w, cudaStream_t st)
 void add_shift(double* y, const double* omega, int64_t n, const double* fro2, double* shift_out, cudaStream_t st);
 void eig_from_sv(const double* s, int ell, const double* shift, double* eig, cudaStream_t st);
 void triu(double* a, int n, int lda, cudaStream_t st);
+void shift_diag(double* w, int n, double coef, cudaStream_t st);
 void fill_gaussian(double* out, int64_t n, uint64_t seed, cudaStream_t st);
 void gather_points(const double* padded, double* compact, Geom gm, cudaStream_t st);
 void scatter_points(const double* compact, double* padded, Geom gm, cudaStream_t st);

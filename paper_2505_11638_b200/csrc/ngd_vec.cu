@@ -30,7 +30,9 @@ void pack(double* dst, int Mp, int Kp, const double* src, int64_t off, int n_out
           const int* skip, cudaStream_t st) {
   const int64_t n = (int64_t)Mp * Kp;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  probe_before(K_PACK, st);
   pack_kernel<<<grid, 256, 0, st>>>(dst, Mp, Kp, src, off, n_out, n_in, trans, skip);
+  probe_after(K_PACK, st);
 }
 
 // --------------------- input jets and output adjoint seeds ------------------
@@ -75,8 +77,12 @@ void init_point_data(double* zin1, double* dlast, Geom gm, const double* x_int, 
                      cudaStream_t st) {
   const int npts = gm.n_pts_pad();
   const int grid = std::max(1, std::min((npts + 255) / 256, 148 * 8));
+  probe_before(K_VEC, st);
   input_jets_kernel<<<grid, 256, 0, st>>>(zin1, gm.s_pad, gm, x_int, x_bnd);
+  probe_after(K_VEC, st);
+  probe_before(K_VEC, st);
   seed_adjoint_kernel<<<grid, 256, 0, st>>>(dlast, gm);
+  probe_after(K_VEC, st);
 }
 
 // ----------------------- deterministic two-stage sums ------------------------
@@ -118,7 +124,9 @@ __global__ void dot_kernel(const double* x, const double* y, int64_t n, double* 
 
 void dot(const double* x, const double* y, int64_t n, double* partials, unsigned int* slot, double* out, const int* done,
          cudaStream_t st) {
+  probe_before(K_VEC, st);
   dot_kernel<<<nblocks_for(n), kThreads, 0, st>>>(x, y, n, partials, slot, out, done);
+  probe_after(K_VEC, st);
 }
 
 // residual / loss: F = metric channel of the output-layer pre-activations;
@@ -141,8 +149,12 @@ __global__ void residual_kernel(const double* pre_last, Geom gm, const double* w
 
 void residual_loss(const double* pre_last, Geom gm, const double* w, const double* off, double* F, double* cot,
                    double* partials, unsigned int* slot, double* loss_sum, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  probe_before(K_VEC, st);
   residual_kernel<<<nblocks_for(gm.n_pts_pad()), kThreads, 0, st>>>(pre_last, gm, w, off, F, cot, partials, slot,
                                                                     loss_sum);
+  probe_after(K_VEC, st);
+  probe_after(K_VEC, st);
 }
 
 // phase A reduction: s[pt] = sum over (layer, mtile) partials in fixed order; cot = w * s
@@ -159,7 +171,9 @@ __global__ void reduce_pha_kernel(const double* partA, int rows, int n_pts_pad, 
 void reduce_pha(const double* partA, int rows, int n_pts_pad, const double* w, double* cot, const int* done,
                 cudaStream_t st) {
   const int grid = std::max(1, std::min((n_pts_pad + 255) / 256, 148 * 8));
+  probe_before(K_VEC, st);
   reduce_pha_kernel<<<grid, 256, 0, st>>>(partA, rows, n_pts_pad, w, cot, done);
+  probe_after(K_VEC, st);
 }
 
 // phase B reduction: out[i] = sum_g part[g][i] (+ mu * v[i])
@@ -177,7 +191,9 @@ __global__ void reduce_splits_kernel(const double* part, int G, int64_t p, doubl
 void reduce_splits(const double* part, int G, int64_t p, double mu, const double* v, double* out, const int* done,
                    cudaStream_t st) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((p + 255) / 256, 148 * 8));
+  probe_before(K_VEC, st);
   reduce_splits_kernel<<<grid, 256, 0, st>>>(part, G, p, mu, v, out, done);
+  probe_after(K_VEC, st);
 }
 
 // out += mu * v
@@ -188,7 +204,9 @@ __global__ void add_scaled_kernel(double* out, double mu, const double* v, int64
 }
 void add_scaled(double* out, double mu, const double* v, int64_t n, const int* done, cudaStream_t st) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+  probe_before(K_VEC, st);
   add_scaled_kernel<<<grid, 256, 0, st>>>(out, mu, v, n, done);
+  probe_after(K_VEC, st);
 }
 
 // padded point order (interior blocks, then boundary blocks) <-> compact order
@@ -202,12 +220,16 @@ __global__ void gather_points_kernel(const double* padded, double* compact, Geom
 }
 void gather_points(const double* padded, double* compact, Geom gm, cudaStream_t st) {
   const int n = gm.n_int + gm.n_bnd;
+  probe_before(K_VEC, st);
   gather_points_kernel<<<std::max(1, std::min((n + 255) / 256, 1184)), 256, 0, st>>>(padded, compact, gm, 0);
+  probe_after(K_VEC, st);
 }
 void scatter_points(const double* compact, double* padded, Geom gm, cudaStream_t st) {
   cudaMemsetAsync(padded, 0, sizeof(double) * gm.n_pts_pad(), st);
   const int n = gm.n_int + gm.n_bnd;
+  probe_before(K_VEC, st);
   gather_points_kernel<<<std::max(1, std::min((n + 255) / 256, 1184)), 256, 0, st>>>(compact, padded, gm, 1);
+  probe_after(K_VEC, st);
 }
 
 // ------------------------- Nystrom preconditioner ---------------------------
@@ -282,7 +304,7 @@ cudaError_t precond_apply(const double* U, int64_t p, int ell, const double* eig
   const int nblk = precond_blocks(p);
   const int64_t rpb = (p + nblk - 1) / nblk;
   const int jch = (ell + 31) / 32;
-#define NGD_UTV(J) utv_kernel<J><<<nblk, kThreads, 0, st>>>(U, p, ell, v, rpb, part, done)
+#define NGD_UTV(J) (probe_before(K_PRECOND, st), utv_kernel<J><<<nblk, kThreads, 0, st>>>(U, p, ell, v, rpb, part, done), probe_after(K_PRECOND, st))
   if (jch <= 1) NGD_UTV(1);
   else if (jch <= 2) NGD_UTV(2);
   else if (jch <= 4) NGD_UTV(4);
@@ -292,9 +314,13 @@ cudaError_t precond_apply(const double* U, int64_t p, int ell, const double* eig
   else if (jch <= 32) NGD_UTV(32);
   else return cudaErrorInvalidValue;
 #undef NGD_UTV
+  probe_before(K_PRECOND, st);
   utv_combine_kernel<<<(ell + 255) / 256, 256, 0, st>>>(part, nblk, ell, eig, mu_p, mu_v, cprime, done);
+  probe_after(K_PRECOND, st);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((p + 7) / 8, 148 * 8));
+  probe_before(K_PRECOND, st);
   uc_kernel<<<grid, kThreads, sizeof(double) * ell, st>>>(U, p, ell, cprime, v, out, done);
+  probe_after(K_PRECOND, st);
   return cudaGetLastError();
 }
 
@@ -390,28 +416,56 @@ __global__ void pcg_final_kernel(PcgState* s) {
 
 static int vgrid(int64_t p) { return (int)std::max<int64_t>(1, std::min<int64_t>((p + 255) / 256, 148 * 8)); }
 
-void pcg_init(PcgState* s, double rel_tol, cudaStream_t st) { pcg_init_kernel<<<1, 1, 0, st>>>(s, rel_tol); }
+void pcg_init(PcgState* s, double rel_tol, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  pcg_init_kernel<<<1, 1, 0, st>>>(s, rel_tol);
+  probe_after(K_VEC, st);
+}
 void pcg_start(const double* b, double* x, double* r, int64_t p, cudaStream_t st) {
+  probe_before(K_VEC, st);
   pcg_start_kernel<<<vgrid(p), 256, 0, st>>>(b, x, r, p);
+  probe_after(K_VEC, st);
 }
 void pcg_first_dir(const double* z, double* d, int64_t p, PcgState* s, cudaStream_t st) {
+  probe_before(K_VEC, st);
   pcg_first_dir_kernel<<<vgrid(p), 256, 0, st>>>(z, d, p, s);
+  probe_after(K_VEC, st);
 }
-void pcg_alpha(PcgState* s, int it, cudaStream_t st) { pcg_alpha_kernel<<<1, 1, 0, st>>>(s, it); }
+void pcg_alpha(PcgState* s, int it, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  pcg_alpha_kernel<<<1, 1, 0, st>>>(s, it);
+  probe_after(K_VEC, st);
+}
 void pcg_update(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s, int recompute,
                 cudaStream_t st) {
+  probe_before(K_VEC, st);
   pcg_update_kernel<<<vgrid(p), 256, 0, st>>>(x, r, d, ad, p, s, recompute);
+  probe_after(K_VEC, st);
 }
 void pcg_true_res(const double* b, const double* ax, double* r, int64_t p, PcgState* s, int count, int final_pass,
                   cudaStream_t st) {
+  probe_before(K_VEC, st);
   pcg_true_res_kernel<<<vgrid(p), 256, 0, st>>>(b, ax, r, p, s, count, final_pass);
+  probe_after(K_VEC, st);
 }
-void pcg_check(PcgState* s, cudaStream_t st) { pcg_check_kernel<<<1, 1, 0, st>>>(s); }
+void pcg_check(PcgState* s, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  pcg_check_kernel<<<1, 1, 0, st>>>(s);
+  probe_after(K_VEC, st);
+}
 void pcg_dir(const double* z, double* d, int64_t p, PcgState* s, cudaStream_t st) {
+  probe_before(K_VEC, st);
   pcg_dir_kernel<<<vgrid(p), 256, 0, st>>>(z, d, p, s);
+  probe_after(K_VEC, st);
+  probe_before(K_VEC, st);
   pcg_rz_roll_kernel<<<1, 1, 0, st>>>(s);
+  probe_after(K_VEC, st);
 }
-void pcg_final(PcgState* s, cudaStream_t st) { pcg_final_kernel<<<1, 1, 0, st>>>(s); }
+void pcg_final(PcgState* s, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  pcg_final_kernel<<<1, 1, 0, st>>>(s);
+  probe_after(K_VEC, st);
+}
 
 // ------------------------------- small maps ---------------------------------
 // out = a - alpha * b  (line-search candidate, optim.py:137)
@@ -420,7 +474,9 @@ __global__ void axpy_kernel(const double* a, double alpha, const double* b, doub
     out[i] = a[i] - alpha * b[i];
 }
 void theta_minus(const double* a, double alpha, const double* b, double* out, int64_t n, cudaStream_t st) {
+  probe_before(K_VEC, st);
   axpy_kernel<<<vgrid(n), 256, 0, st>>>(a, alpha, b, out, n);
+  probe_after(K_VEC, st);
 }
 
 // S[q][j] (col-major R x ell) *= w[q]
@@ -430,7 +486,9 @@ __global__ void scale_rows_kernel(double* S, int64_t R, int ell, const double* w
     S[i] *= w[i % R];
 }
 void scale_rows(double* S, int64_t R, int ell, const double* w, cudaStream_t st) {
+  probe_before(K_VEC, st);
   scale_rows_kernel<<<vgrid(R * ell), 256, 0, st>>>(S, R, ell, w);
+  probe_after(K_VEC, st);
 }
 
 // y += shift * omega where shift = eps * sqrt(*fro2)  (sketch.py:77-78); writes shift
@@ -441,7 +499,9 @@ __global__ void shift_kernel(double* y, const double* omega, int64_t n, const do
     y[i] = y[i] + shift * omega[i];
 }
 void add_shift(double* y, const double* omega, int64_t n, const double* fro2, double* shift_out, cudaStream_t st) {
+  probe_before(K_VEC, st);
   shift_kernel<<<vgrid(n), 256, 0, st>>>(y, omega, n, fro2, shift_out);
+  probe_after(K_VEC, st);
 }
 
 // eig = max(s^2 - shift, 0)  (sketch.py:86)
@@ -450,7 +510,26 @@ __global__ void eig_kernel(const double* s, int ell, const double* shift, double
     eig[j] = fmax(s[j] * s[j] - *shift, 0.0);
 }
 void eig_from_sv(const double* s, int ell, const double* shift, double* eig, cudaStream_t st) {
+  probe_before(K_VEC, st);
   eig_kernel<<<(ell + 255) / 256, 256, 0, st>>>(s, ell, shift, eig);
+  probe_after(K_VEC, st);
+}
+
+// W += coef * trace(W) * I  (sCholQR3 shift, ||B||_F^2 = trace(B^T B)); one block
+__global__ void shift_diag_kernel(double* w, int n, double coef) {
+  __shared__ double sh[kThreads / 32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v += w[(int64_t)i * n + i];
+  const double tr = block_sum(v, sh);
+  __shared__ double s;
+  if (threadIdx.x == 0) s = coef * tr;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) w[(int64_t)i * n + i] += s;
+}
+void shift_diag(double* w, int n, double coef, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  shift_diag_kernel<<<1, kThreads, 0, st>>>(w, n, coef);
+  probe_after(K_VEC, st);
 }
 
 // zero the strictly-lower triangle of an n x n column-major matrix (potrf leaves garbage there)
@@ -462,7 +541,9 @@ __global__ void triu_kernel(double* a, int n, int lda) {
   }
 }
 void triu(double* a, int n, int lda, cudaStream_t st) {
+  probe_before(K_VEC, st);
   triu_kernel<<<vgrid((int64_t)n * n), 256, 0, st>>>(a, n, lda);
+  probe_after(K_VEC, st);
 }
 
 // --------------------------- Philox4x32-10 Gaussians ------------------------
@@ -494,7 +575,9 @@ __global__ void gaussian_kernel(double* out, int64_t n, uint64_t seed) {
   }
 }
 void fill_gaussian(double* out, int64_t n, uint64_t seed, cudaStream_t st) {
+  probe_before(K_VEC, st);
   gaussian_kernel<<<vgrid((n + 1) / 2), 256, 0, st>>>(out, n, seed);
+  probe_after(K_VEC, st);
 }
 
 }  // namespace ngd

@@ -154,86 +154,108 @@ class _StepTimer:
             self.events.append((name, e))
 
 
-def nystrom_ngd_run(problem, theta0, config, quad, quad_eval=None, h1_stop=None, step_hook=None, timer=None):
-    """Natural gradient descent with a randomized Nystrom preconditioner (optim.py:188-270).
+class NystromNgdRunner:
+    """Step-wise form of ``nystrom_ngd_run`` (optim.py:188-270): one ``step()`` is
+    one NGD iteration (linearise, gradient, sketch, damping, PCG, line search,
+    update, rank adaptation).  State (theta, rng, ell, floor boost, matvec
+    total) lives here so benchmarks can time single steps."""
 
-    Returns (theta_final, [RunRecord, ...]); theta_final is a CUDA tensor if
-    theta0 was one, else a numpy array."""
-    torch = _lib.torch_mod()
-    theta = _lib.to_device(theta0).clone()
-    p = theta.shape[0]
-    gamma = _resolve_gamma(config, p)
-    ell_max = _resolve_ell_max(config, p)
-    ell = min(config.ell0, ell_max)
-    rng = np.random.default_rng(config.seed)
-    ctx = problem.context(quad)
-    if ctx.p != p:
-        raise ValueError(f"expected {ctx.p} parameters, got {p}")
-    cand = torch.empty_like(theta)
+    def __init__(self, problem, theta0, config, quad, quad_eval=None):
+        torch = _lib.torch_mod()
+        self.problem, self.config, self.quad, self.quad_eval = problem, config, quad, quad_eval
+        self.theta = _lib.to_device(theta0).clone()
+        p = self.theta.shape[0]
+        self.p = p
+        self.gamma = _resolve_gamma(config, p)
+        self.ell_max = _resolve_ell_max(config, p)
+        self.ell = min(config.ell0, self.ell_max)
+        self.rng = np.random.default_rng(config.seed)
+        self.ctx = problem.context(quad)
+        if self.ctx.p != p:
+            raise ValueError(f"expected {self.ctx.p} parameters, got {p}")
+        self.cand = torch.empty_like(self.theta)
+        self.grad = torch.empty_like(self.theta)
+        self.total_matvecs = 0
+        self.floor_boost = 1.0
+        self.k = 0
 
-    def loss_at(th, alpha, direction):
+    def _loss_at(self, th, alpha, direction):
         out = _lib.ctypes.c_double()
-        ctx.call("ngd_loss_at", _lib.ptr(th), float(alpha), _lib.ptr(direction), _lib.ctypes.byref(out))
+        self.ctx.call("ngd_loss_at", _lib.ptr(th), float(alpha), _lib.ptr(direction), _lib.ctypes.byref(out))
         return float(out.value)
 
-    def dot(a, b):
+    def _dot(self, a, b):
         out = _lib.ctypes.c_double()
-        ctx.call("ngd_dot", _lib.ptr(a), _lib.ptr(b), p, _lib.ctypes.byref(out))
+        self.ctx.call("ngd_dot", _lib.ptr(a), _lib.ptr(b), self.p, _lib.ctypes.byref(out))
         return float(out.value)
 
-    records = []
-    total_matvecs = 0
-    floor_boost = 1.0
-    grad = torch.empty_like(theta)
-    for k in range(config.iterations):
+    def step(self, step_hook=None, timer=None):
+        config, problem, quad = self.config, self.problem, self.quad
+        k = self.k
         tic = time.perf_counter()
         if timer:
             timer.mark("start")
-        gop = GramianOperator.from_problem(problem, theta, quad)  # linearise once: loss, jets, adjoints
+        gop = GramianOperator.from_problem(problem, self.theta, quad)  # linearise once: loss, jets, adjoints
         loss = gop.loss
         if not np.isfinite(loss):
             raise _lib.NonFiniteError(f"non-finite loss at iteration {k}")
-        ctx.call("ngd_loss_grad", _lib.ptr(grad))
-        grad_norm = float(np.sqrt(dot(grad, grad)))
+        self.ctx.call("ngd_loss_grad", _lib.ptr(self.grad))
+        grad = self.grad
+        grad_norm = float(np.sqrt(self._dot(grad, grad)))
         if timer:
             timer.mark("linearize+grad")
-        factor = nystrom_approximate(gop, ell, seed=int(rng.integers(2**63)), omega_source=config.omega_source)
+        factor = nystrom_approximate(gop, self.ell, seed=int(self.rng.integers(2**63)),
+                                     omega_source=config.omega_source)
         if timer:
             timer.mark("sketch")
-        mu = adapt_mu(factor.eig_host[0], gamma, loss, grad_norm, config.mu_floor_mode,
-                      config.mu_floor_coeff * floor_boost, config.mu_floor_exponent)
+        mu = adapt_mu(factor.eig_host[0], self.gamma, loss, grad_norm, config.mu_floor_mode,
+                      config.mu_floor_coeff * self.floor_boost, config.mu_floor_exponent)
         if mu <= 0.0:
-            mu = gamma * EPS_MACH
+            mu = self.gamma * EPS_MACH
         precond = NystromPreconditioner(factor, mu)
         report = pcg(ShiftedOperator(gop, mu), grad, _cg_rel_tol(config.kappa, grad_norm), config.cg_maxit,
                      precond=precond)
         if timer:
             timer.mark("pcg")
         d = report.solution
-        alpha, _ = backtracking_linesearch(theta, d, loss_at, dot(grad, d), shrink=config.ls_shrink,
-                                           max_backtracks=config.ls_max_backtracks,
+        alpha, _ = backtracking_linesearch(self.theta, d, self._loss_at, self._dot(grad, d),
+                                           shrink=config.ls_shrink, max_backtracks=config.ls_max_backtracks,
                                            sufficient_decrease=config.ls_sufficient_decrease, loss0=loss)
         if step_hook is not None:
-            step_hook(k, {"theta": theta.clone(), "grad": grad.clone(), "direction": d.clone(), "alpha": alpha,
-                          "eigenvalues": factor.eig_host, "mu": mu, "report": report})
+            step_hook(k, {"theta": self.theta.clone(), "grad": grad.clone(), "direction": d.clone(),
+                          "alpha": alpha, "eigenvalues": factor.eig_host, "mu": mu, "report": report})
         if alpha == 0.0:
-            floor_boost *= 10.0
+            self.floor_boost *= 10.0
         else:
-            ctx.call("ngd_axpy", _lib.ptr(theta), float(alpha), _lib.ptr(d), _lib.ptr(cand), p)
-            theta, cand = cand, theta
-            floor_boost = 1.0
+            self.ctx.call("ngd_axpy", _lib.ptr(self.theta), float(alpha), _lib.ptr(d), _lib.ptr(self.cand), self.p)
+            self.theta, self.cand = self.cand, self.theta
+            self.floor_boost = 1.0
         if timer:
             timer.mark("linesearch")
-        total_matvecs += gop.matvec_count
+        self.total_matvecs += gop.matvec_count
         h1 = float("nan")
-        if quad_eval is not None:
-            h1 = h1_relative_error(problem, theta, quad_eval)
-        records.append(RunRecord(k, loss, h1, mu, ell, report.iterations, total_matvecs, time.perf_counter() - tic))
+        if self.quad_eval is not None:
+            h1 = h1_relative_error(problem, self.theta, self.quad_eval)
+        rec = RunRecord(k, loss, h1, mu, self.ell, report.iterations, self.total_matvecs, time.perf_counter() - tic)
         if not config.fixed_rank:
-            ell = adapt_rank(factor.eig_host, mu, ell, ell_max, ratio=config.rank_ratio)
+            self.ell = adapt_rank(factor.eig_host, mu, self.ell, self.ell_max, ratio=config.rank_ratio)
+        self.k += 1
+        self.last_matvecs = gop.matvec_count
+        return rec
+
+
+def nystrom_ngd_run(problem, theta0, config, quad, quad_eval=None, h1_stop=None, step_hook=None, timer=None):
+    """Natural gradient descent with a randomized Nystrom preconditioner (optim.py:188-270).
+
+    Returns (theta_final, [RunRecord, ...]); theta_final is a CUDA tensor if
+    theta0 was one, else a numpy array."""
+    runner = NystromNgdRunner(problem, theta0, config, quad, quad_eval)
+    records = []
+    for _ in range(config.iterations):
+        records.append(runner.step(step_hook=step_hook, timer=timer))
         if h1_stop is not None and records[-1].h1_rel_error <= h1_stop:
             break
-    return _lib.like_input(theta, theta0), records
+    return _lib.like_input(runner.theta, theta0), records
 
 
 def h1_relative_error(problem, theta, quad):

@@ -1,0 +1,105 @@
+"""Host-side logic of the drop-in package (CPU only): policies, layout, seeded
+inputs, shard plans.  Mirrors the reference's own KATs (test_optim.py:54-98,
+test_model.py:10-46, test_problems.py:15-38)."""
+
+import numpy as np
+import pytest
+
+from oracle import ngd_oracle as O
+from paper_2505_11638_b200 import distributed, model, optim, problems
+
+
+def test_param_count_and_layout():
+    top = model.MlpTopology((3, 32, 32, 1))
+    assert top.param_count == 1217
+    t2 = model.MlpTopology((2, 5, 3, 1))
+    theta = np.random.default_rng(0).standard_normal(t2.param_count)
+    np.testing.assert_array_equal(t2.flatten(t2.unflatten(theta)), theta)
+    assert model.MlpTopology((2, 256, 256, 256, 1)).param_count == 132609
+    assert model.MlpTopology((10, 256, 256, 256, 256, 1)).param_count == 200449
+
+
+def test_init_matches_reference_draws():
+    for widths in ((2, 32, 32, 1), (2, 64, 64, 64, 1), (5, 128, 128, 128, 1)):
+        np.testing.assert_array_equal(model.init(model.MlpTopology(widths), 0).values, O.init_theta(widths, 0))
+
+
+def test_quadrature_matches_reference_streams():
+    prob = problems.Poisson2D(model.MlpTopology((2, 8, 1)))
+    q = prob.sample_quadrature(900, 120, 0)
+    oq = O.PoissonProblem((2, 8, 1)).sample_quadrature(900, 120, 0)
+    np.testing.assert_array_equal(q.interior_points, oq.interior_points)
+    np.testing.assert_array_equal(q.boundary_points, oq.boundary_points)
+    assert q.boundary_weights.sum() == pytest.approx(4.0, rel=1e-15)
+    for kind, d in (("sinsum", 5), ("gauss", 10)):
+        p = problems.PoissonND(model.MlpTopology((d, 4, 1)), kind)
+        q = p.sample_quadrature(64, 32, 0)
+        oq = O.PoissonProblem((d, 4, 1), kind=kind).sample_quadrature(64, 32, 0)
+        np.testing.assert_array_equal(q.boundary_points, oq.boundary_points)
+        np.testing.assert_allclose(p.source(q.interior_points), O.PoissonProblem((d, 4, 1), kind=kind).source(q.interior_points))
+        assert q.boundary_weights.sum() == pytest.approx(2.0 * d, rel=1e-14)
+        # every boundary point lies on a face
+        on_face = np.any((q.boundary_points == 0.0) | (q.boundary_points == 1.0), axis=1)
+        assert on_face.all()
+
+
+def test_exact_solutions_annihilate_residual():
+    for kind, d in (("sinsum", 5), ("gauss", 10)):
+        p = problems.PoissonND(model.MlpTopology((d, 4, 1)), kind)
+        x = np.random.default_rng(1).random((50, d))
+        # central differences of the exact solution reproduce -source
+        h = 1e-4
+        lap = np.zeros(50)
+        for i in range(d):
+            e = np.zeros(d)
+            e[i] = h
+            lap += (p.exact(x + e) - 2 * p.exact(x) + p.exact(x - e)) / h**2
+        np.testing.assert_allclose(-lap, p.source(x), rtol=1e-5, atol=1e-5)
+
+
+def test_policy_kats():
+    assert optim.adapt_mu(1.0, 1217, 0.0, 0.0, "constant", 0.0, 0.0) == pytest.approx(2.702e-13, rel=1e-3)
+    assert optim.adapt_mu(1e-10, 100, 1e-2, 0.0, "loss-power", 1e-4, 2.0) == pytest.approx(1e-8, rel=1e-12)
+    assert optim.adapt_mu(0.0, 10, 1.0, 1.0, "constant", 1e-9, 0.0) == 1e-9
+    assert optim.adapt_mu(0.0, 10, 0.0, 2.0, "grad-power", 0.5, 2.0) == pytest.approx(2.0)
+    with pytest.raises(ValueError):
+        optim.adapt_mu(-1.0, 1.0, 0.0, 0.0, "constant", 0.0, 0.0)
+    with pytest.raises(ValueError):
+        optim.adapt_mu(1.0, 1.0, 0.0, 0.0, "nope", 0.0, 0.0)
+    assert optim.adapt_rank(np.array([1.0]), mu=0.05, ell=8, ell_max=100) == 16
+    assert optim.adapt_rank(np.array([1.0]), mu=0.05, ell=80, ell_max=100) == 100
+    assert optim.adapt_rank(np.array([1.0, 0.5, 1e-6]), mu=1e-3, ell=3, ell_max=50) == 4
+    assert optim.adapt_rank(np.full(10, 1.0), mu=1e-6, ell=10, ell_max=10) == 10
+    assert optim._cg_rel_tol(1e-300, 5.0) == 1e-300
+    assert optim._cg_rel_tol(0.1, 1e-3) == 1e-3
+
+
+def test_linesearch_control_flow():
+    theta = np.array([2.0, -1.0])
+    f = lambda th, a, d: 0.5 * float((th - a * d) @ (th - a * d))
+    alpha, new = optim.backtracking_linesearch(theta, theta, f, float(theta @ theta))
+    assert alpha == 1.0 and new == 0.0
+    alpha, new = optim.backtracking_linesearch(theta, -theta, f, float(theta @ theta))
+    assert alpha == 0.0 and new == f(theta, 0.0, theta)
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        optim.NystromNgdConfig(ell0=0)
+    with pytest.raises(ValueError):
+        optim.NystromNgdConfig(kappa=1.0)
+    with pytest.raises(ValueError):
+        optim.NystromNgdConfig(omega_source="gpu")
+    assert optim._resolve_ell_max(optim.NystromNgdConfig(ell0=10), 1185) == 500
+
+
+@pytest.mark.parametrize("n_int,n_bnd,nranks", [(900, 120, 2), (131072, 16384, 8), (7, 3, 4), (0, 5, 2)])
+def test_shard_plan_partitions_points(n_int, n_bnd, nranks):
+    seen_i, seen_b, costs = [], [], []
+    for r in range(nranks):
+        si, sb = distributed.shard_slices(n_int, n_bnd, 12, r, nranks)
+        seen_i.extend(range(n_int)[si])
+        seen_b.extend(range(n_bnd)[sb])
+        costs.append(distributed.shard_cost(n_int, n_bnd, 12, r, nranks))
+    assert seen_i == list(range(n_int)) and seen_b == list(range(n_bnd))
+    assert max(costs) - min(costs) <= 13
