@@ -87,23 +87,23 @@ int ngd_gram_matmat(ngd_ctx* ctx, const double* d_V, int64_t ell, int64_t ldv, d
 
 /* ---- randomized Nystrom (nystrom_approximate, sketch.py:58-90) ----------
  * prepare: orthonormalise Omega in place (p x ell, col-major).
- * finish : given Y = G Omega, produce U (p x ell ROW-major) and eigenvalues
+ * finish : given Y = G Omega, produce U (p x ell, column-major) and eigenvalues
  *          (descending, >= 0); returns NGD_E_CHOL when Omega^T Y_nu is not PD. */
 int ngd_fill_gaussian(ngd_ctx* ctx, uint64_t seed, double* d_out, int64_t n);
 int ngd_nystrom_prepare(ngd_ctx* ctx, double* d_omega, int64_t p, int32_t ell);
 int ngd_nystrom_finish(ngd_ctx* ctx, const double* d_omega, double* d_Y, int64_t p, int32_t ell,
-                       double* d_U_rowmajor, double* d_eig, double* h_shift);
+                       double* d_U, double* d_eig, double* h_shift);
 /* dense operator helper (DenseOperator.matmat, gramian.py:101-120): Y = G V */
 int ngd_dense_matmat(ngd_ctx* ctx, const double* d_G, int64_t p, const double* d_V, int64_t ell, double* d_Y);
 
 /* ---- preconditioner (NystromPreconditioner.apply, sketch.py:101-112) ---- */
-int ngd_precond_apply(ngd_ctx* ctx, const double* d_U_rowmajor, const double* d_eig, int32_t ell, double mu,
+int ngd_precond_apply(ngd_ctx* ctx, const double* d_U, const double* d_eig, int32_t ell, double mu,
                       const double* d_v, double* d_out, int64_t p);
 
 /* ---- PCG (krylov.py:24-88) on (G + mu I) at the current linearisation, or on
  * a dense SPD matrix d_dense (p x p) when non-NULL.  U/eig may be NULL (no precond). */
 int ngd_pcg(ngd_ctx* ctx, const double* d_dense, int64_t p, const double* d_b, double mu,
-            const double* d_U_rowmajor, const double* d_eig, int32_t ell, double precond_mu, double rel_tol,
+            const double* d_U, const double* d_eig, int32_t ell, double precond_mu, double rel_tol,
             int32_t maxit, int32_t recompute_every, double* d_x, ngd_solve_report* h_report);
 
 /* ---- tuning knobs: "svd" = 0 (Householder QR + Jacobi SVD) | 1 (shifted Cholesky-QR3 + polar SVD, default) */

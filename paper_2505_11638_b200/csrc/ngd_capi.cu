@@ -20,6 +20,10 @@
 #include "../../include/ngd.h"
 #include "ngd_kernels.h"
 
+#include <atomic>
+namespace ngd {
+extern std::atomic<long long> g_launches;
+}
 using namespace ngd;
 
 namespace {
@@ -85,6 +89,12 @@ struct Buf {
   double* d() const { return static_cast<double*>(p); }
 };
 
+struct PcgGraph {
+  cudaGraphExec_t exec = nullptr;
+  int64_t key = -1;
+  long long kernels = 0;  // kernel nodes (launch accounting on replay)
+};
+
 }  // namespace
 
 struct ngd_ctx {
@@ -109,7 +119,9 @@ struct ngd_ctx {
   // point data
   bool have_points = false;
   Geom gm{};
-  int G = 1, kps = 1;  // phase-B splits
+  int G = 1, kps = 1;  // phase-B splits (G = max over layers)
+  int Gl[kMaxLayers] = {0}, kpsl[kMaxLayers] = {0};
+  RedPlan rplan{};
   Buf w_pad, off_pad, w_c, F, cot_grad, cot, metric_tmp;
   std::vector<Buf> zin, dbuf;  // per layer
   Buf dseed, pre_last, zs0, zs1;
@@ -127,13 +139,20 @@ struct ngd_ctx {
   cusolverDnParams_t dn_params = nullptr;
   std::vector<char> h_work;
   int svd_method = 1;
+  int use_graphs = 1;
+  int graph_gen = 0;
+  cudaStream_t cap_stream = nullptr;
+  Buf pargs, px, pb;
+  PcgGraph pcg_graphs[2];
+  int* h_flags = nullptr;
+  cudaEvent_t poll_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool lin_valid = false;
 
   double* S(int i) { return scal.d() + i; }
   unsigned* counter(int i) { return static_cast<unsigned*>(counters.p) + i; }
 };
 
-enum Scalar { SC_LOSS = 0, SC_FRO2 = 1, SC_SHIFT = 2, SC_TMP = 3, SC_N = 8 };
+enum Scalar { SC_LOSS = 0, SC_FRO2 = 1, SC_SHIFT = 2, SC_TMP = 3, SC_MU = 4, SC_N = 8 };
 
 static int bind(ngd_ctx* c) {
   CK(cudaSetDevice(c->device));
@@ -218,41 +237,59 @@ static int loss_finish(ngd_ctx* c, double* h_loss, double* F, double* cot) {
 // ------------------------------ phase A / B ---------------------------------
 static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double* cot_out, const int* skip) {
   const Geom& gm = c->gm;
+  PackAll pk{};
+  pk.n_layers = c->NL;
+  int64_t off = 0;
   for (int l = 0; l < c->NL; ++l) {
-    pack(c->vp[l].d(), c->Mp_f[l], c->Kp_f[l], v, c->woff[l], c->w[l + 1], c->w[l], 0, skip, c->stream);
-    pack(c->vp[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l], 1, c->Mp_f[l], v, c->boff[l], 1, c->w[l + 1], 0, skip,
-         c->stream);
+    pk.dst[l] = c->vp[l].d();
+    pk.Mp[l] = c->Mp_f[l];
+    pk.Kp[l] = c->Kp_f[l];
+    pk.n_out[l] = c->w[l + 1];
+    pk.n_in[l] = c->w[l];
+    pk.woff[l] = c->woff[l];
+    pk.boff[l] = c->boff[l];
+    pk.start[l] = off;
+    off += (int64_t)c->Mp_f[l] * c->Kp_f[l] + c->Mp_f[l];
   }
+  pk.start[c->NL] = off;
+  pack_all(pk, v, skip, c->stream);
+  PhaAll pa{};
+  pa.n_layers = c->NL;
+  pa.nib = gm.nib;
+  pa.nbb = gm.nbb;
+  pa.int_cols = gm.int_cols();
+  int tiles = 0;
   for (int l = 0; l < c->NL; ++l) {
-    JetArgs a{};
+    JetArgs& a = pa.L[l];
     a.A = c->vp[l].d();
     a.Kp = c->Kp_f[l];
     a.M = c->w[l + 1];
     a.B = c->zin[l].d();
     a.s_pad = gm.s_pad;
+    a.col0 = 0;
+    a.pt0 = 0;
     a.bias = c->vp[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l];
     a.Dk = (l == c->NL - 1) ? c->dseed.d() : c->dbuf[l].d();
     a.partA = c->partA.d() + (int64_t)c->rowbase[l] * gm.n_pts_pad();
     a.n_pts_pad = gm.n_pts_pad();
     a.skip = skip;
-    for (int seg = 0; seg < 2; ++seg) {
-      const int CC = seg == 0 ? gm.C : 1;
-      a.col0 = seg == 0 ? 0 : gm.int_cols();
-      a.pt0 = seg == 0 ? 0 : gm.nib * PB;
-      const int nblk = seg == 0 ? gm.nib : gm.nbb;
-      CK(jet_gemm(CC, PHA, a, nblk, c->mtiles[l], c->stream));
-    }
+    pa.mtiles[l] = c->mtiles[l];
+    pa.tile_start[l] = tiles;
+    tiles += c->mtiles[l] * (gm.nib + gm.nbb);
   }
+  pa.tile_start[c->NL] = tiles;
+  CK(pha_all(gm.C, pa, c->stream));
   reduce_pha(c->partA.d(), c->rows_A, gm.n_pts_pad(), w_or_null, cot_out, skip, c->stream);
   CK(cudaGetLastError());
   return NGD_OK;
 }
 
-// out = J^T cot (+ mu v), all-reduced over ranks
-static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* v, double* out, const int* skip) {
+static void fill_phb(ngd_ctx* c, const double* cot, const int* skip, PhbAll& pb) {
   const Geom& gm = c->gm;
+  pb.n_layers = c->NL;
+  int tiles = 0;
   for (int l = 0; l < c->NL; ++l) {
-    PhbArgs a{};
+    PhbArgs& a = pb.L[l];
     a.D = (l == c->NL - 1) ? c->dseed.d() : c->dbuf[l].d();
     a.Z = c->zin[l].d();
     a.cvec = cot;
@@ -263,27 +300,41 @@ static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* v
     a.C = gm.C;
     a.nib = gm.nib;
     a.ktiles_total = (int)(gm.s_pad / 16);
-    a.ktiles_per_split = c->kps;
+    a.ktiles_per_split = c->kpsl[l];
     a.off = c->woff[l];
     a.part = c->partB.d();
     a.p = c->p;
     a.skip = skip;
-    CK(phase_b(a, c->G, c->stream));
+    pb.tiles_n[l] = (a.N + 63) / 64;
+    pb.tiles_m[l] = (a.M + 63) / 64;
+    pb.G[l] = c->Gl[l];
+    pb.tile_start[l] = tiles;
+    tiles += pb.tiles_n[l] * pb.tiles_m[l] * c->Gl[l];
   }
+  pb.tile_start[c->NL] = tiles;
+}
+
+// out = J^T cot (+ mu v), all-reduced over ranks
+static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* mu_p, const double* v, double* out,
+                       const int* skip) {
+  PhbAll pb{};
+  fill_phb(c, cot, skip, pb);
+  CK(phase_b_all_layers(pb, c->G, c->stream));
+  const bool shifted = v && (mu_p || mu != 0.0);
   if (c->nranks > 1) {
-    reduce_splits(c->partB.d(), c->G, c->p, 0.0, nullptr, out, skip, c->stream);
+    reduce_splits(c->partB.d(), c->rplan, c->p, 0.0, nullptr, nullptr, out, skip, c->stream);
     TRY(allreduce(c, out, c->p));
-    if (v && mu != 0.0) add_scaled(out, mu, v, c->p, skip, c->stream);
+    if (shifted) add_scaled(out, mu, mu_p, v, c->p, skip, c->stream);
   } else {
-    reduce_splits(c->partB.d(), c->G, c->p, mu, (v && mu != 0.0) ? v : nullptr, out, skip, c->stream);
+    reduce_splits(c->partB.d(), c->rplan, c->p, mu, mu_p, shifted ? v : nullptr, out, skip, c->stream);
   }
   CK(cudaGetLastError());
   return NGD_OK;
 }
 
-static int gram_mv(ngd_ctx* c, const double* v, double mu, double* out, const int* skip) {
+static int gram_mv(ngd_ctx* c, const double* v, double mu, const double* mu_p, double* out, const int* skip) {
   TRY(phase_a(c, v, c->w_pad.d(), c->cot.d(), skip));
-  TRY(phase_b_all(c, c->cot.d(), mu, v, out, skip));
+  TRY(phase_b_all(c, c->cot.d(), mu, mu_p, v, out, skip));
   return NGD_OK;
 }
 
@@ -401,10 +452,16 @@ int ngd_ctx_create(const int32_t* widths, int32_t n_widths, int32_t device, ngd_
   ck(c->counters.ensure(sizeof(unsigned) * 64));
   ck(c->scal.ensure(sizeof(double) * SC_N));
   ck(c->pcgs.ensure(sizeof(PcgState)));
+  ck(c->pargs.ensure(2 * sizeof(PrecondArgs)));
   if (rc == NGD_OK) {
     cudaMemset(c->counters.p, 0, c->counters.bytes);
     cudaMemset(c->scal.p, 0, c->scal.bytes);
     if (cudaMallocHost(&c->h_pin, 64 * sizeof(double)) != cudaSuccess) rc = fail(NGD_E_CUDA, "pinned alloc failed");
+    if (cudaMallocHost(&c->h_flags, 8 * sizeof(int)) != cudaSuccess) rc = fail(NGD_E_CUDA, "pinned alloc failed");
+    if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+      rc = fail(NGD_E_CUDA, "stream create failed");
+    for (auto& e : c->poll_ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) rc = fail(NGD_E_CUDA, "event failed");
   }
   if (rc == NGD_OK && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) rc = fail(NGD_E_CUDA, "cublasCreate failed");
   if (rc == NGD_OK && cusolverDnCreate(&c->sol) != CUSOLVER_STATUS_SUCCESS)
@@ -433,6 +490,13 @@ int ngd_ctx_destroy(ngd_ctx* c) {
                  &c->nys_m, &c->nys_tau, &c->nys_r, &c->nys_ur, &c->nys_v, &c->nys_s, &c->nys_work, &c->nys_info})
     b->release();
   if (c->h_pin) cudaFreeHost(c->h_pin);
+  if (c->h_flags) cudaFreeHost(c->h_flags);
+  for (auto& g : c->pcg_graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (auto& e : c->poll_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  for (Buf* b : {&c->pargs, &c->px, &c->pb}) b->release();
   if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
   if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
   if (c->sol) cusolverDnDestroy(c->sol);
@@ -531,16 +595,32 @@ int ngd_set_points(ngd_ctx* c, int64_t n_int, const double* x_int, const double*
   CK(cudaGetLastError());
   // phase-A partial rows and phase-B split plan
   CK(c->partA.ensure(sizeof(double) * (size_t)c->rows_A * npp));
-  int tiles = 1;
-  for (int l = 0; l < c->NL; ++l) tiles = std::max(tiles, ((c->w[l] + 63) / 64) * ((c->w[l + 1] + 63) / 64));
-  const int kt = (int)(gm.s_pad / 16);
-  int G = std::max(1, std::min(kt, (2 * 148 + tiles - 1) / tiles));
-  G = std::max(1, std::min(G, kt / 4 > 0 ? kt / 4 : 1));  // at least 4 k-tiles per split
-  c->kps = (kt + G - 1) / G;
-  c->G = (kt + c->kps - 1) / c->kps;
-  CK(c->partB.ensure(sizeof(double) * (size_t)c->G * c->p));
+  // phase-B split plan: every (layer, tile) gets the same number of K splits (a tile costs the
+  // same per k-tile whatever its fill), so one launch puts ~3 CTAs on every SM; >= 8 k-tiles each.
+  {
+    const int kt = (int)(gm.s_pad / 16);
+    int tiles = 0;
+    for (int l = 0; l < c->NL; ++l) tiles += ((c->w[l] + 63) / 64) * ((c->w[l + 1] + 63) / 64);
+    int G = std::max(1, (int)std::lround(3.0 * 148 / tiles));
+    G = std::min(G, std::max(1, kt / 8));
+    const int kps = (kt + G - 1) / G;
+    G = (kt + kps - 1) / kps;
+    G = (G + kPhbCluster - 1) / kPhbCluster * kPhbCluster;  // whole clusters (trailing splits may be empty)
+    c->G = G;
+    c->kps = kps;
+    c->rplan.n_layers = c->NL;
+    for (int l = 0; l < c->NL; ++l) {
+      c->Gl[l] = G;
+      c->kpsl[l] = kps;
+      c->rplan.start[l] = c->woff[l];
+      c->rplan.G[l] = G / kPhbCluster;  // one partial per cluster
+    }
+    c->rplan.start[c->NL] = c->p;
+  }
+  CK(c->partB.ensure(sizeof(double) * (size_t)(c->G / kPhbCluster) * c->p));
   c->have_points = true;
   c->lin_valid = false;
+  c->graph_gen++;
   return NGD_OK;
 }
 
@@ -594,7 +674,7 @@ int ngd_linearize(ngd_ctx* c, const double* theta, double* h_loss, double* d_met
 int ngd_loss_grad(ngd_ctx* c, double* d_grad) {
   TRY(bind(c));
   TRY(need_lin(c));
-  return phase_b_all(c, c->cot_grad.d(), 0.0, nullptr, d_grad, nullptr);
+  return phase_b_all(c, c->cot_grad.d(), 0.0, nullptr, nullptr, d_grad, nullptr);
 }
 
 int ngd_jvp(ngd_ctx* c, const double* v, double* out) {
@@ -610,13 +690,13 @@ int ngd_vjp(ngd_ctx* c, const double* cot, double* out) {
   TRY(bind(c));
   TRY(need_lin(c));
   scatter_points(cot, c->cot.d(), c->gm, c->stream);
-  return phase_b_all(c, c->cot.d(), 0.0, nullptr, out, nullptr);
+  return phase_b_all(c, c->cot.d(), 0.0, nullptr, nullptr, out, nullptr);
 }
 
 int ngd_gram_matvec(ngd_ctx* c, const double* v, double mu, double* out) {
   TRY(bind(c));
   TRY(need_lin(c));
-  return gram_mv(c, v, mu, out, nullptr);
+  return gram_mv(c, v, mu, nullptr, out, nullptr);
 }
 
 // Y = G V by the J-chunk formulation: per point chunk, explicit Jacobian rows
@@ -774,9 +854,9 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
     // 5. R = U_R diag(s) V^T (polar-decomposition SVD, descending)
     TRY(small_svd_polar(c, ell));
   }
-  // U^T = U_R^T Q^T  (row-major p x ell output)
-  CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_T, ell, (int)p, ell, &one, c->nys_ur.d(), ell, Y, (int)p, &zero,
-                  U_row, ell));
+  // U = Q U_R  (column-major p x ell output)
+  CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)p, ell, ell, &one, Y, (int)p, c->nys_ur.d(), ell, &zero,
+                  U_row, (int)p));
   eig_from_sv(c->nys_s.d(), ell, c->S(SC_SHIFT), eig, c->stream);
   CK(cudaMemcpyAsync(&c->h_pin[0], c->S(SC_SHIFT), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -799,7 +879,67 @@ int ngd_precond_apply(ngd_ctx* c, const double* U, const double* eig, int32_t el
   TRY(bind(c));
   CK(c->ppart.ensure(sizeof(double) * (size_t)precond_blocks(p) * ell));
   CK(c->pcprime.ensure(sizeof(double) * ell));
-  CK(precond_apply(U, p, ell, eig, nullptr, mu, v, out, c->ppart.d(), c->pcprime.d(), nullptr, c->stream));
+  PrecondArgs h{U, eig, mu};
+  PrecondArgs* d = static_cast<PrecondArgs*>(c->pargs.p) + 1;  // slot 1: direct applies
+  CK(cudaMemcpyAsync(d, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  CK(precond_apply(d, p, ell, v, out, c->ppart.d(), c->pcprime.d(), c->counter(10), nullptr, nullptr, 0,
+                   c->redp.d(), c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // the host struct must outlive the copy
+  return NGD_OK;
+}
+
+// One PCG iteration (krylov.py:59-81) on the device.  All scalars live in the
+// PcgState; operands come from ctx-owned buffers and the PrecondArgs slot, so
+// the same launch sequence can be captured once and replayed as a CUDA graph.
+static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, int ell, bool have_pre,
+                         int recompute) {
+  PcgState* sp = static_cast<PcgState*>(c->pcgs.p);
+  const int* done = &sp->done;
+  const double one = 1.0, zero = 0.0;
+  double *x = c->px.d(), *r = c->pr.d(), *z = c->pz.d(), *dv = c->pd.d(), *ad = c->pad.d(), *tmp = c->ptmp.d();
+  const double* b = c->pb.d();
+  double* mu_p = c->S(SC_MU);
+  double* red = c->redp.d();
+  // ad = (A + mu I) d ; dad = d.ad ; alpha / breakdown   (krylov.py:59-66)
+  if (dense) {
+    CKB(cublasDgemv(c->blas, CUBLAS_OP_T, (int)p, (int)p, &one, dense, (int)p, dv, 1, &zero, ad, 1));
+    add_scaled(ad, mu, nullptr, dv, p, done, c->stream);
+    pcg_ad(nullptr, c->rplan, p, mu_p, dv, ad, sp, 1, red, c->counter(4), c->stream);
+  } else {
+    TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done));
+    PhbAll pb{};
+    fill_phb(c, c->cot.d(), done, pb);
+    CK(phase_b_all_layers(pb, c->G, c->stream));
+    if (c->nranks > 1) {
+      reduce_splits(c->partB.d(), c->rplan, p, 0.0, nullptr, nullptr, ad, done, c->stream);
+      TRY(allreduce(c, ad, p));
+      add_scaled(ad, 0.0, mu_p, dv, p, done, c->stream);
+      pcg_ad(nullptr, c->rplan, p, mu_p, dv, ad, sp, 1, red, c->counter(4), c->stream);
+    } else {
+      pcg_ad(c->partB.d(), c->rplan, p, mu_p, dv, ad, sp, 0, red, c->counter(4), c->stream);
+    }
+  }
+  // x += alpha d ; r -= alpha ad (or r = b - A x) ; ||r|| test   (krylov.py:66-74)
+  pcg_update(x, r, dv, ad, p, sp, recompute, red, c->counter(5), c->stream);
+  if (recompute) {
+    if (dense) {
+      CKB(cublasDgemv(c->blas, CUBLAS_OP_T, (int)p, (int)p, &one, dense, (int)p, x, 1, &zero, tmp, 1));
+      add_scaled(tmp, mu, nullptr, x, p, done, c->stream);
+    } else {
+      TRY(gram_mv(c, x, 0.0, mu_p, tmp, done));
+    }
+    pcg_true_res(b, tmp, r, p, sp, 1, 0, red, c->counter(6), c->stream);
+  }
+  // z = P^{-1} r ; beta = r.z / rz ; d = z + beta d   (krylov.py:75-81)
+  if (have_pre) {
+    CK(precond_apply(static_cast<PrecondArgs*>(c->pargs.p), p, ell, r, z, c->ppart.d(), c->pcprime.d(),
+                     c->counter(8), done, sp, 0, red, c->stream));
+    pcg_dir(z, dv, p, sp, c->stream);
+  } else {
+    CK(precond_apply(nullptr, p, 0, r, z, nullptr, nullptr, c->counter(8), done, sp, 0, red, c->stream));
+    pcg_dir(z, dv, p, sp, c->stream);
+  }
+  CK(cudaGetLastError());
   return NGD_OK;
 }
 
@@ -815,78 +955,89 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
     if (p != c->p) return fail(NGD_E_SHAPE, "expected vector of length %lld, got %lld", (long long)c->p, (long long)p);
   }
   if (p < 1) return fail(NGD_E_SHAPE, "empty system");
-  for (Buf* bf : {&c->pr, &c->pz, &c->pd, &c->pad, &c->ptmp}) CK(bf->ensure(sizeof(double) * p));
-  if (U) {
+  for (Buf* bf : {&c->pr, &c->pz, &c->pd, &c->pad, &c->ptmp, &c->px, &c->pb}) CK(bf->ensure(sizeof(double) * p));
+  const bool have_pre = (U != nullptr);
+  if (have_pre) {
     CK(c->ppart.ensure(sizeof(double) * (size_t)precond_blocks(p) * ell));
     CK(c->pcprime.ensure(sizeof(double) * ell));
   }
-  auto* st = static_cast<PcgState*>(c->pcgs.p);
-  const int* done = &st->done;
-  double* r = c->pr.d();
-  double* z = c->pz.d();
-  double* dvec = c->pd.d();
-  double* ad = c->pad.d();
-  double* tmp = c->ptmp.d();
-  const double one = 1.0, zero = 0.0;
-  auto apply_A = [&](const double* in, double* outv, const int* skip) -> int {
-    if (dense) {
-      CKB(cublasDgemv(c->blas, CUBLAS_OP_T, (int)p, (int)p, &one, dense, (int)p, in, 1, &zero, outv, 1));
-      if (mu != 0.0) add_scaled(outv, mu, in, p, skip, c->stream);
-      return NGD_OK;
-    }
-    return gram_mv(c, in, mu, outv, skip);
-  };
-  auto apply_P = [&](const double* in, double* outv, const int* skip) -> int {
-    if (!U) {
-      CK(cudaMemcpyAsync(outv, in, sizeof(double) * p, cudaMemcpyDeviceToDevice, c->stream));
-      return NGD_OK;
-    }
-    CK(precond_apply(U, p, ell, eig, nullptr, precond_mu, in, outv, c->ppart.d(), c->pcprime.d(), skip, c->stream));
-    return NGD_OK;
-  };
-  PcgState* sp = st;
-  // ||b||
-  dot(b, b, p, c->redp.d(), c->counter(2), &sp->bb, nullptr, c->stream);
+  PcgState* sp = static_cast<PcgState*>(c->pcgs.p);
+  const int* done = &sp->done;
+  // operands into stable, ctx-owned locations (graph replay needs fixed addresses)
+  PrecondArgs hpa{U, eig, precond_mu};
+  CK(cudaMemcpyAsync(c->pargs.p, &hpa, sizeof(hpa), cudaMemcpyHostToDevice, c->stream));
+  c->h_pin[48] = mu;
+  CK(cudaMemcpyAsync(c->S(SC_MU), &c->h_pin[48], sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->pb.d(), b, sizeof(double) * p, cudaMemcpyDeviceToDevice, c->stream));
+  double *xx = c->px.d(), *r = c->pr.d(), *z = c->pz.d(), *dv = c->pd.d(), *tmp = c->ptmp.d();
+  // prologue: x = 0, r = b, z = P r, d = z, rz = r.z  (krylov.py:46-54)
+  dot(c->pb.d(), c->pb.d(), p, c->redp.d(), c->counter(2), &sp->bb, nullptr, c->stream);
   pcg_init(sp, rel_tol, c->stream);
-  pcg_start(b, x, r, p, c->stream);
-  TRY(apply_P(r, z, done));
-  dot(r, z, p, c->redp.d(), c->counter(3), &sp->rz_new, done, c->stream);
-  pcg_first_dir(z, dvec, p, sp, c->stream);
-  for (int it = 1; it <= maxit; ++it) {
-    TRY(apply_A(dvec, ad, done));
-    dot(dvec, ad, p, c->redp.d(), c->counter(4), &sp->dad, done, c->stream);
-    pcg_alpha(sp, it, c->stream);
-    const int rec = (it % recompute_every == 0);
-    pcg_update(x, r, dvec, ad, p, sp, rec, c->stream);
-    if (rec) {
-      TRY(apply_A(x, tmp, done));
-      pcg_true_res(b, tmp, r, p, sp, 1, 0, c->stream);
+  pcg_start(c->pb.d(), xx, r, p, c->stream);
+  CK(precond_apply(have_pre ? static_cast<PrecondArgs*>(c->pargs.p) : nullptr, p, have_pre ? ell : 0, r, z,
+                   c->ppart.d(), c->pcprime.d(), c->counter(8), done, sp, 1, c->redp.d(), c->stream));
+  pcg_first_dir(z, dv, p, sp, c->stream);
+
+  // iterations: replay a captured CUDA graph of one iteration (Gram operator), or launch directly
+  const bool use_graph = !dense && c->use_graphs;
+  PcgGraph* graphs = c->pcg_graphs;
+  const int64_t key = ((int64_t)c->graph_gen << 20) ^ ((int64_t)ell << 2) ^ (have_pre ? 1 : 0);
+  if (use_graph) {
+    for (int rec = 0; rec < 2; ++rec) {
+      if (graphs[rec].exec && graphs[rec].key == key) continue;
+      if (graphs[rec].exec) cudaGraphExecDestroy(graphs[rec].exec);
+      graphs[rec].exec = nullptr;
+      cudaStream_t saved = c->stream;
+      c->stream = c->cap_stream;
+      CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+      const long long l0 = ngd::g_launches.load();
+      int rc = pcg_iteration(c, p, nullptr, mu, ell, have_pre, rec);
+      graphs[rec].kernels = ngd::g_launches.load() - l0;
+      ngd::g_launches.fetch_sub(graphs[rec].kernels);  // counted per replay below
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &g);
+      c->stream = saved;
+      if (rc != NGD_OK) return rc;
+      CK(ce);
+      CK(cudaGraphInstantiate(&graphs[rec].exec, g, 0));
+      cudaGraphDestroy(g);
+      graphs[rec].key = key;
     }
-    dot(r, r, p, c->redp.d(), c->counter(5), &sp->rr, done, c->stream);
-    pcg_check(sp, c->stream);
-    TRY(apply_P(r, z, done));
-    dot(r, z, p, c->redp.d(), c->counter(6), &sp->rz_new, done, c->stream);
-    pcg_dir(z, dvec, p, sp, c->stream);
-    if ((it & 7) == 0 && it < maxit) {
-      // cheap host poll so long solves stop issuing work after convergence
-      CK(cudaMemcpyAsync(&c->h_pin[16], &sp->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      int dn = 0;
-      memcpy(&dn, &c->h_pin[16], sizeof(int));
-      if (dn) break;
+  }
+  int issued = 0;
+  for (int it = 1; it <= maxit; ++it) {
+    const int rec = (it % recompute_every == 0);
+    if (use_graph) {
+      CK(cudaGraphLaunch(graphs[rec].exec, c->stream));
+      ngd::g_launches.fetch_add(graphs[rec].kernels);
+    } else {
+      TRY(pcg_iteration(c, p, dense, mu, ell, have_pre, rec));
+    }
+    ++issued;
+    // non-blocking poll of the device 'done' flag (copied to pinned memory after each iteration)
+    const int slot = it & 3;
+    CK(cudaMemcpyAsync(&c->h_flags[slot], &sp->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaEventRecord(c->poll_ev[slot], c->stream));
+    if (it >= 3) {
+      const int old = (it - 2) & 3;
+      if (cudaEventQuery(c->poll_ev[old]) == cudaSuccess && c->h_flags[old] != 0) break;
     }
   }
   // final true residual (krylov.py:83-88)
-  CK(cudaMemcpyAsync(&c->h_pin[16], &sp->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&c->h_flags[4], &sp->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  int dn = 0;
-  memcpy(&dn, &c->h_pin[16], sizeof(int));
+  const int dn = c->h_flags[4];
   if (dn != 2) {
-    TRY(apply_A(x, tmp, nullptr));
-    pcg_true_res(b, tmp, r, p, sp, 0, 1, c->stream);
-    dot(r, r, p, c->redp.d(), c->counter(5), &sp->rr, nullptr, c->stream);
+    if (dense) {
+      const double one = 1.0, zero = 0.0;
+      CKB(cublasDgemv(c->blas, CUBLAS_OP_T, (int)p, (int)p, &one, dense, (int)p, xx, 1, &zero, tmp, 1));
+      add_scaled(tmp, mu, nullptr, xx, p, nullptr, c->stream);
+    } else {
+      TRY(gram_mv(c, xx, 0.0, c->S(SC_MU), tmp, nullptr));
+    }
+    pcg_true_res(c->pb.d(), tmp, r, p, sp, 0, 1, c->redp.d(), c->counter(6), c->stream);
   }
-  pcg_final(sp, c->stream);
+  CK(cudaMemcpyAsync(x, xx, sizeof(double) * p, cudaMemcpyDeviceToDevice, c->stream));
   PcgState hs;
   CK(cudaMemcpyAsync(c->h_pin + 20, sp, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -907,11 +1058,16 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
       rep->breakdown = hs.breakdown;
     }
   }
+  (void)issued;
   return NGD_OK;
 }
 
 int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(NGD_E_SHAPE, "bad option");
+  if (!strcmp(key, "graphs")) {
+    c->use_graphs = value ? 1 : 0;
+    return NGD_OK;
+  }
   if (!strcmp(key, "svd")) {
     if (value < 0 || value > 1) return fail(NGD_E_SHAPE, "svd method must be 0 (geqrf+gesvdj) or 1 (scholqr3+gesvdp)");
     c->svd_method = (int)value;

@@ -17,6 +17,9 @@
 #include "ngd_common.cuh"
 #include "ngd_kernels.h"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace ngd {
 
 
@@ -74,7 +77,7 @@ __device__ __forceinline__ void jet_act_rev(const double (&a)[C], const double (
 }
 
 template <int C, int MODE>
-__global__ void __launch_bounds__(kThreads) jet_gemm_kernel(JetArgs p) {
+__device__ __forceinline__ void jet_tile(const JetArgs& p, const int bx, const int by) {
   constexpr int NC = PB * C;        // columns in one point block
   constexpr int BSTR = NC + 4;      // smem row stride (== 4 mod 16 doubles -> conflict-free B frags)
   constexpr int ASTR = BK + APAD;   // 20 doubles
@@ -86,8 +89,8 @@ __global__ void __launch_bounds__(kThreads) jet_gemm_kernel(JetArgs p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp & 3, wn = warp >> 2;
-  const int m0 = blockIdx.y * BM;
-  const int64_t cblk = p.col0 + (int64_t)blockIdx.x * NC;
+  const int m0 = by * BM;
+  const int64_t cblk = p.col0 + (int64_t)bx * NC;
 
   auto load_stage = [&](int stage, int kt) {
     const int k0 = kt * BK;
@@ -215,8 +218,33 @@ __global__ void __launch_bounds__(kThreads) jet_gemm_kernel(JetArgs p) {
     __syncthreads();
     if (tid < PB) {
       const double s = (red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]);
-      p.partA[(int64_t)blockIdx.y * p.n_pts_pad + p.pt0 + blockIdx.x * PB + tid] = s;
+      p.partA[(int64_t)by * p.n_pts_pad + p.pt0 + bx * PB + tid] = s;
     }
+  }
+}
+
+template <int C, int MODE>
+__global__ void __launch_bounds__(kThreads) jet_gemm_kernel(JetArgs p) {
+  jet_tile<C, MODE>(p, blockIdx.x, blockIdx.y);
+}
+
+// Phase A over ALL layers and both point segments in one launch (tile table).
+template <int C>
+__global__ void __launch_bounds__(kThreads) pha_all_kernel(PhaAll a) {
+  const int t = blockIdx.x;
+  int l = 0;
+  while (l + 1 < a.n_layers && t >= a.tile_start[l + 1]) ++l;
+  const int local = t - a.tile_start[l];
+  const int mt = a.mtiles[l];
+  const int n_int_tiles = a.nib * mt;
+  JetArgs p = a.L[l];
+  if (local < n_int_tiles) {
+    jet_tile<C, PHA>(p, local % a.nib, local / a.nib);
+  } else {
+    const int lb = local - n_int_tiles;
+    p.col0 = a.int_cols;
+    p.pt0 = a.nib * PB;
+    jet_tile<1, PHA>(p, lb % a.nbb, lb / a.nbb);
   }
 }
 
@@ -235,6 +263,37 @@ static cudaError_t launch_jet(const JetArgs& a, int nblocks, int mtiles, cudaStr
   kern<<<dim3(nblocks, mtiles), kThreads, smem, st>>>(a);
   probe_after(MODE == FWD ? K_FWD : (MODE == REV ? K_REV : K_PHA), st);
   return cudaGetLastError();
+}
+
+template <int C>
+static cudaError_t launch_pha_all(const PhaAll& a, cudaStream_t st) {
+  constexpr int NC = PB * C;
+  const size_t smem = sizeof(double) * (2 * BM * (BK + APAD) + 2 * BK * (NC + 4));
+  auto kern = pha_all_kernel<C>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  const int tiles = a.tile_start[a.n_layers];
+  if (tiles <= 0) return cudaSuccess;
+  probe_before(K_PHA, st);
+  kern<<<tiles, kThreads, smem, st>>>(a);
+  probe_after(K_PHA, st);
+  return cudaGetLastError();
+}
+
+cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st) {
+  switch (C) {
+    case 3: return launch_pha_all<3>(a, st);
+    case 4: return launch_pha_all<4>(a, st);
+    case 5: return launch_pha_all<5>(a, st);
+    case 6: return launch_pha_all<6>(a, st);
+    case 7: return launch_pha_all<7>(a, st);
+    case 8: return launch_pha_all<8>(a, st);
+    case 12: return launch_pha_all<12>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles, cudaStream_t st) {
@@ -268,53 +327,65 @@ cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles,
 
 constexpr int PBM = 64, PBN = 64, PSTR = BK + 4;
 
-__device__ __forceinline__ int point_of_col(int64_t j, int64_t int_cols, int C, int nib) {
-  if (j < int_cols) {
-    const int64_t blk = j / (PB * C);
-    return (int)(blk * PB + (j % PB));
+// 32-bit column arithmetic (S < 2^31 for every supported configuration)
+__device__ __forceinline__ int point_of_col(int64_t j64, int64_t int_cols, int C, int nib) {
+  const int j = (int)j64;
+  if (j64 < int_cols) {
+    const int blk = j / (PB * C);
+    return blk * PB + (j & (PB - 1));
   }
-  return nib * PB + (int)(j - int_cols);
+  return nib * PB + (int)(j64 - int_cols);
 }
-__device__ __forceinline__ bool is_value_col(int64_t j, int64_t int_cols, int C) {
-  return j >= int_cols || ((j % (PB * C)) < PB);
+__device__ __forceinline__ bool is_value_col(int64_t j64, int64_t int_cols, int C) {
+  return j64 >= int_cols || (((int)j64 % (PB * C)) < PB);
 }
 
-__global__ void __launch_bounds__(kThreads) phb_kernel(PhbArgs p) {
-  __shared__ __align__(16) double As[2][PBM][PSTR];
-  __shared__ __align__(16) double Bs[2][PBN][PSTR];
-  __shared__ double ccs[2][BK];
-  __shared__ double bias_acc[PBM];
+constexpr int PNST = 4;  // cp.async pipeline depth of phase B
+static_assert(PBM * (PBN + 1) + PBM <= 2 * PNST * PBM * PSTR, "cluster reduction staging must fit");
+constexpr size_t kPhbSmem = sizeof(double) * (2 * PNST * PBM * PSTR + 2 * PNST * BK + PBM);
+
+__device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const int by, const int kt0, const int kt1,
+                                         const int split) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                              // [PNST][PBM][PSTR]
+  double* Bs = As + PNST * PBM * PSTR;            // [PNST][PBN][PSTR]
+  double* ccs = Bs + PNST * PBN * PSTR;           // [PNST][BK]  cotangent per column
+  double* ccv = ccs + PNST * BK;                  // [PNST][BK]  cotangent on value columns (bias)
+  double* bias_acc = ccv + PNST * BK;             // [PBM]
   if (p.skip && *p.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp & 3, wn = warp >> 2;
-  const int n0 = blockIdx.x * PBN, m0 = blockIdx.y * PBM;
-  const int split = blockIdx.z;
-  const int kt0 = split * p.ktiles_per_split;
-  const int kt1 = min(p.ktiles_total, kt0 + p.ktiles_per_split);
-  const bool do_bias = (blockIdx.x == 0);
+  const int n0 = bx * PBN, m0 = by * PBM;
+  const bool do_bias = (bx == 0);
   if (tid < PBM) bias_acc[tid] = 0.0;
 
   auto load_stage = [&](int stage, int kt) {
     const int64_t j0 = (int64_t)kt * BK;
+    double* as = As + stage * PBM * PSTR;
+    double* bs = Bs + stage * PBN * PSTR;
     for (int i = tid; i < PBM * BK / 2; i += kThreads) {
       const int r = i >> 3, c2 = (i & 7) * 2;
       const int row = m0 + r;
       if (row < p.M)
-        cp_async16(&As[stage][r][c2], p.D + (int64_t)row * p.s_pad + j0 + c2);
+        cp_async16(as + r * PSTR + c2, p.D + (int64_t)row * p.s_pad + j0 + c2);
       else
-        *reinterpret_cast<double2*>(&As[stage][r][c2]) = make_double2(0.0, 0.0);
+        *reinterpret_cast<double2*>(as + r * PSTR + c2) = make_double2(0.0, 0.0);
     }
     for (int i = tid; i < PBN * BK / 2; i += kThreads) {
       const int r = i >> 3, c2 = (i & 7) * 2;
       const int row = n0 + r;
       if (row < p.N)
-        cp_async16(&Bs[stage][r][c2], p.Z + (int64_t)row * p.s_pad + j0 + c2);
+        cp_async16(bs + r * PSTR + c2, p.Z + (int64_t)row * p.s_pad + j0 + c2);
       else
-        *reinterpret_cast<double2*>(&Bs[stage][r][c2]) = make_double2(0.0, 0.0);
+        *reinterpret_cast<double2*>(bs + r * PSTR + c2) = make_double2(0.0, 0.0);
     }
-    if (tid < BK) ccs[stage][tid] = p.cvec[point_of_col(j0 + tid, p.int_cols, p.C, p.nib)];
-    cp_async_commit();
+    if (tid < BK) {
+      const int64_t j = j0 + tid;
+      const double cc = p.cvec[point_of_col(j, p.int_cols, p.C, p.nib)];
+      ccs[stage * BK + tid] = cc;
+      ccv[stage * BK + tid] = is_value_col(j, p.int_cols, p.C) ? cc : 0.0;
+    }
   };
 
   double acc[2][4][2];
@@ -323,62 +394,112 @@ __global__ void __launch_bounds__(kThreads) phb_kernel(PhbArgs p) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  if (kt0 < kt1) load_stage(0, kt0);
+#pragma unroll
+  for (int s0 = 0; s0 < PNST - 1; ++s0) {
+    if (kt0 + s0 < kt1) load_stage(s0, kt0 + s0);
+    cp_async_commit();
+  }
   for (int kt = kt0; kt < kt1; ++kt) {
-    const int st = (kt - kt0) & 1;
-    if (kt + 1 < kt1) {
-      load_stage(st ^ 1, kt + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    const int st = (kt - kt0) % PNST;
+    cp_async_wait<PNST - 2>();
     __syncthreads();
+    {
+      const int nk = kt + PNST - 1;
+      if (nk < kt1) load_stage((nk - kt0) % PNST, nk);
+      cp_async_commit();
+    }
+    const double* as = As + st * PBM * PSTR;
+    const double* bs = Bs + st * PBN * PSTR;
+    const double* cs = ccs + st * BK;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      const double cc = ccs[st][kk + t];
-      const double a0 = As[st][wm * 16 + g][kk + t] * cc;
-      const double a1 = As[st][wm * 16 + 8 + g][kk + t] * cc;
+      const double cc = cs[kk + t];
+      const double a0 = as[(wm * 16 + g) * PSTR + kk + t] * cc;
+      const double a1 = as[(wm * 16 + 8 + g) * PSTR + kk + t] * cc;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const double b = Bs[st][wn * 32 + j * 8 + g][kk + t];
+        const double b = bs[(wn * 32 + j * 8 + g) * PSTR + kk + t];
         dmma884(acc[0][j][0], acc[0][j][1], a0, b);
         dmma884(acc[1][j][0], acc[1][j][1], a1, b);
       }
     }
     if (do_bias && tid < PBM) {
-      const int64_t j0 = (int64_t)kt * BK;
-      double s = bias_acc[tid];
+      const double* cv = ccv + st * BK;
+      double sb = bias_acc[tid];
 #pragma unroll
-      for (int kk = 0; kk < BK; ++kk)
-        if (is_value_col(j0 + kk, p.int_cols, p.C)) s = fma(As[st][tid][kk], ccs[st][kk], s);
-      bias_acc[tid] = s;
-    }
-    __syncthreads();
-  }
-  double* out = p.part + (int64_t)split * p.p + p.off;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int row = m0 + wm * 16 + i * 8 + g;
-    if (row >= p.M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = n0 + wn * 32 + j * 8 + 2 * t + e;
-        if (col < p.N) out[(int64_t)row * p.N + col] = acc[i][j][e];
-      }
+      for (int kk = 0; kk < BK; ++kk) sb = fma(as[tid * PSTR + kk], cv[kk], sb);
+      bias_acc[tid] = sb;
     }
   }
-  if (do_bias && tid < PBM && m0 + tid < p.M) out[(int64_t)p.M * p.N + m0 + tid] = bias_acc[tid];
+  cp_async_wait<0>();
+  __syncthreads();
+  // ---- split-K reduction inside the thread-block cluster (DSMEM) ----------
+  // The kPhbCluster CTAs of a cluster are consecutive K splits of the same output
+  // tile: each stages its 64x64 partial in shared memory, then CTA `rank` sums
+  // rows [8 rank, 8 rank + 8) over all ranks in rank order and writes one partial
+  // per cluster (deterministic, kPhbCluster x less partial traffic).
+  constexpr int RSTR = PBN + 1;
+  double* red = smem;                 // [PBM][RSTR]
+  double* red_bias = red + PBM * RSTR;  // [PBM]
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) red[(wm * 16 + i * 8 + g) * RSTR + wn * 32 + j * 8 + 2 * t + e] = acc[i][j][e];
+  if (tid < PBM) red_bias[tid] = do_bias ? bias_acc[tid] : 0.0;
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  const int rank = (int)cl.block_rank();
+  double* out = p.part + (int64_t)(split / kPhbCluster) * p.p + p.off;
+  constexpr int ROWS = PBM / kPhbCluster;
+  for (int e = tid; e < ROWS * PBN; e += kThreads) {
+    const int r = rank * ROWS + e / PBN, col = e % PBN;
+    if (m0 + r < p.M && n0 + col < p.N) {
+      double sum = 0.0;
+#pragma unroll
+      for (int q = 0; q < kPhbCluster; ++q) sum += cl.map_shared_rank(red, q)[r * RSTR + col];
+      out[(int64_t)(m0 + r) * p.N + n0 + col] = sum;
+    }
+  }
+  if (do_bias && rank == 0 && tid < PBM && m0 + tid < p.M) {
+    double sum = 0.0;
+#pragma unroll
+    for (int q = 0; q < kPhbCluster; ++q) sum += cl.map_shared_rank(red_bias, q)[tid];
+    out[(int64_t)p.M * p.N + m0 + tid] = sum;
+  }
+  cl.sync();  // keep this CTA's shared memory alive until the cluster has read it
 }
 
-cudaError_t phase_b(const PhbArgs& a, int splits, cudaStream_t st) {
-  dim3 grid((a.N + PBN - 1) / PBN, (a.M + PBM - 1) / PBM, splits);
+// Phase B over ALL layers in one launch: blockIdx.x enumerates (layer, split, m-tile, n-tile)
+// with a per-layer split count proportional to the layer's work.
+__global__ void __cluster_dims__(kPhbCluster, 1, 1) __launch_bounds__(kThreads) phb_all_kernel(PhbAll a) {
+  const int t = blockIdx.x;
+  int l = 0;
+  while (l + 1 < a.n_layers && t >= a.tile_start[l + 1]) ++l;
+  const int local = t - a.tile_start[l];
+  const int G = a.G[l];
+  const int split = local % G, tile = local / G;  // consecutive CTAs = consecutive splits of one tile
+  const PhbArgs& p = a.L[l];
+  const int kt0 = split * p.ktiles_per_split;
+  phb_tile(p, tile % a.tiles_n[l], tile / a.tiles_n[l], kt0, min(p.ktiles_total, kt0 + p.ktiles_per_split), split);
+}
+
+cudaError_t phase_b_all_layers(const PhbAll& a, int splits, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(phb_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPhbSmem);
+    attr_set = true;
+  }
+  const int tiles = a.tile_start[a.n_layers];
+  if (tiles <= 0) return cudaSuccess;
   probe_before(K_PHB, st);
-  phb_kernel<<<grid, kThreads, 0, st>>>(a);
+  phb_all_kernel<<<tiles, kThreads, kPhbSmem, st>>>(a);
   probe_after(K_PHB, st);
+  (void)splits;
   return cudaGetLastError();
 }
+
 
 // ---------------------------------------------------------------------------
 // Explicit Jacobian rows for the sketch (J-chunk formulation):

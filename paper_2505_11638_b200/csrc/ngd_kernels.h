@@ -14,8 +14,16 @@ void probe_after(int kind, cudaStream_t st);
 
 // device-side PCG scalars (krylov.py:24-88)
 struct PcgState {
-  double bb, norm_b, tol, rz, rz_new, dad, alpha, rr, rel;
-  int iterations, matvecs, breakdown, converged, done;
+  double bb, norm_b, tol, rz, rz_new, dad, alpha, rr, rel, beta;
+  int iterations, matvecs, breakdown, converged, done, it;
+};
+
+// Nystrom preconditioner operands read by the kernels from device memory, so a
+// captured CUDA graph can be replayed for a new factor / damping.
+struct PrecondArgs {
+  const double* U;  // p x ell row-major
+  const double* eig;
+  double mu;
 };
 
 enum JetMode { FWD = 0, REV = 1, PHA = 2 };
@@ -68,8 +76,39 @@ struct FormJArgs {
   int64_t ldj;
 };
 
+constexpr int kMaxLayers = 8;
+constexpr int kPhbCluster = 8;  // phase-B split-K CTAs reduced through DSMEM
+struct PhaAll {
+  JetArgs L[kMaxLayers];      // per layer, interior segment settings
+  int tile_start[kMaxLayers + 1];
+  int mtiles[kMaxLayers];
+  int n_layers, nib, nbb;
+  int64_t int_cols;
+};
+struct PhbAll {
+  PhbArgs L[kMaxLayers];          // per layer (ktiles_per_split set per layer)
+  int tile_start[kMaxLayers + 1];  // flat CTA offsets: layer l owns tiles_m*tiles_n*G_l CTAs
+  int tiles_n[kMaxLayers], tiles_m[kMaxLayers], G[kMaxLayers];
+  int n_layers;
+};
+// fixed-order reduction plan of the phase-B partials: param range of layer l uses G[l] splits
+struct RedPlan {
+  int64_t start[kMaxLayers + 1];
+  int G[kMaxLayers];
+  int n_layers;
+};
+struct PackAll {
+  double* dst[kMaxLayers];
+  int Mp[kMaxLayers], Kp[kMaxLayers], n_out[kMaxLayers], n_in[kMaxLayers];
+  int64_t woff[kMaxLayers], boff[kMaxLayers];
+  int64_t start[kMaxLayers + 1];  // element offsets (packed W + bias row per layer)
+  int n_layers;
+};
+
 cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles, cudaStream_t st);
-cudaError_t phase_b(const PhbArgs& a, int splits, cudaStream_t st);
+cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st);
+cudaError_t phase_b_all_layers(const PhbAll& a, int splits, cudaStream_t st);
+void pack_all(const PackAll& a, const double* src, const int* skip, cudaStream_t st);
 cudaError_t form_j(const FormJArgs& a, int R, int n_layers, cudaStream_t st);
 
 void pack(double* dst, int Mp, int Kp, const double* src, int64_t off, int n_out, int n_in, int trans,
@@ -83,24 +122,25 @@ void residual_loss(const double* pre_last, Geom gm, const double* w, const doubl
                    double* partials, unsigned int* counter, double* loss_sum, cudaStream_t st);
 void reduce_pha(const double* partA, int rows, int n_pts_pad, const double* w, double* cot, const int* done,
                 cudaStream_t st);
-void reduce_splits(const double* part, int G, int64_t p, double mu, const double* v, double* out, const int* done,
-                   cudaStream_t st);
-void add_scaled(double* out, double mu, const double* v, int64_t n, const int* done, cudaStream_t st);
+void reduce_splits(const double* part, const RedPlan& rp, int64_t p, double mu, const double* mu_p, const double* v,
+                   double* out, const int* done, cudaStream_t st);
+void add_scaled(double* out, double mu, const double* mu_p, const double* v, int64_t n, const int* done,
+                cudaStream_t st);
 int precond_blocks(int64_t p);
-cudaError_t precond_apply(const double* U, int64_t p, int ell, const double* eig, const double* mu_p, double mu_v,
-                          const double* v, double* out, double* part, double* cprime, const int* done,
-                          cudaStream_t st);
+// counters: two consecutive unsigned counters (utv combine, uc dot)
+cudaError_t precond_apply(const PrecondArgs* pa, int64_t p, int ell, const double* v, double* out, double* part,
+                          double* cprime, unsigned* counters, const int* done, PcgState* pcg, int first,
+                          double* partials, cudaStream_t st);
 void pcg_init(PcgState* s, double rel_tol, cudaStream_t st);
 void pcg_start(const double* b, double* x, double* r, int64_t p, cudaStream_t st);
 void pcg_first_dir(const double* z, double* d, int64_t p, PcgState* s, cudaStream_t st);
-void pcg_alpha(PcgState* s, int it, cudaStream_t st);
+void pcg_ad(const double* part, const RedPlan& rp, int64_t p, const double* mu_p, const double* d, double* ad,
+            PcgState* s, int ad_ready, double* partials, unsigned* counter, cudaStream_t st);
 void pcg_update(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s, int recompute,
-                cudaStream_t st);
+                double* partials, unsigned* counter, cudaStream_t st);
 void pcg_true_res(const double* b, const double* ax, double* r, int64_t p, PcgState* s, int count, int final_pass,
-                  cudaStream_t st);
-void pcg_check(PcgState* s, cudaStream_t st);
+                  double* partials, unsigned* counter, cudaStream_t st);
 void pcg_dir(const double* z, double* d, int64_t p, PcgState* s, cudaStream_t st);
-void pcg_final(PcgState* s, cudaStream_t st);
 void theta_minus(const double* a, double alpha, const double* b, double* out, int64_t n, cudaStream_t st);
 void scale_rows(double* S, int64_t R, int ell, const double* w, cudaStream_t st);
 void add_shift(double* y, const double* omega, int64_t n, const double* fro2, double* shift_out, cudaStream_t st);

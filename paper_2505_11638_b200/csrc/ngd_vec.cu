@@ -88,10 +88,10 @@ void init_point_data(double* zin1, double* dlast, Geom gm, const double* x_int, 
 // ----------------------- deterministic two-stage sums ------------------------
 // Each launch uses grid = nblocks_for(n) blocks; block b sums a fixed strided set,
 // the last block to finish sums the block partials in index order.
-int nblocks_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048, 296)); }
+int nblocks_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 511) / 512, 1184)); }
 
-template <typename F>
-__device__ __forceinline__ void finish_sum(double v, double* partials, unsigned int* counter, double* out, F&& post) {
+template <typename T, typename F>
+__device__ __forceinline__ void finish_sum(double v, double* partials, unsigned int* counter, T* out, F&& post) {
   __shared__ double sh[kThreads / 32];
   __shared__ bool last;
   const double bs = block_sum(v, sh);
@@ -102,14 +102,33 @@ __device__ __forceinline__ void finish_sum(double v, double* partials, unsigned 
     last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {  // block-uniform: the whole last block combines the partials (fixed order)
     __threadfence();
     double s = 0.0;
-    volatile double* vp = partials;
-    for (unsigned i = 0; i < gridDim.x; ++i) s += vp[i];
-    *counter = 0;
-    post(s, out);
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) s += __ldcg(&partials[i]);
+    const double tot = block_sum(s, sh);
+    if (threadIdx.x == 0) {
+      *counter = 0;
+      post(tot, out);
+    }
   }
+}
+
+// sum_{g<G} part[g*stride + i] in index order, with 8 loads in flight (latency hiding
+// without changing the deterministic summation order)
+template <typename P>
+__device__ __forceinline__ double sum_partials(P part, int G, int64_t stride, int64_t i) {
+  double s = 0.0;
+  int g = 0;
+  for (; g + 8 <= G; g += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(&part[(int64_t)(g + u) * stride + i]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; g < G; ++g) s += __ldcg(&part[(int64_t)g * stride + i]);
+  return s;
 }
 
 // out[0] = sum_i x[i]*y[i]   (skip if *done)
@@ -162,8 +181,7 @@ __global__ void reduce_pha_kernel(const double* partA, int rows, int n_pts_pad, 
                                   const int* done) {
   if (done && *done) return;
   for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < n_pts_pad; pt += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int r = 0; r < rows; ++r) s += partA[(int64_t)r * n_pts_pad + pt];
+    const double s = sum_partials(partA, rows, n_pts_pad, pt);
     cot[pt] = w ? w[pt] * s : s;
   }
 }
@@ -177,35 +195,44 @@ void reduce_pha(const double* partA, int rows, int n_pts_pad, const double* w, d
 }
 
 // phase B reduction: out[i] = sum_g part[g][i] (+ mu * v[i])
-__global__ void reduce_splits_kernel(const double* part, int G, int64_t p, double mu, const double* v, double* out,
-                                     const int* done) {
+__device__ __forceinline__ int plan_G(const RedPlan& rp, int64_t i) {
+  int l = 0;
+  while (l + 1 < rp.n_layers && i >= rp.start[l + 1]) ++l;
+  return rp.G[l];
+}
+
+__global__ void reduce_splits_kernel(const double* part, RedPlan rp, int64_t p, double mu, const double* mu_p,
+                                     const double* v, double* out, const int* done) {
   if (done && *done) return;
+  if (mu_p) mu = *mu_p;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int g = 0; g < G; ++g) s += part[(int64_t)g * p + i];
+    double s = sum_partials(part, plan_G(rp, i), p, i);
     if (v) s = fma(mu, v[i], s);
     out[i] = s;
   }
 }
 
-void reduce_splits(const double* part, int G, int64_t p, double mu, const double* v, double* out, const int* done,
-                   cudaStream_t st) {
+void reduce_splits(const double* part, const RedPlan& rp, int64_t p, double mu, const double* mu_p, const double* v,
+                   double* out, const int* done, cudaStream_t st) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((p + 255) / 256, 148 * 8));
   probe_before(K_VEC, st);
-  reduce_splits_kernel<<<grid, 256, 0, st>>>(part, G, p, mu, v, out, done);
+  reduce_splits_kernel<<<grid, 256, 0, st>>>(part, rp, p, mu, mu_p, v, out, done);
   probe_after(K_VEC, st);
 }
 
 // out += mu * v
-__global__ void add_scaled_kernel(double* out, double mu, const double* v, int64_t n, const int* done) {
+__global__ void add_scaled_kernel(double* out, double mu, const double* mu_p, const double* v, int64_t n,
+                                  const int* done) {
   if (done && *done) return;
+  if (mu_p) mu = *mu_p;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = fma(mu, v[i], out[i]);
 }
-void add_scaled(double* out, double mu, const double* v, int64_t n, const int* done, cudaStream_t st) {
+void add_scaled(double* out, double mu, const double* mu_p, const double* v, int64_t n, const int* done,
+                cudaStream_t st) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
   probe_before(K_VEC, st);
-  add_scaled_kernel<<<grid, 256, 0, st>>>(out, mu, v, n, done);
+  add_scaled_kernel<<<grid, 256, 0, st>>>(out, mu, mu_p, v, n, done);
   probe_after(K_VEC, st);
 }
 
@@ -234,110 +261,112 @@ void scatter_points(const double* compact, double* padded, Geom gm, cudaStream_t
 
 // ------------------------- Nystrom preconditioner ---------------------------
 // P^{-1} v = U((scale*inv - 1) o (U^T v)) + v   (sketch.py:101-112, fused into 2 passes over U)
-// U row-major p x ell.  Pass 1: per row-block partial U^T v.
-template <int JCH>
-__global__ void __launch_bounds__(kThreads) utv_kernel(const double* U, int64_t p, int ell, const double* v,
-                                                       int64_t rows_per_blk, double* part, const int* done) {
+// U column-major p x ell (each basis vector contiguous).
+// Pass 1 (utv_kernel): one block per basis vector: c'_j = (scale/(lam_j+mu) - 1) * <u_j, v>.
+// Pass 2 (uc_kernel): out = v + U c', optionally with the PCG dot r.z fused in.
+__global__ void __launch_bounds__(kThreads) utv_kernel(const PrecondArgs* pa, int64_t p, int ell, const double* v,
+                                                       double* cprime, const int* done) {
   if (done && *done) return;
-  __shared__ double sh[JCH * 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double acc[JCH];
+  __shared__ double sh[kThreads / 32];
+  const int j = blockIdx.x;
+  const double* u = pa->U + (int64_t)j * p;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t i = threadIdx.x;
+  for (; i + 3 * kThreads < p; i += 4 * kThreads) {
 #pragma unroll
-  for (int j = 0; j < JCH; ++j) acc[j] = 0.0;
-  const int64_t r0 = blockIdx.x * rows_per_blk, r1 = std::min<int64_t>(p, r0 + rows_per_blk);
-  for (int64_t i = r0 + warp; i < r1; i += kThreads / 32) {
-    const double vi = v[i];
-    const double* row = U + i * ell;
-#pragma unroll
-    for (int j = 0; j < JCH; ++j) {
-      const int col = j * 32 + lane;
-      if (col < ell) acc[j] = fma(row[col], vi, acc[j]);
-    }
+    for (int q = 0; q < 4; ++q) acc[q] = fma(u[i + q * kThreads], v[i + q * kThreads], acc[q]);
   }
-  // fixed-order cross-warp accumulation (warp 0 first)
-  for (int w = 0; w < kThreads / 32; ++w) {
-    if (warp == w) {
-#pragma unroll
-      for (int j = 0; j < JCH; ++j) sh[j * 32 + lane] = (w == 0 ? 0.0 : sh[j * 32 + lane]) + acc[j];
-    }
-    __syncthreads();
-  }
-  for (int col = threadIdx.x; col < ell; col += kThreads) part[(int64_t)blockIdx.x * ell + col] = sh[col];
-}
-
-// combine partials and scale:  c'[j] = (scale*inv[j] - 1) * sum_b part[b][j]
-__global__ void utv_combine_kernel(const double* part, int nblk, int ell, const double* eig, const double* mu_p,
-                                   double mu_v, double* cprime, const int* done) {
-  if (done && *done) return;
-  const double mu = mu_p ? *mu_p : mu_v;
-  const double scale = eig[ell - 1] + mu;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ell; j += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * ell + j];
-    cprime[j] = (scale / (eig[j] + mu) - 1.0) * s;
+  for (; i < p; i += kThreads) acc[0] = fma(u[i], v[i], acc[0]);
+  const double tot = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), sh);
+  if (threadIdx.x == 0) {
+    const double mu = pa->mu;
+    const double* eig = pa->eig;
+    cprime[j] = ((eig[ell - 1] + mu) / (eig[j] + mu) - 1.0) * tot;
   }
 }
 
-// out[i] = v[i] + sum_j U[i][j] c'[j]; one warp per row.  Optionally also
-// accumulates r.z for PCG (rz_out) -- fused dot.
-__global__ void __launch_bounds__(kThreads) uc_kernel(const double* U, int64_t p, int ell, const double* cprime,
-                                                      const double* v, double* out, const int* done) {
+// out[i] = v[i] + sum_j U[j p + i] c'_j.  Block = 64 rows x 4 column groups (fixed-order
+// combine in shared memory).  With pcg != null the dot r.z (r = v, z = out) is finished by
+// the last block: first pass rz = r.z; otherwise beta = r.z_new / rz, rz = r.z_new (krylov.py:75-78).
+__global__ void __launch_bounds__(kThreads) uc_kernel(const PrecondArgs* pa, int64_t p, int ell, const double* cprime,
+                                                      const double* v, double* out, const int* done, PcgState* pcg,
+                                                      int first, double* partials, unsigned* counter) {
   if (done && *done) return;
-  extern __shared__ double cs[];
+  extern __shared__ double cs[];  // [ell] c' then [4][64] partial rows
+  double* part = cs + ell;
   for (int j = threadIdx.x; j < ell; j += blockDim.x) cs[j] = cprime[j];
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + warp; i < p; i += (int64_t)gridDim.x * (kThreads / 32)) {
-    const double* row = U + i * ell;
-    double s = 0.0;
-    for (int j = lane; j < ell; j += 32) s = fma(row[j], cs[j], s);
-    s = warp_sum(s);
-    if (lane == 0) out[i] = v[i] + s;
+  const int rl = threadIdx.x & 63, grp = threadIdx.x >> 6;
+  const int64_t i = (int64_t)blockIdx.x * 64 + rl;
+  double s = 0.0;
+  if (i < p && ell > 0) {
+    const double* U = pa->U;
+    const int j0 = grp * ((ell + 3) / 4), j1 = min(ell, j0 + (ell + 3) / 4);
+    int j = j0;
+    for (; j + 8 <= j1; j += 8) {
+      double u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) u[q] = U[(int64_t)(j + q) * p + i];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s = fma(u[q], cs[j + q], s);
+    }
+    for (; j < j1; ++j) s = fma(U[(int64_t)j * p + i], cs[j], s);
   }
+  part[grp * 64 + rl] = s;
+  __syncthreads();
+  double rz = 0.0;
+  if (grp == 0 && i < p) {
+    const double z = v[i] + (((part[rl] + part[64 + rl]) + part[128 + rl]) + part[192 + rl]);
+    out[i] = z;
+    rz = v[i] * z;
+  }
+  if (!pcg) return;
+  finish_sum(rz, partials, counter, pcg, [first](double sum, PcgState* st) {
+    st->rz_new = sum;
+    if (first) {
+      st->rz = sum;
+    } else {
+      st->beta = sum / st->rz;
+      st->rz = sum;
+    }
+  });
 }
 
-int precond_blocks(int64_t p) { return (int)std::max<int64_t>(1, std::min<int64_t>((p + 63) / 64, 296)); }
+int precond_blocks(int64_t p) { return (int)std::max<int64_t>(1, (p + 63) / 64); }
 
-cudaError_t precond_apply(const double* U, int64_t p, int ell, const double* eig, const double* mu_p, double mu_v,
-                          const double* v, double* out, double* part, double* cprime, const int* done,
-                          cudaStream_t st) {
-  const int nblk = precond_blocks(p);
-  const int64_t rpb = (p + nblk - 1) / nblk;
-  const int jch = (ell + 31) / 32;
-#define NGD_UTV(J) (probe_before(K_PRECOND, st), utv_kernel<J><<<nblk, kThreads, 0, st>>>(U, p, ell, v, rpb, part, done), probe_after(K_PRECOND, st))
-  if (jch <= 1) NGD_UTV(1);
-  else if (jch <= 2) NGD_UTV(2);
-  else if (jch <= 4) NGD_UTV(4);
-  else if (jch <= 8) NGD_UTV(8);
-  else if (jch <= 16) NGD_UTV(16);
-  else if (jch <= 24) NGD_UTV(24);
-  else if (jch <= 32) NGD_UTV(32);
-  else return cudaErrorInvalidValue;
-#undef NGD_UTV
+cudaError_t precond_apply(const PrecondArgs* pa, int64_t p, int ell, const double* v, double* out, double* part,
+                          double* cprime, unsigned* counters, const int* done, PcgState* pcg, int first,
+                          double* partials, cudaStream_t st) {
+  (void)part;
+  if (ell > 0) {
+    probe_before(K_PRECOND, st);
+    utv_kernel<<<ell, kThreads, 0, st>>>(pa, p, ell, v, cprime, done);
+    probe_after(K_PRECOND, st);
+  }
+  const int grid = precond_blocks(p);
   probe_before(K_PRECOND, st);
-  utv_combine_kernel<<<(ell + 255) / 256, 256, 0, st>>>(part, nblk, ell, eig, mu_p, mu_v, cprime, done);
-  probe_after(K_PRECOND, st);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((p + 7) / 8, 148 * 8));
-  probe_before(K_PRECOND, st);
-  uc_kernel<<<grid, kThreads, sizeof(double) * ell, st>>>(U, p, ell, cprime, v, out, done);
+  uc_kernel<<<grid, kThreads, sizeof(double) * (std::max(ell, 1) + 256), st>>>(pa, p, ell, cprime, v, out, done, pcg,
+                                                                              first, partials, counters + 1);
   probe_after(K_PRECOND, st);
   return cudaGetLastError();
 }
 
 // ------------------------------ PCG device state ----------------------------
-// krylov.py:24-88, scalar logic executed by one thread on the device so the
-// whole solve runs without host round trips.
+// krylov.py:24-88, scalar logic executed on the device (last block of the
+// fused reductions) so a whole solve runs without host round trips.
 __global__ void pcg_init_kernel(PcgState* s, double rel_tol) {
   s->norm_b = sqrt(s->bb);
   s->tol = rel_tol;
   s->iterations = 0;
+  s->it = 0;
   s->matvecs = 0;
   s->breakdown = 0;
   s->converged = 0;
+  s->beta = 0.0;
   s->done = (s->norm_b == 0.0) ? 2 : 0;  // 2 = zero right-hand side
 }
 
-// x = 0, r = b, (z computed by precond afterwards), copy
+// x = 0, r = b
 __global__ void pcg_start_kernel(const double* b, double* x, double* r, int64_t p) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
     x[i] = 0.0;
@@ -345,76 +374,101 @@ __global__ void pcg_start_kernel(const double* b, double* x, double* r, int64_t 
   }
 }
 
-// d = z ; rz already computed into s->rz_new
+// d = z
 __global__ void pcg_first_dir_kernel(const double* z, double* d, int64_t p, PcgState* s) {
   if (s->done) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x)
     d[i] = z[i];
-  if (blockIdx.x == 0 && threadIdx.x == 0) s->rz = s->rz_new;
 }
 
-// after A d and dad: breakdown test, alpha  (krylov.py:60-66)
-__global__ void pcg_alpha_kernel(PcgState* s, int it) {
+// ad = sum_g part[g] + mu d ; dad = d.ad ; breakdown test and alpha (krylov.py:59-66)
+__global__ void pcg_ad_kernel(const double* part, RedPlan rp, int64_t p, const double* mu_p, const double* d,
+                              double* ad, PcgState* s, int ad_ready, double* partials, unsigned* counter) {
   if (s->done) return;
-  s->matvecs += 1;
-  if (s->dad <= 0.0) {
-    s->breakdown = 1;
-    s->done = 1;
-    return;
+  const double mu = *mu_p;
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
+    double a;
+    if (ad_ready) {
+      a = ad[i];
+    } else {
+      a = sum_partials(part, plan_G(rp, i), p, i);
+      a = fma(mu, d[i], a);
+      ad[i] = a;
+    }
+    v = fma(d[i], a, v);
   }
-  s->alpha = s->rz / s->dad;
-  s->iterations = it;
+  finish_sum(v, partials, counter, s, [](double sum, PcgState* st) {
+    st->dad = sum;
+    const int it = ++st->it;
+    st->matvecs += 1;
+    if (sum <= 0.0) {
+      st->breakdown = 1;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rz / sum;
+    st->iterations = it;
+  });
 }
 
-// x += alpha d ; r -= alpha Ad (unless this is a recompute iteration)
+// x += alpha d ; r -= alpha ad ; rr = r.r ; convergence test (krylov.py:66-74)
 __global__ void pcg_update_kernel(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s,
-                                  int recompute) {
+                                  int recompute, double* partials, unsigned* counter) {
   if (s->done) return;
   const double a = s->alpha;
+  double v = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
     x[i] = x[i] + a * d[i];
-    if (!recompute) r[i] = r[i] - a * ad[i];
+    if (!recompute) {
+      const double ri = r[i] - a * ad[i];
+      r[i] = ri;
+      v = fma(ri, ri, v);
+    }
   }
+  if (recompute) return;
+  finish_sum(v, partials, counter, s, [](double sum, PcgState* st) {
+    st->rr = sum;
+    st->rel = sqrt(sum) / st->norm_b;
+    if (st->rel <= st->tol) st->done = 3;
+  });
 }
 
-// r = b - Ax (true residual recompute, krylov.py:69-71)
+// r = b - Ax (true residual, krylov.py:69-71 and 83-85) ; rr ; test
 __global__ void pcg_true_res_kernel(const double* b, const double* ax, double* r, int64_t p, PcgState* s,
-                                    int count_matvec, int final_pass) {
+                                    int count_matvec, int final_pass, double* partials, unsigned* counter) {
   if (!final_pass && s->done) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x)
-    r[i] = b[i] - ax[i];
-  if (count_matvec && blockIdx.x == 0 && threadIdx.x == 0) s->matvecs += 1;
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = b[i] - ax[i];
+    r[i] = ri;
+    v = fma(ri, ri, v);
+  }
+  finish_sum(v, partials, counter, s, [count_matvec, final_pass](double sum, PcgState* st) {
+    st->rr = sum;
+    if (count_matvec) st->matvecs += 1;
+    st->rel = sqrt(sum) / st->norm_b;
+    if (final_pass) {
+      if (st->done != 2) {
+        st->matvecs += 1;
+        st->converged = (!st->breakdown) && (st->rel <= st->tol);
+      }
+    } else if (st->rel <= st->tol) {
+      st->done = 3;
+    }
+  });
 }
 
-// convergence test on ||r||/||b|| (krylov.py:72-74)
-__global__ void pcg_check_kernel(PcgState* s) {
-  if (s->done) return;
-  const double rel = sqrt(s->rr) / s->norm_b;
-  s->rel = rel;
-  if (rel <= s->tol) s->done = 3;  // converged by tolerance
-}
-
-// beta = r.z_new / rz ; d = z + beta d  (krylov.py:75-81)
+// d = z + beta d  (krylov.py:79-81)
 __global__ void pcg_dir_kernel(const double* z, double* d, int64_t p, PcgState* s) {
   if (s->done) return;
-  const double beta = s->rz_new / s->rz;
+  const double beta = s->beta;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x)
     d[i] = z[i] + beta * d[i];
 }
-__global__ void pcg_rz_roll_kernel(PcgState* s) {
-  if (s->done) return;
-  s->rz = s->rz_new;
-}
-
-// final report (krylov.py:83-88)
-__global__ void pcg_final_kernel(PcgState* s) {
-  if (s->done == 2) return;  // zero rhs: report stays (0 its, 0 matvecs, converged)
-  s->matvecs += 1;
-  s->rel = sqrt(s->rr) / s->norm_b;
-  s->converged = (!s->breakdown) && (s->rel <= s->tol);
-}
 
 static int vgrid(int64_t p) { return (int)std::max<int64_t>(1, std::min<int64_t>((p + 255) / 256, 148 * 8)); }
+static int rgrid(int64_t p) { return nblocks_for(p); }
 
 void pcg_init(PcgState* s, double rel_tol, cudaStream_t st) {
   probe_before(K_VEC, st);
@@ -431,40 +485,56 @@ void pcg_first_dir(const double* z, double* d, int64_t p, PcgState* s, cudaStrea
   pcg_first_dir_kernel<<<vgrid(p), 256, 0, st>>>(z, d, p, s);
   probe_after(K_VEC, st);
 }
-void pcg_alpha(PcgState* s, int it, cudaStream_t st) {
+void pcg_ad(const double* part, const RedPlan& rp, int64_t p, const double* mu_p, const double* d, double* ad,
+            PcgState* s, int ad_ready, double* partials, unsigned* counter, cudaStream_t st) {
   probe_before(K_VEC, st);
-  pcg_alpha_kernel<<<1, 1, 0, st>>>(s, it);
+  pcg_ad_kernel<<<rgrid(p), kThreads, 0, st>>>(part, rp, p, mu_p, d, ad, s, ad_ready, partials, counter);
   probe_after(K_VEC, st);
 }
 void pcg_update(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s, int recompute,
-                cudaStream_t st) {
+                double* partials, unsigned* counter, cudaStream_t st) {
   probe_before(K_VEC, st);
-  pcg_update_kernel<<<vgrid(p), 256, 0, st>>>(x, r, d, ad, p, s, recompute);
+  pcg_update_kernel<<<rgrid(p), kThreads, 0, st>>>(x, r, d, ad, p, s, recompute, partials, counter);
   probe_after(K_VEC, st);
 }
 void pcg_true_res(const double* b, const double* ax, double* r, int64_t p, PcgState* s, int count, int final_pass,
-                  cudaStream_t st) {
+                  double* partials, unsigned* counter, cudaStream_t st) {
   probe_before(K_VEC, st);
-  pcg_true_res_kernel<<<vgrid(p), 256, 0, st>>>(b, ax, r, p, s, count, final_pass);
-  probe_after(K_VEC, st);
-}
-void pcg_check(PcgState* s, cudaStream_t st) {
-  probe_before(K_VEC, st);
-  pcg_check_kernel<<<1, 1, 0, st>>>(s);
+  pcg_true_res_kernel<<<rgrid(p), kThreads, 0, st>>>(b, ax, r, p, s, count, final_pass, partials, counter);
   probe_after(K_VEC, st);
 }
 void pcg_dir(const double* z, double* d, int64_t p, PcgState* s, cudaStream_t st) {
   probe_before(K_VEC, st);
   pcg_dir_kernel<<<vgrid(p), 256, 0, st>>>(z, d, p, s);
   probe_after(K_VEC, st);
-  probe_before(K_VEC, st);
-  pcg_rz_roll_kernel<<<1, 1, 0, st>>>(s);
-  probe_after(K_VEC, st);
 }
-void pcg_final(PcgState* s, cudaStream_t st) {
-  probe_before(K_VEC, st);
-  pcg_final_kernel<<<1, 1, 0, st>>>(s);
-  probe_after(K_VEC, st);
+
+// pack all layers' weight matrices (+ bias rows) of a parameter-layout vector in one launch
+__global__ void pack_all_kernel(PackAll a, const double* src, const int* skip) {
+  if (skip && *skip) return;
+  const int64_t n = a.start[a.n_layers];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int l = 0;
+    while (l + 1 < a.n_layers && i >= a.start[l + 1]) ++l;
+    const int64_t k = i - a.start[l];
+    const int64_t mat = (int64_t)a.Mp[l] * a.Kp[l];
+    double v = 0.0;
+    if (k < mat) {
+      const int m = (int)(k / a.Kp[l]), c = (int)(k % a.Kp[l]);
+      if (m < a.n_out[l] && c < a.n_in[l]) v = src[a.woff[l] + (int64_t)m * a.n_in[l] + c];
+    } else {
+      const int m = (int)(k - mat);
+      if (m < a.n_out[l]) v = src[a.boff[l] + m];
+    }
+    a.dst[l][k] = v;
+  }
+}
+void pack_all(const PackAll& a, const double* src, const int* skip, cudaStream_t st) {
+  const int64_t n = a.start[a.n_layers];
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+  probe_before(K_PACK, st);
+  pack_all_kernel<<<grid, 256, 0, st>>>(a, src, skip);
+  probe_after(K_PACK, st);
 }
 
 // ------------------------------- small maps ---------------------------------

@@ -61,6 +61,8 @@ def pcg(op, b, rel_tol, maxit, precond=None, recompute_every=50):
         pmu = 0.0
         if precond is not None:
             U, eig, ell = precond.factor.basis, precond.factor.eigenvalues, precond.factor.rank
+            if U.stride(0) != 1:
+                U = U.t().contiguous().t()
             pmu = precond.mu
         if isinstance(base, GramianOperator):
             base._ensure()

@@ -37,7 +37,8 @@ class SketchFailure(RuntimeError):
 @dataclass(frozen=True)
 class NystromFactor:
     """G ~= U diag(eigenvalues) U^T (sketch.py:27-49).  ``basis`` is a (p, l)
-    CUDA tensor (row-major); ``eigenvalues`` a (l,) CUDA tensor."""
+    CUDA tensor view of column-major storage (each basis vector contiguous);
+    ``eigenvalues`` a (l,) CUDA tensor."""
 
     basis: object
     eigenvalues: object
@@ -106,17 +107,17 @@ def nystrom_approximate(op, rank, seed, max_retries=3, omega_source=None, omega_
             op.matmat_colmajor(omega, Y)
         else:  # generic operator with a (p, l) matmat
             Y.copy_(_lib.to_device(op.matmat(omega.t().cpu().numpy())).t())
-        U = torch.empty((p, rank), dtype=torch.float64, device=omega.device)
+        Ucm = torch.empty((rank, p), dtype=torch.float64, device=omega.device)  # p x rank column-major
         eig = torch.empty(rank, dtype=torch.float64, device=omega.device)
         shift = _lib.ctypes.c_double()
         try:
-            ctx.call("ngd_nystrom_finish", _lib.ptr(omega), _lib.ptr(Y), p, rank, _lib.ptr(U), _lib.ptr(eig),
+            ctx.call("ngd_nystrom_finish", _lib.ptr(omega), _lib.ptr(Y), p, rank, _lib.ptr(Ucm), _lib.ptr(eig),
                      _lib.ctypes.byref(shift))
         except _lib.CholeskyFailure as err:
             last_err = err
             continue
         eh = eig.cpu().numpy()
-        return NystromFactor(U, eig, eh, float(shift.value))
+        return NystromFactor(Ucm.t(), eig, eh, float(shift.value))
     raise SketchFailure(f"sketch Cholesky failed after {max_retries} attempts") from last_err
 
 
@@ -137,6 +138,8 @@ class NystromPreconditioner:
         if out is None:
             out = torch.empty_like(v)
         U = self.factor.basis
+        if U.stride(0) != 1:  # caller-built factor: make it column-major
+            U = U.t().contiguous().t()
         self.ctx.call("ngd_precond_apply", _lib.ptr(U), _lib.ptr(self.factor.eigenvalues), U.shape[1], self.mu,
                       _lib.ptr(v), _lib.ptr(out), U.shape[0])
         return out
