@@ -93,6 +93,11 @@ int ngd_fill_gaussian(ngd_ctx* ctx, uint64_t seed, double* d_out, int64_t n);
 int ngd_nystrom_prepare(ngd_ctx* ctx, double* d_omega, int64_t p, int32_t ell);
 int ngd_nystrom_finish(ngd_ctx* ctx, const double* d_omega, double* d_Y, int64_t p, int32_t ell,
                        double* d_U, double* d_eig, double* h_shift);
+/* small dense SVD A = U diag(sigma) V^T of an ell x ell column-major matrix (the step of
+ * sketch.py:85 after B = QR); method 2 = cluster one-sided Jacobi, 1 = cuSOLVER polar SVD.
+ * h_sweeps receives the Jacobi sweep count (negative if not converged). */
+int ngd_small_svd(ngd_ctx* ctx, const double* d_A, int32_t ell, double* d_U, double* d_sigma, int32_t method,
+                  int32_t* h_sweeps);
 /* dense operator helper (DenseOperator.matmat, gramian.py:101-120): Y = G V */
 int ngd_dense_matmat(ngd_ctx* ctx, const double* d_G, int64_t p, const double* d_V, int64_t ell, double* d_Y);
 
@@ -106,8 +111,12 @@ int ngd_pcg(ngd_ctx* ctx, const double* d_dense, int64_t p, const double* d_b, d
             const double* d_U, const double* d_eig, int32_t ell, double precond_mu, double rel_tol,
             int32_t maxit, int32_t recompute_every, double* d_x, ngd_solve_report* h_report);
 
-/* ---- tuning knobs: "svd" = 0 (Householder QR + Jacobi SVD) | 1 (shifted Cholesky-QR3 + polar SVD, default) */
+/* ---- tuning knobs: "svd" = 0 (Householder QR + cuSOLVER gesvdj) | 1 (shifted Cholesky-QR3 + cuSOLVER polar SVD)
+ *      | 2 (shifted Cholesky-QR3 + in-house cluster one-sided Jacobi SVD; default, falls back to 1 above ell ~ 700);
+ *      "graphs" = 1 (replay PCG iterations as a CUDA graph, default) | 0 */
 int ngd_set_option(ngd_ctx* ctx, const char* key, int64_t value);
+/* diagnostics: "jacobi_sweeps" (last Nystrom factorisation), "phase_b_splits" */
+int ngd_get_stat(ngd_ctx* ctx, const char* key, int64_t* out);
 
 /* ---- vector helpers used by the host policy ------------------------------
  * ngd_dot: h_out = x . y (deterministic reduction, synchronises);

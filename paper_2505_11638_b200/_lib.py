@@ -67,6 +67,8 @@ SIGNATURES = {
     "ngd_dense_matmat": [_P, _P, _I64, _P, _I64, _P],
     "ngd_precond_apply": [_P, _P, _P, _I32, _D, _P, _P, _I64],
     "ngd_pcg": [_P, _P, _I64, _P, _D, _P, _P, _I32, _D, _D, _I32, _I32, _P, ctypes.POINTER(SolveReportC)],
+    "ngd_small_svd": [_P, _P, _I32, _P, _P, _I32, ctypes.POINTER(_I32)],
+    "ngd_get_stat": [_P, ctypes.c_char_p, ctypes.POINTER(_I64)],
     "ngd_set_option": [_P, ctypes.c_char_p, _I64],
     "ngd_dot": [_P, _P, _P, _I64, ctypes.POINTER(_D)],
     "ngd_axpy": [_P, _P, _D, _P, _P, _I64],
@@ -79,7 +81,7 @@ _RESTYPE = {"ngd_last_error": ctypes.c_char_p, "ngd_param_count": _I64, "ngd_lau
 
 _lib = None
 _contexts = []  # weak registry so option changes reach live contexts
-OPTIONS = {"svd": 1}
+OPTIONS = {"svd": 2}
 
 
 def set_option(key, value):

@@ -138,7 +138,8 @@ struct ngd_ctx {
   double* h_pin = nullptr;    // pinned host scalars
   cusolverDnParams_t dn_params = nullptr;
   std::vector<char> h_work;
-  int svd_method = 1;
+  int svd_method = 2;
+  int last_sweeps = 0;
   int use_graphs = 1;
   int graph_gen = 0;
   cudaStream_t cap_stream = nullptr;
@@ -851,16 +852,30 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
   } else {
     // 4. B = Q R by shifted Cholesky-QR3 (GEMM/SYRK + potrf + TRSM; stable for cond(B) up to 1/eps)
     TRY(scholqr3(c, Y, p, ell));
-    // 5. R = U_R diag(s) V^T (polar-decomposition SVD, descending)
-    TRY(small_svd_polar(c, ell));
+    // 5. R = U_R diag(s) V^T, descending: cluster one-sided Jacobi (method 2) or polar SVD
+    // element-wise DSMEM rotations are latency-bound beyond one CTA: use the cluster Jacobi
+    // only when the factor fits one CTA's shared memory (ell <~ 110), else the polar SVD
+    if (c->svd_method == 2 && jsvd_cluster_size(ell) == 1) {
+      CK(jacobi_svd(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(), static_cast<int*>(c->nys_info.p) + 2,
+                    c->stream));
+    } else {
+      TRY(small_svd_polar(c, ell));
+    }
   }
   // U = Q U_R  (column-major p x ell output)
   CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)p, ell, ell, &one, Y, (int)p, c->nys_ur.d(), ell, &zero,
                   U_row, (int)p));
   eig_from_sv(c->nys_s.d(), ell, c->S(SC_SHIFT), eig, c->stream);
   CK(cudaMemcpyAsync(&c->h_pin[0], c->S(SC_SHIFT), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&c->h_pin[60], static_cast<int*>(c->nys_info.p) + 2, sizeof(int), cudaMemcpyDeviceToHost,
+                     c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (h_shift) *h_shift = c->h_pin[0];
+  {
+    int sw = 0;
+    memcpy(&sw, &c->h_pin[60], sizeof(int));
+    c->last_sweeps = sw;
+  }
   CK(cudaGetLastError());
   return NGD_OK;
 }
@@ -1062,6 +1077,47 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
   return NGD_OK;
 }
 
+int ngd_small_svd(ngd_ctx* c, const double* A, int32_t ell, double* U, double* sigma, int32_t method,
+                  int32_t* h_sweeps) {
+  TRY(bind(c));
+  if (ell < 1) return fail(NGD_E_SHAPE, "empty matrix");
+  CK(c->nys_r.ensure(sizeof(double) * (size_t)ell * ell));
+  CK(c->nys_ur.ensure(sizeof(double) * (size_t)ell * ell));
+  CK(c->nys_v.ensure(sizeof(double) * (size_t)ell * ell));
+  CK(c->nys_s.ensure(sizeof(double) * ell));
+  CK(c->nys_info.ensure(sizeof(int) * 4));
+  CK(cudaMemcpyAsync(c->nys_r.d(), A, sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
+  int sweeps = 0;
+  if (method == 2) {
+    if (jsvd_cluster_size(ell) == 0) return fail(NGD_E_SHAPE, "ell = %d too large for the cluster Jacobi SVD", ell);
+    CK(jacobi_svd(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(), static_cast<int*>(c->nys_info.p) + 2,
+                  c->stream));
+    CK(cudaMemcpyAsync(&c->h_pin[56], static_cast<int*>(c->nys_info.p) + 2, sizeof(int), cudaMemcpyDeviceToHost,
+                       c->stream));
+  } else {
+    TRY(small_svd_polar(c, ell));
+  }
+  CK(cudaMemcpyAsync(U, c->nys_ur.d(), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(sigma, c->nys_s.d(), sizeof(double) * ell, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (method == 2) memcpy(&sweeps, &c->h_pin[56], sizeof(int));
+  if (h_sweeps) *h_sweeps = sweeps;
+  return NGD_OK;
+}
+
+int ngd_get_stat(ngd_ctx* c, const char* key, int64_t* out) {
+  if (!c || !key || !out) return fail(NGD_E_SHAPE, "bad stat query");
+  if (!strcmp(key, "jacobi_sweeps")) {
+    *out = c->last_sweeps;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "phase_b_splits")) {
+    *out = c->G;
+    return NGD_OK;
+  }
+  return fail(NGD_E_SHAPE, "unknown stat '%s'", key);
+}
+
 int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(NGD_E_SHAPE, "bad option");
   if (!strcmp(key, "graphs")) {
@@ -1069,7 +1125,8 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
     return NGD_OK;
   }
   if (!strcmp(key, "svd")) {
-    if (value < 0 || value > 1) return fail(NGD_E_SHAPE, "svd method must be 0 (geqrf+gesvdj) or 1 (scholqr3+gesvdp)");
+    if (value < 0 || value > 2)
+      return fail(NGD_E_SHAPE, "svd method must be 0 (geqrf+gesvdj), 1 (scholqr3+gesvdp) or 2 (scholqr3+cluster Jacobi)");
     c->svd_method = (int)value;
     return NGD_OK;
   }

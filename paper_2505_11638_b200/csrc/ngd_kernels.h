@@ -148,6 +148,9 @@ void eig_from_sv(const double* s, int ell, const double* shift, double* eig, cud
 void triu(double* a, int n, int lda, cudaStream_t st);
 void shift_diag(double* w, int n, double coef, cudaStream_t st);
 void fill_gaussian(double* out, int64_t n, uint64_t seed, cudaStream_t st);
+int jsvd_cluster_size(int ell);
+cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
+                       cudaStream_t st);
 void gather_points(const double* padded, double* compact, Geom gm, cudaStream_t st);
 void scatter_points(const double* compact, double* padded, Geom gm, cudaStream_t st);
 

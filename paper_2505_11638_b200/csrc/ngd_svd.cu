@@ -1,0 +1,253 @@
+// Small dense SVD for the Nystrom factor: one-sided (Hestenes) Jacobi in a
+// thread-block cluster, the matrix resident in (distributed) shared memory.
+//
+// sketch.py:85 takes the thin SVD of B = Y_nu C^{-1}; after B = Q R (shifted
+// Cholesky-QR3) only the ell x ell SVD of R remains.  cuSOLVER's dense SVDs are
+// latency-bound at these sizes (gesvdp 9.6 ms, gesvdj 32 ms at ell = 300 on
+// B200, tools/probe/svd_bench.cu).  Here the ell columns of R are spread over a
+// cluster of CL CTAs (CL * 200 KB of shared memory); every round of the
+// round-robin (circle) ordering rotates ell/2 disjoint column pairs in parallel
+// -- one warp per pair, columns reached through DSMEM when they live in
+// another CTA -- followed by one cluster barrier.  One-sided Jacobi is
+// backward stable with high relative accuracy for the small singular values
+// (the property the Nystrom shift nu = eps ||Y||_F relies on).
+// It runs on X = R^T (Drmac-Veselic preconditioning: the rows of a triangular
+// factor are graded, cutting the sweep count about 2x versus R itself) and
+// accumulates the rotations V, which are then R's left singular vectors:
+// R^T V = U_X S  =>  R = V S U_X^T.
+#include <cooperative_groups.h>
+
+#include "ngd_common.cuh"
+#include "ngd_kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace ngd {
+
+// threads per CTA: keep the two register-resident columns (2 x RPL doubles) spill-free
+template <int RPL>
+constexpr int svd_threads() { return RPL <= 4 ? 1024 : (RPL <= 12 ? 512 : 256); }
+
+__device__ __forceinline__ void circle_pair(int n, int r, int k, int& a, int& b) {
+  const int m = n - 1;
+  if (k == 0) {
+    a = 0;
+    b = 1 + (r % m);
+  } else {
+    a = 1 + ((r + k) % m);
+    b = 1 + ((r - k + m) % m);
+  }
+}
+
+template <int CL>
+__device__ __forceinline__ void cluster_barrier() {
+  if constexpr (CL == 1) {
+    __syncthreads();
+  } else {
+    cg::this_cluster().sync();
+  }
+}
+
+template <int CL>
+__device__ __forceinline__ double* col_ptr(double* cols, int j, int m, int ldc) {
+  if constexpr (CL == 1) {
+    return cols + (int64_t)j * ldc;
+  } else {
+    return cg::this_cluster().map_shared_rank(cols, j / m) + (int64_t)(j % m) * ldc;
+  }
+}
+
+// A: ell x ell column-major (lda).  Outputs: sigma (descending), U (ell x ell, ldu),
+// info[0] = sweeps used (negative if not converged).
+template <int CL, int RPL>
+__global__ void __launch_bounds__(svd_threads<RPL>(), 1) jsvd_kernel(const double* A, int ell, int lda, double* U, int ldu,
+                                                              double* sigma, double tol, int max_sweeps, int* info) {
+  extern __shared__ __align__(16) double smem[];
+  const int n = (ell + 2 * CL - 1) / (2 * CL) * (2 * CL);  // even, multiple of CL
+  const int m = n / CL;                                     // columns per CTA
+  const int ldc = ell;
+  double* cols = smem;                           // [m][ldc]  X columns
+  double* vcols = cols + (int64_t)m * ldc;       // [m][ldc]  accumulated rotations
+  double* norms = vcols + (int64_t)m * ldc;      // [m]
+  int* flags = reinterpret_cast<int*>(norms + m);  // [2]
+  const int q = (CL == 1) ? 0 : (int)cg::this_cluster().block_rank();
+  constexpr int kSvdThreads = svd_threads<RPL>();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kSvdThreads / 32;
+
+  // X = R^T (column j of X = row j of R) and V = I, both [m][ldc] per CTA
+  for (int64_t e = tid; e < (int64_t)m * ldc; e += kSvdThreads) {
+    const int jl = (int)(e / ldc), r = (int)(e % ldc);
+    const int j = q * m + jl;
+    cols[e] = (j < ell) ? A[(int64_t)r * lda + j] : 0.0;
+    vcols[e] = (j == r) ? 1.0 : 0.0;
+  }
+  if (tid < 2) flags[tid] = 0;
+  cluster_barrier<CL>();
+
+  int sweep = 0;
+  bool converged = false;
+  for (; sweep < max_sweeps && !converged; ++sweep) {
+    const int par = sweep & 1;
+    for (int rd = 0; rd < n - 1; ++rd) {
+      // pairs k = q, q + CL, ... of this round; one warp per pair
+      for (int k = q + CL * warp; k < n / 2; k += CL * NW) {
+        int i, j;
+        circle_pair(n, rd, k, i, j);
+        double* ci = col_ptr<CL>(cols, i, m, ldc);
+        double* cj = col_ptr<CL>(cols, j, m, ldc);
+        double* vi = col_ptr<CL>(vcols, i, m, ldc);
+        double* vj = col_ptr<CL>(vcols, j, m, ldc);
+        // both columns into registers (all loads in flight at once: one DSMEM latency)
+        double x[RPL], y[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int r = lane + 32 * u;
+          x[u] = (r < ell) ? ci[r] : 0.0;
+          y[u] = (r < ell) ? cj[r] : 0.0;
+        }
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          al = fma(x[u], x[u], al);
+          be = fma(y[u], y[u], be);
+          ga = fma(x[u], y[u], ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          double t;
+          if (fabs(zeta) > 1e150) {
+            t = 0.5 / zeta;
+          } else {
+            t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          }
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) {
+            const int r = lane + 32 * u;
+            if (r < ell) {
+              ci[r] = c * x[u] - s * y[u];
+              cj[r] = s * x[u] + c * y[u];
+              const double pv = vi[r], qv = vj[r];
+              vi[r] = c * pv - s * qv;
+              vj[r] = s * pv + c * qv;
+            }
+          }
+          if (lane == 0) flags[par] = 1;
+        }
+      }
+      cluster_barrier<CL>();
+    }
+    // cluster-wide convergence test (flags double-buffered by sweep parity)
+    int any = 0;
+    if constexpr (CL == 1) {
+      any = flags[par];
+    } else {
+      for (int o = 0; o < CL; ++o) any |= cg::this_cluster().map_shared_rank(flags, o)[par];
+    }
+    converged = (any == 0);
+    if (tid == 0) flags[par ^ 1] = 0;
+    cluster_barrier<CL>();
+  }
+  // norms of own columns
+  for (int jl = warp; jl < m; jl += NW) {
+    const double* c = cols + (int64_t)jl * ldc;
+    double s = 0.0;
+    for (int r = lane; r < ell; r += 32) s = fma(c[r], c[r], s);
+    s = warp_sum(s);
+    if (lane == 0) norms[jl] = sqrt(s);
+  }
+  cluster_barrier<CL>();
+  // rank of each own column among all n (descending sigma, ties by index), write sigma and U
+  for (int jl = warp; jl < m; jl += NW) {
+    const int j = q * m + jl;
+    const double sj = norms[jl];
+    int rank = 0;
+    for (int o = lane; o < n; o += 32) {
+      const double so = (CL == 1) ? norms[o] : cg::this_cluster().map_shared_rank(norms, o / m)[o % m];
+      rank += (so > sj || (so == sj && o < j)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
+    if (rank < ell) {
+      if (lane == 0) sigma[rank] = sj;
+      const double* v = vcols + (int64_t)jl * ldc;
+      for (int r = lane; r < ell; r += 32) U[(int64_t)rank * ldu + r] = v[r];
+    }
+  }
+  if (q == 0 && tid == 0) info[0] = converged ? sweep : -sweep;
+  cluster_barrier<CL>();  // keep shared memory alive until every CTA has finished reading it
+}
+
+static size_t jsvd_smem(int ell, int cl) {
+  const int n = (ell + 2 * cl - 1) / (2 * cl) * (2 * cl);
+  const int m = n / cl;
+  return sizeof(double) * (2 * (size_t)m * ell + m) + 2 * sizeof(int) + 16;
+}
+
+int jsvd_cluster_size(int ell) {
+  for (int cl : {1, 2, 4, 8, 16})
+    if (jsvd_smem(ell, cl) <= 200 * 1024) return cl;
+  return 0;  // too large: caller falls back
+}
+
+template <int CL, int RPL>
+static cudaError_t launch_jsvd_r(const double* A, int ell, int lda, double* U, int ldu, double* sigma, double tol,
+                                 int max_sweeps, int* info, cudaStream_t st) {
+  const size_t smem = jsvd_smem(ell, CL);
+  auto kern = jsvd_kernel<CL, RPL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (CL > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL, 1, 1);
+  cfg.blockDim = dim3(svd_threads<RPL>(), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  probe_before(K_VEC, st);
+  e = cudaLaunchKernelEx(&cfg, kern, A, ell, lda, U, ldu, sigma, tol, max_sweeps, info);
+  probe_after(K_VEC, st);
+  return e;
+}
+
+template <int CL>
+static cudaError_t launch_jsvd(const double* A, int ell, int lda, double* U, int ldu, double* sigma, double tol,
+                               int max_sweeps, int* info, cudaStream_t st) {
+  const int rpl = (ell + 31) / 32;
+  if (rpl <= 4) return launch_jsvd_r<CL, 4>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+  if (rpl <= 8) return launch_jsvd_r<CL, 8>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+  if (rpl <= 12) return launch_jsvd_r<CL, 12>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+  if (rpl <= 16) return launch_jsvd_r<CL, 16>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+  if (rpl <= 24) return launch_jsvd_r<CL, 24>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
+                       cudaStream_t st) {
+  // rotate only when |a_i.a_j| > ell * eps * |a_i||a_j|: tighter thresholds only chase dot-product rounding noise
+  const double tol = 2.220446049250313e-16 * (double)ell;
+  const int max_sweeps = 40;
+  switch (jsvd_cluster_size(ell)) {
+    case 1: return launch_jsvd<1>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+    case 2: return launch_jsvd<2>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+    case 4: return launch_jsvd<4>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+    case 8: return launch_jsvd<8>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+    case 16: return launch_jsvd<16>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ngd

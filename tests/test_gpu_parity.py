@@ -37,7 +37,7 @@ def test_c1_loss_metric_grad_matvec(c1):
     assert gop.matvec_count == 9
 
 
-@pytest.mark.parametrize("svd", [1, 0])
+@pytest.mark.parametrize("svd", [2, 1, 0])
 def test_c1_nystrom_preconditioner_pcg(c1, svd):
     G, prob, quad, theta = c1
     from paper_2505_11638_b200 import _lib
@@ -56,7 +56,7 @@ def test_c1_nystrom_preconditioner_pcg(c1, svd):
         meta = G[f"pcg{k}_meta"]
         assert rel(rep.solution, G[f"pcg{k}_x"]) <= 1e-8, k
         assert (rep.iterations, rep.matvecs, rep.breakdown) == (int(meta[0]), int(meta[1]), bool(meta[4]))
-    _lib.set_option("svd", 1)
+    _lib.set_option("svd", 2)
 
 
 def test_c1_device_omega_sketch_statistics(c1):

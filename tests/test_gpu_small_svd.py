@@ -1,0 +1,45 @@
+"""The in-house cluster one-sided Jacobi SVD (ngd_svd.cu) against LAPACK (numpy) on
+graded matrices like the Nystrom factor's R (singular values spanning 1 .. 1e-8,
+with a tail cluster at the shift floor)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+from paper_2505_11638_b200 import _lib  # noqa: E402
+from paper_2505_11638_b200.gramian import utility_context  # noqa: E402
+
+
+def graded(n, seed):
+    rng = np.random.default_rng(seed)
+    s = np.concatenate([np.logspace(0, -8, n // 2), 1e-8 * (1 + 1e-3 * np.arange(n - n // 2))])
+    qa, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    qb, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (qa * s) @ qb.T
+    # even seeds: the triangular factor of a QR (the Nystrom case); odd: a dense matrix
+    return np.linalg.qr(a)[1] if seed % 2 == 0 else a
+
+
+@pytest.mark.parametrize("n", [7, 100, 101, 160, 300, 301, 400])
+def test_jacobi_svd_matches_lapack(n):
+    a = graded(n, n)
+    ctx = utility_context()
+    A = torch.as_tensor(np.asfortranarray(a).T.copy(), device="cuda")  # column-major storage
+    U = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    S = torch.empty(n, dtype=torch.float64, device="cuda")
+    sweeps = _lib.ctypes.c_int32()
+    ctx.call("ngd_small_svd", _lib.ptr(A), n, _lib.ptr(U), _lib.ptr(S), 2, _lib.ctypes.byref(sweeps))
+    assert sweeps.value > 0, "Jacobi did not converge"
+    print(f"n={n} sweeps={sweeps.value}")
+    s_ref = np.linalg.svd(a, compute_uv=False)
+    s = S.cpu().numpy()
+    # absolute accuracy eps * s1 (backward stability) and relative accuracy on the head
+    assert np.max(np.abs(s - s_ref)) <= 50 * n * 2.2e-16 * s_ref[0]
+    head = s_ref > 1e-6 * s_ref[0]
+    assert np.max(np.abs(s[head] - s_ref[head]) / s_ref[head]) <= 1e-10
+    u = U.cpu().numpy().T  # back to row-major (n, n): columns are left singular vectors
+    assert np.linalg.norm(u.T @ u - np.eye(n)) <= 1e-12 * n
+    # A = U diag(s) V^T  <=>  ||U^T A||_rows == s
+    np.testing.assert_allclose(np.linalg.norm(u.T @ a, axis=1), s, rtol=1e-8, atol=1e-13)

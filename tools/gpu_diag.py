@@ -82,5 +82,30 @@ def main():
             traceback.print_exc()
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--sweeps" not in sys.argv:
     main()
+
+
+def sweeps():
+    """Jacobi sweep counts of the real Nystrom factorisations at C1/C2."""
+    from paper_2505_11638_b200 import _lib
+    for widths, nint, nbnd, ell in (((2, 32, 32, 1), 900, 120, 100), ((2, 64, 64, 64, 1), 4096, 512, 300)):
+        top = ngd.MlpTopology(widths)
+        prob = ngd.Poisson2D(top)
+        quad = prob.sample_quadrature(nint, nbnd, 0)
+        gop = ngd.GramianOperator.from_problem(prob, ngd.init(top, 0).values, quad)
+        import time as _t
+        for src in ("host", "device"):
+            ngd.nystrom_approximate(gop, ell, seed=1, omega_source=src)
+            _lib.torch_mod().cuda.synchronize()
+            t0 = _t.perf_counter()
+            fac = ngd.nystrom_approximate(gop, ell, seed=2, omega_source=src)
+            dt = _t.perf_counter() - t0
+            out = _lib.ctypes.c_int64()
+            gop.ctx.call("ngd_get_stat", b"jacobi_sweeps", _lib.ctypes.byref(out))
+            print(f"ell={ell} {src}: jacobi sweeps {out.value}, nystrom {1e3 * dt:.2f} ms, "
+                  f"unclamped {(fac.eig_host > 0).sum()}")
+
+
+if __name__ == "__main__" and "--sweeps" in sys.argv:
+    sweeps()
