@@ -176,6 +176,7 @@ static int forward(ngd_ctx* c, bool store) {
     JetArgs a{};
     a.A = c->apf[l].d();
     a.Kp = c->Kp_f[l];
+    a.K = c->w[l];
     a.M = c->w[l + 1];
     a.s_pad = gm.s_pad;
     a.bias = nullptr;  // theta bias added through the packed bias vector below
@@ -264,6 +265,7 @@ static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double*
     JetArgs& a = pa.L[l];
     a.A = c->vp[l].d();
     a.Kp = c->Kp_f[l];
+    a.K = c->w[l];
     a.M = c->w[l + 1];
     a.B = c->zin[l].d();
     a.s_pad = gm.s_pad;
@@ -653,6 +655,7 @@ int ngd_linearize(ngd_ctx* c, const double* theta, double* h_loss, double* d_met
     JetArgs a{};
     a.A = c->apr[l].d();
     a.Kp = c->Kp_r[l];
+    a.K = c->w[l + 2];
     a.M = c->w[l + 1];
     a.B = (l + 1 == c->NL - 1) ? c->dseed.d() : c->dbuf[l + 1].d();
     a.s_pad = gm.s_pad;

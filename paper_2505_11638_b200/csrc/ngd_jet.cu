@@ -116,6 +116,9 @@ __device__ __forceinline__ void jet_tile(const JetArgs& p, const int bx, const i
     for (int c = 0; c < C; ++c) acc[mi][c][0] = acc[mi][c][1] = 0.0;
 
   const int ktiles = p.Kp / BK;
+  // skip MMA work on all-padding rows (output layer: M = 1) and all-padding k-steps (input layer: K = d)
+  const bool m_active = (m0 + wm * 16) < p.M;
+  const int kvalid = p.K > 0 ? p.K : p.Kp;
   load_stage(0, 0);
   for (int kt = 0; kt < ktiles; ++kt) {
     if (kt + 1 < ktiles) {
@@ -129,6 +132,7 @@ __device__ __forceinline__ void jet_tile(const JetArgs& p, const int bx, const i
     const double* bs = Bs + (kt & 1) * BK * BSTR + t * BSTR + wn * 8 + g;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
+      if (!m_active || kt * BK + kk >= kvalid) break;
       const double a0 = as[kk];
       const double a1 = as[8 * ASTR + kk];
 #pragma unroll
@@ -358,7 +362,9 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
   const int wm = warp & 3, wn = warp >> 2;
   const int n0 = bx * PBN, m0 = by * PBM;
   const bool do_bias = (bx == 0);
-  if (tid < PBM) bias_acc[tid] = 0.0;
+  // warps whose 16 x 32 sub-tile is all padding (output layer M = 1, input layer N = d) skip the MMAs
+  const bool w_active = (m0 + wm * 16) < p.M && (n0 + wn * 32) < p.N;
+  double bsum = 0.0;  // bias partial: row tid >> 2, k-quarter tid & 3
 
   auto load_stage = [&](int stage, int kt) {
     const int64_t j0 = (int64_t)kt * BK;
@@ -413,6 +419,7 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
     const double* cs = ccs + st * BK;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
+      if (!w_active) break;
       const double cc = cs[kk + t];
       const double a0 = as[(wm * 16 + g) * PSTR + kk + t] * cc;
       const double a1 = as[(wm * 16 + 8 + g) * PSTR + kk + t] * cc;
@@ -423,14 +430,17 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
         dmma884(acc[1][j][0], acc[1][j][1], a1, b);
       }
     }
-    if (do_bias && tid < PBM) {
+    if (do_bias) {
       const double* cv = ccv + st * BK;
-      double sb = bias_acc[tid];
+      const int br = tid >> 2, bq = (tid & 3) * 4;
 #pragma unroll
-      for (int kk = 0; kk < BK; ++kk) sb = fma(as[tid * PSTR + kk], cv[kk], sb);
-      bias_acc[tid] = sb;
+      for (int u = 0; u < 4; ++u) bsum = fma(as[br * PSTR + bq + u], cv[bq + u], bsum);
     }
   }
+  // combine the 4 k-quarters of each bias row (fixed order)
+  bsum += __shfl_xor_sync(0xffffffffu, bsum, 1);
+  bsum += __shfl_xor_sync(0xffffffffu, bsum, 2);
+  if (do_bias && (tid & 3) == 0) bias_acc[tid >> 2] = bsum;
   cp_async_wait<0>();
   __syncthreads();
   // ---- split-K reduction inside the thread-block cluster (DSMEM) ----------
@@ -447,6 +457,7 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) red[(wm * 16 + i * 8 + g) * RSTR + wn * 32 + j * 8 + 2 * t + e] = acc[i][j][e];
+  __syncthreads();
   if (tid < PBM) red_bias[tid] = do_bias ? bias_acc[tid] : 0.0;
   cg::cluster_group cl = cg::this_cluster();
   cl.sync();

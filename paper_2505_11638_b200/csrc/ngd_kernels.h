@@ -31,6 +31,7 @@ enum JetMode { FWD = 0, REV = 1, PHA = 2 };
 struct JetArgs {
   const double* A;     // packed operand, row-major [Mp][Kp] (zero padded)
   int Kp;              // padded K (multiple of 16)
+  int K;               // real K (0 = use Kp); k-steps beyond K are skipped
   int M;               // real rows
   const double* B;     // [Kp rows][s_pad], zero rows beyond K
   int64_t s_pad;
