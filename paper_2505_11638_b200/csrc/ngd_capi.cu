@@ -120,6 +120,7 @@ struct ngd_ctx {
   bool have_points = false;
   Geom gm{};
   int G = 1, kps = 1;  // phase-B splits (G = max over layers)
+  int phb_cluster = 1;
   int Gl[kMaxLayers] = {0}, kpsl[kMaxLayers] = {0};
   RedPlan rplan{};
   Buf w_pad, off_pad, w_c, F, cot_grad, cot, metric_tmp;
@@ -315,6 +316,7 @@ static void fill_phb(ngd_ctx* c, const double* cot, const int* skip, PhbAll& pb)
     tiles += pb.tiles_n[l] * pb.tiles_m[l] * c->Gl[l];
   }
   pb.tile_start[c->NL] = tiles;
+  pb.cluster = c->phb_cluster;
 }
 
 // out = J^T cot (+ mu v), all-reduced over ranks
@@ -598,29 +600,36 @@ int ngd_set_points(ngd_ctx* c, int64_t n_int, const double* x_int, const double*
   CK(cudaGetLastError());
   // phase-A partial rows and phase-B split plan
   CK(c->partA.ensure(sizeof(double) * (size_t)c->rows_A * npp));
-  // phase-B split plan: every (layer, tile) gets the same number of K splits (a tile costs the
-  // same per k-tile whatever its fill), so one launch puts ~3 CTAs on every SM; >= 8 k-tiles each.
+  // phase-B split plan: every (layer, tile) gets the same number G of K splits (a tile costs the
+  // same per k-tile whatever its fill).  G is the largest that keeps the whole launch in ONE
+  // wave of 3 CTAs/SM (no tail wave); when G >= 16 the splits are grouped into clusters of 8
+  // whose partial tiles are reduced through DSMEM (G/8 partials per parameter).
   {
     const int kt = (int)(gm.s_pad / 16);
     int tiles = 0;
     for (int l = 0; l < c->NL; ++l) tiles += ((c->w[l] + 63) / 64) * ((c->w[l + 1] + 63) / 64);
-    int G = std::max(1, (int)std::lround(3.0 * 148 / tiles));
+    const int slots = 3 * 148;
+    int G = std::max(1, slots / tiles);
     G = std::min(G, std::max(1, kt / 8));
+    int CS = 1;
+    if (G >= 16) {
+      G = G / 8 * 8;
+      CS = 8;
+    }
     const int kps = (kt + G - 1) / G;
-    G = (kt + kps - 1) / kps;
-    G = (G + kPhbCluster - 1) / kPhbCluster * kPhbCluster;  // whole clusters (trailing splits may be empty)
     c->G = G;
     c->kps = kps;
+    c->phb_cluster = CS;
     c->rplan.n_layers = c->NL;
     for (int l = 0; l < c->NL; ++l) {
       c->Gl[l] = G;
       c->kpsl[l] = kps;
       c->rplan.start[l] = c->woff[l];
-      c->rplan.G[l] = G / kPhbCluster;  // one partial per cluster
+      c->rplan.G[l] = G / CS;  // one partial per cluster
     }
     c->rplan.start[c->NL] = c->p;
   }
-  CK(c->partB.ensure(sizeof(double) * (size_t)(c->G / kPhbCluster) * c->p));
+  CK(c->partB.ensure(sizeof(double) * (size_t)(c->G / c->phb_cluster) * c->p));
   c->have_points = true;
   c->lin_valid = false;
   c->graph_gen++;
@@ -710,9 +719,11 @@ int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, doubl
   TRY(need_lin(c));
   if (ell < 1 || ldv < c->p || ldy < c->p) return fail(NGD_E_SHAPE, "bad matmat shape");
   const Geom& gm = c->gm;
-  const int nq = gm.n_int + gm.n_bnd;
+  // chunks of whole point blocks in padded point order (padded points have w = 0)
+  const int nblk_total = gm.nib + gm.nbb;
   const size_t budget = (size_t)8 << 30;  // bytes for one Jacobian chunk
-  int64_t R = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(budget / (sizeof(double) * c->p))));
+  const int bpc = (int)std::max<int64_t>(1, std::min<int64_t>(nblk_total, (int64_t)(budget / (sizeof(double) * c->p * PB))));
+  const int64_t R = (int64_t)bpc * PB;
   CK(c->jt.ensure(sizeof(double) * (size_t)R * c->p));
   CK(c->smat.ensure(sizeof(double) * (size_t)R * ell));
   // device tables for FormJ
@@ -748,14 +759,21 @@ int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, doubl
   fa.Jt = c->jt.d();
   fa.ldj = c->p;
   const double one = 1.0, zero = 0.0;
-  for (int64_t q0 = 0; q0 < nq; q0 += R) {
-    const int64_t r = std::min<int64_t>(R, nq - q0);
-    fa.q0 = (int)q0;
-    CK(form_j(fa, (int)r, NL, c->stream));
+  int max_nin = 1, max_nout = 1;
+  for (int l = 0; l < NL; ++l) {
+    max_nin = std::max(max_nin, c->w[l]);
+    max_nout = std::max(max_nout, c->w[l + 1]);
+  }
+  for (int b0 = 0; b0 < nblk_total; b0 += bpc) {
+    const int nb = std::min(bpc, nblk_total - b0);
+    const int64_t r = (int64_t)nb * PB;
+    const int64_t q0 = (int64_t)b0 * PB;
+    fa.blk0 = b0;
+    CK(form_j(fa, nb, NL, max_nin, max_nout, c->stream));
     // S (r x ell) = Jt_chunk (r x p) * V  -> col-major: S = Jt^T(p x r)^T V
     CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)r, (int)ell, (int)c->p, &one, c->jt.d(), (int)c->p, V,
                     (int)ldv, &zero, c->smat.d(), (int)r));
-    scale_rows(c->smat.d(), r, (int)ell, c->w_c.d() + q0, c->stream);
+    scale_rows(c->smat.d(), r, (int)ell, c->w_pad.d() + q0, c->stream);
     const double beta = (q0 == 0) ? 0.0 : 1.0;
     CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)c->p, (int)ell, (int)r, &one, c->jt.d(), (int)c->p,
                     c->smat.d(), (int)r, &beta, Y, (int)ldy));

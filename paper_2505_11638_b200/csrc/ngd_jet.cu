@@ -344,7 +344,7 @@ __device__ __forceinline__ bool is_value_col(int64_t j64, int64_t int_cols, int 
   return j64 >= int_cols || (((int)j64 % (PB * C)) < PB);
 }
 
-constexpr int PNST = 4;  // cp.async pipeline depth of phase B
+constexpr int PNST = 3;  // cp.async pipeline depth of phase B (3 CTAs / SM)
 static_assert(PBM * (PBN + 1) + PBM <= 2 * PNST * PBM * PSTR, "cluster reduction staging must fit");
 constexpr size_t kPhbSmem = sizeof(double) * (2 * PNST * PBM * PSTR + 2 * PNST * BK + PBM);
 
@@ -444,10 +444,10 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
   cp_async_wait<0>();
   __syncthreads();
   // ---- split-K reduction inside the thread-block cluster (DSMEM) ----------
-  // The kPhbCluster CTAs of a cluster are consecutive K splits of the same output
+  // The CS (runtime cluster size) CTAs of a cluster are consecutive K splits of the same output
   // tile: each stages its 64x64 partial in shared memory, then CTA `rank` sums
   // rows [8 rank, 8 rank + 8) over all ranks in rank order and writes one partial
-  // per cluster (deterministic, kPhbCluster x less partial traffic).
+  // per cluster (deterministic, CS x less partial traffic).
   constexpr int RSTR = PBN + 1;
   double* red = smem;                 // [PBM][RSTR]
   double* red_bias = red + PBM * RSTR;  // [PBM]
@@ -460,31 +460,30 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
   __syncthreads();
   if (tid < PBM) red_bias[tid] = do_bias ? bias_acc[tid] : 0.0;
   cg::cluster_group cl = cg::this_cluster();
-  cl.sync();
-  const int rank = (int)cl.block_rank();
-  double* out = p.part + (int64_t)(split / kPhbCluster) * p.p + p.off;
-  constexpr int ROWS = PBM / kPhbCluster;
+  const int CS = (int)cl.num_blocks();  // runtime cluster size (1, 2, 4 or 8)
+  if (CS > 1) cl.sync(); else __syncthreads();
+  const int rank = CS > 1 ? (int)cl.block_rank() : 0;
+  double* out = p.part + (int64_t)(split / CS) * p.p + p.off;
+  const int ROWS = PBM / CS;
   for (int e = tid; e < ROWS * PBN; e += kThreads) {
     const int r = rank * ROWS + e / PBN, col = e % PBN;
     if (m0 + r < p.M && n0 + col < p.N) {
       double sum = 0.0;
-#pragma unroll
-      for (int q = 0; q < kPhbCluster; ++q) sum += cl.map_shared_rank(red, q)[r * RSTR + col];
+      for (int q = 0; q < CS; ++q) sum += (CS > 1 ? cl.map_shared_rank(red, q) : red)[r * RSTR + col];
       out[(int64_t)(m0 + r) * p.N + n0 + col] = sum;
     }
   }
   if (do_bias && rank == 0 && tid < PBM && m0 + tid < p.M) {
     double sum = 0.0;
-#pragma unroll
-    for (int q = 0; q < kPhbCluster; ++q) sum += cl.map_shared_rank(red_bias, q)[tid];
+    for (int q = 0; q < CS; ++q) sum += (CS > 1 ? cl.map_shared_rank(red_bias, q) : red_bias)[tid];
     out[(int64_t)p.M * p.N + m0 + tid] = sum;
   }
-  cl.sync();  // keep this CTA's shared memory alive until the cluster has read it
+  if (CS > 1) cl.sync();  // keep this CTA's shared memory alive until the cluster has read it
 }
 
 // Phase B over ALL layers in one launch: blockIdx.x enumerates (layer, split, m-tile, n-tile)
 // with a per-layer split count proportional to the layer's work.
-__global__ void __cluster_dims__(kPhbCluster, 1, 1) __launch_bounds__(kThreads) phb_all_kernel(PhbAll a) {
+__global__ void __launch_bounds__(kThreads) phb_all_kernel(PhbAll a) {
   const int t = blockIdx.x;
   int l = 0;
   while (l + 1 < a.n_layers && t >= a.tile_start[l + 1]) ++l;
@@ -504,57 +503,98 @@ cudaError_t phase_b_all_layers(const PhbAll& a, int splits, cudaStream_t st) {
   }
   const int tiles = a.tile_start[a.n_layers];
   if (tiles <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = kPhbSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   probe_before(K_PHB, st);
-  phb_all_kernel<<<tiles, kThreads, kPhbSmem, st>>>(a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, phb_all_kernel, a);
   probe_after(K_PHB, st);
   (void)splits;
-  return cudaGetLastError();
+  return e;
 }
 
 
 // ---------------------------------------------------------------------------
 // Explicit Jacobian rows for the sketch (J-chunk formulation):
-//   Jt[q][off_k + a*n_in + b] = sum_c D_k[a][(r,c)] Zin_k[b][(r,c)],  Jt[q][off_bk + a] = D_k[a][(r,0)]
-// One CTA per (point, layer); threads stride over b, loop over a.  Write-bound.
-// ---------------------------------------------------------------------------
+//   Jt[pt][off_l + a*n_in + b] = sum_c D_l[a][(pt,c)] Zin_l[b][(pt,c)],  Jt[pt][off_bl + a] = D_l[a][(pt,0)]
+// One CTA per (point block of 16, layer, 32-row a-tile, 64-col b-tile): the D and Zin
+// slices of the block are staged in shared memory with coalesced 128-B reads, every
+// staged value is reused 16-64x, and the Jacobian rows are written coalesced along b.
+// Write-bound: 8 * p bytes per point.
+constexpr int FJ_A = 32, FJ_B = 64;
 
 __global__ void __launch_bounds__(kThreads) formj_kernel(FormJArgs a) {
-  const int q = a.q0 + blockIdx.x;
-  const int k = blockIdx.y;
-  const int nin = a.n_in[k], nout = a.n_out[k];
-  const double* Z = a.Z[k];
-  const double* D = a.D[k];
-  double* row = a.Jt + (int64_t)blockIdx.x * a.ldj + a.off[k];
-  int64_t col0;
-  int nch;
-  if (q < a.n_int) {
-    col0 = col_int(q, 0, a.C);
-    nch = a.C;
-  } else {
-    col0 = a.int_cols + (q - a.n_int);
-    nch = 1;
+  extern __shared__ __align__(16) double sm[];
+  const int l = blockIdx.y;
+  const int nin = a.n_in[l], nout = a.n_out[l];
+  const int tiles_b = (nin + FJ_B - 1) / FJ_B;
+  const int a0 = (blockIdx.z / tiles_b) * FJ_A, b0 = (blockIdx.z % tiles_b) * FJ_B;
+  if (a0 >= nout) return;
+  const int blk = a.blk0 + blockIdx.x;  // global point block
+  const bool interior = blk < a.nib;
+  const int Cs = interior ? a.C : 1;
+  const int ncols = PB * Cs;
+  const int stride = ncols + 1;  // odd -> conflict-free column reads
+  const int64_t cbase = interior ? (int64_t)blk * PB * a.C : a.int_cols + (int64_t)(blk - a.nib) * PB;
+  double* Zs = sm;                      // [FJ_B][stride]
+  double* Ds = sm + FJ_B * stride;      // [FJ_A][stride]
+  const double* Z = a.Z[l];
+  const double* D = a.D[l];
+  const int nb = min(FJ_B, nin - b0), na = min(FJ_A, nout - a0);
+  for (int e = threadIdx.x; e < nb * ncols; e += blockDim.x) {
+    const int r = e / ncols, cc = e % ncols;
+    Zs[r * stride + cc] = Z[(int64_t)(b0 + r) * a.s_pad + cbase + cc];
   }
-  for (int b = threadIdx.x; b < nin; b += blockDim.x) {
-    double z[12];
+  for (int e = threadIdx.x; e < na * ncols; e += blockDim.x) {
+    const int r = e / ncols, cc = e % ncols;
+    Ds[r * stride + cc] = D[(int64_t)(a0 + r) * a.s_pad + cbase + cc];
+  }
+  __syncthreads();
+  const int bi = threadIdx.x % FJ_B, ar = threadIdx.x / FJ_B;  // 4 a-rows in flight
+  const int64_t prow0 = (int64_t)blockIdx.x * PB;                // chunk-local padded point row
+  const int64_t off = a.off[l];
+  for (int r = 0; r < PB; ++r) {
+    double* row = a.Jt + (prow0 + r) * a.ldj;
+    if (bi < nb) {
+      double z[12];
 #pragma unroll
-    for (int c = 0; c < 12; ++c) z[c] = (c < nch) ? Z[(int64_t)b * a.s_pad + col0 + c * PB] : 0.0;
-    for (int o = 0; o < nout; ++o) {
-      const double* drow = D + (int64_t)o * a.s_pad + col0;
-      double s = 0.0;
+      for (int c = 0; c < 12; ++c) z[c] = (c < Cs) ? Zs[bi * stride + c * PB + r] : 0.0;
+      for (int ai = ar; ai < na; ai += kThreads / FJ_B) {
+        const double* dr = Ds + ai * stride + r;
+        double s = 0.0;
 #pragma unroll
-      for (int c = 0; c < 12; ++c)
-        if (c < nch) s = fma(drow[c * PB], z[c], s);
-      row[(int64_t)o * nin + b] = s;
+        for (int c = 0; c < 12; ++c)
+          if (c < Cs) s = fma(dr[c * PB], z[c], s);
+        row[off + (int64_t)(a0 + ai) * nin + b0 + bi] = s;
+      }
     }
+    if (b0 == 0)  // bias entries: value channel of D
+      for (int ai = threadIdx.x; ai < na; ai += blockDim.x) row[off + (int64_t)nout * nin + a0 + ai] = Ds[ai * stride + r];
   }
-  for (int o = threadIdx.x; o < nout; o += blockDim.x)
-    row[(int64_t)nout * nin + o] = D[(int64_t)o * a.s_pad + col0];
 }
 
-cudaError_t form_j(const FormJArgs& a, int R, int n_layers, cudaStream_t st) {
-  if (R <= 0) return cudaSuccess;
+size_t formj_smem(int C) { return sizeof(double) * (FJ_B + FJ_A) * (PB * C + 1); }
+
+cudaError_t form_j(const FormJArgs& a, int nblocks, int n_layers, int max_nin, int max_nout, cudaStream_t st) {
+  if (nblocks <= 0) return cudaSuccess;
+  const size_t smem = formj_smem(a.C);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(formj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  const int tz = ((max_nout + FJ_A - 1) / FJ_A) * ((max_nin + FJ_B - 1) / FJ_B);
   probe_before(K_FORMJ, st);
-  formj_kernel<<<dim3(R, n_layers), kThreads, 0, st>>>(a);
+  formj_kernel<<<dim3(nblocks, n_layers, tz), kThreads, smem, st>>>(a);
   probe_after(K_FORMJ, st);
   return cudaGetLastError();
 }

@@ -72,13 +72,12 @@ struct FormJArgs {
   const int64_t* off;       // W_k offset in the parameter vector
   int64_t s_pad, int_cols;
   int C, nib, n_int;
-  int q0;                   // first real point of this chunk (interior first, then boundary)
-  double* Jt;               // [R][ldj]
+  int blk0;                 // first point block of this chunk (padded point order)
+  double* Jt;               // [16 * blocks][ldj], row = padded point within the chunk
   int64_t ldj;
 };
 
 constexpr int kMaxLayers = 8;
-constexpr int kPhbCluster = 8;  // phase-B split-K CTAs reduced through DSMEM
 struct PhaAll {
   JetArgs L[kMaxLayers];      // per layer, interior segment settings
   int tile_start[kMaxLayers + 1];
@@ -91,6 +90,7 @@ struct PhbAll {
   int tile_start[kMaxLayers + 1];  // flat CTA offsets: layer l owns tiles_m*tiles_n*G_l CTAs
   int tiles_n[kMaxLayers], tiles_m[kMaxLayers], G[kMaxLayers];
   int n_layers;
+  int cluster;  // split-K CTAs reduced per cluster through DSMEM (divides G)
 };
 // fixed-order reduction plan of the phase-B partials: param range of layer l uses G[l] splits
 struct RedPlan {
@@ -110,7 +110,7 @@ cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles,
 cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st);
 cudaError_t phase_b_all_layers(const PhbAll& a, int splits, cudaStream_t st);
 void pack_all(const PackAll& a, const double* src, const int* skip, cudaStream_t st);
-cudaError_t form_j(const FormJArgs& a, int R, int n_layers, cudaStream_t st);
+cudaError_t form_j(const FormJArgs& a, int nblocks, int n_layers, int max_nin, int max_nout, cudaStream_t st);
 
 void pack(double* dst, int Mp, int Kp, const double* src, int64_t off, int n_out, int n_in, int trans,
           const int* skip, cudaStream_t st);

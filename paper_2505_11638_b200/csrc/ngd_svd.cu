@@ -26,7 +26,7 @@ namespace ngd {
 
 // threads per CTA: keep the two register-resident columns (2 x RPL doubles) spill-free
 template <int RPL>
-constexpr int svd_threads() { return RPL <= 4 ? 1024 : (RPL <= 12 ? 512 : 256); }
+constexpr int svd_threads() { return RPL <= 4 ? 1024 : (RPL <= 8 ? 512 : 256); }
 
 __device__ __forceinline__ void circle_pair(int n, int r, int k, int& a, int& b) {
   const int m = n - 1;
@@ -98,13 +98,17 @@ __global__ void __launch_bounds__(svd_threads<RPL>(), 1) jsvd_kernel(const doubl
         double* cj = col_ptr<CL>(cols, j, m, ldc);
         double* vi = col_ptr<CL>(vcols, i, m, ldc);
         double* vj = col_ptr<CL>(vcols, j, m, ldc);
-        // both columns into registers (all loads in flight at once: one DSMEM latency)
-        double x[RPL], y[RPL];
+        // both columns and their rotation-accumulator columns into registers up front
+        // (all loads in flight at once: one (D)SMEM latency per pair)
+        double x[RPL], y[RPL], pv[RPL], qv[RPL];
 #pragma unroll
         for (int u = 0; u < RPL; ++u) {
           const int r = lane + 32 * u;
-          x[u] = (r < ell) ? ci[r] : 0.0;
-          y[u] = (r < ell) ? cj[r] : 0.0;
+          const bool in = r < ell;
+          x[u] = in ? ci[r] : 0.0;
+          y[u] = in ? cj[r] : 0.0;
+          pv[u] = in ? vi[r] : 0.0;
+          qv[u] = in ? vj[r] : 0.0;
         }
         double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
@@ -116,24 +120,20 @@ __global__ void __launch_bounds__(svd_threads<RPL>(), 1) jsvd_kernel(const doubl
         al = warp_sum(al);
         be = warp_sum(be);
         ga = warp_sum(ga);
-        if (ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+        // rotate iff |ga| > tol sqrt(al be)  (squared form: no square roots on the test)
+        if (ga != 0.0 && ga * ga > tol * tol * al * be) {
           const double zeta = (be - al) / (2.0 * ga);
-          double t;
-          if (fabs(zeta) > 1e150) {
-            t = 0.5 / zeta;
-          } else {
-            t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          }
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          const double az = fabs(zeta);
+          const double t = (az > 1e150) ? 0.5 / zeta : copysign(1.0 / (az + sqrt(fma(az, az, 1.0))), zeta);
+          const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
 #pragma unroll
           for (int u = 0; u < RPL; ++u) {
             const int r = lane + 32 * u;
             if (r < ell) {
               ci[r] = c * x[u] - s * y[u];
               cj[r] = s * x[u] + c * y[u];
-              const double pv = vi[r], qv = vj[r];
-              vi[r] = c * pv - s * qv;
-              vj[r] = s * pv + c * qv;
+              vi[r] = c * pv[u] - s * qv[u];
+              vj[r] = s * pv[u] + c * qv[u];
             }
           }
           if (lane == 0) flags[par] = 1;
