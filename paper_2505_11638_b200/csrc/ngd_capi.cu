@@ -804,19 +804,18 @@ int ngd_nystrom_prepare(ngd_ctx* c, double* omega, int64_t p, int32_t ell) {
   CKS(cusolverDnDpotrf_bufferSize(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, &lwork));
   CK(c->nys_work.ensure(sizeof(double) * std::max(lwork, 1)));
   const double one = 1.0, zero = 0.0;
-  for (int pass = 0; pass < 2; ++pass) {
+  // A Gaussian p x ell block with p >= 4 ell has cond <= ~(sqrt(p)+sqrt(ell))/(sqrt(p)-sqrt(ell)) < 3, so
+  // one Cholesky-QR pass is already orthonormal to O(eps cond^2); squarer blocks get a second pass.
+  const int passes = (p >= 4 * (int64_t)ell) ? 1 : 2;
+  for (int pass = 0; pass < passes; ++pass) {
     CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, omega, (int)p, &zero,
                     c->nys_m.d(), ell));
     CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, c->nys_work.d(), lwork,
-                         static_cast<int*>(c->nys_info.p)));
+                         static_cast<int*>(c->nys_info.p) + 1));
     CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p,
                     ell, &one, c->nys_m.d(), ell, omega, (int)p));
   }
-  int info = 0;
-  CK(cudaMemcpyAsync(&c->h_pin[8], c->nys_info.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  memcpy(&info, &c->h_pin[8], sizeof(int));
-  if (info != 0) return fail(NGD_E_CHOL, "test matrix is numerically rank deficient (potrf info %d)", info);
+  // the potrf status is checked (no extra host sync) together with the sketch Cholesky in ngd_nystrom_finish
   return NGD_OK;
 }
 
@@ -851,11 +850,9 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
   CK(c->nys_work.ensure(sizeof(double) * std::max(lw, 1)));
   int* info = static_cast<int*>(c->nys_info.p);
   CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, c->nys_work.d(), lw_potrf, info));
-  CK(cudaMemcpyAsync(&c->h_pin[8], info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  int hinfo = 0;
-  memcpy(&hinfo, &c->h_pin[8], sizeof(int));
-  if (hinfo != 0) return fail(NGD_E_CHOL, "sketch Cholesky failed (potrf info %d)", hinfo);
+  // status of this Cholesky (and of Omega's Cholesky-QR) is read back with the results below: one host
+  // sync per sketch; on failure the (discarded) remaining work runs on garbage and NGD_E_CHOL is returned
+  CK(cudaMemcpyAsync(&c->h_pin[8], info, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   // 3. B = Y_nu C^{-1}
   CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p, ell,
                   &one, c->nys_m.d(), ell, Y, (int)p));
@@ -874,11 +871,11 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
     // 4. B = Q R by shifted Cholesky-QR3 (GEMM/SYRK + potrf + TRSM; stable for cond(B) up to 1/eps)
     TRY(scholqr3(c, Y, p, ell));
     // 5. R = U_R diag(s) V^T, descending: cluster one-sided Jacobi (method 2) or polar SVD
-    // element-wise DSMEM rotations are latency-bound beyond one CTA: use the cluster Jacobi
-    // only when the factor fits one CTA's shared memory (ell <~ 110), else the polar SVD
-    if (c->svd_method == 2 && jsvd_cluster_size(ell) == 1) {
-      CK(jacobi_svd(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(), static_cast<int*>(c->nys_info.p) + 2,
-                    c->stream));
+    // in-house block-exchange cluster Jacobi (all rotations in local shared memory) where the
+    // factor fits a cluster (ell <~ 310); cuSOLVER's polar SVD above
+    if (c->svd_method == 2 && jsvd_block_supported(ell) > 0) {
+      CK(jacobi_svd_block(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(),
+                          static_cast<int*>(c->nys_info.p) + 2, c->stream));
     } else {
       TRY(small_svd_polar(c, ell));
     }
@@ -891,6 +888,12 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
   CK(cudaMemcpyAsync(&c->h_pin[60], static_cast<int*>(c->nys_info.p) + 2, sizeof(int), cudaMemcpyDeviceToHost,
                      c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  {
+    int hinfo[2] = {0, 0};
+    memcpy(hinfo, &c->h_pin[8], 2 * sizeof(int));
+    if (hinfo[1] != 0) return fail(NGD_E_CHOL, "test matrix is numerically rank deficient (potrf info %d)", hinfo[1]);
+    if (hinfo[0] != 0) return fail(NGD_E_CHOL, "sketch Cholesky failed (potrf info %d)", hinfo[0]);
+  }
   if (h_shift) *h_shift = c->h_pin[0];
   {
     int sw = 0;
@@ -1109,10 +1112,17 @@ int ngd_small_svd(ngd_ctx* c, const double* A, int32_t ell, double* U, double* s
   CK(c->nys_info.ensure(sizeof(int) * 4));
   CK(cudaMemcpyAsync(c->nys_r.d(), A, sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
   int sweeps = 0;
-  if (method == 2) {
-    if (jsvd_cluster_size(ell) == 0) return fail(NGD_E_SHAPE, "ell = %d too large for the cluster Jacobi SVD", ell);
-    CK(jacobi_svd(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(), static_cast<int*>(c->nys_info.p) + 2,
-                  c->stream));
+  if (method == 2 || method == 3) {
+    if (method == 2 && jsvd_cluster_size(ell) == 0)
+      return fail(NGD_E_SHAPE, "ell = %d too large for the cluster Jacobi SVD", ell);
+    if (method == 3 && jsvd_block_supported(ell) == 0)
+      return fail(NGD_E_SHAPE, "ell = %d too large for the block-exchange Jacobi SVD", ell);
+    if (method == 2)
+      CK(jacobi_svd(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(), static_cast<int*>(c->nys_info.p) + 2,
+                    c->stream));
+    else
+      CK(jacobi_svd_block(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(),
+                          static_cast<int*>(c->nys_info.p) + 2, c->stream));
     CK(cudaMemcpyAsync(&c->h_pin[56], static_cast<int*>(c->nys_info.p) + 2, sizeof(int), cudaMemcpyDeviceToHost,
                        c->stream));
   } else {
@@ -1121,7 +1131,7 @@ int ngd_small_svd(ngd_ctx* c, const double* A, int32_t ell, double* U, double* s
   CK(cudaMemcpyAsync(U, c->nys_ur.d(), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaMemcpyAsync(sigma, c->nys_s.d(), sizeof(double) * ell, cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  if (method == 2) memcpy(&sweeps, &c->h_pin[56], sizeof(int));
+  if (method >= 2) memcpy(&sweeps, &c->h_pin[56], sizeof(int));
   if (h_sweeps) *h_sweeps = sweeps;
   return NGD_OK;
 }

@@ -152,6 +152,9 @@ void fill_gaussian(double* out, int64_t n, uint64_t seed, cudaStream_t st);
 int jsvd_cluster_size(int ell);
 cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
                        cudaStream_t st);
+int jsvd_block_supported(int ell);
+cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
+                             cudaStream_t st);
 void gather_points(const double* padded, double* compact, Geom gm, cudaStream_t st);
 void scatter_points(const double* compact, double* padded, Geom gm, cudaStream_t st);
 

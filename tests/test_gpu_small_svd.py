@@ -22,15 +22,16 @@ def graded(n, seed):
     return np.linalg.qr(a)[1] if seed % 2 == 0 else a
 
 
-@pytest.mark.parametrize("n", [7, 100, 101, 160, 300, 301, 400])
-def test_jacobi_svd_matches_lapack(n):
+@pytest.mark.parametrize("method,n", [(2, 7), (2, 100), (2, 101), (2, 160), (2, 300), (2, 301), (2, 400),
+                                      (3, 7), (3, 100), (3, 101), (3, 160), (3, 300), (3, 301), (3, 310)])
+def test_jacobi_svd_matches_lapack(method, n):
     a = graded(n, n)
     ctx = utility_context()
     A = torch.as_tensor(np.asfortranarray(a).T.copy(), device="cuda")  # column-major storage
     U = torch.empty((n, n), dtype=torch.float64, device="cuda")
     S = torch.empty(n, dtype=torch.float64, device="cuda")
     sweeps = _lib.ctypes.c_int32()
-    ctx.call("ngd_small_svd", _lib.ptr(A), n, _lib.ptr(U), _lib.ptr(S), 2, _lib.ctypes.byref(sweeps))
+    ctx.call("ngd_small_svd", _lib.ptr(A), n, _lib.ptr(U), _lib.ptr(S), method, _lib.ctypes.byref(sweeps))
     assert sweeps.value > 0, "Jacobi did not converge"
     print(f"n={n} sweeps={sweeps.value}")
     s_ref = np.linalg.svd(a, compute_uv=False)

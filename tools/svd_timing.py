@@ -15,7 +15,7 @@ for n in (100, 160, 300, 400):
     r = np.linalg.qr((qa * s) @ qb.T)[1]
     A = torch.as_tensor(r.T.copy(), device="cuda")
     U = torch.empty((n, n), dtype=torch.float64, device="cuda"); S = torch.empty(n, dtype=torch.float64, device="cuda")
-    for method in (2, 1):
+    for method in (3, 2, 1):
         sw = _lib.ctypes.c_int32()
         try:
             ctx.call("ngd_small_svd", _lib.ptr(A), n, _lib.ptr(U), _lib.ptr(S), method, _lib.ctypes.byref(sw))
