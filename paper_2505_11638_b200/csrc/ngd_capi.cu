@@ -140,6 +140,8 @@ struct ngd_ctx {
   cusolverDnParams_t dn_params = nullptr;
   std::vector<char> h_work;
   int svd_method = 2;
+  int use_own_chol = 1;
+  Buf chol_work;
   int last_sweeps = 0;
   int use_graphs = 1;
   int graph_gen = 0;
@@ -349,6 +351,20 @@ static int need_lin(ngd_ctx* c) {
   return NGD_OK;
 }
 
+// Upper Cholesky of a small ell x ell matrix: in-house one-CTA kernel (ngd_chol.cu), cuSOLVER
+// potrf when it does not fit shared memory.  info follows LAPACK (0 ok, j+1 first bad pivot).
+static int potrf_upper(ngd_ctx* c, double* A, int n, int* info) {
+  if (c->use_own_chol && chol_supported(n)) {
+    CK(chol_upper(A, n, n, info, c->stream));
+    return NGD_OK;
+  }
+  int lw = 0;
+  CKS(cusolverDnDpotrf_bufferSize(c->sol, CUBLAS_FILL_MODE_UPPER, n, A, n, &lw));
+  CK(c->chol_work.ensure(sizeof(double) * std::max(lw, 1)));
+  CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, n, A, n, c->chol_work.d(), lw, info));
+  return NGD_OK;
+}
+
 // Shifted Cholesky-QR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020) in place:
 // B (p x ell, col-major) <- Q, nys_r <- R (upper, ell x ell, col-major).
 static int scholqr3(ngd_ctx* c, double* B, int64_t p, int ell) {
@@ -363,7 +379,7 @@ static int scholqr3(ngd_ctx* c, double* B, int64_t p, int ell) {
     double* W = c->nys_m.d();
     CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, B, (int)p, &zero, W, ell));
     if (pass == 0) shift_diag(W, ell, shift_coef, c->stream);
-    CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, ell, W, ell, c->nys_work.d(), lw, info));
+    TRY(potrf_upper(c, W, ell, info));
     triu(W, ell, ell, c->stream);
     CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p, ell,
                     &one, W, ell, B, (int)p));
@@ -501,7 +517,7 @@ int ngd_ctx_destroy(ngd_ctx* c) {
   for (auto& e : c->poll_ev)
     if (e) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  for (Buf* b : {&c->pargs, &c->px, &c->pb}) b->release();
+  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work}) b->release();
   if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
   if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
   if (c->sol) cusolverDnDestroy(c->sol);
@@ -810,8 +826,7 @@ int ngd_nystrom_prepare(ngd_ctx* c, double* omega, int64_t p, int32_t ell) {
   for (int pass = 0; pass < passes; ++pass) {
     CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, omega, (int)p, &zero,
                     c->nys_m.d(), ell));
-    CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, c->nys_work.d(), lwork,
-                         static_cast<int*>(c->nys_info.p) + 1));
+    TRY(potrf_upper(c, c->nys_m.d(), ell, static_cast<int*>(c->nys_info.p) + 1));
     CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p,
                     ell, &one, c->nys_m.d(), ell, omega, (int)p));
   }
@@ -849,7 +864,7 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
   const int lw = std::max(std::max(lw_potrf, lw_geqrf), std::max(lw_orgqr, lw_svd));
   CK(c->nys_work.ensure(sizeof(double) * std::max(lw, 1)));
   int* info = static_cast<int*>(c->nys_info.p);
-  CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, c->nys_work.d(), lw_potrf, info));
+  TRY(potrf_upper(c, c->nys_m.d(), ell, info));
   // status of this Cholesky (and of Omega's Cholesky-QR) is read back with the results below: one host
   // sync per sketch; on failure the (discarded) remaining work runs on garbage and NGD_E_CHOL is returned
   CK(cudaMemcpyAsync(&c->h_pin[8], info, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -1151,6 +1166,10 @@ int ngd_get_stat(ngd_ctx* c, const char* key, int64_t* out) {
 
 int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(NGD_E_SHAPE, "bad option");
+  if (!strcmp(key, "chol")) {
+    c->use_own_chol = value ? 1 : 0;
+    return NGD_OK;
+  }
   if (!strcmp(key, "graphs")) {
     c->use_graphs = value ? 1 : 0;
     return NGD_OK;

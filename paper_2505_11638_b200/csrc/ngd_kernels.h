@@ -153,6 +153,8 @@ int jsvd_cluster_size(int ell);
 cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
                        cudaStream_t st);
 int jsvd_block_supported(int ell);
+bool chol_supported(int n);
+cudaError_t chol_upper(double* A, int n, int lda, int* info, cudaStream_t st);
 cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
                              cudaStream_t st);
 void gather_points(const double* padded, double* compact, Geom gm, cudaStream_t st);

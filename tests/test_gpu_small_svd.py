@@ -44,3 +44,20 @@ def test_jacobi_svd_matches_lapack(method, n):
     assert np.linalg.norm(u.T @ u - np.eye(n)) <= 1e-12 * n
     # A = U diag(s) V^T  <=>  ||U^T A||_rows == s
     np.testing.assert_allclose(np.linalg.norm(u.T @ a, axis=1), s, rtol=1e-8, atol=1e-13)
+
+
+@pytest.mark.parametrize("n", [1, 5, 16, 17, 100, 160, 300])
+def test_small_cholesky_matches_lapack(n):
+    """In-house Cholesky (ngd_chol.cu) via the Nystrom prepare path: Omega <- Omega R^{-1}
+    must be orthonormal and R upper with R^T R = Omega0^T Omega0."""
+    rng = np.random.default_rng(n)
+    p = 4 * n + 3
+    om0 = rng.standard_normal((p, n))
+    ctx = utility_context()
+    Om = torch.as_tensor(om0.T.copy(), device="cuda")  # p x n column-major
+    ctx.call("ngd_nystrom_prepare", _lib.ptr(Om), p, n)
+    q = Om.cpu().numpy().T
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-13 * max(n, 1)
+    r = q.T @ om0
+    np.testing.assert_allclose(np.triu(r), r, atol=1e-11)
+    np.testing.assert_allclose(np.abs(np.diag(r)), np.abs(np.diag(np.linalg.qr(om0)[1])), rtol=1e-10)
