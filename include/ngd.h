@@ -129,7 +129,7 @@ int ngd_axpy(ngd_ctx* ctx, const double* d_a, double alpha, const double* d_b, d
  * ngd_launch_count: number of this library's kernel launches so far (process-wide).
  * ngd_probe_start(kind, n): bracket the next n launches of kernel class `kind`
  *   (1 FWD jets, 2 REV jets, 3 phase A, 4 phase B, 5 J rows, 6 preconditioner,
- *   7 vector/scalar, 8 pack) with CUDA events on their launch stream;
+ *   7 vector/scalar, 8 pack, 9 small SVD, 10 small Cholesky) with CUDA events on their launch stream;
  *   ngd_probe_stop returns the summed device time and the launch count. */
 int ngd_stream_sync(ngd_ctx* ctx);
 int64_t ngd_launch_count(void);

@@ -113,9 +113,9 @@ cudaError_t chol_upper(double* A, int n, int lda, int* info, cudaStream_t st) {
     cudaFuncSetAttribute(chol_upper_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024));
     attr = 200 * 1024;
   }
-  probe_before(K_VEC, st);
+  probe_before(K_CHOL, st);
   chol_upper_kernel<16><<<1, kCholThreads, smem, st>>>(A, n, lda, info);
-  probe_after(K_VEC, st);
+  probe_after(K_CHOL, st);
   return cudaGetLastError();
 }
 

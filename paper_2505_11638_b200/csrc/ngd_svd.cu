@@ -217,9 +217,9 @@ static cudaError_t launch_jsvd_r(const double* A, int ell, int lda, double* U, i
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  probe_before(K_VEC, st);
+  probe_before(K_SVD, st);
   e = cudaLaunchKernelEx(&cfg, kern, A, ell, lda, U, ldu, sigma, tol, max_sweeps, info);
-  probe_after(K_VEC, st);
+  probe_after(K_SVD, st);
   return e;
 }
 
@@ -518,9 +518,9 @@ static cudaError_t launch_jsvd_block_r(const double* A, int ell, int lda, double
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  probe_before(K_VEC, st);
+  probe_before(K_SVD, st);
   e = cudaLaunchKernelEx(&cfg, kern, A, ell, lda, U, ldu, sigma, tol, max_sweeps, h, info);
-  probe_after(K_VEC, st);
+  probe_after(K_SVD, st);
   return e;
 }
 
