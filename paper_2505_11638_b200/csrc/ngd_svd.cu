@@ -28,14 +28,19 @@ namespace ngd {
 template <int RPL>
 constexpr int svd_threads() { return RPL <= 4 ? 1024 : (RPL <= 8 ? 512 : 256); }
 
+// circle-method round robin on n players (n even): round r in [0, n-1), pair k in [0, n/2)
 __device__ __forceinline__ void circle_pair(int n, int r, int k, int& a, int& b) {
   const int m = n - 1;
   if (k == 0) {
     a = 0;
-    b = 1 + (r % m);
+    b = 1 + r;
   } else {
-    a = 1 + ((r + k) % m);
-    b = 1 + ((r - k + m) % m);
+    int x = r + k;
+    x = (x >= m) ? x - m : x;
+    int y = r - k;
+    y = (y < 0) ? y + m : y;
+    a = 1 + x;
+    b = 1 + y;
   }
 }
 
@@ -275,23 +280,29 @@ __device__ __forceinline__ void copy_remote(double2* dst, const double2* src, si
   for (; e < n; e += T) dst[e] = src[e];
 }
 
-template <int RPL>
-__device__ __forceinline__ bool rotate_pair(double* ci, double* cj, double* vi, double* vj, int ell, int lane,
+template <int RPL>  // RPL = double2 per lane per column (rows 2q, 2q+1 for q = lane + 32 u)
+__device__ __forceinline__ bool rotate_pair(double* ci, double* cj, double* vi, double* vj, int ldc, int lane,
                                             double tol) {
-  double x[RPL], y[RPL];
+  const int nq = ldc >> 1;  // double2 per column (ldc even; padding rows are zero)
+  const double2* ci2 = reinterpret_cast<const double2*>(ci);
+  const double2* cj2 = reinterpret_cast<const double2*>(cj);
+  double2 x[RPL], y[RPL];
 #pragma unroll
   for (int u = 0; u < RPL; ++u) {
-    const int r = lane + 32 * u;
-    const bool in = r < ell;
-    x[u] = in ? ci[r] : 0.0;
-    y[u] = in ? cj[r] : 0.0;
+    const int q = lane + 32 * u;
+    const bool in = q < nq;
+    x[u] = in ? ci2[q] : make_double2(0.0, 0.0);
+    y[u] = in ? cj2[q] : make_double2(0.0, 0.0);
   }
   double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
   for (int u = 0; u < RPL; ++u) {
-    al = fma(x[u], x[u], al);
-    be = fma(y[u], y[u], be);
-    ga = fma(x[u], y[u], ga);
+    al = fma(x[u].x, x[u].x, al);
+    al = fma(x[u].y, x[u].y, al);
+    be = fma(y[u].x, y[u].x, be);
+    be = fma(y[u].y, y[u].y, be);
+    ga = fma(x[u].x, y[u].x, ga);
+    ga = fma(x[u].y, y[u].y, ga);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {  // three interleaved butterfly reductions
@@ -300,19 +311,24 @@ __device__ __forceinline__ bool rotate_pair(double* ci, double* cj, double* vi, 
     ga += __shfl_xor_sync(0xffffffffu, ga, o);
   }
   if (!(ga != 0.0 && ga * ga > tol * tol * al * be)) return false;
-  const double zeta = (be - al) / (2.0 * ga);
+  // rotation parameters (Rutishauser); __drcp_rn keeps the divide off the slow path
+  const double zeta = 0.5 * (be - al) * __drcp_rn(ga);
   const double az = fabs(zeta);
-  const double t = (az > 1e150) ? 0.5 / zeta : copysign(1.0 / (az + sqrt(fma(az, az, 1.0))), zeta);
+  const double t = (az > 1e150) ? 0.5 * __drcp_rn(zeta) : copysign(__drcp_rn(az + sqrt(fma(az, az, 1.0))), zeta);
   const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
+  double2* wi = reinterpret_cast<double2*>(ci);
+  double2* wj = reinterpret_cast<double2*>(cj);
+  double2* pi = reinterpret_cast<double2*>(vi);
+  double2* pj = reinterpret_cast<double2*>(vj);
 #pragma unroll
   for (int u = 0; u < RPL; ++u) {
-    const int r = lane + 32 * u;
-    if (r < ell) {
-      ci[r] = c * x[u] - s * y[u];
-      cj[r] = s * x[u] + c * y[u];
-      const double pv = vi[r], qv = vj[r];
-      vi[r] = c * pv - s * qv;
-      vj[r] = s * pv + c * qv;
+    const int q = lane + 32 * u;
+    if (q < nq) {
+      wi[q] = make_double2(c * x[u].x - s * y[u].x, c * x[u].y - s * y[u].y);
+      wj[q] = make_double2(s * x[u].x + c * y[u].x, s * x[u].y + c * y[u].y);
+      const double2 pv = pi[q], qv = pj[q];
+      pi[q] = make_double2(c * pv.x - s * qv.x, c * pv.y - s * qv.y);
+      pj[q] = make_double2(s * pv.x + c * qv.x, s * pv.y + c * qv.y);
     }
   }
   return true;
@@ -334,7 +350,8 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   const int k = (int)cl.block_rank();
   const int nb = 2 * CL;  // blocks
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const size_t slot_sz = (size_t)h * ell;  // one block of X (or V)
+  const int ldc = ell + (ell & 1);             // even column stride: 16-B aligned double2 columns
+  const size_t slot_sz = (size_t)h * ldc;  // one block of X (or V)
   // buf[phase][slot][0 = X, 1 = V][h][ell]
   auto bufp = [&](double* base, int phase, int slot, int which) {
     return base + ((size_t)(phase * 2 + slot) * 2 + which) * slot_sz;
@@ -348,10 +365,10 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
     double* X = bufp(smem, 0, sl, 0);
     double* V = bufp(smem, 0, sl, 1);
     for (int64_t e = tid; e < (int64_t)slot_sz; e += T) {
-      const int i = (int)(e / ell), r = (int)(e % ell);
+      const int i = (int)(e / ldc), r = (int)(e % ldc);
       const int j = blk[sl] * h + i;  // global column id
-      X[e] = (j < ell) ? A[(int64_t)r * lda + j] : 0.0;
-      V[e] = (j == r) ? 1.0 : 0.0;
+      X[e] = (j < ell && r < ell) ? A[(int64_t)r * lda + j] : 0.0;
+      V[e] = (j == r && r < ell) ? 1.0 : 0.0;
     }
   }
   if (tid < 2) flags[tid] = 0;
@@ -374,8 +391,8 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
             circle_pair(h, rr, kk, i, j);
             double* X = sl ? X1 : X0;
             double* V = sl ? V1 : V0;
-            rotated |= rotate_pair<RPL>(X + (size_t)i * ell, X + (size_t)j * ell, V + (size_t)i * ell,
-                                        V + (size_t)j * ell, ell, lane, tol);
+            rotated |= rotate_pair<RPL>(X + (size_t)i * ldc, X + (size_t)j * ldc, V + (size_t)i * ldc,
+                                        V + (size_t)j * ldc, ldc, lane, tol);
           }
           __syncthreads();
         }
@@ -383,9 +400,9 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       // cross pairs of the two blocks: h rounds of h disjoint pairs
       for (int sft = 0; sft < h; ++sft) {
         for (int i = warp; i < h; i += NW) {
-          const int j = (i + sft) % h;
-          rotated |= rotate_pair<RPL>(X0 + (size_t)i * ell, X1 + (size_t)j * ell, V0 + (size_t)i * ell,
-                                      V1 + (size_t)j * ell, ell, lane, tol);
+          const int j = (i + sft >= h) ? i + sft - h : i + sft;
+          rotated |= rotate_pair<RPL>(X0 + (size_t)i * ldc, X1 + (size_t)j * ldc, V0 + (size_t)i * ldc,
+                                      V1 + (size_t)j * ldc, ldc, lane, tol);
         }
         __syncthreads();
       }
@@ -440,7 +457,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   }
   // norms of the held columns, ranks over the cluster, outputs
   for (int q = warp; q < 2 * h; q += NW) {
-    const double* c = bufp(smem, phase, q / h, 0) + (size_t)(q % h) * ell;
+    const double* c = bufp(smem, phase, q / h, 0) + (size_t)(q % h) * ldc;
     double sacc = 0.0;
     for (int r = lane; r < ell; r += 32) sacc = fma(c[r], c[r], sacc);
     sacc = warp_sum(sacc);
@@ -467,7 +484,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
     for (int off = 16; off > 0; off >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
     if (rank < ell) {
       if (lane == 0) sigma[rank] = sj;
-      const double* v = bufp(smem, phase, q / h, 1) + (size_t)(q % h) * ell;
+      const double* v = bufp(smem, phase, q / h, 1) + (size_t)(q % h) * ldc;
       for (int r = lane; r < ell; r += 32) U[(int64_t)rank * ldu + r] = v[r];
     }
   }
@@ -482,7 +499,7 @@ static bool jsvd_block_plan(int ell, int& cl, int& h) {
     int hh = (ell + 2 * c - 1) / (2 * c);
     hh += hh & 1;  // even (circle method inside a block)
     if (hh > 16 && c < 16) continue;
-    if (sizeof(double) * (8 * (size_t)hh * ell + 2 * hh) + 64 > 200 * 1024) continue;
+    if (sizeof(double) * (8 * (size_t)hh * (ell + (ell & 1)) + 2 * hh) + 64 > 200 * 1024) continue;
     cl = c;
     h = hh;
     return true;
@@ -498,7 +515,7 @@ int jsvd_block_supported(int ell) {
 template <int RPL>
 static cudaError_t launch_jsvd_block_r(const double* A, int ell, int lda, double* U, int ldu, double* sigma,
                                        double tol, int max_sweeps, int cl, int h, int* info, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (8 * (size_t)h * ell + 2 * h) + 64;
+  const size_t smem = sizeof(double) * (8 * (size_t)h * (ell + (ell & 1)) + 2 * h) + 64;
   auto kern = jsvd_block_kernel<RPL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -530,12 +547,18 @@ cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int l
   if (!jsvd_block_plan(ell, cl, h)) return cudaErrorInvalidValue;
   const double tol = 2.220446049250313e-16 * (double)ell;
   const int max_sweeps = 40;
-  const int rpl = (ell + 31) / 32;
-  if (rpl <= 4) return launch_jsvd_block_r<4>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-  if (rpl <= 8) return launch_jsvd_block_r<8>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-  if (rpl <= 12) return launch_jsvd_block_r<12>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-  if (rpl <= 16) return launch_jsvd_block_r<16>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-  return cudaErrorInvalidValue;
+  const int rpl = (ell + 63) / 64;  // double2 per lane
+  switch (rpl) {
+    case 1: return launch_jsvd_block_r<1>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
+    case 2: return launch_jsvd_block_r<2>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
+    case 3: return launch_jsvd_block_r<3>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
+    case 4: return launch_jsvd_block_r<4>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
+    case 5: return launch_jsvd_block_r<5>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
+    case 6: return launch_jsvd_block_r<6>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
+    case 7: return launch_jsvd_block_r<7>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
+    case 8: return launch_jsvd_block_r<8>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace ngd
