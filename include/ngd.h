@@ -65,9 +65,28 @@ int ngd_ctx_set_comm(ngd_ctx* ctx, const uint8_t* h_id /* 128 bytes */, int32_t 
 int ngd_set_points(ngd_ctx* ctx, int64_t n_int, const double* d_x_int, const double* d_w_int,
                    const double* d_off_int, int64_t n_bnd, const double* d_x_bnd, const double* d_w_bnd,
                    const double* d_off_bnd);
+/* General row set (heat1p1d's metric and residual stacks differ, problems.py:294-311):
+ * "head" rows at the interior points and "value" rows (F = u) at the second point set,
+ * each with a METRIC weight wm (Gramian) and a RESIDUAL weight wr (loss / gradient);
+ * a row absent from one stack carries weight 0 there.  ngd_set_points(...) ==
+ * ngd_set_rows(..., w_int, w_int, ..., w_bnd, w_bnd, ...). */
+int ngd_set_rows(ngd_ctx* ctx, int64_t n_int, const double* d_x_int, const double* d_wm_int,
+                 const double* d_wr_int, const double* d_off_int, int64_t n_val, const double* d_x_val,
+                 const double* d_wm_val, const double* d_wr_val, const double* d_off_val);
+/* Output head of the interior rows.  coef: C = d+2 coefficients over the
+ * output channels (value, d_1 u .. d_d u, Lambda), Lambda = sum_{i in lap_mask} d_ii u;
+ * metric row  F = coef.o + 3 kappa ubar^2 u   (ubar = u at theta_bar, frozen),
+ * residual    R = coef.o + kappa u^3 + off.
+ * poisson*: coef = e_Lambda, kappa 0, mask all; heat1p1d: coef = e_{d_t} - e_Lambda,
+ * mask {x}; nlpoisson2d: coef = e_Lambda, kappa = -1 (problems.py:161-385).
+ * Default: the Poisson head. */
+int ngd_set_head(ngd_ctx* ctx, const double* h_coef, int32_t n_coef, double kappa, uint32_t lap_mask);
 
 /* ---- loss (PdeProblem.loss_value, problems.py:92-99); all-reduced ------- */
 int ngd_loss(ngd_ctx* ctx, const double* d_theta, double* h_loss);
+/* relative H1 error at the interior points (PdeProblem.h1_relative_error, problems.py:104-119):
+ * d_exact = per interior point [u*, grad u*] ((n_int, d+1) row-major); weights = interior metric weights */
+int ngd_h1_error(ngd_ctx* ctx, const double* d_theta, const double* d_exact, double* h_err);
 /* loss at theta - alpha * dir (backtracking_linesearch candidate, optim.py:137) */
 int ngd_loss_at(ngd_ctx* ctx, const double* d_theta, double alpha, const double* d_dir, double* h_loss);
 
@@ -75,6 +94,11 @@ int ngd_loss_at(ngd_ctx* ctx, const double* d_theta, double alpha, const double*
  * caches jets + adjoints at theta; also returns the loss (may be NULL) and,
  * if d_metric != NULL, the metric stack values [Lap u]_int ++ [u]_bnd. */
 int ngd_linearize(ngd_ctx* ctx, const double* d_theta, double* h_loss, double* d_metric);
+/* as ngd_linearize, with the metric coefficient frozen at d_theta_bar (NULL: theta; the
+ * metric_stack(theta, freeze(theta_bar)) of problems.py:364-373) and, if d_resid != NULL,
+ * the residual rows.  After a theta_bar != theta linearisation ngd_loss_grad is refused. */
+int ngd_linearize_ex(ngd_ctx* ctx, const double* d_theta, const double* d_theta_bar, double* h_loss,
+                     double* d_metric, double* d_resid);
 /* gradient J^T (w o r) at the current linearisation (PdeProblem.loss_grad, problems.py:101-102) */
 int ngd_loss_grad(ngd_ctx* ctx, double* d_grad);
 /* metric-stack JVP / VJP at the current linearisation (LinearizedMap.jvp/vjp, autodiff.py:605-609) */

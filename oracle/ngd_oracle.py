@@ -132,6 +132,8 @@ class Quadrature:
     interior_weights: np.ndarray
     boundary_points: np.ndarray
     boundary_weights: np.ndarray
+    initial_points: np.ndarray | None = None
+    initial_weights: np.ndarray | None = None
 
 
 def _uniform_box(rng, n, d):  # problems.py:122-125 on the unit box
@@ -161,10 +163,63 @@ def _hypercube_boundary(rng, n, d):
     return pts
 
 
-class PoissonProblem:
+@dataclass
+class StackRows:
+    """A metric or residual stack in the two row kinds every reference problem uses.
+
+    * head rows at ``x_int``: F = alpha*u + sum_i beta_i d_i u + sum_i gamma_i d_ii u
+      (Laplacian: gamma = 1; heat operator u_t - u_xx: beta = e_t, gamma = -e_x;
+      nonlinear Poisson Gauss-Newton row: gamma = 1, alpha = -3 ubar^2 per point),
+    * value rows at ``x_val``: F = u.
+    """
+
+    x_int: np.ndarray
+    alpha: np.ndarray | float
+    beta: np.ndarray
+    gamma: np.ndarray
+    x_val: np.ndarray
+
+
+class StackProblem:
+    """Least-squares problem from a residual stack (problems.py:50-119)."""
+
+    has_initial = False
+
+    def residual_stack(self, theta, quad):
+        raise NotImplementedError
+
+    def stack_rows(self, theta, theta_bar, quad, which):
+        raise NotImplementedError
+
+    def metric_stack(self, theta, quad, theta_bar=None):  # gramian.py:33-41 (metric frozen at theta_bar)
+        return Linearization(self, theta, quad, "metric", theta_bar).value
+
+    def loss_value(self, theta, quad):  # problems.py:92-99
+        r = self.residual_stack(theta, quad)
+        w = self.residual_weights(quad)
+        return float(0.5 * np.sum(w * r * r))
+
+    def loss_grad(self, theta, quad):  # problems.py:101-102: grad of the loss = J_res^T (w * r)
+        lin = Linearization(self, theta, quad, "residual")
+        return lin.vjp(self.residual_weights(quad) * self.residual_stack(theta, quad))
+
+    def h1_relative_error(self, theta, quad):  # problems.py:104-119 (space-time gradient for heat)
+        x, w = quad.interior_points, quad.interior_weights
+        u, gu, _ = mlp_jets(self.widths, theta, x)
+        ue, ge = self.exact(x), self.exact_grad(x)
+        num = np.sum(w * (u - ue) ** 2) + np.sum(w * np.sum((gu - ge) ** 2, axis=1))
+        den = np.sum(w * ue**2) + np.sum(w * np.sum(ge**2, axis=1))
+        if den == 0.0:
+            raise ZeroDivisionError("exact solution has zero H1 norm")
+        return float(np.sqrt(num / den))
+
+
+class PoissonProblem(StackProblem):
     """-Laplace(u) = f on (0,1)^d with Dirichlet data.
 
     kind = 'sin2d'  : Poisson2D, u* = sin(pi x) sin(pi y)        (problems.py:190-219)
+    kind = 'sin1d'  : Poisson1D, u* = sin(pi x), boundary = the two endpoints with
+                      unit weights                                (problems.py:128-177)
     kind = 'sinsum' : u* = sum_i sin(pi x_i)                     (BASELINE C3)
     kind = 'gauss'  : u* = exp(-|x|^2/10)                          (BASELINE C5)
     interior_only   : metric/residual stack without boundary rows (BASELINE C4,
@@ -182,12 +237,14 @@ class PoissonProblem:
         self.interior_only = interior_only
         if kind == "sin2d" and self.d != 2:
             raise ValueError("sin2d needs d = 2")
+        if kind == "sin1d" and self.d != 1:
+            raise ValueError("sin1d needs d = 1")
 
     # exact solution and data ------------------------------------------------
     def exact(self, x):
         if self.kind == "sin2d":
             return np.sin(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1])
-        if self.kind == "sinsum":
+        if self.kind in ("sinsum", "sin1d"):
             return np.sum(np.sin(np.pi * x), axis=1)
         return np.exp(-np.sum(x * x, axis=1) / 10.0)
 
@@ -196,15 +253,15 @@ class PoissonProblem:
             sx, cx = np.sin(np.pi * x[:, 0]), np.cos(np.pi * x[:, 0])
             sy, cy = np.sin(np.pi * x[:, 1]), np.cos(np.pi * x[:, 1])
             return np.pi * np.stack([cx * sy, sx * cy], axis=1)
-        if self.kind == "sinsum":
+        if self.kind in ("sinsum", "sin1d"):
             return np.pi * np.cos(np.pi * x)
         return -x / 5.0 * self.exact(x)[:, None]
 
     def source(self, x):
         if self.kind == "sin2d":
             return 2.0 * np.pi**2 * self.exact(x)  # problems.py:211-212
-        if self.kind == "sinsum":
-            return np.pi**2 * np.sum(np.sin(np.pi * x), axis=1)
+        if self.kind in ("sinsum", "sin1d"):
+            return np.pi**2 * np.sum(np.sin(np.pi * x), axis=1)  # problems.py:147-148 for d = 1
         r2 = np.sum(x * x, axis=1)
         return (self.d / 5.0 - r2 / 25.0) * self.exact(x)
 
@@ -215,9 +272,11 @@ class PoissonProblem:
         return 4.0 if self.d == 2 else 2.0 * self.d
 
     def sample_quadrature(self, n_interior, n_boundary, seed):
-        """problems.py:210-219 for d=2; the hypercube analogue otherwise."""
+        """problems.py:210-219 for d=2, 150-159 for d=1; the hypercube analogue otherwise."""
         rng = np.random.default_rng(seed)
         pts = _uniform_box(rng, n_interior, self.d)
+        if self.kind == "sin1d":
+            return Quadrature(pts, np.full(n_interior, 1.0 / n_interior), np.array([[0.0], [1.0]]), np.ones(2))
         if self.interior_only or n_boundary == 0:
             bnd = np.zeros((0, self.d))
             wb = np.zeros(0)
@@ -232,11 +291,8 @@ class PoissonProblem:
 
     residual_weights = metric_weights
 
-    def metric_stack(self, theta, quad):  # problems.py:168-172
-        _, _, sec = mlp_jets(self.widths, theta, quad.interior_points)
-        lap = np.sum(sec, axis=1)
-        ub = mlp_forward(self.widths, theta, quad.boundary_points) if len(quad.boundary_points) else np.zeros(0)
-        return np.concatenate([lap, ub])
+    def stack_rows(self, theta, theta_bar, quad, which):  # problems.py:161-172: same rows both stacks
+        return StackRows(quad.interior_points, 0.0, np.zeros(self.d), np.ones(self.d), quad.boundary_points)
 
     def data_offsets(self, quad):
         """Residual minus metric stack: [f]_int ++ [-g]_bnd (problems.py:161-166)."""
@@ -251,23 +307,109 @@ class PoissonProblem:
             boundary = np.zeros(0)
         return np.concatenate([interior, boundary])
 
-    def loss_value(self, theta, quad):  # problems.py:92-99
-        r = self.residual_stack(theta, quad)
-        w = self.residual_weights(quad)
-        return float(0.5 * np.sum(w * r * r))
-
-    def loss_grad(self, theta, quad):  # problems.py:101-102: J_r^T (w * r)
+    def loss_grad(self, theta, quad):  # linear stack: residual = metric + offsets
         lin = Linearization(self, theta, quad)
         r = lin.value + self.data_offsets(quad)
         return lin.vjp(self.residual_weights(quad) * r)
 
-    def h1_relative_error(self, theta, quad):  # problems.py:104-119
-        x, w = quad.interior_points, quad.interior_weights
-        u, gu, _ = mlp_jets(self.widths, theta, x)
-        ue, ge = self.exact(x), self.exact_grad(x)
-        num = np.sum(w * (u - ue) ** 2) + np.sum(w * np.sum((gu - ge) ** 2, axis=1))
-        den = np.sum(w * ue**2) + np.sum(w * np.sum(ge**2, axis=1))
-        return float(np.sqrt(num / den))
+
+class NonlinearPoissonProblem(PoissonProblem):
+    """-Laplace(u) + u^3 = f on (0,1)^2, Gauss-Newton metric (problems.py:334-385).
+
+    Residual [Lap u - u^3 + f]_int ++ [u - g]_bnd; metric rows
+    [Lap u - 3 ubar^2 u]_int ++ [u]_bnd with ubar = u_{theta_bar} frozen.
+    """
+
+    def __init__(self, widths):
+        super().__init__(widths, kind="sin2d")
+
+    def source(self, x):  # problems.py:350-352
+        u = self.exact(x)
+        return 2.0 * np.pi**2 * u + u**3
+
+    def residual_stack(self, theta, quad):  # problems.py:354-362
+        _, _, sec = mlp_jets(self.widths, theta, quad.interior_points)
+        u = mlp_forward(self.widths, theta, quad.interior_points)
+        interior = np.sum(sec, axis=1) - u**3 + self.source(quad.interior_points)
+        boundary = mlp_forward(self.widths, theta, quad.boundary_points) - self.dirichlet(quad.boundary_points)
+        return np.concatenate([interior, boundary])
+
+    def stack_rows(self, theta, theta_bar, quad, which):  # problems.py:364-373
+        # the residual's Jacobian at theta is the metric row frozen at theta_bar = theta
+        ref = theta if which == "residual" else theta_bar
+        ubar = mlp_forward(self.widths, ref, quad.interior_points)
+        return StackRows(quad.interior_points, -3.0 * ubar**2, np.zeros(2), np.ones(2), quad.boundary_points)
+
+    def data_offsets(self, quad):
+        raise TypeError("the nonlinear Poisson residual is not metric + offsets")
+
+    loss_grad = StackProblem.loss_grad
+
+
+class HeatProblem(StackProblem):
+    """u_t - u_xx = f on (t,x) in (0,1)^2, u* = cos(pi x) exp(-pi^2 t/4) (problems.py:235-331).
+
+    Residual [u_t - u_xx - f]_int ++ [u - g]_lateral ++ [u - u0]_initial with weights
+    [1/N, 2/N_b, 1/N_0]; metric [u_t - u_xx]_int ++ [u]_int (bulk) ++ [u]_initial with
+    weights [1/N, 1/N, 1/N_0] -- the two stacks have different row sets.
+    """
+
+    has_initial = True
+
+    def __init__(self, widths):
+        self.topology = Topology(widths)
+        self.widths = self.topology.widths
+        self.d = 2
+        if self.widths[0] != 2:
+            raise ValueError("heat1p1d needs input dim 2 (t, x)")
+
+    def exact(self, x):
+        return np.cos(np.pi * x[:, 1]) * np.exp(-np.pi**2 * x[:, 0] / 4.0)
+
+    def exact_grad(self, x):
+        u = self.exact(x)
+        dt = -np.pi**2 / 4.0 * u
+        dx = -np.pi * np.sin(np.pi * x[:, 1]) * np.exp(-np.pi**2 * x[:, 0] / 4.0)
+        return np.stack([dt, dx], axis=1)
+
+    def source(self, x):
+        return 0.75 * np.pi**2 * self.exact(x)
+
+    def dirichlet(self, x):
+        return self.exact(x)
+
+    def initial_value(self, x):
+        return np.cos(np.pi * x[:, 1])
+
+    def sample_quadrature(self, n_interior, n_boundary, seed):  # problems.py:266-287
+        rng = np.random.default_rng(seed)
+        pts = _uniform_box(rng, n_interior, 2)
+        t = rng.random(n_boundary)
+        side = rng.integers(0, 2, n_boundary).astype(float)
+        bnd = np.stack([t, side], axis=1)
+        n_init = max(n_boundary // 2, 1)
+        xi = rng.random(n_init)
+        init = np.stack([np.zeros(n_init), xi], axis=1)
+        return Quadrature(pts, np.full(n_interior, 1.0 / n_interior), bnd, np.full(n_boundary, 2.0 / n_boundary),
+                          init, np.full(n_init, 1.0 / n_init))
+
+    def residual_weights(self, quad):
+        return np.concatenate([quad.interior_weights, quad.boundary_weights, quad.initial_weights])
+
+    def metric_weights(self, quad):
+        return np.concatenate([quad.interior_weights, quad.interior_weights, quad.initial_weights])
+
+    def stack_rows(self, theta, theta_bar, quad, which):  # problems.py:294-311
+        beta, gamma = np.array([1.0, 0.0]), np.array([0.0, -1.0])
+        second = quad.interior_points if which == "metric" else quad.boundary_points
+        return StackRows(quad.interior_points, 0.0, beta, gamma, np.concatenate([second, quad.initial_points]))
+
+    def residual_stack(self, theta, quad):  # problems.py:294-301
+        _, g, sec = mlp_jets(self.widths, theta, quad.interior_points)
+        interior = g[:, 0] - sec[:, 1] - self.source(quad.interior_points)
+        boundary = mlp_forward(self.widths, theta, quad.boundary_points) - self.dirichlet(quad.boundary_points)
+        initial = mlp_forward(self.widths, theta, quad.initial_points) - self.initial_value(quad.initial_points)
+        return np.concatenate([interior, boundary, initial])
 
 
 # ---------------------------------------------------------------------------
@@ -276,17 +418,23 @@ class PoissonProblem:
 
 
 class Linearization:
-    """The metric stack traced at theta: cached primal jets, then JVP (tangent
-    sweep) and VJP (adjoint sweep) through the same arithmetic the reference
-    tape records for mlp_input_derivatives / forward (autodiff.py:164-328)."""
+    """A stack (metric by default, or the residual's) traced at theta: cached
+    primal jets, then JVP (tangent sweep) and VJP (adjoint sweep) through the
+    same arithmetic the reference tape records for mlp_input_derivatives /
+    forward (autodiff.py:164-328).  Head rows follow StackRows."""
 
-    def __init__(self, problem, theta, quad):
+    def __init__(self, problem, theta, quad, which="metric", theta_bar=None):
         self.widths = problem.widths
         self.top = problem.topology
         self.theta = np.asarray(theta, dtype=float)
         self.layers = self.top.unflatten(self.theta)
-        self.xi = np.asarray(quad.interior_points, dtype=float)
-        self.xb = np.asarray(quad.boundary_points, dtype=float)
+        rows = problem.stack_rows(self.theta, self.theta if theta_bar is None else np.asarray(theta_bar, float),
+                                  quad, which)
+        self.xi = np.asarray(rows.x_int, dtype=float)
+        self.xb = np.asarray(rows.x_val, dtype=float)
+        self.alpha = rows.alpha
+        self.beta = np.asarray(rows.beta, dtype=float)
+        self.gamma = np.asarray(rows.gamma, dtype=float)
         self.nl = len(self.layers)
         d = self.widths[0]
         q = self.xi.shape[0]
@@ -309,8 +457,9 @@ class Linearization:
                 g = [d1 * gai for gai in ga]
                 z = t
             self.cache_i.append(ent)
-        lap = np.sum(np.stack([hai.reshape(q) for hai in self.cache_i[-1]["ha"]], axis=1), axis=1)
-        # boundary: plain forward cache
+        last = self.cache_i[-1]
+        head = self._head(q, last["a"], last["ga"], last["ha"])
+        # value rows: plain forward cache
         zb = self.xb
         self.cache_b = []
         for k, (w, b) in enumerate(self.layers):
@@ -322,12 +471,25 @@ class Linearization:
                 zb = t
             self.cache_b.append(ent)
         ub = self.cache_b[-1]["a"].reshape(self.xb.shape[0]) if self.xb.shape[0] else np.zeros(0)
-        self.value = np.concatenate([lap, ub])
+        self.value = np.concatenate([head, ub])
         self.n_int = q
         self.n_bnd = self.xb.shape[0]
 
+    def _head(self, q, a, ga, ha):
+        """alpha*u + beta . grad + gamma . second at the output layer (zero coefficients skipped)."""
+        out = np.zeros(q)
+        for gi, hai in zip(self.gamma, ha):
+            if gi != 0.0:
+                out = out + (hai.reshape(q) if gi == 1.0 else gi * hai.reshape(q))
+        for bi, gai in zip(self.beta, ga):
+            if bi != 0.0:
+                out = out + bi * gai.reshape(q)
+        if np.any(np.asarray(self.alpha) != 0.0):
+            out = out + self.alpha * a.reshape(q)
+        return out
+
     def jvp(self, v):
-        """Tangent sweep: d/de metric_stack(theta + e v) at e = 0."""
+        """Tangent sweep: d/de stack(theta + e v) at e = 0."""
         vl = self.top.unflatten(np.asarray(v, dtype=float))
         d = self.widths[0]
         q = self.n_int
@@ -349,8 +511,8 @@ class Linearization:
                 dg = [dd1 * gai + d1 * dgai for gai, dgai in zip(c["ga"], dga)]
                 dz = dt
             else:
-                dlap = np.sum(np.stack([x.reshape(q) for x in dha], axis=1), axis=1)
-        # boundary rows
+                dhead = self._head(q, da, dga, dha)
+        # value rows
         if self.n_bnd:
             dzb = np.zeros_like(self.xb)
             for k, ((w, _), (vw, vb)) in enumerate(zip(self.layers, vl)):
@@ -360,18 +522,21 @@ class Linearization:
             dub = dzb.reshape(self.n_bnd)
         else:
             dub = np.zeros(0)
-        return np.concatenate([dlap, dub])
+        return np.concatenate([dhead, dub])
 
     def vjp(self, cot):
-        """Adjoint sweep: J^T cot for the metric stack."""
+        """Adjoint sweep: J^T cot for the stack."""
         cot = np.asarray(cot, dtype=float)
         ci, cb = cot[: self.n_int], cot[self.n_int:]
         d = self.widths[0]
         grads = [(np.zeros_like(w), np.zeros_like(b)) for w, b in self.layers]
-        # interior: Lap u = sum_i ha_i at the output layer
-        abar = np.zeros_like(self.cache_i[-1]["a"])
-        gabar = [np.zeros_like(abar) for _ in range(d)]
-        habar = [ci[:, None] * np.ones_like(abar) for _ in range(d)]
+        # head rows: seeds alpha (value), beta_i (gradient), gamma_i (second derivative)
+        ones = np.ones_like(self.cache_i[-1]["a"])
+        ci2 = ci[:, None]
+        alpha = np.asarray(self.alpha, dtype=float)
+        abar = (ci * alpha)[:, None] * ones if alpha.ndim else ci2 * alpha * ones
+        gabar = [ci2 * bi * ones for bi in self.beta]
+        habar = [ci2 * ones if gi == 1.0 else ci2 * gi * ones for gi in self.gamma]
         for k in range(self.nl - 1, -1, -1):
             w, _ = self.layers[k]
             c = self.cache_i[k]
@@ -396,7 +561,7 @@ class Linearization:
             zbar_in = abar @ w
             gbar_in = [gab @ w for gab in gabar]
             hbar_in = [hab @ w for hab in habar]
-        # boundary rows: u = last-layer value
+        # value rows: u = last-layer value
         if self.n_bnd:
             abar = cb[:, None] * np.ones((self.n_bnd, 1))
             for k in range(self.nl - 1, -1, -1):

@@ -53,9 +53,13 @@ SIGNATURES = {
     "ngd_nccl_unique_id": [ctypes.c_char_p],
     "ngd_ctx_set_comm": [_P, ctypes.c_char_p, _I32, _I32],
     "ngd_set_points": [_P, _I64, _P, _P, _P, _I64, _P, _P, _P],
+    "ngd_set_rows": [_P, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _P],
+    "ngd_set_head": [_P, _P, _I32, _D, ctypes.c_uint32],
     "ngd_loss": [_P, _P, ctypes.POINTER(_D)],
     "ngd_loss_at": [_P, _P, _D, _P, ctypes.POINTER(_D)],
     "ngd_linearize": [_P, _P, ctypes.POINTER(_D), _P],
+    "ngd_h1_error": [_P, _P, _P, ctypes.POINTER(_D)],
+    "ngd_linearize_ex": [_P, _P, _P, ctypes.POINTER(_D), _P, _P],
     "ngd_loss_grad": [_P, _P],
     "ngd_jvp": [_P, _P, _P],
     "ngd_vjp": [_P, _P, _P],

@@ -124,6 +124,9 @@ struct ngd_ctx {
   int Gl[kMaxLayers] = {0}, kpsl[kMaxLayers] = {0};
   RedPlan rplan{};
   Buf w_pad, off_pad, w_c, F, cot_grad, cot, metric_tmp;
+  Buf wr_pad, R_pad, alpha_bar;  // residual weights, residual rows, frozen 3 kappa ubar^2
+  Head head{};
+  unsigned lap_mask = 0;
   std::vector<Buf> zin, dbuf;  // per layer
   Buf dseed, pre_last, zs0, zs1;
   Buf partA, partB;
@@ -151,12 +154,13 @@ struct ngd_ctx {
   int* h_flags = nullptr;
   cudaEvent_t poll_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool lin_valid = false;
+  bool lin_frozen = false;  // linearised with a separate theta_bar
 
   double* S(int i) { return scal.d() + i; }
   unsigned* counter(int i) { return static_cast<unsigned*>(counters.p) + i; }
 };
 
-enum Scalar { SC_LOSS = 0, SC_FRO2 = 1, SC_SHIFT = 2, SC_TMP = 3, SC_MU = 4, SC_N = 8 };
+enum Scalar { SC_LOSS = 0, SC_FRO2 = 1, SC_SHIFT = 2, SC_TMP = 3, SC_MU = 4, SC_H1 = 5 /* 2 slots */, SC_N = 8 };
 
 static int bind(ngd_ctx* c) {
   CK(cudaSetDevice(c->device));
@@ -200,6 +204,7 @@ static int forward(ngd_ctx* c, bool store) {
     a.z_out = zout;
     a.pre_out = pre;
     a.bias = c->apf[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l];  // packed bias follows the packed W
+    a.lap_mask = c->lap_mask;
     for (int seg = 0; seg < 2; ++seg) {
       const int CC = seg == 0 ? gm.C : 1;
       a.col0 = seg == 0 ? 0 : gm.int_cols();
@@ -225,10 +230,11 @@ static int pack_theta(ngd_ctx* c, const double* theta, bool rev) {
   return NGD_OK;
 }
 
-static int loss_finish(ngd_ctx* c, double* h_loss, double* F, double* cot) {
+static int loss_finish(ngd_ctx* c, double* h_loss, double* F, double* cot, double* dseed = nullptr,
+                       const double* alpha_bar = nullptr, double* R = nullptr) {
   const Geom& gm = c->gm;
-  residual_loss(c->pre_last.d(), gm, c->w_pad.d(), c->off_pad.d(), F, cot, c->redp.d(), c->counter(0),
-                c->S(SC_LOSS), c->stream);
+  residual_loss(c->pre_last.d(), gm, c->head, c->wr_pad.d(), c->off_pad.d(), alpha_bar, F, R, cot, dseed,
+                c->redp.d(), c->counter(0), c->S(SC_LOSS), c->stream);
   TRY(allreduce(c, c->S(SC_LOSS), 1));
   if (h_loss) {
     CK(cudaMemcpyAsync(c->h_pin, c->S(SC_LOSS), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -432,6 +438,9 @@ int ngd_ctx_create(const int32_t* widths, int32_t n_widths, int32_t device, ngd_
   c->NL = n_widths - 1;
   c->d = widths[0];
   c->C = c->d + 2;
+  // default head: the Laplacian metric of the Poisson problems
+  c->head.coef[c->C - 1] = 1.0;
+  c->lap_mask = (1u << c->d) - 1u;
   int64_t off = 0;
   c->rows_A = 0;
   for (int l = 0; l < c->NL; ++l) {
@@ -562,6 +571,12 @@ int ngd_ctx_set_comm(ngd_ctx* c, const uint8_t* h_id, int32_t rank, int32_t nran
 
 int ngd_set_points(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w_int, const double* off_int,
                    int64_t n_bnd, const double* x_bnd, const double* w_bnd, const double* off_bnd) {
+  return ngd_set_rows(c, n_int, x_int, w_int, w_int, off_int, n_bnd, x_bnd, w_bnd, w_bnd, off_bnd);
+}
+
+int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* wm_int, const double* wr_int,
+                 const double* off_int, int64_t n_bnd, const double* x_bnd, const double* wm_bnd,
+                 const double* wr_bnd, const double* off_bnd) {
   TRY(bind(c));
   if (n_int < 0 || n_bnd < 0 || n_int + n_bnd == 0) return fail(NGD_E_SHAPE, "need at least one point");
   if (n_int + n_bnd > (int64_t)1 << 30) return fail(NGD_E_SHAPE, "too many points");
@@ -593,24 +608,27 @@ int ngd_set_points(ngd_ctx* c, int64_t n_int, const double* x_int, const double*
   CK(c->zs1.ensure(col_b * maxw));
   CK(cudaMemsetAsync(c->zs0.p, 0, col_b * maxw, c->stream));
   CK(cudaMemsetAsync(c->zs1.p, 0, col_b * maxw, c->stream));
-  for (Buf* b : {&c->w_pad, &c->off_pad, &c->F, &c->cot_grad, &c->cot}) {
+  for (Buf* b : {&c->w_pad, &c->off_pad, &c->F, &c->cot_grad, &c->cot, &c->wr_pad, &c->R_pad, &c->alpha_bar}) {
     CK(b->ensure(sizeof(double) * npp));
     CK(cudaMemsetAsync(b->p, 0, sizeof(double) * npp, c->stream));
   }
   CK(c->w_c.ensure(sizeof(double) * (n_int + n_bnd)));
-  CK(c->metric_tmp.ensure(sizeof(double) * npp));
+  CK(c->metric_tmp.ensure(sizeof(double) * 2 * npp));  // also the H1 error terms
   // weights / offsets into padded point order
   if (n_int) {
-    CK(cudaMemcpyAsync(c->w_pad.d(), w_int, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->w_pad.d(), wm_int, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->wr_pad.d(), wr_int, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(c->off_pad.d(), off_int, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->w_c.d(), w_int, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->w_c.d(), wm_int, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, c->stream));
   }
   if (n_bnd) {
-    CK(cudaMemcpyAsync(c->w_pad.d() + (int64_t)gm.nib * PB, w_bnd, sizeof(double) * n_bnd, cudaMemcpyDeviceToDevice,
+    CK(cudaMemcpyAsync(c->w_pad.d() + (int64_t)gm.nib * PB, wm_bnd, sizeof(double) * n_bnd, cudaMemcpyDeviceToDevice,
                        c->stream));
+    CK(cudaMemcpyAsync(c->wr_pad.d() + (int64_t)gm.nib * PB, wr_bnd, sizeof(double) * n_bnd,
+                       cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(c->off_pad.d() + (int64_t)gm.nib * PB, off_bnd, sizeof(double) * n_bnd,
                        cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->w_c.d() + n_int, w_bnd, sizeof(double) * n_bnd, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->w_c.d() + n_int, wm_bnd, sizeof(double) * n_bnd, cudaMemcpyDeviceToDevice, c->stream));
   }
   init_point_data(c->zin[0].d(), c->dseed.d(), gm, x_int, x_bnd, c->stream);
   CK(cudaGetLastError());
@@ -652,12 +670,51 @@ int ngd_set_points(ngd_ctx* c, int64_t n_int, const double* x_int, const double*
   return NGD_OK;
 }
 
+int ngd_set_head(ngd_ctx* c, const double* coef, int32_t n_coef, double kappa, uint32_t lap_mask) {
+  if (!c) return fail(NGD_E_STATE, "null context");
+  if (n_coef != c->C || c->C > kMaxC) return fail(NGD_E_SHAPE, "head needs %d coefficients, got %d", c->C, n_coef);
+  if (lap_mask == 0 || (lap_mask >> c->d) != 0u) return fail(NGD_E_SHAPE, "lap_mask 0x%x is not a nonempty subset of %d coordinates", lap_mask, c->d);
+  for (int i = 0; i < n_coef; ++i)
+    if (!std::isfinite(coef[i])) return fail(NGD_E_SHAPE, "non-finite head coefficient");
+  if (!std::isfinite(kappa)) return fail(NGD_E_SHAPE, "non-finite kappa");
+  Head h{};
+  for (int i = 0; i < n_coef; ++i) h.coef[i] = coef[i];
+  h.kappa = kappa;
+  c->head = h;
+  c->lap_mask = lap_mask;
+  c->lin_valid = false;
+  return NGD_OK;
+}
+
 int ngd_loss(ngd_ctx* c, const double* theta, double* h_loss) {
   TRY(bind(c));
   if (!c->have_points) return fail(NGD_E_STATE, "ngd_set_points has not been called");
   TRY(pack_theta(c, theta, false));
   TRY(forward(c, false));
   return loss_finish(c, h_loss, nullptr, nullptr);
+}
+
+int ngd_h1_error(ngd_ctx* c, const double* theta, const double* exact, double* h_err) {
+  TRY(bind(c));
+  if (!c->have_points) return fail(NGD_E_STATE, "ngd_set_points has not been called");
+  if (c->gm.n_int == 0) return fail(NGD_E_SHAPE, "H1 error needs interior points");
+  const Geom& gm = c->gm;
+  const int64_t n = (int64_t)gm.nib * PB;
+  CK(c->metric_tmp.ensure(sizeof(double) * 2 * n));
+  TRY(pack_theta(c, theta, false));
+  TRY(forward(c, false));
+  double* num = c->metric_tmp.d();
+  double* den = num + n;
+  h1_terms(c->pre_last.d(), gm, exact, num, den, c->stream);
+  dot(c->w_pad.d(), num, n, c->redp.d(), c->counter(0), c->S(SC_H1), nullptr, c->stream);
+  dot(c->w_pad.d(), den, n, c->redp.d(), c->counter(0), c->S(SC_H1 + 1), nullptr, c->stream);
+  TRY(allreduce(c, c->S(SC_H1), 2));
+  CK(cudaMemcpyAsync(c->h_pin, c->S(SC_H1), 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->h_pin[1] == 0.0) return fail(NGD_E_SHAPE, "exact solution has zero H1 norm");
+  *h_err = std::sqrt(c->h_pin[0] / c->h_pin[1]);
+  if (!std::isfinite(*h_err)) return fail(NGD_E_NONFINITE, "non-finite H1 error");
+  return NGD_OK;
 }
 
 int ngd_loss_at(ngd_ctx* c, const double* theta, double alpha, const double* dir, double* h_loss) {
@@ -668,12 +725,26 @@ int ngd_loss_at(ngd_ctx* c, const double* theta, double alpha, const double* dir
 }
 
 int ngd_linearize(ngd_ctx* c, const double* theta, double* h_loss, double* d_metric) {
+  return ngd_linearize_ex(c, theta, nullptr, h_loss, d_metric, nullptr);
+}
+
+int ngd_linearize_ex(ngd_ctx* c, const double* theta, const double* theta_bar, double* h_loss, double* d_metric,
+                     double* d_resid) {
   TRY(bind(c));
   if (!c->have_points) return fail(NGD_E_STATE, "ngd_set_points has not been called");
   c->lin_valid = false;
+  const double* alpha_bar = nullptr;
+  if (theta_bar && theta_bar != theta && c->head.kappa != 0.0) {
+    // metric coefficient frozen at theta_bar (gramian.py:36-40, problems.py:364-368)
+    TRY(pack_theta(c, theta_bar, false));
+    TRY(forward(c, false));
+    frozen_alpha(c->pre_last.d(), c->gm, c->head.kappa, c->alpha_bar.d(), c->stream);
+    alpha_bar = c->alpha_bar.d();
+  }
+  c->lin_frozen = alpha_bar != nullptr;
   TRY(pack_theta(c, theta, true));
   TRY(forward(c, true));
-  TRY(loss_finish(c, h_loss, c->F.d(), c->cot_grad.d()));
+  TRY(loss_finish(c, h_loss, c->F.d(), c->cot_grad.d(), c->dseed.d(), alpha_bar, c->R_pad.d()));
   // reverse sweep over the jets: D_l from D_{l+1}
   const Geom& gm = c->gm;
   for (int l = c->NL - 2; l >= 0; --l) {
@@ -686,6 +757,7 @@ int ngd_linearize(ngd_ctx* c, const double* theta, double* h_loss, double* d_met
     a.s_pad = gm.s_pad;
     a.dbuf = c->dbuf[l].d();
     a.n_pts_pad = gm.n_pts_pad();
+    a.lap_mask = c->lap_mask;
     for (int seg = 0; seg < 2; ++seg) {
       const int CC = seg == 0 ? gm.C : 1;
       a.col0 = seg == 0 ? 0 : gm.int_cols();
@@ -695,6 +767,7 @@ int ngd_linearize(ngd_ctx* c, const double* theta, double* h_loss, double* d_met
     }
   }
   if (d_metric) gather_points(c->F.d(), d_metric, gm, c->stream);
+  if (d_resid) gather_points(c->R_pad.d(), d_resid, gm, c->stream);
   CK(cudaGetLastError());
   c->lin_valid = true;
   return NGD_OK;
@@ -703,6 +776,7 @@ int ngd_linearize(ngd_ctx* c, const double* theta, double* h_loss, double* d_met
 int ngd_loss_grad(ngd_ctx* c, double* d_grad) {
   TRY(bind(c));
   TRY(need_lin(c));
+  if (c->lin_frozen) return fail(NGD_E_STATE, "gradient needs a linearisation with theta_bar == theta");
   return phase_b_all(c, c->cot_grad.d(), 0.0, nullptr, nullptr, d_grad, nullptr);
 }
 

@@ -34,9 +34,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// forward jet nonlinearity (tanh, forward-Laplacian channels)
+// forward jet nonlinearity (tanh, forward-Laplacian channels).
+// The last channel carries Lambda_S = sum_{i in S} d_ii of the coordinate subset
+// S = lap_mask (all coordinates: the Laplacian; heat1p1d: {x}, problems.py:290-292).
 template <int C>
-__device__ __forceinline__ void jet_act(const double (&a)[C], double (&z)[C]) {
+__device__ __forceinline__ void jet_act(const double (&a)[C], double (&z)[C], unsigned mask) {
   const double t = tanh(a[0]);
   z[0] = t;
   if constexpr (C > 1) {
@@ -46,7 +48,7 @@ __device__ __forceinline__ void jet_act(const double (&a)[C], double (&z)[C]) {
 #pragma unroll
     for (int i = 1; i < C - 1; ++i) {
       z[i] = s1 * a[i];
-      q += a[i] * a[i];
+      if ((mask >> (i - 1)) & 1u) q += a[i] * a[i];
     }
     z[C - 1] = s2 * q + s1 * a[C - 1];
   }
@@ -54,7 +56,8 @@ __device__ __forceinline__ void jet_act(const double (&a)[C], double (&z)[C]) {
 
 // reverse of jet_act: adjoints of the outputs -> adjoints of the pre-activations
 template <int C>
-__device__ __forceinline__ void jet_act_rev(const double (&a)[C], const double (&g)[C], double (&o)[C]) {
+__device__ __forceinline__ void jet_act_rev(const double (&a)[C], const double (&g)[C], double (&o)[C],
+                                            unsigned mask) {
   const double t = tanh(a[0]);
   const double s1 = 1.0 - t * t;
   if constexpr (C == 1) {
@@ -65,9 +68,10 @@ __device__ __forceinline__ void jet_act_rev(const double (&a)[C], const double (
     double q = 0.0, s1b = lb * a[C - 1];
 #pragma unroll
     for (int i = 1; i < C - 1; ++i) {
-      q += a[i] * a[i];
+      const bool in_s = (mask >> (i - 1)) & 1u;
+      if (in_s) q += a[i] * a[i];
       s1b += g[i] * a[i];
-      o[i] = g[i] * s1 + 2.0 * lb * s2 * a[i];
+      o[i] = in_s ? g[i] * s1 + 2.0 * lb * s2 * a[i] : g[i] * s1;
     }
     o[C - 1] = lb * s1;
     const double s2b = lb * q;
@@ -175,7 +179,7 @@ __device__ __forceinline__ void jet_tile(const JetArgs& p, const int bx, const i
           }
           if (p.z_out) {
             double z[C];
-            jet_act<C>(v, z);
+            jet_act<C>(v, z, p.lap_mask);
 #pragma unroll
             for (int c = 0; c < C; ++c) p.z_out[cbase + c * PB] = z[c];
           }
@@ -183,7 +187,7 @@ __device__ __forceinline__ void jet_tile(const JetArgs& p, const int bx, const i
           double a[C], o[C];
 #pragma unroll
           for (int c = 0; c < C; ++c) a[c] = p.dbuf[cbase + c * PB];
-          jet_act_rev<C>(a, v, o);
+          jet_act_rev<C>(a, v, o, p.lap_mask);
 #pragma unroll
           for (int c = 0; c < C; ++c) p.dbuf[cbase + c * PB] = o[c];
         }

@@ -47,6 +47,19 @@ struct JetArgs {
   double* partA;       // PHA: [mtiles][n_pts_pad] partial (J v) per point
   int n_pts_pad;
   const int* skip;     // PCG done flag (kernel returns immediately when set)
+  unsigned lap_mask;   // FWD/REV: coordinates summed into the second-derivative channel
+};
+
+// Output head of the interior ("head") rows, SURVEY 8f #3.  With o the output
+// channels (value, d_1..d_d, Lambda_S):
+//   metric row   F = coef . o + alpha_p u      (alpha_p = 3 kappa ubar_p^2, ubar at theta_bar)
+//   residual row R = coef . o + kappa u^3 + off
+// Poisson: coef = e_Lambda, kappa = 0; heat: coef = e_{d_t} - e_Lambda (S = {x});
+// nonlinear Poisson: coef = e_Lambda, kappa = -1 (problems.py:161-385).
+constexpr int kMaxC = 16;
+struct Head {
+  double coef[kMaxC];
+  double kappa;
 };
 
 struct PhbArgs {
@@ -121,8 +134,12 @@ void init_point_data(double* zin1, double* dlast, Geom gm, const double* x_int, 
 int nblocks_for(int64_t n);
 void dot(const double* x, const double* y, int64_t n, double* partials, unsigned int* counter, double* out,
          const int* done, cudaStream_t st);
-void residual_loss(const double* pre_last, Geom gm, const double* w, const double* off, double* F, double* cot,
-                   double* partials, unsigned int* counter, double* loss_sum, cudaStream_t st);
+// residual / loss of the stack; when dseed != null also the metric rows F and the output
+// adjoint seeds (linearisation); alpha_bar != null supplies a frozen per-point 3 kappa ubar^2
+void residual_loss(const double* pre_last, Geom gm, const Head& hd, const double* w_res, const double* off,
+                   const double* alpha_bar, double* F, double* R, double* cot, double* dseed, double* partials,
+                   unsigned int* counter, double* loss_sum, cudaStream_t st);
+void frozen_alpha(const double* pre_last, Geom gm, double kappa, double* alpha, cudaStream_t st);
 void reduce_pha(const double* partA, int rows, int n_pts_pad, const double* w, double* cot, const int* done,
                 cudaStream_t st);
 void reduce_splits(const double* part, const RedPlan& rp, int64_t p, double mu, const double* mu_p, const double* v,
@@ -159,6 +176,7 @@ bool chol_supported(int n);
 cudaError_t chol_upper(double* A, int n, int lda, int* info, cudaStream_t st);
 cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
                              cudaStream_t st);
+void h1_terms(const double* pre_last, Geom gm, const double* exact, double* num, double* den, cudaStream_t st);
 void gather_points(const double* padded, double* compact, Geom gm, cudaStream_t st);
 void scatter_points(const double* compact, double* padded, Geom gm, cudaStream_t st);
 

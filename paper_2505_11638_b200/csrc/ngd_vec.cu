@@ -60,19 +60,6 @@ __global__ void input_jets_kernel(double* z, int64_t s_pad, Geom gm, const doubl
   }
 }
 
-// D_{L+1}: dF/d(output pre-activation jets) = indicator of the metric channel
-// (Laplacian channel on interior points, value channel on boundary points).
-__global__ void seed_adjoint_kernel(double* d, Geom gm) {
-  const int npts = gm.n_pts_pad();
-  for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < npts; pt += gridDim.x * blockDim.x) {
-    if (pt < gm.nib * PB) {
-      for (int c = 0; c < gm.C; ++c) d[col_int(pt, c, gm.C)] = (c == gm.C - 1) ? 1.0 : 0.0;
-    } else {
-      d[gm.int_cols() + (pt - gm.nib * PB)] = 1.0;
-    }
-  }
-}
-
 void init_point_data(double* zin1, double* dlast, Geom gm, const double* x_int, const double* x_bnd,
                      cudaStream_t st) {
   const int npts = gm.n_pts_pad();
@@ -80,9 +67,7 @@ void init_point_data(double* zin1, double* dlast, Geom gm, const double* x_int, 
   probe_before(K_VEC, st);
   input_jets_kernel<<<grid, 256, 0, st>>>(zin1, gm.s_pad, gm, x_int, x_bnd);
   probe_after(K_VEC, st);
-  probe_before(K_VEC, st);
-  seed_adjoint_kernel<<<grid, 256, 0, st>>>(dlast, gm);
-  probe_after(K_VEC, st);
+  (void)dlast;  // output adjoint seeds are written per linearisation (residual_kernel)
 }
 
 // ----------------------- deterministic two-stage sums ------------------------
@@ -148,31 +133,72 @@ void dot(const double* x, const double* y, int64_t n, double* partials, unsigned
   probe_after(K_VEC, st);
 }
 
-// residual / loss: F = metric channel of the output-layer pre-activations;
-// R = F + off;  loss = 0.5 * sum w R R  (problems.py:92-96, 161-166); cot = w R
-__global__ void residual_kernel(const double* pre_last, Geom gm, const double* w, const double* off, double* F,
-                                double* cot, double* partials, unsigned int* slot, double* loss_sum) {
+// residual / loss of the stack (problems.py:92-96, 161-385).  Head rows (interior
+// points, C channels o): F = coef.o + alpha u, R = coef.o + kappa u^3 + off with
+// alpha = 3 kappa ubar^2 (ubar = u at theta unless alpha_bar supplies a frozen
+// theta_bar value); value rows: F = u, R = u + off.  loss = 0.5 sum w_res R^2,
+// cot = w_res R (gradient cotangent: the residual's Jacobian is the metric row
+// frozen at theta).  When linearising, dseed receives dF/d(output jets).
+__global__ void residual_kernel(const double* pre_last, Geom gm, Head hd, const double* w, const double* off,
+                                const double* alpha_bar, double* F, double* R, double* cot, double* dseed,
+                                double* partials, unsigned int* slot, double* loss_sum) {
   const int npts = gm.n_pts_pad();
   double v = 0.0;
   for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < npts; pt += gridDim.x * blockDim.x) {
-    const int64_t col = pt < gm.nib * PB ? col_int(pt, gm.C - 1, gm.C) : gm.int_cols() + (pt - gm.nib * PB);
-    const double f = pre_last[col];
-    const double r = f + off[pt];
+    double f, r;
+    if (pt < gm.nib * PB) {
+      double lin = 0.0;
+      for (int c = 0; c < gm.C; ++c) {
+        const double cc = hd.coef[c];
+        if (cc != 0.0) lin = fma(cc, pre_last[col_int(pt, c, gm.C)], lin);
+      }
+      f = lin;
+      r = lin;
+      double alpha = 0.0;
+      if (hd.kappa != 0.0) {
+        const double u = pre_last[col_int(pt, 0, gm.C)];
+        alpha = alpha_bar ? alpha_bar[pt] : 3.0 * hd.kappa * u * u;
+        f = fma(alpha, u, lin);
+        r = fma(hd.kappa * u * u, u, lin);
+      }
+      if (dseed)
+        for (int c = 0; c < gm.C; ++c) dseed[col_int(pt, c, gm.C)] = hd.coef[c] + (c == 0 ? alpha : 0.0);
+    } else {
+      const int64_t col = gm.int_cols() + (pt - gm.nib * PB);
+      f = r = pre_last[col];
+      if (dseed) dseed[col] = 1.0;
+    }
+    r += off[pt];
     const double wr = w[pt] * r;
     if (F) F[pt] = f;
+    if (R) R[pt] = r;
     if (cot) cot[pt] = wr;
     v = fma(wr, r, v);
   }
   finish_sum(v, partials, slot, loss_sum, [](double s, double* o) { o[0] = s; });
 }
 
-void residual_loss(const double* pre_last, Geom gm, const double* w, const double* off, double* F, double* cot,
-                   double* partials, unsigned int* slot, double* loss_sum, cudaStream_t st) {
+void residual_loss(const double* pre_last, Geom gm, const Head& hd, const double* w_res, const double* off,
+                   const double* alpha_bar, double* F, double* R, double* cot, double* dseed, double* partials,
+                   unsigned int* slot, double* loss_sum, cudaStream_t st) {
   probe_before(K_VEC, st);
-  probe_before(K_VEC, st);
-  residual_kernel<<<nblocks_for(gm.n_pts_pad()), kThreads, 0, st>>>(pre_last, gm, w, off, F, cot, partials, slot,
-                                                                    loss_sum);
+  residual_kernel<<<nblocks_for(gm.n_pts_pad()), kThreads, 0, st>>>(pre_last, gm, hd, w_res, off, alpha_bar, F, R,
+                                                                    cot, dseed, partials, slot, loss_sum);
   probe_after(K_VEC, st);
+}
+
+// alpha[pt] = 3 kappa ubar^2 from a forward pass at theta_bar (problems.py:364-368: ubar frozen)
+__global__ void frozen_alpha_kernel(const double* pre_last, Geom gm, double kappa, double* alpha) {
+  for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < gm.nib * PB; pt += gridDim.x * blockDim.x) {
+    const double u = pre_last[col_int(pt, 0, gm.C)];
+    alpha[pt] = 3.0 * kappa * u * u;
+  }
+}
+
+void frozen_alpha(const double* pre_last, Geom gm, double kappa, double* alpha, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  frozen_alpha_kernel<<<std::max(1, std::min((gm.nib * PB + 255) / 256, 1184)), 256, 0, st>>>(pre_last, gm, kappa,
+                                                                                              alpha);
   probe_after(K_VEC, st);
 }
 
@@ -233,6 +259,33 @@ void add_scaled(double* out, double mu, const double* mu_p, const double* v, int
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
   probe_before(K_VEC, st);
   add_scaled_kernel<<<grid, 256, 0, st>>>(out, mu, mu_p, v, n, done);
+  probe_after(K_VEC, st);
+}
+
+// per-point H1 error terms at the interior points (problems.py:104-119):
+// num = (u - ue)^2 + |grad u - ge|^2, den = ue^2 + |ge|^2; exact = [ue, ge_1..ge_d] per point
+__global__ void h1_terms_kernel(const double* pre_last, Geom gm, const double* exact, double* num, double* den) {
+  for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < gm.nib * PB; pt += gridDim.x * blockDim.x) {
+    double nu = 0.0, de = 0.0;
+    if (pt < gm.n_int) {
+      const double* ex = exact + (int64_t)pt * (gm.d + 1);
+      const double e0 = pre_last[col_int(pt, 0, gm.C)] - ex[0];
+      nu = e0 * e0;
+      de = ex[0] * ex[0];
+      for (int i = 0; i < gm.d; ++i) {
+        const double ei = pre_last[col_int(pt, 1 + i, gm.C)] - ex[1 + i];
+        nu = fma(ei, ei, nu);
+        de = fma(ex[1 + i], ex[1 + i], de);
+      }
+    }
+    num[pt] = nu;
+    den[pt] = de;
+  }
+}
+void h1_terms(const double* pre_last, Geom gm, const double* exact, double* num, double* den, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  h1_terms_kernel<<<std::max(1, std::min((gm.nib * PB + 255) / 256, 1184)), 256, 0, st>>>(pre_last, gm, exact, num,
+                                                                                         den);
   probe_after(K_VEC, st);
 }
 

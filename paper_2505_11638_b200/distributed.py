@@ -50,31 +50,36 @@ def shard_cost(n_int, n_bnd, channels, rank, nranks):
 
 
 class NcclComm:
-    """Binds libngd contexts to an NCCL communicator created from a
-    torch.distributed process group (unique id broadcast from rank 0)."""
+    """Binds libngd contexts to NCCL communicators created from a torch.distributed
+    process group.  Every bound context gets its own communicator: rank 0 makes a
+    fresh unique id per ``bind`` and broadcasts it (all ranks bind in the same order)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
 
+        self.group = group
         self.rank = dist.get_rank(group)
         self.nranks = dist.get_world_size(group)
-        uid = bytearray(128)
+
+    def _unique_id(self):
+        import torch.distributed as dist
+
+        uid = bytes(128)
         if self.rank == 0:
             buf = (ctypes.c_char * 128)()
             _lib.check(_lib.load().ngd_nccl_unique_id(buf))
-            uid = bytearray(buf.raw)
-        obj = [bytes(uid)]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        self.uid = obj[0]
+            uid = bytes(buf.raw)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0, group=self.group)
+        return obj[0]
 
     def bind(self, ctx):
-        ctx.call("ngd_ctx_set_comm", self.uid, self.rank, self.nranks)
+        ctx.call("ngd_ctx_set_comm", self._unique_id(), self.rank, self.nranks)
 
 
 def attach(problem, comm):
     """Make ``problem`` compute on this rank's shard with all-reduced results."""
     problem.shard = (comm.rank, comm.nranks)
     problem.comm = comm
-    problem._ctx = None
-    problem._ctx_quad = None
+    problem._ctxs = []
     return problem

@@ -259,6 +259,5 @@ def nystrom_ngd_run(problem, theta0, config, quad, quad_eval=None, h1_stop=None,
 
 
 def h1_relative_error(problem, theta, quad):
-    """Relative H1 error (problems.py:104-119).  Not yet a device kernel: evaluated
-    from device jets when available; raises otherwise."""
-    raise NotImplementedError("h1_relative_error on the device is not implemented yet")
+    """Relative H1 error (problems.py:104-119), evaluated on the device (ngd_h1_error)."""
+    return problem.h1_relative_error(theta, quad)

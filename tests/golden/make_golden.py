@@ -154,6 +154,47 @@ def case_c4(n):
     return {"x": x, "v": v, "gv": gop.matvec(v)}
 
 
+def _traj(prob, theta, quad, iterations, ell, seed):
+    """Fixed-rank NGD trajectory (adapt_rank patched out, as in case_c1)."""
+    cfg = optim.NystromNgdConfig(ell0=ell, ell_max=ell, cg_maxit=20, kappa=1e-300,
+                                 mu_floor_mode="grad-power", mu_floor_coeff=1e-6,
+                                 mu_floor_exponent=1.0, iterations=iterations, seed=seed)
+    saved = optim.adapt_rank
+    optim.adapt_rank = lambda eigenvalues, mu, ell, ell_max, ratio=10.0: ell
+    try:
+        theta_f, recs = optim.nystrom_ngd_run(prob, theta, cfg, quad)
+    finally:
+        optim.adapt_rank = saved
+    return {"traj_loss": np.array([r.loss for r in recs]), "traj_pcg": np.array([r.pcg_iters for r in recs]),
+            "traj_matvecs": np.array([r.matvecs for r in recs]), "traj_mu": np.array([r.mu for r in recs])}
+
+
+def case_problem(name, widths, n_int, n_bnd, ell):
+    """The reference's other problems (problems.py:128-385) at a small size."""
+    prob = problems.make_problem(name, topology=model.MlpTopology(widths))
+    quad = prob.sample_quadrature(n_int, n_bnd, 0)
+    theta = model.init(prob.topology, 0).values
+    p = theta.shape[0]
+    out = _basic(prob, theta, quad, np.random.default_rng(1).standard_normal(p))
+    out["theta0"] = theta
+    out["residual"] = np.asarray(ad.primal_value(prob.residual_stack(theta, quad)))
+    out["h1"] = np.array(prob.h1_relative_error(theta, quad))
+    # metric frozen at theta_bar != theta (the stop-gradient path, autodiff.py:521-527)
+    theta1 = theta + 0.05 * np.random.default_rng(2).standard_normal(p)
+    out["theta1"] = theta1
+    out["metric_bar"] = np.asarray(ad.primal_value(prob.metric_stack(theta1, ad.freeze(theta), quad)))
+    lin = ad.linearize(lambda th: prob.metric_stack(th, ad.freeze(theta), quad), theta1)
+    out["jvp_bar"] = lin.jvp(out["v"])
+    omega, _ = np.linalg.qr(np.random.default_rng(123).standard_normal((p, 8)), mode="reduced")
+    gop = gramian.GramianOperator.from_problem(prob, theta, quad)
+    out["omega8"] = omega
+    out["y8"] = gop.matmat(omega)
+    t0 = time.time()
+    out.update(_traj(prob, theta, quad, 6, ell, 0))
+    print(f"  {name} 6 NGD steps in {time.time() - t0:.1f}s")
+    return out
+
+
 def main():
     cases = {
         "c1": case_c1,
@@ -161,6 +202,9 @@ def main():
         "c3_sub": lambda: case_nd((5, 128, 128, 128, 1), "sinsum", 256, 64),
         "c5_sub": lambda: case_nd((10, 256, 256, 256, 256, 1), "gauss", 24, 8),
         "c4_sub": lambda: case_c4(96),
+        "poisson1d": lambda: case_problem("poisson1d", (1, 16, 16, 1), 200, 2, 20),
+        "heat1p1d": lambda: case_problem("heat1p1d", (2, 24, 24, 1), 600, 80, 40),
+        "nlpoisson2d": lambda: case_problem("nlpoisson2d", (2, 24, 24, 1), 600, 80, 40),
     }
     only = sys.argv[1:]
     for name, fn in cases.items():

@@ -97,3 +97,51 @@ def test_policy_kats():
     assert O.adapt_rank(np.array([1.0, 0.5, 1e-6]), 1e-3, 3, 50) == 4
     assert O.adapt_rank(np.full(10, 1.0), 1e-6, 10, 10) == 10
     assert O.Topology((3, 32, 32, 1)).param_count == 1217
+
+
+def oracle_problem(name, widths):
+    if name == "poisson1d":
+        return O.PoissonProblem(widths, kind="sin1d")
+    if name == "heat1p1d":
+        return O.HeatProblem(widths)
+    return O.NonlinearPoissonProblem(widths)
+
+
+PROBLEM_CASES = [("poisson1d", (1, 16, 16, 1), 200, 2, 20),
+                 ("heat1p1d", (2, 24, 24, 1), 600, 80, 40),
+                 ("nlpoisson2d", (2, 24, 24, 1), 600, 80, 40)]
+
+
+@pytest.mark.parametrize("name,widths,nint,nbnd,ell", PROBLEM_CASES)
+def test_other_problems_stacks(gold, name, widths, nint, nbnd, ell):
+    """poisson1d / heat1p1d / nlpoisson2d (problems.py:128-385): stacks, loss, gradient,
+    Gramian, the frozen-coefficient metric and H1 error against the live reference."""
+    g = gold(name)
+    prob = oracle_problem(name, widths)
+    quad = prob.sample_quadrature(nint, nbnd, 0)
+    theta = O.init_theta(widths, 0)
+    assert np.array_equal(theta, g["theta0"])
+    assert rel(prob.residual_stack(theta, quad), g["residual"]) <= 1e-13
+    assert prob.loss_value(theta, quad) == pytest.approx(float(g["loss"]), rel=1e-13)
+    assert rel(prob.metric_stack(theta, quad), g["metric"]) <= 1e-13
+    assert rel(prob.loss_grad(theta, quad), g["grad"]) <= 1e-12
+    gop = O.GramianOracle(prob, theta, quad)
+    assert rel(gop.matvec(g["v"]), g["gv"]) <= 1e-12
+    assert rel(gop.matmat(g["omega8"]), g["y8"]) <= 1e-12
+    assert prob.h1_relative_error(theta, quad) == pytest.approx(float(g["h1"]), rel=1e-13)
+    lin = O.Linearization(prob, g["theta1"], quad, "metric", theta_bar=theta)
+    assert rel(lin.value, g["metric_bar"]) <= 1e-13
+    assert rel(lin.jvp(g["v"]), g["jvp_bar"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name,widths,nint,nbnd,ell", PROBLEM_CASES)
+def test_other_problems_trajectory(gold, name, widths, nint, nbnd, ell):
+    g = gold(name)
+    prob = oracle_problem(name, widths)
+    quad = prob.sample_quadrature(nint, nbnd, 0)
+    theta = O.init_theta(widths, 0)
+    cfg = O.NgdConfigOracle(ell0=ell, ell_max=ell, cg_maxit=20, kappa=1e-300, mu_floor_mode="grad-power",
+                            mu_floor_coeff=1e-6, mu_floor_exponent=1.0, iterations=4, seed=0, fixed_rank=True)
+    _, recs = O.nystrom_ngd_run(prob, theta, cfg, quad)
+    np.testing.assert_allclose([r.loss for r in recs], g["traj_loss"][:4], rtol=1e-6)
+    assert [r.pcg_iters for r in recs] == list(g["traj_pcg"][:4].astype(int))
