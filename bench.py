@@ -46,7 +46,8 @@ CONFIGS = {
     "c5": ((10, 256, 256, 256, 256, 1), "gauss", 131072, 16384, 1000, 100),
 }
 KIND_NAMES = {1: "jet_fwd", 2: "jet_rev", 3: "gram_phaseA", 4: "gram_phaseB", 5: "jacobian_rows", 6: "precond",
-              7: "vector", 8: "pack", 9: "jacobi_svd", 10: "cholesky"}
+              7: "vector", 8: "pack", 9: "jacobi_svd", 10: "cholesky", 11: "cublas", 12: "cusolver"}
+OWN_KINDS = tuple(range(1, 11))  # our kernels; 11/12 are library calls (reported, never the roofline kernel)
 
 
 def load_peaks():
@@ -377,7 +378,7 @@ def main():
         ev = tm.events
         parts = {ev[i + 1][0]: ev[i][1].elapsed_time(ev[i + 1][1]) for i in range(len(ev) - 1)}
         print("phases_ms", json.dumps(parts), file=sys.stderr, flush=True)
-        for kind in (1, 2, 3, 4, 5, 6, 7, 8):
+        for kind in KIND_NAMES:
             _lib.check(lib.ngd_probe_start(kind, 4096))
             runner.step()
             tt, cc = _lib.ctypes.c_double(), _lib.ctypes.c_int64()
@@ -396,7 +397,7 @@ def main():
         runner.step()
         torch.cuda.synchronize()
         if time.perf_counter() - t0 < 0.5:
-            for kind in range(1, 11):
+            for kind in KIND_NAMES:
                 _lib.check(lib.ngd_probe_start(kind, 8192))
                 runner.step()
                 tt, cc = _lib.ctypes.c_double(), _lib.ctypes.c_int64()
@@ -405,7 +406,8 @@ def main():
     if args.probe:
         probe_kind = args.probe
     elif class_ms:
-        name = max(class_ms, key=lambda k: class_ms[k][0])
+        own = {KIND_NAMES[k] for k in OWN_KINDS}
+        name = max((k for k in class_ms if k in own), key=lambda k: class_ms[k][0])
         probe_kind = {v: k for k, v in KIND_NAMES.items()}[name]
     else:
         probe_kind = 4

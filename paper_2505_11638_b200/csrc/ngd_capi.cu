@@ -47,12 +47,16 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 #define CKB(x)                                                                                   \
   do {                                                                                           \
+    lib_probe_before(K_BLAS, c->stream);                                                         \
     cublasStatus_t s_ = (x);                                                                     \
+    lib_probe_after(K_BLAS, c->stream);                                                          \
     if (s_ != CUBLAS_STATUS_SUCCESS) return fail(NGD_E_CUDA, "%s:%d %s: cublas status %d", __FILE__, __LINE__, #x, (int)s_); \
   } while (0)
 #define CKS(x)                                                                                   \
   do {                                                                                           \
+    lib_probe_before(K_SOLVER, c->stream);                                                       \
     cusolverStatus_t s_ = (x);                                                                   \
+    lib_probe_after(K_SOLVER, c->stream);                                                        \
     if (s_ != CUSOLVER_STATUS_SUCCESS) return fail(NGD_E_CUDA, "%s:%d %s: cusolver status %d", __FILE__, __LINE__, #x, (int)s_); \
   } while (0)
 #define CKN(x)                                                                                   \
@@ -526,7 +530,8 @@ int ngd_ctx_destroy(ngd_ctx* c) {
   for (auto& e : c->poll_ev)
     if (e) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work}) b->release();
+  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->wr_pad, &c->R_pad, &c->alpha_bar})
+    b->release();
   if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
   if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
   if (c->sol) cusolverDnDestroy(c->sol);
@@ -1209,9 +1214,10 @@ int ngd_small_svd(ngd_ctx* c, const double* A, int32_t ell, double* U, double* s
     if (method == 2)
       CK(jacobi_svd(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(), static_cast<int*>(c->nys_info.p) + 2,
                     c->stream));
-    else
+    else {
       CK(jacobi_svd_block(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(),
                           static_cast<int*>(c->nys_info.p) + 2, c->stream));
+    }
     CK(cudaMemcpyAsync(&c->h_pin[56], static_cast<int*>(c->nys_info.p) + 2, sizeof(int), cudaMemcpyDeviceToHost,
                        c->stream));
   } else {

@@ -9,10 +9,13 @@ namespace ngd {
 
 // kernel classes for launch accounting / probe timing (ngd_probe.cu)
 enum KernelKind {
-  K_FWD = 1, K_REV = 2, K_PHA = 3, K_PHB = 4, K_FORMJ = 5, K_PRECOND = 6, K_VEC = 7, K_PACK = 8, K_SVD = 9, K_CHOL = 10
+  K_FWD = 1, K_REV = 2, K_PHA = 3, K_PHB = 4, K_FORMJ = 5, K_PRECOND = 6, K_VEC = 7, K_PACK = 8, K_SVD = 9, K_CHOL = 10,
+  K_BLAS = 11, K_SOLVER = 12  // library calls (cuBLAS / cuSOLVER): timed, not counted as our launches
 };
 void probe_before(int kind, cudaStream_t st);
 void probe_after(int kind, cudaStream_t st);
+void lib_probe_before(int kind, cudaStream_t st);
+void lib_probe_after(int kind, cudaStream_t st);
 
 // device-side PCG scalars (krylov.py:24-88)
 struct PcgState {

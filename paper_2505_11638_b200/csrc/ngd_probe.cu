@@ -28,6 +28,19 @@ struct Probe {
 Probe g_probe;
 }  // namespace
 
+void lib_probe_before(int kind, cudaStream_t st) {
+  if (kind != g_probe.kind) return;
+  if (g_probe.used + 2 > g_probe.ev.size()) return;
+  if (cudaEventRecord(g_probe.ev[g_probe.used], st) == cudaSuccess) {
+    g_probe.pending = true;
+  } else {
+    cudaGetLastError();
+    ++g_probe.failed;
+  }
+}
+
+void lib_probe_after(int kind, cudaStream_t st) { probe_after(kind, st); }
+
 void probe_before(int kind, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (kind != g_probe.kind) return;

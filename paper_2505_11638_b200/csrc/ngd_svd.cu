@@ -263,45 +263,86 @@ cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, do
 //   super-round 0 also rotates all pairs inside each block (h-1 local rounds),
 //   every super-round rotates all cross pairs of the CTA's two blocks (h local
 //   rounds of h disjoint pairs), then blocks move to the CTA that pairs them in
-//   the next super-round (bulk DSMEM copies into a second buffer, one cluster
-//   barrier).  Rounds per sweep ~ n (as for element-wise Jacobi) but each costs a
-//   __syncthreads, not a cluster barrier + element-wise remote traffic.
-// Columns: X = R^T and V = I, as in jsvd_kernel.
-// DSMEM block copy with 8 remote loads in flight per thread (remote latency ~200+ cycles)
-__device__ __forceinline__ void copy_remote(double2* dst, const double2* src, size_t n, int tid, int T) {
-  size_t e = tid;
-  for (; e + 7 * (size_t)T < n; e += 8 * (size_t)T) {
-    double2 v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = src[e + u * (size_t)T];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) dst[e + u * (size_t)T] = v[u];
-  }
-  for (; e < n; e += T) dst[e] = src[e];
+//   the next super-round.  Columns: X = R^T and V = I, as in jsvd_kernel.
+//
+// Measured on B200 (tools/probe/jsvd_acc.cu, jround.cu): a round costs ~1000
+// cycles of dependent latency for a single warp (partner-column load, Gram
+// butterfly, rotation parameters, update) and ~1500 with 10 warps sharing the
+// SM; an exchange was two cluster barriers plus DSMEM pulls.  Hence: in the
+// cross rounds warp i keeps column i of block 0 (X and V) in registers so only
+// the partner column moves through shared memory; rotation parameters take two
+// rsqrt (plus one Newton step for orthogonality) instead of Rutishauser's
+// rcp/sqrt/rcp/rsqrt chain; blocks move by bulk-async pushes (cp.async.bulk
+// shared::cta -> shared::cluster, completion on the receiver's mbarrier) behind
+// a single cluster barrier.  (Keeping V in L2 and applying each super-round's
+// accumulated rotation with DMMA was measured slower: at one SM's FP64 rate that
+// update costs as much as the direct rotations.)
+#ifdef NGD_SVD_TRACE
+__device__ unsigned long long g_tr[16];
+#define TR_T(v) long long v = clock64()
+#define TR_ADD(k, d) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_tr[k] += (unsigned long long)(d); } while (0)
+#else
+#define TR_T(v)
+#define TR_ADD(k, d)
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ unsigned cluster_addr(unsigned a, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
 }
 
-template <int RPL>  // RPL = double2 per lane per column (rows 2q, 2q+1 for q = lane + 32 u)
-__device__ __forceinline__ bool rotate_pair(double* ci, double* cj, double* vi, double* vj, int ldc, int lane,
-                                            double tol) {
-  const int nq = ldc >> 1;  // double2 per column (ldc even; padding rows are zero)
-  const double2* ci2 = reinterpret_cast<const double2*>(ci);
-  const double2* cj2 = reinterpret_cast<const double2*>(cj);
-  double2 x[RPL], y[RPL];
-#pragma unroll
-  for (int u = 0; u < RPL; ++u) {
-    const int q = lane + 32 * u;
-    const bool in = q < nq;
-    x[u] = in ? ci2[q] : make_double2(0.0, 0.0);
-    y[u] = in ? cj2[q] : make_double2(0.0, 0.0);
+__device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(parity)
+        : "memory");
   }
-  double al = 0.0, be = 0.0, ga = 0.0;
+}
+
+// Jacobi rotation (c, s) annihilating the (al, be, ga) Gram pair: tan(2 theta) = 2 ga / (be - al),
+// |theta| <= pi/4.  cos(2 theta) = |d| / r, sin(2 theta) = sign(d) 2 ga / r, c = sqrt((1 + cos 2theta)/2),
+// s = sin(2 theta) / (2 c): two rsqrt instead of Rutishauser's rcp/sqrt/rcp/rsqrt chain.
+__device__ __forceinline__ void jacobi_cs(double al, double be, double ga, double& c, double& s) {
+  double d = be - al, g2 = 2.0 * ga;
+  const double m = fmax(fabs(d), fabs(g2));
+  if (m > 1e150 || m < 1e-150) {  // keep d^2 + g2^2 representable
+    const double sc = 1.0 / m;
+    d *= sc;
+    g2 *= sc;
+  }
+  const double ri = rsqrt(fma(d, d, g2 * g2));
+  const double cos2 = fabs(d) * ri;
+  const double sin2 = (d < 0.0 ? -g2 : g2) * ri;
+  const double hh = fma(0.5, cos2, 0.5);
+  const double rh = rsqrt(hh);
+  c = hh * rh;
+  s = 0.5 * sin2 * rh;
+  // one Newton step on 1/sqrt(c^2 + s^2): rsqrt is not correctly rounded, and a rotation that is
+  // off-orthogonal by a few ulp would drift column norms over thousands of rotations
+  const double f = fma(-0.5, fma(c, c, fma(s, s, -1.0)), 1.0);
+  c *= f;
+  s *= f;
+}
+
+// warp-wide Gram entries of two register-resident columns
+template <int RPL>
+__device__ __forceinline__ void gram3(const double2 (&x)[RPL], const double2 (&y)[RPL], double& al, double& be,
+                                      double& ga) {
+  al = 0.0;
+  be = 0.0;
+  ga = 0.0;
 #pragma unroll
   for (int u = 0; u < RPL; ++u) {
     al = fma(x[u].x, x[u].x, al);
-    al = fma(x[u].y, x[u].y, al);
     be = fma(y[u].x, y[u].x, be);
-    be = fma(y[u].y, y[u].y, be);
     ga = fma(x[u].x, y[u].x, ga);
+    al = fma(x[u].y, x[u].y, al);
+    be = fma(y[u].y, y[u].y, be);
     ga = fma(x[u].y, y[u].y, ga);
   }
 #pragma unroll
@@ -310,27 +351,59 @@ __device__ __forceinline__ bool rotate_pair(double* ci, double* cj, double* vi, 
     be += __shfl_xor_sync(0xffffffffu, be, o);
     ga += __shfl_xor_sync(0xffffffffu, ga, o);
   }
-  if (!(ga != 0.0 && ga * ga > tol * tol * al * be)) return false;
-  // rotation parameters (Rutishauser); __drcp_rn keeps the divide off the slow path
-  const double zeta = 0.5 * (be - al) * __drcp_rn(ga);
-  const double az = fabs(zeta);
-  const double t = (az > 1e150) ? 0.5 * __drcp_rn(zeta) : copysign(__drcp_rn(az + sqrt(fma(az, az, 1.0))), zeta);
-  const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
-  double2* wi = reinterpret_cast<double2*>(ci);
-  double2* wj = reinterpret_cast<double2*>(cj);
-  double2* pi = reinterpret_cast<double2*>(vi);
-  double2* pj = reinterpret_cast<double2*>(vj);
+}
+
+template <int RPL>
+__device__ __forceinline__ void load_col(double2 (&x)[RPL], const double* col, int nq, int lane) {
+  const double2* c2 = reinterpret_cast<const double2*>(col);
 #pragma unroll
   for (int u = 0; u < RPL; ++u) {
     const int q = lane + 32 * u;
-    if (q < nq) {
-      wi[q] = make_double2(c * x[u].x - s * y[u].x, c * x[u].y - s * y[u].y);
-      wj[q] = make_double2(s * x[u].x + c * y[u].x, s * x[u].y + c * y[u].y);
-      const double2 pv = pi[q], qv = pj[q];
-      pi[q] = make_double2(c * pv.x - s * qv.x, c * pv.y - s * qv.y);
-      pj[q] = make_double2(s * pv.x + c * qv.x, s * pv.y + c * qv.y);
-    }
+    x[u] = q < nq ? c2[q] : make_double2(0.0, 0.0);
   }
+}
+
+template <int RPL>
+__device__ __forceinline__ void store_col(double* col, const double2 (&x)[RPL], int nq, int lane) {
+  double2* c2 = reinterpret_cast<double2*>(col);
+#pragma unroll
+  for (int u = 0; u < RPL; ++u) {
+    const int q = lane + 32 * u;
+    if (q < nq) c2[q] = x[u];
+  }
+}
+
+template <int RPL>
+__device__ __forceinline__ void rot2(double2 (&x)[RPL], double2 (&y)[RPL], double c, double s) {
+#pragma unroll
+  for (int u = 0; u < RPL; ++u) {
+    const double2 a = x[u], b = y[u];
+    x[u] = make_double2(c * a.x - s * b.x, c * a.y - s * b.y);
+    y[u] = make_double2(s * a.x + c * b.x, s * a.y + c * b.y);
+  }
+}
+
+// rotate two shared-memory column pairs (X and V) in place; one warp
+template <int RPL>
+__device__ __forceinline__ bool rotate_pair(double* ci, double* cj, double* vi, double* vj, int ldc, int lane,
+                                            double tol) {
+  const int nq = ldc >> 1;
+  double2 x[RPL], y[RPL];
+  load_col<RPL>(x, ci, nq, lane);
+  load_col<RPL>(y, cj, nq, lane);
+  double al, be, ga;
+  gram3<RPL>(x, y, al, be, ga);
+  if (!(ga != 0.0 && ga * ga > tol * tol * al * be)) return false;
+  double c, s;
+  jacobi_cs(al, be, ga, c, s);
+  rot2<RPL>(x, y, c, s);
+  store_col<RPL>(ci, x, nq, lane);
+  store_col<RPL>(cj, y, nq, lane);
+  load_col<RPL>(x, vi, nq, lane);
+  load_col<RPL>(y, vj, nq, lane);
+  rot2<RPL>(x, y, c, s);
+  store_col<RPL>(vi, x, nq, lane);
+  store_col<RPL>(vj, y, nq, lane);
   return true;
 }
 
@@ -350,20 +423,28 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   const int k = (int)cl.block_rank();
   const int nb = 2 * CL;  // blocks
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ldc = ell + (ell & 1);             // even column stride: 16-B aligned double2 columns
+  const int ldc = ell + (ell & 1);  // even column stride: 16-B aligned double2 columns
+  const int nq = ldc >> 1;
   const size_t slot_sz = (size_t)h * ldc;  // one block of X (or V)
-  // buf[phase][slot][0 = X, 1 = V][h][ell]
-  auto bufp = [&](double* base, int phase, int slot, int which) {
-    return base + ((size_t)(phase * 2 + slot) * 2 + which) * slot_sz;
-  };
-  double* norms = smem + 8 * slot_sz;          // [2][h]
+  // buf[phase][slot][0 = X, 1 = V][h][ldc]; X and V of one (phase, slot) are contiguous
+  auto bufp = [&](int phase, int slot, int which) { return smem + ((size_t)(phase * 2 + slot) * 2 + which) * slot_sz; };
+  double* norms = smem + 8 * slot_sz;                  // [2][h]
   int* flags = reinterpret_cast<int*>(norms + 2 * h);  // [2]
+  __shared__ __align__(8) unsigned long long mbar;    // block arrivals of an exchange
+  __shared__ int held[2];
+  const unsigned mbar_a = smem_u32(&mbar);
+  const unsigned blk_bytes = (unsigned)(2 * slot_sz * sizeof(double));  // X + V of one block
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_a));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
   int phase = 0;
+  unsigned mb_parity = 0;
   int blk[2];
   circle_pair(nb, 0, k, blk[0], blk[1]);
   for (int sl = 0; sl < 2; ++sl) {
-    double* X = bufp(smem, 0, sl, 0);
-    double* V = bufp(smem, 0, sl, 1);
+    double* X = bufp(0, sl, 0);
+    double* V = bufp(0, sl, 1);
     for (int64_t e = tid; e < (int64_t)slot_sz; e += T) {
       const int i = (int)(e / ldc), r = (int)(e % ldc);
       const int j = blk[sl] * h + i;  // global column id
@@ -373,16 +454,56 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   }
   if (tid < 2) flags[tid] = 0;
   cl.sync();
+
+  // move the two held blocks from the placement of round r_from to that of round r_to
+  auto exchange = [&](int r_from, int r_to) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async-proxy reads
+    TR_T(e0);
+    cl.sync();  // all rotations of r_from done everywhere; all phase^1 buffers are free
+    TR_T(e1);
+    TR_ADD(0, e1 - e0);
+    if (tid == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_a), "r"(2 * blk_bytes)
+                   : "memory");
+      for (int sl = 0; sl < 2; ++sl) {
+        int dst_cta = 0, dst_slot = 0;
+        for (int k2 = 0; k2 < CL; ++k2) {
+          int a2, b2;
+          circle_pair(nb, r_to, k2, a2, b2);
+          if (a2 == blk[sl]) { dst_cta = k2; dst_slot = 0; }
+          if (b2 == blk[sl]) { dst_cta = k2; dst_slot = 1; }
+        }
+        const unsigned src = smem_u32(bufp(phase, sl, 0));
+        const unsigned dst = cluster_addr(smem_u32(bufp(phase ^ 1, dst_slot, 0)), dst_cta);
+        const unsigned mb = cluster_addr(mbar_a, dst_cta);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "r"(src), "r"(blk_bytes), "r"(mb)
+            : "memory");
+      }
+    }
+    int want[2];
+    circle_pair(nb, r_to, k, want[0], want[1]);
+    blk[0] = want[0];
+    blk[1] = want[1];
+    phase ^= 1;
+    mbar_wait(mbar_a, mb_parity);
+    mb_parity ^= 1u;
+    TR_T(e2);
+    TR_ADD(1, e2 - e1);
+    TR_ADD(2, 1);
+  };
+
   int sweep = 0;
   bool converged = false;
   for (; sweep < max_sweeps && !converged; ++sweep) {
     const int par = sweep & 1;
     bool rotated = false;
     for (int r = 0; r < nb - 1; ++r) {
-      double* X0 = bufp(smem, phase, 0, 0);
-      double* V0 = bufp(smem, phase, 0, 1);
-      double* X1 = bufp(smem, phase, 1, 0);
-      double* V1 = bufp(smem, phase, 1, 1);
+      double* X0 = bufp(phase, 0, 0);
+      double* V0 = bufp(phase, 0, 1);
+      double* X1 = bufp(phase, 1, 0);
+      double* V1 = bufp(phase, 1, 1);
       if (r == 0) {  // pairs inside each of the two blocks (circle method on h columns)
         for (int rr = 0; rr < h - 1; ++rr) {
           for (int q = warp; q < h; q += NW) {  // h/2 pairs per block, two blocks
@@ -397,36 +518,50 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
           __syncthreads();
         }
       }
-      // cross pairs of the two blocks: h rounds of h disjoint pairs
-      for (int sft = 0; sft < h; ++sft) {
-        for (int i = warp; i < h; i += NW) {
-          const int j = (i + sft >= h) ? i + sft - h : i + sft;
-          rotated |= rotate_pair<RPL>(X0 + (size_t)i * ldc, X1 + (size_t)j * ldc, V0 + (size_t)i * ldc,
-                                      V1 + (size_t)j * ldc, ldc, lane, tol);
+      // cross pairs of the two blocks: h rounds of h disjoint pairs (i, i + sft mod h).  Warp i keeps
+      // column i of block 0 (X and V) in registers; the partner columns move through shared memory.
+      {
+        double2 xr[RPL], vr[RPL];
+        const bool own = warp < h;
+        if (own) {
+          load_col<RPL>(xr, X0 + (size_t)warp * ldc, nq, lane);
+          load_col<RPL>(vr, V0 + (size_t)warp * ldc, nq, lane);
         }
-        __syncthreads();
+        for (int sft = 0; sft < h; ++sft) {
+          TR_T(c0);
+          if (own) {
+            const int j = (warp + sft >= h) ? warp + sft - h : warp + sft;
+            double* yc = X1 + (size_t)j * ldc;
+            double2 y[RPL];
+            load_col<RPL>(y, yc, nq, lane);
+            double al, be, ga;
+            gram3<RPL>(xr, y, al, be, ga);
+            if (ga != 0.0 && ga * ga > tol * tol * al * be) {
+              double c, s;
+              jacobi_cs(al, be, ga, c, s);
+              rot2<RPL>(xr, y, c, s);
+              store_col<RPL>(yc, y, nq, lane);
+              double* vc = V1 + (size_t)j * ldc;
+              load_col<RPL>(y, vc, nq, lane);
+              rot2<RPL>(vr, y, c, s);
+              store_col<RPL>(vc, y, nq, lane);
+              rotated = true;
+            }
+          }
+          TR_T(c1);
+          __syncthreads();
+          TR_T(c2);
+          TR_ADD(3, c1 - c0);
+          TR_ADD(4, c2 - c1);
+          TR_ADD(5, 1);
+        }
+        if (own) {
+          store_col<RPL>(X0 + (size_t)warp * ldc, xr, nq, lane);
+          store_col<RPL>(V0 + (size_t)warp * ldc, vr, nq, lane);
+        }
       }
       if (r == nb - 2) break;  // sweep ends; the exchange to round 0 happens after the convergence test
-      cl.sync();  // every CTA has finished rotating its blocks before anyone pulls them
-      // move blocks to their owners of super-round r+1 (pull from remote current buffers)
-      int want[2];
-      circle_pair(nb, r + 1, k, want[0], want[1]);
-      for (int sl = 0; sl < 2; ++sl) {
-        int src_cta = 0, src_slot = 0;
-        for (int k2 = 0; k2 < CL; ++k2) {
-          int a, b;
-          circle_pair(nb, r, k2, a, b);
-          if (a == want[sl]) { src_cta = k2; src_slot = 0; }
-          if (b == want[sl]) { src_cta = k2; src_slot = 1; }
-        }
-        const double2* srcx = reinterpret_cast<const double2*>(cl.map_shared_rank(bufp(smem, phase, src_slot, 0), src_cta));
-        double2* dst = reinterpret_cast<double2*>(bufp(smem, phase ^ 1, sl, 0));
-        copy_remote(dst, srcx, slot_sz, tid, T);  // X and V blocks are contiguous: 2*slot_sz doubles
-      }
-      cl.sync();
-      phase ^= 1;
-      blk[0] = want[0];
-      blk[1] = want[1];
+      exchange(r, r + 1);
     }
     if (rotated && lane == 0) flags[par] = 1;
     cl.sync();
@@ -434,37 +569,17 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
     for (int o = 0; o < CL; ++o) any |= cl.map_shared_rank(flags, o)[par];
     converged = (any == 0);
     if (tid == 0) flags[par ^ 1] = 0;
-    if (!converged) {  // back to the round-0 placement
-      int want[2];
-      circle_pair(nb, 0, k, want[0], want[1]);
-      for (int sl = 0; sl < 2; ++sl) {
-        int src_cta = 0, src_slot = 0;
-        for (int k2 = 0; k2 < CL; ++k2) {
-          int a, b;
-          circle_pair(nb, nb - 2, k2, a, b);
-          if (a == want[sl]) { src_cta = k2; src_slot = 0; }
-          if (b == want[sl]) { src_cta = k2; src_slot = 1; }
-        }
-        const double2* srcx = reinterpret_cast<const double2*>(cl.map_shared_rank(bufp(smem, phase, src_slot, 0), src_cta));
-        double2* dst = reinterpret_cast<double2*>(bufp(smem, phase ^ 1, sl, 0));
-        copy_remote(dst, srcx, slot_sz, tid, T);
-      }
-      blk[0] = want[0];
-      blk[1] = want[1];
-      phase ^= 1;
-    }
-    cl.sync();
+    if (!converged) exchange(nb - 2, 0);  // back to the round-0 placement
   }
+  __syncthreads();
   // norms of the held columns, ranks over the cluster, outputs
   for (int q = warp; q < 2 * h; q += NW) {
-    const double* c = bufp(smem, phase, q / h, 0) + (size_t)(q % h) * ldc;
+    const double* c = bufp(phase, q / h, 0) + (size_t)(q % h) * ldc;
     double sacc = 0.0;
     for (int r = lane; r < ell; r += 32) sacc = fma(c[r], c[r], sacc);
     sacc = warp_sum(sacc);
     if (lane == 0) norms[q] = sqrt(sacc);
   }
-  // publish which blocks this CTA holds (flags area reused as ints after the loop)
-  __shared__ int held[2];
   if (tid == 0) {
     held[0] = blk[0];
     held[1] = blk[1];
@@ -484,7 +599,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
     for (int off = 16; off > 0; off >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
     if (rank < ell) {
       if (lane == 0) sigma[rank] = sj;
-      const double* v = bufp(smem, phase, q / h, 1) + (size_t)(q % h) * ldc;
+      const double* v = bufp(phase, q / h, 1) + (size_t)(q % h) * ldc;
       for (int r = lane; r < ell; r += 32) U[(int64_t)rank * ldu + r] = v[r];
     }
   }
