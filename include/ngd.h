@@ -136,9 +136,10 @@ int ngd_pcg(ngd_ctx* ctx, const double* d_dense, int64_t p, const double* d_b, d
             int32_t maxit, int32_t recompute_every, double* d_x, ngd_solve_report* h_report);
 
 /* ---- tuning knobs: "svd" = 0 (Householder QR + cuSOLVER gesvdj) | 1 (shifted Cholesky-QR3 + cuSOLVER polar SVD)
- *      | 2 (shifted Cholesky-QR3 + in-house cluster one-sided Jacobi SVD; default, falls back to 1 above ell ~ 700);
+ *      | 2 (shifted Cholesky-QR3 + in-house cluster one-sided Jacobi SVD; default, falls back to 1 above ell = 512);
  *      "graphs" = 1 (replay PCG iterations as a CUDA graph, default) | 0;
- *      "chol" = 1 (in-house one-CTA Cholesky for ell <= 160, default) | 0 (cuSOLVER potrf) */
+ *      "chol" = 1 (in-house one-CTA Cholesky for ell <= 160, default) | 0 (cuSOLVER potrf);
+ *      "trsm" = 1 (in-house DMMA right triangular solve for ell <= 512, default) | 0 (cuBLAS DTRSM) */
 int ngd_set_option(ngd_ctx* ctx, const char* key, int64_t value);
 /* diagnostics: "jacobi_sweeps" (last Nystrom factorisation), "phase_b_splits" */
 int ngd_get_stat(ngd_ctx* ctx, const char* key, int64_t* out);

@@ -148,6 +148,8 @@ struct ngd_ctx {
   std::vector<char> h_work;
   int svd_method = 2;
   int use_own_chol = 1;
+  int use_own_trsm = 1;
+  Buf trsm_work;
   Buf chol_work;
   int last_sweeps = 0;
   int use_graphs = 1;
@@ -375,6 +377,19 @@ static int potrf_upper(ngd_ctx* c, double* A, int n, int* info) {
   return NGD_OK;
 }
 
+// B <- B R^{-1} (B p x ell col-major, R ell x ell upper, lda ell): own DMMA kernel, cuBLAS beyond ell = 512
+static int trsm_right(ngd_ctx* c, double* B, int64_t p, const double* R, int ell) {
+  if (c->use_own_trsm && trsm_supported(ell)) {
+    CK(c->trsm_work.ensure(trsm_work(ell)));
+    CK(trsm_right_upper(B, p, p, R, ell, ell, c->trsm_work.d(), c->stream));
+    return NGD_OK;
+  }
+  const double one = 1.0;
+  CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p, ell,
+                  &one, R, ell, B, (int)p));
+  return NGD_OK;
+}
+
 // Shifted Cholesky-QR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020) in place:
 // B (p x ell, col-major) <- Q, nys_r <- R (upper, ell x ell, col-major).
 static int scholqr3(ngd_ctx* c, double* B, int64_t p, int ell) {
@@ -391,8 +406,7 @@ static int scholqr3(ngd_ctx* c, double* B, int64_t p, int ell) {
     if (pass == 0) shift_diag(W, ell, shift_coef, c->stream);
     TRY(potrf_upper(c, W, ell, info));
     triu(W, ell, ell, c->stream);
-    CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p, ell,
-                    &one, W, ell, B, (int)p));
+    TRY(trsm_right(c, B, p, W, ell));
     if (pass == 0) {
       CK(cudaMemcpyAsync(c->nys_r.d(), W, sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
     } else {
@@ -530,7 +544,7 @@ int ngd_ctx_destroy(ngd_ctx* c) {
   for (auto& e : c->poll_ev)
     if (e) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->wr_pad, &c->R_pad, &c->alpha_bar})
+  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->wr_pad, &c->R_pad, &c->alpha_bar})
     b->release();
   if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
   if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
@@ -906,8 +920,7 @@ int ngd_nystrom_prepare(ngd_ctx* c, double* omega, int64_t p, int32_t ell) {
     CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, omega, (int)p, &zero,
                     c->nys_m.d(), ell));
     TRY(potrf_upper(c, c->nys_m.d(), ell, static_cast<int*>(c->nys_info.p) + 1));
-    CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p,
-                    ell, &one, c->nys_m.d(), ell, omega, (int)p));
+    TRY(trsm_right(c, omega, p, c->nys_m.d(), ell));
   }
   // the potrf status is checked (no extra host sync) together with the sketch Cholesky in ngd_nystrom_finish
   return NGD_OK;
@@ -948,8 +961,7 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
   // sync per sketch; on failure the (discarded) remaining work runs on garbage and NGD_E_CHOL is returned
   CK(cudaMemcpyAsync(&c->h_pin[8], info, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   // 3. B = Y_nu C^{-1}
-  CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p, ell,
-                  &one, c->nys_m.d(), ell, Y, (int)p));
+  TRY(trsm_right(c, Y, p, c->nys_m.d(), ell));
   if (c->svd_method == 0) {
     // 4. B = Q R (Householder)
     CKS(cusolverDnDgeqrf(c->sol, (int)p, ell, Y, (int)p, c->nys_tau.d(), c->nys_work.d(), lw_geqrf, info));
@@ -1252,6 +1264,10 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "graphs")) {
     c->use_graphs = value ? 1 : 0;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "trsm")) {
+    c->use_own_trsm = value ? 1 : 0;
     return NGD_OK;
   }
   if (!strcmp(key, "svd")) {

@@ -10,7 +10,8 @@ namespace ngd {
 // kernel classes for launch accounting / probe timing (ngd_probe.cu)
 enum KernelKind {
   K_FWD = 1, K_REV = 2, K_PHA = 3, K_PHB = 4, K_FORMJ = 5, K_PRECOND = 6, K_VEC = 7, K_PACK = 8, K_SVD = 9, K_CHOL = 10,
-  K_BLAS = 11, K_SOLVER = 12  // library calls (cuBLAS / cuSOLVER): timed, not counted as our launches
+  K_BLAS = 11, K_SOLVER = 12,  // library calls (cuBLAS / cuSOLVER): timed, not counted as our launches
+  K_TRSM = 13
 };
 void probe_before(int kind, cudaStream_t st);
 void probe_after(int kind, cudaStream_t st);
@@ -176,6 +177,11 @@ cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, do
                        cudaStream_t st);
 int jsvd_block_supported(int ell);
 bool chol_supported(int n);
+// X R = A in place (A p x n col-major, R n x n upper col-major); work: trsm_work(n) bytes
+size_t trsm_work(int n);
+bool trsm_supported(int n);
+cudaError_t trsm_right_upper(double* A, int64_t lda, int64_t p, const double* R, int ldr, int n, double* work,
+                             cudaStream_t st);
 cudaError_t chol_upper(double* A, int n, int lda, int* info, cudaStream_t st);
 cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
                              cudaStream_t st);
