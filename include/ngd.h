@@ -135,10 +135,16 @@ int ngd_pcg(ngd_ctx* ctx, const double* d_dense, int64_t p, const double* d_b, d
             const double* d_U, const double* d_eig, int32_t ell, double precond_mu, double rel_tol,
             int32_t maxit, int32_t recompute_every, double* d_x, ngd_solve_report* h_report);
 
+/* upper Cholesky A = U^T U in place (A n x n column-major, upper triangle read/written), the
+ * factorisation inside ngd_nystrom_* exposed for testing: method 0 cuSOLVER potrf, 1 one-CTA
+ * (n <= 160), 2 8-CTA cluster (n <= 512); *h_info = 0 or the first failing pivot + 1 (potrf) */
+int ngd_small_cholesky(ngd_ctx* ctx, double* d_A, int32_t n, int32_t method, int32_t* h_info);
+
 /* ---- tuning knobs: "svd" = 0 (Householder QR + cuSOLVER gesvdj) | 1 (shifted Cholesky-QR3 + cuSOLVER polar SVD)
  *      | 2 (shifted Cholesky-QR3 + in-house cluster one-sided Jacobi SVD; default, falls back to 1 above ell = 512);
  *      "graphs" = 1 (replay PCG iterations as a CUDA graph, default) | 0;
- *      "chol" = 1 (in-house one-CTA Cholesky for ell <= 160, default) | 0 (cuSOLVER potrf);
+ *      "chol" = 1 (in-house: one-CTA Cholesky for ell <= 32, 8-CTA cluster Cholesky up to 512; default)
+ *               | 2 (cluster Cholesky for every ell <= 512) | 0 (cuSOLVER potrf);
  *      "trsm" = 1 (in-house DMMA right triangular solve for ell <= 512, default) | 0 (cuBLAS DTRSM) */
 int ngd_set_option(ngd_ctx* ctx, const char* key, int64_t value);
 /* diagnostics: "jacobi_sweeps" (last Nystrom factorisation), "phase_b_splits" */

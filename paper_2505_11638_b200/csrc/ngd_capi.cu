@@ -366,8 +366,13 @@ static int need_lin(ngd_ctx* c) {
 // Upper Cholesky of a small ell x ell matrix: in-house one-CTA kernel (ngd_chol.cu), cuSOLVER
 // potrf when it does not fit shared memory.  info follows LAPACK (0 ok, j+1 first bad pivot).
 static int potrf_upper(ngd_ctx* c, double* A, int n, int* info) {
-  if (c->use_own_chol && chol_supported(n)) {
+  if (c->use_own_chol == 1 && n <= 32) {  // one CTA: no cluster barriers for a single block
     CK(chol_upper(A, n, n, info, c->stream));
+    return NGD_OK;
+  }
+  if (c->use_own_chol && chol_cluster_supported(n)) {  // 8-CTA cluster, look-ahead
+    CK(c->chol_work.ensure(sizeof(int) * 4));
+    CK(chol_upper_cluster(A, n, n, info, static_cast<int*>(c->chol_work.p), c->stream));
     return NGD_OK;
   }
   int lw = 0;
@@ -1243,6 +1248,32 @@ int ngd_small_svd(ngd_ctx* c, const double* A, int32_t ell, double* U, double* s
   return NGD_OK;
 }
 
+int ngd_small_cholesky(ngd_ctx* c, double* A, int32_t n, int32_t method, int32_t* h_info) {
+  TRY(bind(c));
+  if (n < 1) return fail(NGD_E_SHAPE, "empty matrix");
+  CK(c->nys_info.ensure(sizeof(int) * 4));
+  int* info = static_cast<int*>(c->nys_info.p) + 3;
+  CK(cudaMemsetAsync(info, 0, sizeof(int), c->stream));
+  if (method == 1) {
+    if (!chol_supported(n)) return fail(NGD_E_SHAPE, "n = %d too large for the one-CTA Cholesky", n);
+    CK(chol_upper(A, n, n, info, c->stream));
+  } else if (method == 2) {
+    if (!chol_cluster_supported(n)) return fail(NGD_E_SHAPE, "n = %d too large for the cluster Cholesky", n);
+    CK(c->chol_work.ensure(sizeof(int) * 4));
+    CK(chol_upper_cluster(A, n, n, info, static_cast<int*>(c->chol_work.p), c->stream));
+  } else {
+    const int saved = c->use_own_chol;
+    c->use_own_chol = 0;
+    const int rc = potrf_upper(c, A, n, info);
+    c->use_own_chol = saved;
+    TRY(rc);
+  }
+  CK(cudaMemcpyAsync(&c->h_pin[60], info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  memcpy(h_info, &c->h_pin[60], sizeof(int));
+  return NGD_OK;
+}
+
 int ngd_get_stat(ngd_ctx* c, const char* key, int64_t* out) {
   if (!c || !key || !out) return fail(NGD_E_SHAPE, "bad stat query");
   if (!strcmp(key, "jacobi_sweeps")) {
@@ -1259,7 +1290,8 @@ int ngd_get_stat(ngd_ctx* c, const char* key, int64_t* out) {
 int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(NGD_E_SHAPE, "bad option");
   if (!strcmp(key, "chol")) {
-    c->use_own_chol = value ? 1 : 0;
+    if (value < 0 || value > 2) return fail(NGD_E_SHAPE, "chol must be 0 (cuSOLVER), 1 (auto) or 2 (cluster)");
+    c->use_own_chol = (int)value;
     return NGD_OK;
   }
   if (!strcmp(key, "graphs")) {

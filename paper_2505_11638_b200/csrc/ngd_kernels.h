@@ -183,6 +183,9 @@ bool trsm_supported(int n);
 cudaError_t trsm_right_upper(double* A, int64_t lda, int64_t p, const double* R, int ldr, int n, double* work,
                              cudaStream_t st);
 cudaError_t chol_upper(double* A, int n, int lda, int* info, cudaStream_t st);
+// cluster Cholesky (8 CTAs), n <= 512; flag: one int of device scratch
+bool chol_cluster_supported(int n);
+cudaError_t chol_upper_cluster(double* A, int n, int lda, int* info, int* flag, cudaStream_t st);
 cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
                              cudaStream_t st);
 void h1_terms(const double* pre_last, Geom gm, const double* exact, double* num, double* den, cudaStream_t st);

@@ -61,3 +61,42 @@ def test_small_cholesky_matches_lapack(n):
     r = q.T @ om0
     np.testing.assert_allclose(np.triu(r), r, atol=1e-11)
     np.testing.assert_allclose(np.abs(np.diag(r)), np.abs(np.diag(np.linalg.qr(om0)[1])), rtol=1e-10)
+
+
+@pytest.mark.parametrize("method", [1, 2, 0])
+@pytest.mark.parametrize("n", [1, 5, 31, 32, 33, 100, 160, 300, 512])
+def test_cholesky_kernels(n, method):
+    """ngd_small_cholesky: one-CTA (n <= 160), cluster and cuSOLVER factors agree with LAPACK."""
+    if method == 1 and n > 160:
+        pytest.skip("one-CTA kernel limited to n <= 160")
+    rng = np.random.default_rng(100 + n)
+    g = rng.standard_normal((2 * n + 5, n))
+    a = g.T @ g + 1e-3 * np.eye(n)
+    ctx = utility_context()
+    A = torch.as_tensor(a.T.copy(), device="cuda")  # column-major
+    info = _lib.ctypes.c_int32()
+    ctx.call("ngd_small_cholesky", _lib.ptr(A), n, method, _lib.ctypes.byref(info))
+    assert info.value == 0
+    u = np.triu(A.cpu().numpy().T)
+    ref = np.linalg.cholesky(a).T
+    assert np.linalg.norm(u - ref) <= 1e-12 * np.linalg.norm(ref) * max(1.0, np.linalg.cond(ref))
+    np.testing.assert_allclose(u.T @ u, a, rtol=0, atol=1e-12 * np.abs(a).max())
+
+
+@pytest.mark.parametrize("method", [1, 2, 0])
+@pytest.mark.parametrize("n,k", [(40, 0), (40, 17), (300, 250), (300, 31), (300, 32)])
+def test_cholesky_failure_index(n, k, method):
+    """Non-positive pivot k: info = k + 1 (LAPACK potrf semantics) for every method."""
+    if method == 1 and n > 160:
+        pytest.skip("one-CTA kernel limited to n <= 160")
+    d = np.ones(n)
+    d[k] = -1.0
+    q, _ = np.linalg.qr(np.random.default_rng(n + k).standard_normal((n, n)))
+    # block structure keeps the leading k x k minor positive definite and makes pivot k fail
+    a = np.diag(d)
+    a[:k, :k] = q[:k, :k] @ q[:k, :k].T + np.eye(k)
+    ctx = utility_context()
+    A = torch.as_tensor(a.T.copy(), device="cuda")
+    info = _lib.ctypes.c_int32()
+    ctx.call("ngd_small_cholesky", _lib.ptr(A), n, method, _lib.ctypes.byref(info))
+    assert info.value == k + 1
