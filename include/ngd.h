@@ -108,6 +108,9 @@ int ngd_vjp(ngd_ctx* ctx, const double* d_cot /* n_int + n_bnd */, double* d_out
 /* ---- Gramian (GramianOperator.matvec/matmat, ShiftedOperator; gramian.py:48-61,123-135) */
 int ngd_gram_matvec(ngd_ctx* ctx, const double* d_v, double mu, double* d_out);
 int ngd_gram_matmat(ngd_ctx* ctx, const double* d_V, int64_t ell, int64_t ldv, double* d_Y, int64_t ldy);
+/* dense G = J^T diag(w) J (p x p column-major, ldg >= p), one DSYRK per Jacobian-row chunk
+ * (assemble_dense, gramian.py:138-145; the spectrum of harness.py:237-266) */
+int ngd_gram_dense(ngd_ctx* ctx, double* d_G, int64_t ldg);
 
 /* ---- randomized Nystrom (nystrom_approximate, sketch.py:58-90) ----------
  * prepare: orthonormalise Omega in place (p x ell, col-major).

@@ -58,6 +58,7 @@ SIGNATURES = {
     "ngd_loss": [_P, _P, ctypes.POINTER(_D)],
     "ngd_loss_at": [_P, _P, _D, _P, ctypes.POINTER(_D)],
     "ngd_linearize": [_P, _P, ctypes.POINTER(_D), _P],
+    "ngd_gram_dense": [_P, _P, _I64],
     "ngd_small_cholesky": [_P, _P, _I32, _I32, ctypes.POINTER(_I32)],
     "ngd_h1_error": [_P, _P, _P, ctypes.POINTER(_D)],
     "ngd_linearize_ex": [_P, _P, _P, ctypes.POINTER(_D), _P, _P],

@@ -828,19 +828,21 @@ int ngd_gram_matvec(ngd_ctx* c, const double* v, double mu, double* out) {
 
 // Y = G V by the J-chunk formulation: per point chunk, explicit Jacobian rows
 // Jt (R x p), S = Jt V, Y += Jt^T (w o S)  -- two DGEMMs on FP64 tensor cores.
-int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, double* Y, int64_t ldy) {
-  TRY(bind(c));
-  TRY(need_lin(c));
-  if (ell < 1 || ldv < c->p || ldy < c->p) return fail(NGD_E_SHAPE, "bad matmat shape");
+// explicit Jacobian rows (FormJ) setup shared by the J-chunk sketch and the dense Gramian:
+// chunks of whole point blocks in padded point order (padded points have w = 0)
+struct FormJPlan {
+  FormJArgs fa;
+  int nblk_total, bpc, max_nin, max_nout;
+  int64_t R;
+};
+
+static int formj_plan(ngd_ctx* c, FormJPlan& pl) {
   const Geom& gm = c->gm;
-  // chunks of whole point blocks in padded point order (padded points have w = 0)
   const int nblk_total = gm.nib + gm.nbb;
   const size_t budget = (size_t)8 << 30;  // bytes for one Jacobian chunk
   const int bpc = (int)std::max<int64_t>(1, std::min<int64_t>(nblk_total, (int64_t)(budget / (sizeof(double) * c->p * PB))));
   const int64_t R = (int64_t)bpc * PB;
   CK(c->jt.ensure(sizeof(double) * (size_t)R * c->p));
-  CK(c->smat.ensure(sizeof(double) * (size_t)R * ell));
-  // device tables for FormJ
   const int NL = c->NL;
   const size_t tab_bytes = NL * (2 * sizeof(double*) + 2 * sizeof(int) + sizeof(int64_t)) + 64;
   CK(c->fj_tab.ensure(tab_bytes));
@@ -857,6 +859,7 @@ int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, doubl
     hin[l] = c->w[l];
     hout[l] = c->w[l + 1];
   }
+  // pageable source: the copy is staged before cudaMemcpyAsync returns, so h may go out of scope
   CK(cudaMemcpyAsync(c->fj_tab.p, h.data(), tab_bytes, cudaMemcpyHostToDevice, c->stream));
   char* db = static_cast<char*>(c->fj_tab.p);
   FormJArgs fa{};
@@ -872,12 +875,59 @@ int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, doubl
   fa.n_int = gm.n_int;
   fa.Jt = c->jt.d();
   fa.ldj = c->p;
-  const double one = 1.0, zero = 0.0;
   int max_nin = 1, max_nout = 1;
   for (int l = 0; l < NL; ++l) {
     max_nin = std::max(max_nin, c->w[l]);
     max_nout = std::max(max_nout, c->w[l + 1]);
   }
+  pl.fa = fa;
+  pl.nblk_total = nblk_total;
+  pl.bpc = bpc;
+  pl.R = R;
+  pl.max_nin = max_nin;
+  pl.max_nout = max_nout;
+  return NGD_OK;
+}
+
+// G = J^T diag(w) J assembled densely: per chunk, Jacobian rows scaled by sqrt(w), one DSYRK
+// (gramian.py:138-145 assembles column by column; the spectrum dump of harness.py:237-266 uses it)
+int ngd_gram_dense(ngd_ctx* c, double* G, int64_t ldg) {
+  TRY(bind(c));
+  TRY(need_lin(c));
+  if (ldg < c->p) return fail(NGD_E_SHAPE, "ldg < p");
+  FormJPlan pl;
+  TRY(formj_plan(c, pl));
+  const double one = 1.0;
+  for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
+    const int nb = std::min(pl.bpc, pl.nblk_total - b0);
+    const int64_t r = (int64_t)nb * PB;
+    const int64_t q0 = (int64_t)b0 * PB;
+    pl.fa.blk0 = b0;
+    CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));
+    scale_cols_sqrt(c->jt.d(), c->p, r, c->w_pad.d() + q0, c->stream);
+    const double beta = (q0 == 0) ? 0.0 : 1.0;
+    CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, (int)c->p, (int)r, &one, c->jt.d(), (int)c->p,
+                    &beta, G, (int)ldg));
+  }
+  symmetrize_upper(G, c->p, ldg, c->stream);
+  if (c->nranks > 1) {
+    if (ldg != c->p) return fail(NGD_E_SHAPE, "multi-rank dense Gramian needs ldg == p");
+    TRY(allreduce(c, G, (size_t)c->p * c->p));
+  }
+  CK(cudaGetLastError());
+  return NGD_OK;
+}
+
+int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, double* Y, int64_t ldy) {
+  TRY(bind(c));
+  TRY(need_lin(c));
+  if (ell < 1 || ldv < c->p || ldy < c->p) return fail(NGD_E_SHAPE, "bad matmat shape");
+  FormJPlan pl;
+  TRY(formj_plan(c, pl));
+  CK(c->smat.ensure(sizeof(double) * (size_t)pl.R * ell));
+  FormJArgs& fa = pl.fa;
+  const int nblk_total = pl.nblk_total, bpc = pl.bpc, max_nin = pl.max_nin, max_nout = pl.max_nout, NL = c->NL;
+  const double one = 1.0, zero = 0.0;
   for (int b0 = 0; b0 < nblk_total; b0 += bpc) {
     const int nb = std::min(bpc, nblk_total - b0);
     const int64_t r = (int64_t)nb * PB;

@@ -614,6 +614,32 @@ void scale_rows(double* S, int64_t R, int ell, const double* w, cudaStream_t st)
   probe_after(K_VEC, st);
 }
 
+// Jt (p x R column-major, one Jacobian row per column) columns scaled by sqrt(w)
+__global__ void scale_cols_sqrt_kernel(double* J, int64_t p, int64_t R, const double* w) {
+  const int64_t n = p * R;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    J[i] *= sqrt(w[i / p]);
+}
+void scale_cols_sqrt(double* J, int64_t p, int64_t R, const double* w, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  scale_cols_sqrt_kernel<<<vgrid(p * R), 256, 0, st>>>(J, p, R, w);
+  probe_after(K_VEC, st);
+}
+
+// lower triangle <- upper triangle
+__global__ void symmetrize_upper_kernel(double* G, int64_t n, int64_t ld) {
+  const int64_t tot = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % n, j = e / n;  // element (i, j), column-major
+    if (i > j) G[j * ld + i] = G[i * ld + j];
+  }
+}
+void symmetrize_upper(double* G, int64_t n, int64_t ld, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  symmetrize_upper_kernel<<<vgrid(n * n), 256, 0, st>>>(G, n, ld);
+  probe_after(K_VEC, st);
+}
+
 // y += shift * omega where shift = eps * sqrt(*fro2)  (sketch.py:77-78); writes shift
 __global__ void shift_kernel(double* y, const double* omega, int64_t n, const double* fro2, double* shift_out) {
   const double shift = 2.220446049250313e-16 * sqrt(*fro2);

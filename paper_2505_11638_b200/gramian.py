@@ -171,10 +171,19 @@ class ShiftedOperator:
 
 
 def assemble_dense(op, guard=DENSE_GUARD):
-    """Assemble an operator column by column (gramian.py:138-145): one matmat of I."""
+    """Assemble an operator densely (gramian.py:138-145).  A Gramian is formed as
+    J^T diag(w) J from explicit Jacobian rows with one DSYRK per row chunk
+    (ngd_gram_dense); other operators by one matmat of I.  numpy in -> numpy out."""
     p = op.dim
     if p > guard:
         raise ValueError(f"dense assembly guard: p={p} exceeds {guard}")
+    if isinstance(op, GramianOperator):
+        torch = _lib.torch_mod()
+        op._ensure()
+        G = torch.empty((p, p), dtype=torch.float64, device=op.ctx.device)
+        op.ctx.call("ngd_gram_dense", _lib.ptr(G), p)
+        op.matvec_count += p
+        return G.cpu().numpy()
     if hasattr(op, "matmat"):
         return np.asarray(_lib.like_input(_lib.to_device(op.matmat(np.eye(p))), np.eye(1)))
     return np.column_stack([op.matvec(np.eye(p)[:, i]) for i in range(p)])

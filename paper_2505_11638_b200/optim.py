@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .gramian import GramianOperator, ShiftedOperator
+from .gramian import DENSE_GUARD, GramianOperator, ShiftedOperator, assemble_dense
 from .krylov import pcg
 from .sketch import NystromPreconditioner, nystrom_approximate
 
@@ -261,3 +261,212 @@ def nystrom_ngd_run(problem, theta0, config, quad, quad_eval=None, h1_stop=None,
 def h1_relative_error(problem, theta, quad):
     """Relative H1 error (problems.py:104-119), evaluated on the device (ngd_h1_error)."""
     return problem.h1_relative_error(theta, quad)
+
+
+# ---------------------------------------------------------------------------
+# Baselines of the reference's comparison protocol (optim.py:273-455), on the same
+# device path: NGD-CG (unpreconditioned PCG on the Gramian), dense NGD
+# (assembled Gramian, pseudoinverse), gradient descent and dense BFGS.
+# ---------------------------------------------------------------------------
+
+
+def _baseline_mu(loss, cap=1e-5):  # optim.py:273-275
+    return max(min(cap, loss), 1e-14)
+
+
+class _DeviceIterate:
+    """theta on the device plus the context helpers the baselines share with the runner."""
+
+    def __init__(self, problem, theta0, quad):
+        torch = _lib.torch_mod()
+        self.problem, self.quad = problem, quad
+        self.theta = _lib.to_device(theta0).clone()
+        self.p = self.theta.shape[0]
+        self.ctx = problem.context(quad)
+        self.grad = torch.empty_like(self.theta)
+        self.cand = torch.empty_like(self.theta)
+
+    def loss_at(self, th, alpha, direction):
+        out = _lib.ctypes.c_double()
+        self.ctx.call("ngd_loss_at", _lib.ptr(th), float(alpha), _lib.ptr(direction), _lib.ctypes.byref(out))
+        return float(out.value)
+
+    def dot(self, a, b):
+        out = _lib.ctypes.c_double()
+        self.ctx.call("ngd_dot", _lib.ptr(a), _lib.ptr(b), self.p, _lib.ctypes.byref(out))
+        return float(out.value)
+
+    def linearize(self):
+        """Gramian operator at theta (one linearisation), loss and gradient."""
+        gop = GramianOperator.from_problem(self.problem, self.theta, self.quad)
+        if not np.isfinite(gop.loss):
+            raise _lib.NonFiniteError("non-finite loss")
+        self.ctx.call("ngd_loss_grad", _lib.ptr(self.grad))
+        return gop, gop.loss, self.grad
+
+    def loss_grad(self, th):
+        self.problem.linearize(th, self.quad)
+        self.ctx.call("ngd_loss_grad", _lib.ptr(self.grad))
+        return self.grad.clone()
+
+    def step(self, direction, grad_dot_dir, loss0):
+        """Armijo line search along -direction and update (default line-search knobs, optim.py:121)."""
+        alpha, _ = backtracking_linesearch(self.theta, direction, self.loss_at, grad_dot_dir, loss0=loss0)
+        if alpha > 0.0:
+            self.ctx.call("ngd_axpy", _lib.ptr(self.theta), float(alpha), _lib.ptr(direction), _lib.ptr(self.cand),
+                          self.p)
+            self.theta, self.cand = self.cand, self.theta
+        return alpha
+
+
+def _h1(problem, theta, quad_eval):
+    return float("nan") if quad_eval is None else problem.h1_relative_error(theta, quad_eval)
+
+
+def ngd_cg_step(problem, theta, quad, mu, kappa, maxit_total, loss_fn=None):
+    """One matrix-free NGD step solved with plain CG, no preconditioner (optim.py:278-292).
+    Returns (theta_next, SolveReport, matvecs)."""
+    it = _DeviceIterate(problem, theta, quad)
+    gop, loss, g = it.linearize()
+    gnorm = float(np.sqrt(it.dot(g, g)))
+    report = pcg(ShiftedOperator(gop, mu), g, _cg_rel_tol(kappa, gnorm), maxit_total)
+    d = _lib.to_device(report.solution)
+    it.step(d, it.dot(g, d), loss)
+    return _lib.like_input(it.theta, theta), report, gop.matvec_count
+
+
+def ngd_cg_run(problem, theta0, config, quad, quad_eval=None, matvec_budget=None):
+    """Unpreconditioned NGD-CG baseline (optim.py:295-327): CG capped at cg_maxit + ell_max."""
+    it = _DeviceIterate(problem, theta0, quad)
+    maxit_total = config.cg_maxit + _resolve_ell_max(config, it.p)
+    records, total = [], 0
+    for k in range(config.iterations):
+        tic = time.perf_counter()
+        gop, loss, g = it.linearize()
+        mu = _baseline_mu(loss)
+        gnorm = float(np.sqrt(it.dot(g, g)))
+        report = pcg(ShiftedOperator(gop, mu), g, _cg_rel_tol(config.kappa, gnorm), maxit_total)
+        d = _lib.to_device(report.solution)
+        it.step(d, it.dot(g, d), loss)
+        total += gop.matvec_count
+        records.append(RunRecord(k, loss, _h1(problem, it.theta, quad_eval), mu, 0, report.iterations, total,
+                                 time.perf_counter() - tic))
+        if matvec_budget is not None and total >= matvec_budget:
+            break
+    return _lib.like_input(it.theta, theta0), records
+
+
+def _pinv_solve(matrix, rhs):
+    """Pseudoinverse solve of a symmetric matrix with the numerical-rank cutoff p eps s_1
+    (optim.py:350-355), by a device eigendecomposition (SVD of a symmetric matrix = |eig|)."""
+    torch = _lib.torch_mod()
+    lam, vec = torch.linalg.eigh(matrix)
+    s = lam.abs()
+    cutoff = matrix.shape[0] * EPS_MACH * float(s.max())
+    inv = torch.where(s > cutoff, 1.0 / torch.where(s > cutoff, lam, torch.ones_like(lam)), torch.zeros_like(lam))
+    return vec @ (inv * (vec.T @ rhs))
+
+
+def ngd_dense_step(problem, theta, quad, mu, guard=DENSE_GUARD):
+    """One NGD step with the assembled (G + mu I) and its pseudoinverse (optim.py:330-341)."""
+    torch = _lib.torch_mod()
+    it = _DeviceIterate(problem, theta, quad)
+    gop, loss, g = it.linearize()
+    dense = _lib.to_device(assemble_dense(gop, guard=guard)) + mu * torch.eye(gop.dim, dtype=torch.float64,
+                                                                                device=g.device)
+    d = _pinv_solve(dense, g).contiguous()
+    it.step(d, it.dot(g, d), loss)
+    return _lib.like_input(it.theta, theta), _lib.like_input(d, theta)
+
+
+def ngd_dense_run(problem, theta0, config, quad, quad_eval=None):
+    """Dense NGD baseline (optim.py:358-380)."""
+    torch = _lib.torch_mod()
+    it = _DeviceIterate(problem, theta0, quad)
+    records, total = [], 0
+    for k in range(config.iterations):
+        tic = time.perf_counter()
+        gop, loss, g = it.linearize()
+        mu = _baseline_mu(loss)
+        dense = _lib.to_device(assemble_dense(gop)) + mu * torch.eye(it.p, dtype=torch.float64, device=g.device)
+        d = _pinv_solve(dense, g).contiguous()
+        it.step(d, it.dot(g, d), loss)
+        total += it.p
+        records.append(RunRecord(k, loss, _h1(problem, it.theta, quad_eval), mu, 0, 0, total,
+                                 time.perf_counter() - tic))
+    return _lib.like_input(it.theta, theta0), records
+
+
+def gradient_descent_step(problem, theta, quad):
+    """Plain gradient descent with Armijo backtracking (optim.py:383-388)."""
+    it = _DeviceIterate(problem, theta, quad)
+    _, loss, g = it.linearize()
+    it.step(g, it.dot(g, g), loss)
+    return _lib.like_input(it.theta, theta)
+
+
+def gradient_descent_run(problem, theta0, config, quad, quad_eval=None):
+    """optim.py:391-411"""
+    it = _DeviceIterate(problem, theta0, quad)
+    records = []
+    for k in range(config.iterations):
+        tic = time.perf_counter()
+        _, loss, g = it.linearize()
+        it.step(g, it.dot(g, g), loss)
+        records.append(RunRecord(k, loss, _h1(problem, it.theta, quad_eval), 0.0, 0, 0, 0,
+                                 time.perf_counter() - tic))
+    return _lib.like_input(it.theta, theta0), records
+
+
+def bfgs_update(h, s, y):
+    """Inverse-Hessian BFGS update (optim.py:149-162); skipped when s^T y <= 0."""
+    torch = _lib.torch_mod()
+    sy = float(s @ y)
+    if sy <= 0.0:
+        return h
+    rho = 1.0 / sy
+    hy = h @ y
+    coeff = rho + rho**2 * float(y @ hy)
+    return h + coeff * torch.outer(s, s) - rho * (torch.outer(hy, s) + torch.outer(s, hy))
+
+
+def bfgs_run(problem, theta0, config, quad, quad_eval=None, guard=5000):
+    """Dense BFGS baseline (optim.py:414-438), inverse Hessian resident on the device."""
+    torch = _lib.torch_mod()
+    it = _DeviceIterate(problem, theta0, quad)
+    if it.p > guard:
+        raise ValueError(f"dense BFGS guard: p={it.p} exceeds {guard}")
+    h = torch.eye(it.p, dtype=torch.float64, device=it.theta.device)
+    g = it.loss_grad(it.theta)
+    records = []
+    for k in range(config.iterations):
+        tic = time.perf_counter()
+        loss = it.loss_at(it.theta, 0.0, g)
+        d = (h @ g).contiguous()
+        prev = it.theta.clone()
+        alpha = it.step(d, it.dot(g, d), loss)
+        if alpha > 0.0:
+            g_next = it.loss_grad(it.theta)
+            h = bfgs_update(h, it.theta - prev, g_next - g)
+            g = g_next
+        records.append(RunRecord(k, loss, _h1(problem, it.theta, quad_eval), 0.0, 0, 0, 0,
+                                 time.perf_counter() - tic))
+    return _lib.like_input(it.theta, theta0), records
+
+
+OPTIMIZER_NAMES = ("nystrom_ngd", "ngd_cg", "ngd_dense", "gd", "bfgs")
+
+_RUNNERS = {
+    "nystrom_ngd": nystrom_ngd_run,
+    "ngd_cg": ngd_cg_run,
+    "ngd_dense": ngd_dense_run,
+    "gd": gradient_descent_run,
+    "bfgs": bfgs_run,
+}
+
+
+def run_optimizer(name, problem, theta0, config, quad, quad_eval=None):
+    """Dispatch by name (optim.py:441-455)."""
+    if name not in _RUNNERS:
+        raise KeyError(f"unknown optimizer {name!r}; available: {OPTIMIZER_NAMES}")
+    return _RUNNERS[name](problem, theta0, config, quad, quad_eval=quad_eval)

@@ -195,6 +195,26 @@ def case_problem(name, widths, n_int, n_bnd, ell):
     return out
 
 
+def case_baselines():
+    """The reference's baseline optimizers (optim.py:273-455) and spectrum (harness.py:237-266)."""
+    from nystromngd import harness
+    widths = (2, 8, 8, 1)
+    prob = problems.make_problem("poisson2d", topology=model.MlpTopology(widths))
+    quad = prob.sample_quadrature(200, 40, 0)
+    theta = model.init(prob.topology, 0).values
+    cfg = optim.NystromNgdConfig(ell0=10, ell_max=40, cg_maxit=20, iterations=4, seed=0)
+    out = {"theta0": theta}
+    for name in ("ngd_cg", "ngd_dense", "gd", "bfgs"):
+        _, recs = optim.run_optimizer(name, prob, theta, cfg, quad, quad_eval=quad)
+        out[f"{name}_loss"] = np.array([r.loss for r in recs])
+        out[f"{name}_h1"] = np.array([r.h1_rel_error for r in recs])
+        out[f"{name}_mu"] = np.array([r.mu for r in recs])
+        out[f"{name}_pcg"] = np.array([r.pcg_iters for r in recs])
+        out[f"{name}_matvecs"] = np.array([r.matvecs for r in recs])
+    out["spectrum"] = harness.gramian_spectrum(prob, theta, quad, top=30)
+    return out
+
+
 def main():
     cases = {
         "c1": case_c1,
@@ -205,6 +225,7 @@ def main():
         "poisson1d": lambda: case_problem("poisson1d", (1, 16, 16, 1), 200, 2, 20),
         "heat1p1d": lambda: case_problem("heat1p1d", (2, 24, 24, 1), 600, 80, 40),
         "nlpoisson2d": lambda: case_problem("nlpoisson2d", (2, 24, 24, 1), 600, 80, 40),
+        "baselines": case_baselines,
     }
     only = sys.argv[1:]
     for name, fn in cases.items():

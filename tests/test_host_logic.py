@@ -103,3 +103,18 @@ def test_shard_plan_partitions_points(n_int, n_bnd, nranks):
         costs.append(distributed.shard_cost(n_int, n_bnd, 12, r, nranks))
     assert seen_i == list(range(n_int)) and seen_b == list(range(n_bnd))
     assert max(costs) - min(costs) <= 13
+
+
+def test_harness_config_parsing():
+    """harness.parse_config (harness.py:123-146): comments, types, gamma = p, errors."""
+    from paper_2505_11638_b200 import harness
+
+    cfg = harness.parse_config("# comment\nproblem = heat1p1d  # trailing\niterations = 7\nkappa = 0.5\ngamma = p\n\n")
+    assert (cfg.problem, cfg.iterations, cfg.kappa, cfg.gamma) == ("heat1p1d", 7, 0.5, None)
+    assert harness.parse_config("gamma = 3.5").gamma == 3.5
+    for bad in ("nonsense", "colour = red", "iterations = 1\niterations = 2", "problem = stokes3d",
+                "optimizer = adam", "repetitions = 0"):
+        with pytest.raises(ValueError):
+            harness.parse_config(bad)
+    oc = cfg.optimizer_config(seed=4)
+    assert oc.seed == 4 and oc.kappa == 0.5 and oc.iterations == 7
