@@ -46,8 +46,8 @@ CONFIGS = {
     "c5": ((10, 256, 256, 256, 256, 1), "gauss", 131072, 16384, 1000, 100),
 }
 KIND_NAMES = {1: "jet_fwd", 2: "jet_rev", 3: "gram_phaseA", 4: "gram_phaseB", 5: "jacobian_rows", 6: "precond",
-              7: "vector", 8: "pack", 9: "jacobi_svd", 10: "cholesky", 11: "cublas", 12: "cusolver", 13: "trsm"}
-OWN_KINDS = tuple(range(1, 11)) + (13,)  # our kernels; 11/12 are library calls (reported, never the roofline kernel)
+              7: "vector", 8: "pack", 9: "jacobi_svd", 10: "cholesky", 11: "cublas", 12: "cusolver", 13: "trsm", 14: "fused_matvec"}
+OWN_KINDS = tuple(range(1, 11)) + (13, 14)  # our kernels; 11/12 are library calls (reported, never the roofline kernel)
 
 
 def load_peaks():
@@ -263,6 +263,8 @@ def roofline_entry(kind, widths, n_int, n_bnd, ell, p, sweeps, count, total_ms, 
         work = 9.0 * ell * ell * (ell - 1) * max(sweeps, 1)
     elif kind == 10:
         work = ell ** 3 / 3.0
+    elif kind == 14:  # fused narrow matvec: one launch = one full J^T diag(w) J v
+        work = 4.0 * pw * S
     elif kind == 13:  # right triangular solve p x ell (2 launches: diagonal-block inverse + solve): p ell^2 FLOP
         work = p * ell * ell / 2.0
     else:  # memory-bound classes

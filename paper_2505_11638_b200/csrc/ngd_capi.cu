@@ -76,8 +76,16 @@ inline int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool view = false;  // points into another Buf (never freed here)
+  void set_view(void* ptr, size_t n) {
+    release();
+    p = ptr;
+    bytes = n;
+    view = true;
+  }
   cudaError_t ensure(size_t n) {
     if (n <= bytes) return cudaSuccess;
+    if (view) return cudaErrorInvalidValue;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -86,9 +94,10 @@ struct Buf {
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p && !view) cudaFree(p);
     p = nullptr;
     bytes = 0;
+    view = false;
   }
   double* d() const { return static_cast<double*>(p); }
 };
@@ -133,6 +142,16 @@ struct ngd_ctx {
   unsigned lap_mask = 0;
   std::vector<Buf> zin, dbuf;  // per layer
   Buf dseed, pre_last, zs0, zs1;
+  Buf jets;  // arena behind zin / dbuf / dseed
+  int use_fused = 0;  // opt-in: measured slower than the two-phase path at C1/C2
+  bool fused_ok = false;
+  int fgrid = 0;
+  Buf partF;
+  RedPlan rplan_f{};
+  int use_l2_window = 1;
+  int l2_window_max = 0;
+  bool l2_attr_set = false;
+  cudaStreamAttrValue l2_attr{};
   Buf partA, partB;
   Buf redp;         // reduction partials
   Buf counters;     // unsigned counters
@@ -351,7 +370,56 @@ static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* m
   return NGD_OK;
 }
 
+// fused narrow-network matvec (ngd_fused.cu): one kernel writes per-CTA partials into partF
+static int fused_partials(ngd_ctx* c, const double* v, const int* skip) {
+  const Geom& gm = c->gm;
+  FusedArgs a{};
+  a.v = v;
+  int vt = 0;
+  for (int l = 0; l < c->NL; ++l) {
+    a.Z[l] = c->zin[l].d();
+    a.D[l] = (l == c->NL - 1) ? c->dseed.d() : c->dbuf[l].d();
+    a.n_in[l] = c->w[l];
+    a.n_out[l] = c->w[l + 1];
+    a.woff[l] = c->woff[l];
+    a.boff[l] = c->boff[l];
+    const int k4 = (int)rup(c->w[l], 4);
+    a.vs[l] = (k4 + 27) / 32 * 32 + 4;  // == 4 (mod 32): conflict-free DMMA A fragments
+    const int mr = (int)rup(c->w[l + 1], 8);
+    a.vso[l] = vt;
+    vt += mr * a.vs[l];
+    a.vbo[l] = vt;
+    vt += mr;
+  }
+  a.v_total = (vt + 1) & ~1;
+  a.n_layers = c->NL;
+  a.C = gm.C;
+  a.nib = gm.nib;
+  a.nbb = gm.nbb;
+  a.s_pad = gm.s_pad;
+  a.int_cols = gm.int_cols();
+  a.w = c->w_pad.d();
+  a.part = c->partF.d();
+  a.p = c->p;
+  a.skip = skip;
+  CK(fused_mv(a, c->fgrid, c->stream));
+  return NGD_OK;
+}
+
 static int gram_mv(ngd_ctx* c, const double* v, double mu, const double* mu_p, double* out, const int* skip) {
+  if (c->fused_ok) {
+    TRY(fused_partials(c, v, skip));
+    const bool shifted = v && (mu_p || mu != 0.0);
+    if (c->nranks > 1) {
+      reduce_splits(c->partF.d(), c->rplan_f, c->p, 0.0, nullptr, nullptr, out, skip, c->stream);
+      TRY(allreduce(c, out, c->p));
+      if (shifted) add_scaled(out, mu, mu_p, v, c->p, skip, c->stream);
+    } else {
+      reduce_splits(c->partF.d(), c->rplan_f, c->p, mu, mu_p, shifted ? v : nullptr, out, skip, c->stream);
+    }
+    CK(cudaGetLastError());
+    return NGD_OK;
+  }
   TRY(phase_a(c, v, c->w_pad.d(), c->cot.d(), skip));
   TRY(phase_b_all(c, c->cot.d(), mu, mu_p, v, out, skip));
   return NGD_OK;
@@ -437,6 +505,33 @@ static int small_svd_polar(ngd_ctx* c, int ell) {
   CKS(cusolverDnXgesvdp(c->sol, c->dn_params, CUSOLVER_EIG_MODE_VECTOR, 1, ell, ell, CUDA_R_64F, c->nys_r.d(), ell,
                         CUDA_R_64F, c->nys_s.d(), CUDA_R_64F, c->nys_ur.d(), ell, CUDA_R_64F, c->nys_v.d(), ell,
                         CUDA_R_64F, c->nys_work.p, wd, c->h_work.data(), wh, static_cast<int*>(c->nys_info.p), &err));
+  return NGD_OK;
+}
+
+// L2 persisting window over the jets arena (B200: 79 MB persisting capacity, 128 MB max window)
+static int set_l2_window(ngd_ctx* c, void* base, size_t bytes) {
+  if (!c->use_l2_window) return NGD_OK;
+  static int persist_max = -1;
+  if (persist_max < 0) {
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, c->device));
+    persist_max = prop.persistingL2CacheMaxSize;
+    if (persist_max > 0) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_max));
+    c->l2_window_max = prop.accessPolicyMaxWindowSize;
+  }
+  if (persist_max <= 0) return NGD_OK;
+  cudaStreamAttrValue attr{};
+  const size_t win = std::min(bytes, (size_t)std::max(c->l2_window_max, 1));
+  attr.accessPolicyWindow.base_ptr = base;
+  attr.accessPolicyWindow.num_bytes = win;
+  attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist_max / (double)win);
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  if (c->stream && cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess)
+    cudaGetLastError();
+  if (c->cap_stream) CK(cudaStreamSetAttribute(c->cap_stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+  c->l2_attr = attr;
+  c->l2_attr_set = true;
   return NGD_OK;
 }
 
@@ -549,7 +644,7 @@ int ngd_ctx_destroy(ngd_ctx* c) {
   for (auto& e : c->poll_ev)
     if (e) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->wr_pad, &c->R_pad, &c->alpha_bar})
+  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->jets, &c->partF, &c->wr_pad, &c->R_pad, &c->alpha_bar})
     b->release();
   if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
   if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
@@ -565,6 +660,9 @@ int ngd_ctx_set_stream(ngd_ctx* c, void* stream) {
   c->stream = static_cast<cudaStream_t>(stream);
   CKB(cublasSetStream(c->blas, c->stream));
   CKS(cusolverDnSetStream(c->sol, c->stream));
+  if (c->l2_attr_set && c->stream &&
+      cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &c->l2_attr) != cudaSuccess)
+    cudaGetLastError();  // best effort on a caller-owned stream
   return NGD_OK;
 }
 
@@ -615,18 +713,34 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
   c->gm = gm;
   const int npp = gm.n_pts_pad();
   const size_t col_b = sizeof(double) * gm.s_pad;
+  // the linearisation's jets and adjoints (read twice per Gramian matvec) live in one arena that is
+  // made an L2 persisting access-policy window on the compute streams
   int maxw = 16;
+  std::vector<size_t> zoff(c->NL), doff(c->NL);
+  size_t arena = 0;
   for (int l = 0; l < c->NL; ++l) {
-    CK(c->zin[l].ensure(col_b * rup(c->w[l], 16)));
-    CK(cudaMemsetAsync(c->zin[l].p, 0, col_b * rup(c->w[l], 16), c->stream));
+    zoff[l] = arena;
+    arena += rup(col_b * rup(c->w[l], 16), 256);
     if (l + 1 < c->NL) {
-      CK(c->dbuf[l].ensure(col_b * rup(c->w[l + 1], 16)));
-      CK(cudaMemsetAsync(c->dbuf[l].p, 0, col_b * rup(c->w[l + 1], 16), c->stream));
+      doff[l] = arena;
+      arena += rup(col_b * rup(c->w[l + 1], 16), 256);
       maxw = std::max<int>(maxw, (int)rup(c->w[l + 1], 16));
     }
   }
-  CK(c->dseed.ensure(col_b * 16));
-  CK(cudaMemsetAsync(c->dseed.p, 0, col_b * 16, c->stream));
+  const size_t soff = arena;
+  arena += col_b * 16;
+  for (auto& b : c->zin) b.release();
+  for (auto& b : c->dbuf) b.release();
+  c->dseed.release();
+  CK(c->jets.ensure(arena));
+  CK(cudaMemsetAsync(c->jets.p, 0, arena, c->stream));
+  char* jb = static_cast<char*>(c->jets.p);
+  for (int l = 0; l < c->NL; ++l) {
+    c->zin[l].set_view(jb + zoff[l], col_b * rup(c->w[l], 16));
+    if (l + 1 < c->NL) c->dbuf[l].set_view(jb + doff[l], col_b * rup(c->w[l + 1], 16));
+  }
+  c->dseed.set_view(jb + soff, col_b * 16);
+  TRY(set_l2_window(c, c->jets.p, arena));
   CK(c->pre_last.ensure(col_b * 16));
   CK(c->zs0.ensure(col_b * maxw));
   CK(c->zs1.ensure(col_b * maxw));
@@ -688,6 +802,14 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
     c->rplan.start[c->NL] = c->p;
   }
   CK(c->partB.ensure(sizeof(double) * (size_t)(c->G / c->phb_cluster) * c->p));
+  // fused narrow-network matvec: persistent CTAs over point blocks, one partial each
+  c->fused_ok = c->use_fused && fused_supported(c->w.data(), c->NL, gm.C);
+  if (c->fused_ok) {
+    c->fgrid = std::min(gm.nib + gm.nbb, 148);
+    CK(c->partF.ensure(sizeof(double) * (size_t)c->fgrid * c->p));
+    c->rplan_f = c->rplan;
+    for (int l = 0; l < c->NL; ++l) c->rplan_f.G[l] = c->fgrid;
+  }
   c->have_points = true;
   c->lin_valid = false;
   c->graph_gen++;
@@ -1106,17 +1228,25 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
     add_scaled(ad, mu, nullptr, dv, p, done, c->stream);
     pcg_ad(nullptr, c->rplan, p, mu_p, dv, ad, sp, 1, red, c->counter(4), c->stream);
   } else {
-    TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done));
-    PhbAll pb{};
-    fill_phb(c, c->cot.d(), done, pb);
-    CK(phase_b_all_layers(pb, c->G, c->stream));
+    const double* part = c->partB.d();
+    const RedPlan* rp = &c->rplan;
+    if (c->fused_ok) {
+      TRY(fused_partials(c, dv, done));
+      part = c->partF.d();
+      rp = &c->rplan_f;
+    } else {
+      TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done));
+      PhbAll pb{};
+      fill_phb(c, c->cot.d(), done, pb);
+      CK(phase_b_all_layers(pb, c->G, c->stream));
+    }
     if (c->nranks > 1) {
-      reduce_splits(c->partB.d(), c->rplan, p, 0.0, nullptr, nullptr, ad, done, c->stream);
+      reduce_splits(part, *rp, p, 0.0, nullptr, nullptr, ad, done, c->stream);
       TRY(allreduce(c, ad, p));
       add_scaled(ad, 0.0, mu_p, dv, p, done, c->stream);
-      pcg_ad(nullptr, c->rplan, p, mu_p, dv, ad, sp, 1, red, c->counter(4), c->stream);
+      pcg_ad(nullptr, *rp, p, mu_p, dv, ad, sp, 1, red, c->counter(4), c->stream);
     } else {
-      pcg_ad(c->partB.d(), c->rplan, p, mu_p, dv, ad, sp, 0, red, c->counter(4), c->stream);
+      pcg_ad(part, *rp, p, mu_p, dv, ad, sp, 0, red, c->counter(4), c->stream);
     }
   }
   // x += alpha d ; r -= alpha ad (or r = b - A x) ; ||r|| test   (krylov.py:66-74)
@@ -1346,6 +1476,18 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "graphs")) {
     c->use_graphs = value ? 1 : 0;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "fused")) {
+    c->use_fused = value ? 1 : 0;
+    if (c->have_points) {
+      c->fused_ok = false;  // re-planned by the next ngd_set_points / ngd_set_rows
+      c->graph_gen++;
+    }
+    return NGD_OK;
+  }
+  if (!strcmp(key, "l2window")) {
+    c->use_l2_window = value ? 1 : 0;
     return NGD_OK;
   }
   if (!strcmp(key, "trsm")) {

@@ -11,7 +11,7 @@ namespace ngd {
 enum KernelKind {
   K_FWD = 1, K_REV = 2, K_PHA = 3, K_PHB = 4, K_FORMJ = 5, K_PRECOND = 6, K_VEC = 7, K_PACK = 8, K_SVD = 9, K_CHOL = 10,
   K_BLAS = 11, K_SOLVER = 12,  // library calls (cuBLAS / cuSOLVER): timed, not counted as our launches
-  K_TRSM = 13
+  K_TRSM = 13, K_FUSED = 14
 };
 void probe_before(int kind, cudaStream_t st);
 void probe_after(int kind, cudaStream_t st);
@@ -124,6 +124,26 @@ struct PackAll {
   int64_t start[kMaxLayers + 1];  // element offsets (packed W + bias row per layer)
   int n_layers;
 };
+
+// fused narrow-network Gramian matvec (ngd_fused.cu)
+struct FusedArgs {
+  const double* v;                  // flat parameter-space vector (model.py:41-51 layout)
+  const double* Z[kMaxLayers];      // input jets per layer
+  const double* D[kMaxLayers];      // adjoints per layer (dseed for the output layer)
+  int n_in[kMaxLayers], n_out[kMaxLayers];
+  int64_t woff[kMaxLayers], boff[kMaxLayers];
+  int vso[kMaxLayers], vbo[kMaxLayers], vs[kMaxLayers];  // shared-memory layout of V_l and v_b
+  int v_total;
+  int n_layers, C, nib, nbb;
+  int64_t s_pad, int_cols;
+  const double* w;                  // metric weight per padded point
+  double* part;                     // [grid][p] per-CTA partials
+  int64_t p;
+  const int* skip;
+};
+bool fused_supported(const int* widths, int n_layers, int C);
+size_t fused_smem(const FusedArgs& a);
+cudaError_t fused_mv(const FusedArgs& a, int grid, cudaStream_t st);
 
 cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles, cudaStream_t st);
 cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st);

@@ -214,3 +214,39 @@ def test_pcg_recompute_every_accounting():
     want = O.pcg(O.DenseOracle(a @ a.T + 1e-3 * np.eye(60)), b, 1e-300, 7, recompute_every=3)
     assert (rep.iterations, rep.matvecs) == (want.iterations, want.matvecs)
     np.testing.assert_allclose(rep.solution, want.solution, rtol=1e-8)
+
+
+@pytest.mark.parametrize("name,widths,nint,nbnd", [
+    ("poisson2d", (2, 32, 32, 1), 900, 120),
+    ("poisson2d", (2, 64, 64, 64, 1), 4096, 512),
+    ("heat1p1d", (2, 24, 24, 1), 600, 80),
+    ("poisson1d", (1, 16, 16, 1), 200, 2),
+    ("poisson2d", (2, 64, 1), 37, 0),
+])
+def test_fused_matvec_matches_factored(name, widths, nint, nbnd):
+    """The fused narrow-network matvec (ngd_fused.cu) against the two-phase factored path and the
+    oracle: same operator (1e-12), and the PCG fast path gives the same direction."""
+    from paper_2505_11638_b200 import _lib
+
+    top = ngd.MlpTopology(widths)
+    res = {}
+    try:
+        for fused in (1, 0):
+            _lib.set_option("fused", fused)  # applies to contexts created below
+            prob = ngd.make_problem(name, topology=top)
+            if nbnd or name != "poisson2d":
+                quad = prob.sample_quadrature(nint, nbnd, 0)
+            else:  # interior-only rows
+                quad = ngd.QuadratureSet(np.random.default_rng(3).random((nint, 2)), np.full(nint, 1.0 / nint),
+                                         np.zeros((0, 2)), np.zeros(0))
+            theta = ngd.init(top, 1).values
+            v = np.random.default_rng(4).standard_normal(top.param_count)
+            g = prob.loss_grad(theta, quad)
+            gop = ngd.GramianOperator.from_problem(prob, theta, quad)
+            rep = ngd.pcg(ngd.ShiftedOperator(gop, 1e-3), g, 1e-300, 3)  # few its: CG amplifies 1e-16 differences
+            res[fused] = (gop.matvec(v), rep.solution, rep.iterations)
+    finally:
+        _lib.set_option("fused", 1)
+    np.testing.assert_allclose(res[1][0], res[0][0], rtol=1e-12, atol=1e-12 * np.abs(res[0][0]).max())
+    assert res[1][2] == res[0][2]
+    np.testing.assert_allclose(res[1][1], res[0][1], rtol=1e-9, atol=1e-9 * np.abs(res[0][1]).max())

@@ -9,6 +9,11 @@ import paper_2505_11638_b200 as ngd
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+if len(sys.argv) > 3:
+    from paper_2505_11638_b200 import _lib
+    _lib.set_option("l2window", int(sys.argv[3]))
+side = torch.cuda.Stream()
+torch.cuda.set_stream(side)  # a non-default stream can carry the L2 access-policy window
 prob, quad, theta0, _ = bench.make_problem(ngd, cfg, 1, 0)
 gop = ngd.GramianOperator.from_problem(prob, theta0, quad)
 v = torch.randn(gop.dim, dtype=torch.float64, device="cuda")
@@ -21,4 +26,4 @@ s.record()
 for _ in range(20):
     gop.matvec_device(v, 0.0, out)
 e.record(); e.synchronize()
-print(f"{cfg}: matvec {1e3 * s.elapsed_time(e) / 20:.1f} us")
+print(f"{cfg}: matvec {1e3 * s.elapsed_time(e) / 20:.1f} us  (args {sys.argv[1:]})")
