@@ -460,6 +460,14 @@ def main():
     runner.ctx.call("ngd_get_stat", b"jacobi_sweeps", _lib.ctypes.byref(sweeps))
     roof = roofline_entry(probe_kind, widths, n_int, n_bnd, ell, len(theta0), abs(sweeps.value), kcnt.value,
                           ktot.value, peaks)
+    try:  # measured DRAM traffic of this kernel at this config (one ncu --set full capture)
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_r01.json")) as fh:
+            tr = json.load(fh).get(f"{args.config}/{roof['kernel']}")
+        if tr:
+            roof["traffic"] = tr["bytes_per_launch"]
+            roof["traffic_source"] = tr["source"]
+    except (OSError, ValueError):
+        pass
     roof["class_ms_per_step"] = class_ms
     # north-star kernels measured standalone after the timed region (they run inside CUDA graphs in PCG)
     extra = standalone_rooflines(ngd, _lib, lib, prob, quad, theta0, widths, n_int, n_bnd, ell, peaks) if rank == 0 else {}
