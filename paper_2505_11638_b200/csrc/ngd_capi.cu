@@ -168,6 +168,7 @@ struct ngd_ctx {
   int svd_method = 2;
   int use_own_chol = 1;
   int use_own_trsm = 1;
+  int use_syrk = 0;
   Buf trsm_work;
   Buf chol_work;
   int last_sweeps = 0;
@@ -450,6 +451,19 @@ static int potrf_upper(ngd_ctx* c, double* A, int n, int* info) {
   return NGD_OK;
 }
 
+// W = A^T A for a tall p x ell column-major A (upper triangle used).  cuBLAS DSYRK picks a
+// 32x32-tile kernel with little parallelism for these shapes (~7 TF/s at 8577 x 300);
+// the full DGEMM (2x the FLOPs, split over more CTAs) is faster ("syrk" option = 1 keeps DSYRK).
+static int gram_tall(ngd_ctx* c, const double* A, int64_t p, int ell, double* W) {
+  const double one = 1.0, zero = 0.0;
+  if (c->use_syrk) {
+    CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, A, (int)p, &zero, W, ell));
+  } else {
+    CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, (int)p, &one, A, (int)p, A, (int)p, &zero, W, ell));
+  }
+  return NGD_OK;
+}
+
 // B <- B R^{-1} (B p x ell col-major, R ell x ell upper, lda ell): own DMMA kernel, cuBLAS beyond ell = 512
 static int trsm_right(ngd_ctx* c, double* B, int64_t p, const double* R, int ell) {
   if (c->use_own_trsm && trsm_supported(ell)) {
@@ -475,7 +489,7 @@ static int scholqr3(ngd_ctx* c, double* B, int64_t p, int ell) {
   const double shift_coef = 11.0 * ((double)p * ell + (double)ell * (ell + 1)) * 2.220446049250313e-16;
   for (int pass = 0; pass < 3; ++pass) {
     double* W = c->nys_m.d();
-    CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, B, (int)p, &zero, W, ell));
+    TRY(gram_tall(c, B, p, ell, W));
     if (pass == 0) shift_diag(W, ell, shift_coef, c->stream);
     TRY(potrf_upper(c, W, ell, info));
     triu(W, ell, ell, c->stream);
@@ -1094,8 +1108,7 @@ int ngd_nystrom_prepare(ngd_ctx* c, double* omega, int64_t p, int32_t ell) {
   // one Cholesky-QR pass is already orthonormal to O(eps cond^2); squarer blocks get a second pass.
   const int passes = (p >= 4 * (int64_t)ell) ? 1 : 2;
   for (int pass = 0; pass < passes; ++pass) {
-    CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, omega, (int)p, &zero,
-                    c->nys_m.d(), ell));
+    TRY(gram_tall(c, omega, p, ell, c->nys_m.d()));
     TRY(potrf_upper(c, c->nys_m.d(), ell, static_cast<int*>(c->nys_info.p) + 1));
     TRY(trsm_right(c, omega, p, c->nys_m.d(), ell));
   }
@@ -1488,6 +1501,10 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "l2window")) {
     c->use_l2_window = value ? 1 : 0;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "syrk")) {
+    c->use_syrk = value ? 1 : 0;
     return NGD_OK;
   }
   if (!strcmp(key, "trsm")) {
