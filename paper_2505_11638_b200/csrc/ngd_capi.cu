@@ -168,6 +168,7 @@ struct ngd_ctx {
   int svd_method = 2;
   int use_own_chol = 1;
   int use_own_trsm = 1;
+  Buf rinv, tsq;  // explicit-inverse TRSM scratch
   int use_syrk = 0;
   Buf trsm_work;
   Buf chol_work;
@@ -466,6 +467,20 @@ static int gram_tall(ngd_ctx* c, const double* A, int64_t p, int ell, double* W)
 
 // B <- B R^{-1} (B p x ell col-major, R ell x ell upper, lda ell): own DMMA kernel, cuBLAS beyond ell = 512
 static int trsm_right(ngd_ctx* c, double* B, int64_t p, const double* R, int ell) {
+  if (c->use_own_trsm == 2 && trsm_supported(ell)) {
+    // explicit inverse: Rinv by the DMMA solve on the identity (ell x ell), then B <- B Rinv as one
+    // cuBLAS DGEMM into scratch (the triangle's zeros multiply through; the GEMM runs near peak)
+    CK(c->trsm_work.ensure(trsm_work(ell)));
+    CK(c->rinv.ensure(sizeof(double) * (size_t)ell * ell));
+    CK(c->tsq.ensure(sizeof(double) * (size_t)p * ell));
+    set_identity(c->rinv.d(), ell, c->stream);
+    CK(trsm_right_upper(c->rinv.d(), ell, ell, R, ell, ell, c->trsm_work.d(), c->stream));
+    const double one = 1.0, zero = 0.0;
+    CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)p, ell, ell, &one, B, (int)p, c->rinv.d(), ell, &zero,
+                    c->tsq.d(), (int)p));
+    CK(cudaMemcpyAsync(B, c->tsq.d(), sizeof(double) * (size_t)p * ell, cudaMemcpyDeviceToDevice, c->stream));
+    return NGD_OK;
+  }
   if (c->use_own_trsm && trsm_supported(ell)) {
     CK(c->trsm_work.ensure(trsm_work(ell)));
     CK(trsm_right_upper(B, p, p, R, ell, ell, c->trsm_work.d(), c->stream));
@@ -658,7 +673,7 @@ int ngd_ctx_destroy(ngd_ctx* c) {
   for (auto& e : c->poll_ev)
     if (e) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->jets, &c->partF, &c->wr_pad, &c->R_pad, &c->alpha_bar})
+  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->rinv, &c->tsq, &c->jets, &c->partF, &c->wr_pad, &c->R_pad, &c->alpha_bar})
     b->release();
   if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
   if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
@@ -1508,7 +1523,8 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
     return NGD_OK;
   }
   if (!strcmp(key, "trsm")) {
-    c->use_own_trsm = value ? 1 : 0;
+    if (value < 0 || value > 2) return fail(NGD_E_SHAPE, "trsm must be 0 (cuBLAS), 1 (DMMA solve) or 2 (inverse + GEMM)");
+    c->use_own_trsm = (int)value;
     return NGD_OK;
   }
   if (!strcmp(key, "svd")) {

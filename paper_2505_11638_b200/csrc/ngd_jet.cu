@@ -368,7 +368,10 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
   const bool do_bias = (bx == 0);
   // warps whose 16 x 32 sub-tile is all padding (output layer M = 1, input layer N = d) skip the MMAs
   const bool w_active = (m0 + wm * 16) < p.M && (n0 + wn * 32) < p.N;
-  double bsum = 0.0;  // bias partial: row tid >> 2, k-quarter tid & 3
+  // bias partials from the A fragments already in registers (rows wm*16 + g, +8; columns kk + t):
+  // D c over value columns = the scaled fragment where the column is a value column
+  const bool bias_warp = do_bias && wn == 0 && w_active;
+  double bsum0 = 0.0, bsum1 = 0.0;
 
   auto load_stage = [&](int stage, int kt) {
     const int64_t j0 = (int64_t)kt * BK;
@@ -394,7 +397,7 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
       const int64_t j = j0 + tid;
       const double cc = p.cvec[point_of_col(j, p.int_cols, p.C, p.nib)];
       ccs[stage * BK + tid] = cc;
-      ccv[stage * BK + tid] = is_value_col(j, p.int_cols, p.C) ? cc : 0.0;
+      ccv[stage * BK + tid] = is_value_col(j, p.int_cols, p.C) ? 1.0 : 0.0;  // value-column flag
     }
   };
 
@@ -421,6 +424,7 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
     const double* as = As + st * PBM * PSTR;
     const double* bs = Bs + st * PBN * PSTR;
     const double* cs = ccs + st * BK;
+    const double* vf = ccv + st * BK;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       if (!w_active) break;
@@ -433,18 +437,22 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
         dmma884(acc[0][j][0], acc[0][j][1], a0, b);
         dmma884(acc[1][j][0], acc[1][j][1], a1, b);
       }
-    }
-    if (do_bias) {
-      const double* cv = ccv + st * BK;
-      const int br = tid >> 2, bq = (tid & 3) * 4;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) bsum = fma(as[br * PSTR + bq + u], cv[bq + u], bsum);
+      if (bias_warp) {
+        const double f = vf[kk + t];
+        bsum0 = fma(f, a0, bsum0);
+        bsum1 = fma(f, a1, bsum1);
+      }
     }
   }
-  // combine the 4 k-quarters of each bias row (fixed order)
-  bsum += __shfl_xor_sync(0xffffffffu, bsum, 1);
-  bsum += __shfl_xor_sync(0xffffffffu, bsum, 2);
-  if (do_bias && (tid & 3) == 0) bias_acc[tid >> 2] = bsum;
+  // combine the 4 column phases t of each bias row (fixed order)
+  bsum0 += __shfl_xor_sync(0xffffffffu, bsum0, 1);
+  bsum0 += __shfl_xor_sync(0xffffffffu, bsum0, 2);
+  bsum1 += __shfl_xor_sync(0xffffffffu, bsum1, 1);
+  bsum1 += __shfl_xor_sync(0xffffffffu, bsum1, 2);
+  if (do_bias && wn == 0 && t == 0) {
+    bias_acc[wm * 16 + g] = bsum0;
+    bias_acc[wm * 16 + 8 + g] = bsum1;
+  }
   cp_async_wait<0>();
   __syncthreads();
   // ---- split-K reduction inside the thread-block cluster (DSMEM) ----------

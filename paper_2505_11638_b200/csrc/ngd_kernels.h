@@ -189,6 +189,7 @@ void theta_minus(const double* a, double alpha, const double* b, double* out, in
 void scale_rows(double* S, int64_t R, int ell, const double* w, cudaStream_t st);
 void scale_cols_sqrt(double* J, int64_t p, int64_t R, const double* w, cudaStream_t st);
 void symmetrize_upper(double* G, int64_t n, int64_t ld, cudaStream_t st);
+void set_identity(double* a, int n, cudaStream_t st);
 void add_shift(double* y, const double* omega, int64_t n, const double* fro2, double* shift_out, cudaStream_t st);
 void eig_from_sv(const double* s, int ell, const double* shift, double* eig, cudaStream_t st);
 void triu(double* a, int n, int lda, cudaStream_t st);

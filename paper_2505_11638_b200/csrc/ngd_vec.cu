@@ -626,6 +626,18 @@ void scale_cols_sqrt(double* J, int64_t p, int64_t R, const double* w, cudaStrea
   probe_after(K_VEC, st);
 }
 
+// n x n identity (column-major, ld = n)
+__global__ void identity_kernel(double* a, int n) {
+  const int64_t tot = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x)
+    a[e] = (e % n == e / n) ? 1.0 : 0.0;
+}
+void set_identity(double* a, int n, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  identity_kernel<<<vgrid((int64_t)n * n), 256, 0, st>>>(a, n);
+  probe_after(K_VEC, st);
+}
+
 // lower triangle <- upper triangle
 __global__ void symmetrize_upper_kernel(double* G, int64_t n, int64_t ld) {
   const int64_t tot = n * n;
