@@ -143,6 +143,7 @@ struct ngd_ctx {
   std::vector<Buf> zin, dbuf;  // per layer
   Buf dseed, pre_last, zs0, zs1;
   Buf jets;  // arena behind zin / dbuf / dseed
+  int force_comm = 0;  // "force_comm": build a communicator (and take the multi-rank paths) even for 1 rank
   int use_fused = 0;  // opt-in: measured slower than the two-phase path at C1/C2
   bool fused_ok = false;
   int fgrid = 0;
@@ -195,7 +196,7 @@ static int bind(ngd_ctx* c) {
 }
 
 static int allreduce(ngd_ctx* c, double* buf, size_t n) {
-  if (c->nranks <= 1 || !c->comm) return NGD_OK;
+  if (!c->comm) return NGD_OK;
   CKN(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, c->comm, c->stream));
   return NGD_OK;
 }
@@ -361,7 +362,7 @@ static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* m
   fill_phb(c, cot, skip, pb);
   CK(phase_b_all_layers(pb, c->G, c->stream));
   const bool shifted = v && (mu_p || mu != 0.0);
-  if (c->nranks > 1) {
+  if (c->comm) {
     reduce_splits(c->partB.d(), c->rplan, c->p, 0.0, nullptr, nullptr, out, skip, c->stream);
     TRY(allreduce(c, out, c->p));
     if (shifted) add_scaled(out, mu, mu_p, v, c->p, skip, c->stream);
@@ -412,7 +413,7 @@ static int gram_mv(ngd_ctx* c, const double* v, double mu, const double* mu_p, d
   if (c->fused_ok) {
     TRY(fused_partials(c, v, skip));
     const bool shifted = v && (mu_p || mu != 0.0);
-    if (c->nranks > 1) {
+    if (c->comm) {
       reduce_splits(c->partF.d(), c->rplan_f, c->p, 0.0, nullptr, nullptr, out, skip, c->stream);
       TRY(allreduce(c, out, c->p));
       if (shifted) add_scaled(out, mu, mu_p, v, c->p, skip, c->stream);
@@ -707,7 +708,8 @@ int ngd_nccl_unique_id(uint8_t* h_id) {
 
 int ngd_ctx_set_comm(ngd_ctx* c, const uint8_t* h_id, int32_t rank, int32_t nranks) {
   TRY(bind(c));
-  if (nranks <= 1) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NGD_E_SHAPE, "bad rank %d / world %d", rank, nranks);
+  if (nranks == 1 && !c->force_comm) {
     c->rank = 0;
     c->nranks = 1;
     return NGD_OK;
@@ -1061,7 +1063,7 @@ int ngd_gram_dense(ngd_ctx* c, double* G, int64_t ldg) {
                     &beta, G, (int)ldg));
   }
   symmetrize_upper(G, c->p, ldg, c->stream);
-  if (c->nranks > 1) {
+  if (c->comm) {
     if (ldg != c->p) return fail(NGD_E_SHAPE, "multi-rank dense Gramian needs ldg == p");
     TRY(allreduce(c, G, (size_t)c->p * c->p));
   }
@@ -1093,7 +1095,7 @@ int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, doubl
     CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)c->p, (int)ell, (int)r, &one, c->jt.d(), (int)c->p,
                     c->smat.d(), (int)r, &beta, Y, (int)ldy));
   }
-  if (c->nranks > 1) {
+  if (c->comm) {
     if (ldy != c->p) return fail(NGD_E_SHAPE, "multi-rank matmat needs ldy == p");
     TRY(allreduce(c, Y, (size_t)c->p * ell));
   }
@@ -1268,7 +1270,7 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
       fill_phb(c, c->cot.d(), done, pb);
       CK(phase_b_all_layers(pb, c->G, c->stream));
     }
-    if (c->nranks > 1) {
+    if (c->comm) {
       reduce_splits(part, *rp, p, 0.0, nullptr, nullptr, ad, done, c->stream);
       TRY(allreduce(c, ad, p));
       add_scaled(ad, 0.0, mu_p, dv, p, done, c->stream);
@@ -1504,6 +1506,10 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "graphs")) {
     c->use_graphs = value ? 1 : 0;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "force_comm")) {
+    c->force_comm = value ? 1 : 0;
     return NGD_OK;
   }
   if (!strcmp(key, "fused")) {
