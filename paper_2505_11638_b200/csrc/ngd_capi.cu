@@ -244,16 +244,44 @@ static int forward(ngd_ctx* c, bool store) {
   return NGD_OK;
 }
 
+// theta -> zero-padded operand tiles of the forward sweep (W_l with its bias row) and, for the
+// reverse sweep, W_{l+1}^T: one launch
 static int pack_theta(ngd_ctx* c, const double* theta, bool rev) {
+  PackAll pk{};
+  int e = 0;
+  int64_t off = 0;
   for (int l = 0; l < c->NL; ++l) {
-    pack(c->apf[l].d(), c->Mp_f[l], c->Kp_f[l], theta, c->woff[l], c->w[l + 1], c->w[l], 0, nullptr, c->stream);
-    // bias row appended after the packed matrix (length Mp_f)
-    pack(c->apf[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l], 1, c->Mp_f[l], theta, c->boff[l], 1, c->w[l + 1], 0,
-         nullptr, c->stream);
-    if (rev && l + 1 < c->NL)
-      pack(c->apr[l].d(), c->Mp_r[l], c->Kp_r[l], theta, c->woff[l + 1], c->w[l + 2], c->w[l + 1], 1, nullptr,
-           c->stream);
+    pk.dst[e] = c->apf[l].d();
+    pk.Mp[e] = c->Mp_f[l];
+    pk.Kp[e] = c->Kp_f[l];
+    pk.n_out[e] = c->w[l + 1];
+    pk.n_in[e] = c->w[l];
+    pk.trans[e] = 0;
+    pk.woff[e] = c->woff[l];
+    pk.boff[e] = c->boff[l];
+    pk.start[e] = off;
+    off += (int64_t)c->Mp_f[l] * c->Kp_f[l] + c->Mp_f[l];  // bias row appended after the packed matrix
+    ++e;
   }
+  if (rev) {
+    for (int l = 0; l + 1 < c->NL; ++l) {
+      pk.dst[e] = c->apr[l].d();
+      pk.Mp[e] = c->Mp_r[l];
+      pk.Kp[e] = c->Kp_r[l];
+      pk.n_out[e] = c->w[l + 2];
+      pk.n_in[e] = c->w[l + 1];
+      pk.trans[e] = 1;
+      pk.woff[e] = c->woff[l + 1];
+      pk.boff[e] = 0;
+      pk.start[e] = off;
+      // no bias row: the entry ends where its matrix ends (k < mat always)
+      off += (int64_t)c->Mp_r[l] * c->Kp_r[l];
+      ++e;
+    }
+  }
+  pk.start[e] = off;
+  pk.n_layers = e;
+  pack_all(pk, theta, nullptr, c->stream);
   CK(cudaGetLastError());
   return NGD_OK;
 }

@@ -117,12 +117,13 @@ struct RedPlan {
   int G[kMaxLayers];
   int n_layers;
 };
-struct PackAll {
-  double* dst[kMaxLayers];
-  int Mp[kMaxLayers], Kp[kMaxLayers], n_out[kMaxLayers], n_in[kMaxLayers];
-  int64_t woff[kMaxLayers], boff[kMaxLayers];
-  int64_t start[kMaxLayers + 1];  // element offsets (packed W + bias row per layer)
-  int n_layers;
+struct PackAll {  // entries: forward W_l (+ bias row) and, for the reverse sweep, W_{l+1}^T (no bias)
+  double* dst[2 * kMaxLayers];
+  int Mp[2 * kMaxLayers], Kp[2 * kMaxLayers], n_out[2 * kMaxLayers], n_in[2 * kMaxLayers];
+  int trans[2 * kMaxLayers];       // 1: dst = W^T (W is n_out x n_in), no bias row
+  int64_t woff[2 * kMaxLayers], boff[2 * kMaxLayers];
+  int64_t start[2 * kMaxLayers + 1];  // element offsets (packed matrix [+ bias row] per entry)
+  int n_layers;                       // number of entries
 };
 
 // fused narrow-network Gramian matvec (ngd_fused.cu)

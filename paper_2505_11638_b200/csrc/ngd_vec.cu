@@ -574,7 +574,11 @@ __global__ void pack_all_kernel(PackAll a, const double* src, const int* skip) {
     double v = 0.0;
     if (k < mat) {
       const int m = (int)(k / a.Kp[l]), c = (int)(k % a.Kp[l]);
-      if (m < a.n_out[l] && c < a.n_in[l]) v = src[a.woff[l] + (int64_t)m * a.n_in[l] + c];
+      if (a.trans[l]) {
+        if (m < a.n_in[l] && c < a.n_out[l]) v = src[a.woff[l] + (int64_t)c * a.n_in[l] + m];
+      } else if (m < a.n_out[l] && c < a.n_in[l]) {
+        v = src[a.woff[l] + (int64_t)m * a.n_in[l] + c];
+      }
     } else {
       const int m = (int)(k - mat);
       if (m < a.n_out[l]) v = src[a.boff[l] + m];
