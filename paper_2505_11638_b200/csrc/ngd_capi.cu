@@ -233,13 +233,7 @@ static int forward(ngd_ctx* c, bool store) {
     a.pre_out = pre;
     a.bias = c->apf[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l];  // packed bias follows the packed W
     a.lap_mask = c->lap_mask;
-    for (int seg = 0; seg < 2; ++seg) {
-      const int CC = seg == 0 ? gm.C : 1;
-      a.col0 = seg == 0 ? 0 : gm.int_cols();
-      a.pt0 = seg == 0 ? 0 : gm.nib * PB;
-      const int nblk = seg == 0 ? gm.nib : gm.nbb;
-      CK(jet_gemm(CC, FWD, a, nblk, c->mtiles[l], c->stream));
-    }
+    CK(jet_gemm_both(gm.C, FWD, a, gm.nib, gm.nbb, gm.int_cols(), c->mtiles[l], c->stream));
   }
   return NGD_OK;
 }
@@ -963,13 +957,7 @@ int ngd_linearize_ex(ngd_ctx* c, const double* theta, const double* theta_bar, d
     a.dbuf = c->dbuf[l].d();
     a.n_pts_pad = gm.n_pts_pad();
     a.lap_mask = c->lap_mask;
-    for (int seg = 0; seg < 2; ++seg) {
-      const int CC = seg == 0 ? gm.C : 1;
-      a.col0 = seg == 0 ? 0 : gm.int_cols();
-      a.pt0 = seg == 0 ? 0 : gm.nib * PB;
-      const int nblk = seg == 0 ? gm.nib : gm.nbb;
-      CK(jet_gemm(CC, REV, a, nblk, c->mtiles[l], c->stream));
-    }
+    CK(jet_gemm_both(gm.C, REV, a, gm.nib, gm.nbb, gm.int_cols(), c->mtiles[l], c->stream));
   }
   if (d_metric) gather_points(c->F.d(), d_metric, gm, c->stream);
   if (d_resid) gather_points(c->R_pad.d(), d_resid, gm, c->stream);

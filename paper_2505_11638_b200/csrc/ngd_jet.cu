@@ -304,6 +304,60 @@ cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st) {
   }
 }
 
+// Both point segments of a forward / reverse layer sweep in one launch: CTAs [0, nib) take the
+// interior blocks (C channels), CTAs [nib, nib + nbb) the boundary blocks (value channel only).
+template <int C, int MODE>
+__global__ void __launch_bounds__(kThreads) jet_both_kernel(JetArgs p, int nib, int64_t int_cols) {
+  if ((int)blockIdx.x < nib) {
+    jet_tile<C, MODE>(p, blockIdx.x, blockIdx.y);
+  } else {
+    JetArgs q = p;
+    q.col0 = int_cols;
+    q.pt0 = nib * PB;
+    jet_tile<1, MODE>(q, blockIdx.x - nib, blockIdx.y);
+  }
+}
+
+template <int C, int MODE>
+static cudaError_t launch_jet_both(const JetArgs& a, int nib, int nbb, int64_t int_cols, int mtiles, cudaStream_t st) {
+  constexpr int NC = PB * C;
+  const size_t smem = sizeof(double) * (2 * BM * (BK + APAD) + 2 * BK * (NC + 4));
+  auto kern = jet_both_kernel<C, MODE>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  if (nib + nbb <= 0 || mtiles <= 0) return cudaSuccess;
+  JetArgs b = a;
+  b.col0 = 0;
+  b.pt0 = 0;
+  probe_before(MODE == FWD ? K_FWD : K_REV, st);
+  kern<<<dim3(nib + nbb, mtiles), kThreads, smem, st>>>(b, nib, int_cols);
+  probe_after(MODE == FWD ? K_FWD : K_REV, st);
+  return cudaGetLastError();
+}
+
+cudaError_t jet_gemm_both(int C, int mode, const JetArgs& a, int nib, int nbb, int64_t int_cols, int mtiles,
+                          cudaStream_t st) {
+#define NGD_JET_BOTH(CC)                                                                          \
+  case CC:                                                                                        \
+    return mode == FWD ? launch_jet_both<CC, FWD>(a, nib, nbb, int_cols, mtiles, st)              \
+                       : launch_jet_both<CC, REV>(a, nib, nbb, int_cols, mtiles, st);
+  switch (C) {
+    NGD_JET_BOTH(3)
+    NGD_JET_BOTH(4)
+    NGD_JET_BOTH(5)
+    NGD_JET_BOTH(6)
+    NGD_JET_BOTH(7)
+    NGD_JET_BOTH(8)
+    NGD_JET_BOTH(12)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef NGD_JET_BOTH
+}
+
 cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles, cudaStream_t st) {
 #define NGD_JET_CASE(CC)                                              \
   case CC:                                                            \

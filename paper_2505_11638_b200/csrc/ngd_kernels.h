@@ -147,6 +147,8 @@ size_t fused_smem(const FusedArgs& a);
 cudaError_t fused_mv(const FusedArgs& a, int grid, cudaStream_t st);
 
 cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles, cudaStream_t st);
+cudaError_t jet_gemm_both(int C, int mode, const JetArgs& a, int nib, int nbb, int64_t int_cols, int mtiles,
+                          cudaStream_t st);
 cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st);
 cudaError_t phase_b_all_layers(const PhbAll& a, int splits, cudaStream_t st);
 void pack_all(const PackAll& a, const double* src, const int* skip, cudaStream_t st);
