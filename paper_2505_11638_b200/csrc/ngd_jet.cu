@@ -447,12 +447,13 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
       else
         *reinterpret_cast<double2*>(bs + r * PSTR + c2) = make_double2(0.0, 0.0);
     }
-    if (tid < BK) {
-      const int64_t j = j0 + tid;
-      const double cc = p.cvec[point_of_col(j, p.int_cols, p.C, p.nib)];
-      ccs[stage * BK + tid] = cc;
-      ccv[stage * BK + tid] = is_value_col(j, p.int_cols, p.C) ? 1.0 : 0.0;  // value-column flag
+    // the k-tile's 16 columns are one channel run of one point block, i.e. 16 consecutive points:
+    // their cotangents are one contiguous 128-byte run -> asynchronous copy (warp 0 never stalls)
+    if (tid < BK / 2) {
+      const int pt0 = point_of_col(j0, p.int_cols, p.C, p.nib);
+      cp_async16(ccs + stage * BK + 2 * tid, p.cvec + pt0 + 2 * tid);
     }
+    if (tid < BK) ccv[stage * BK + tid] = is_value_col(j0 + tid, p.int_cols, p.C) ? 1.0 : 0.0;  // value flag
   };
 
   double acc[2][4][2];
