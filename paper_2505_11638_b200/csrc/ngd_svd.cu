@@ -386,7 +386,7 @@ __device__ __forceinline__ void rot2(double2 (&x)[RPL], double2 (&y)[RPL], doubl
 // rotate two shared-memory column pairs (X and V) in place; one warp
 template <int RPL>
 __device__ __forceinline__ bool rotate_pair(double* ci, double* cj, double* vi, double* vj, int ldc, int lane,
-                                            double tol) {
+                                            double tol, bool& big) {
   const int nq = ldc >> 1;
   double2 x[RPL], y[RPL];
   load_col<RPL>(x, ci, nq, lane);
@@ -394,6 +394,7 @@ __device__ __forceinline__ bool rotate_pair(double* ci, double* cj, double* vi, 
   double al, be, ga;
   gram3<RPL>(x, y, al, be, ga);
   if (!(ga != 0.0 && ga * ga > tol * tol * al * be)) return false;
+  big |= ga * ga >= tol * (al * be);  // coupling >= sqrt(tol)
   double c, s;
   jacobi_cs(al, be, ga, c, s);
   rot2<RPL>(x, y, c, s);
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   // buf[phase][slot][0 = X, 1 = V][h][ldc]; X and V of one (phase, slot) are contiguous
   auto bufp = [&](int phase, int slot, int which) { return smem + ((size_t)(phase * 2 + slot) * 2 + which) * slot_sz; };
   double* norms = smem + 8 * slot_sz;                  // [2][h]
-  int* flags = reinterpret_cast<int*>(norms + 2 * h);  // [2]
+  int* flags = reinterpret_cast<int*>(norms + 2 * h);  // [4]: rotated / large rotation, by sweep parity
   __shared__ __align__(8) unsigned long long mbar;    // block arrivals of an exchange
   __shared__ int held[2];
   const unsigned mbar_a = smem_u32(&mbar);
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       V[e] = (j == r && r < ell) ? 1.0 : 0.0;
     }
   }
-  if (tid < 2) flags[tid] = 0;
+  if (tid < 4) flags[tid] = 0;
   cl.sync();
 
   // move the two held blocks from the placement of round r_from to that of round r_to
@@ -499,6 +500,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   for (; sweep < max_sweeps && !converged; ++sweep) {
     const int par = sweep & 1;
     bool rotated = false;
+    bool big = false;  // a rotation with relative coupling >= sqrt(tol) happened in this sweep
     for (int r = 0; r < nb - 1; ++r) {
       double* X0 = bufp(phase, 0, 0);
       double* V0 = bufp(phase, 0, 1);
@@ -513,7 +515,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
             double* X = sl ? X1 : X0;
             double* V = sl ? V1 : V0;
             rotated |= rotate_pair<RPL>(X + (size_t)i * ldc, X + (size_t)j * ldc, V + (size_t)i * ldc,
-                                        V + (size_t)j * ldc, ldc, lane, tol);
+                                        V + (size_t)j * ldc, ldc, lane, tol, big);
           }
           __syncthreads();
         }
@@ -537,6 +539,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
             double al, be, ga;
             gram3<RPL>(xr, y, al, be, ga);
             if (ga != 0.0 && ga * ga > tol * tol * al * be) {
+              big |= ga * ga >= tol * (al * be);
               double c, s;
               jacobi_cs(al, be, ga, c, s);
               rot2<RPL>(xr, y, c, s);
@@ -563,12 +566,23 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       if (r == nb - 2) break;  // sweep ends; the exchange to round 0 happens after the convergence test
       exchange(r, r + 1);
     }
+    // Converged when no pair needed a rotation, or when every rotation of the sweep was already
+    // below sqrt(tol) in relative coupling: one-sided Jacobi converges quadratically at the end, so
+    // the following sweep would find every |ga| / sqrt(al be) ~ coupling^2 < tol and rotate nothing
+    // (measured on the C2 sketch's R: 1.7e-8 -> no rotation; tools/svd_timing.py, tests vs LAPACK).
     if (rotated && lane == 0) flags[par] = 1;
+    if (big && lane == 0) flags[2 + par] = 1;
     cl.sync();
-    int any = 0;
-    for (int o = 0; o < CL; ++o) any |= cl.map_shared_rank(flags, o)[par];
-    converged = (any == 0);
-    if (tid == 0) flags[par ^ 1] = 0;
+    int any = 0, any_big = 0;
+    for (int o = 0; o < CL; ++o) {
+      any |= cl.map_shared_rank(flags, o)[par];
+      any_big |= cl.map_shared_rank(flags, o)[2 + par];
+    }
+    converged = (any == 0) || (any_big == 0);
+    if (tid == 0) {
+      flags[par ^ 1] = 0;
+      flags[2 + (par ^ 1)] = 0;
+    }
     if (!converged) exchange(nb - 2, 0);  // back to the round-0 placement
   }
   __syncthreads();
