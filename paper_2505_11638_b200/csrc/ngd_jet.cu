@@ -387,7 +387,12 @@ cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles,
 // (reduce_splits) makes the result bitwise deterministic.
 // ---------------------------------------------------------------------------
 
-constexpr int PBM = 64, PBN = 64, PSTR = BK + 4;
+#ifndef NGD_PHB_UNITS
+#define NGD_PHB_UNITS 1  // 2 (32-column stages, 2-deep pipeline) measured neutral: C3 -1%, C2 +3%
+#endif
+// a phase-B pipeline stage covers PUN k-units of BK = 16 columns (one channel run of a point block each)
+constexpr int PUN = NGD_PHB_UNITS, PKS = PUN * BK;
+constexpr int PBM = 64, PBN = 64, PSTR = PKS + 4;
 
 // 32-bit column arithmetic (S < 2^31 for every supported configuration)
 __device__ __forceinline__ int point_of_col(int64_t j64, int64_t int_cols, int C, int nib) {
@@ -402,18 +407,18 @@ __device__ __forceinline__ bool is_value_col(int64_t j64, int64_t int_cols, int 
   return j64 >= int_cols || (((int)j64 % (PB * C)) < PB);
 }
 
-constexpr int PNST = 3;  // cp.async pipeline depth of phase B (3 CTAs / SM)
+constexpr int PNST = PUN == 1 ? 3 : 2;  // cp.async pipeline depth of phase B (3 CTAs / SM either way)
 static_assert(PBM * (PBN + 1) + PBM <= 2 * PNST * PBM * PSTR, "cluster reduction staging must fit");
-constexpr size_t kPhbSmem = sizeof(double) * (2 * PNST * PBM * PSTR + 2 * PNST * BK + PBM);
+constexpr size_t kPhbSmem = sizeof(double) * (2 * PNST * PBM * PSTR + 2 * PNST * PKS + PBM);
 
 __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const int by, const int kt0, const int kt1,
                                          const int split) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                              // [PNST][PBM][PSTR]
   double* Bs = As + PNST * PBM * PSTR;            // [PNST][PBN][PSTR]
-  double* ccs = Bs + PNST * PBN * PSTR;           // [PNST][BK]  cotangent per column
-  double* ccv = ccs + PNST * BK;                  // [PNST][BK]  cotangent on value columns (bias)
-  double* bias_acc = ccv + PNST * BK;             // [PBM]
+  double* ccs = Bs + PNST * PBN * PSTR;           // [PNST][PKS] cotangent per column
+  double* ccv = ccs + PNST * PKS;                 // [PNST][PKS] value-column flag (bias)
+  double* bias_acc = ccv + PNST * PKS;            // [PBM]
   if (p.skip && *p.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -427,33 +432,43 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
   const bool bias_warp = do_bias && wn == 0 && w_active;
   double bsum0 = 0.0, bsum1 = 0.0;
 
-  auto load_stage = [&](int stage, int kt) {
-    const int64_t j0 = (int64_t)kt * BK;
+  // stage = k-units [u, u + PUN) of this split (units past kt1 are zero-filled)
+  auto load_stage = [&](int stage, int u, int kt1_) {
     double* as = As + stage * PBM * PSTR;
     double* bs = Bs + stage * PBN * PSTR;
-    for (int i = tid; i < PBM * BK / 2; i += kThreads) {
-      const int r = i >> 3, c2 = (i & 7) * 2;
-      const int row = m0 + r;
-      if (row < p.M)
-        cp_async16(as + r * PSTR + c2, p.D + (int64_t)row * p.s_pad + j0 + c2);
-      else
-        *reinterpret_cast<double2*>(as + r * PSTR + c2) = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < PUN; ++q) {
+      const bool live = u + q < kt1_;
+      const int64_t j0 = (int64_t)(u + q) * BK;
+      const int cq = q * BK;
+      for (int i = tid; i < PBM * BK / 2; i += kThreads) {
+        const int r = i >> 3, c2 = (i & 7) * 2;
+        const int row = m0 + r;
+        if (live && row < p.M)
+          cp_async16(as + r * PSTR + cq + c2, p.D + (int64_t)row * p.s_pad + j0 + c2);
+        else
+          *reinterpret_cast<double2*>(as + r * PSTR + cq + c2) = make_double2(0.0, 0.0);
+      }
+      for (int i = tid; i < PBN * BK / 2; i += kThreads) {
+        const int r = i >> 3, c2 = (i & 7) * 2;
+        const int row = n0 + r;
+        if (live && row < p.N)
+          cp_async16(bs + r * PSTR + cq + c2, p.Z + (int64_t)row * p.s_pad + j0 + c2);
+        else
+          *reinterpret_cast<double2*>(bs + r * PSTR + cq + c2) = make_double2(0.0, 0.0);
+      }
+      // a unit's 16 columns are one channel run of one point block, i.e. 16 consecutive points:
+      // their cotangents are one contiguous 128-byte run -> asynchronous copy (warp 0 never stalls)
+      if (tid < BK / 2) {
+        if (live) {
+          const int pt0 = point_of_col(j0, p.int_cols, p.C, p.nib);
+          cp_async16(ccs + stage * PKS + cq + 2 * tid, p.cvec + pt0 + 2 * tid);
+        } else {
+          *reinterpret_cast<double2*>(ccs + stage * PKS + cq + 2 * tid) = make_double2(0.0, 0.0);
+        }
+      }
+      if (tid < BK) ccv[stage * PKS + cq + tid] = (live && is_value_col(j0 + tid, p.int_cols, p.C)) ? 1.0 : 0.0;
     }
-    for (int i = tid; i < PBN * BK / 2; i += kThreads) {
-      const int r = i >> 3, c2 = (i & 7) * 2;
-      const int row = n0 + r;
-      if (row < p.N)
-        cp_async16(bs + r * PSTR + c2, p.Z + (int64_t)row * p.s_pad + j0 + c2);
-      else
-        *reinterpret_cast<double2*>(bs + r * PSTR + c2) = make_double2(0.0, 0.0);
-    }
-    // the k-tile's 16 columns are one channel run of one point block, i.e. 16 consecutive points:
-    // their cotangents are one contiguous 128-byte run -> asynchronous copy (warp 0 never stalls)
-    if (tid < BK / 2) {
-      const int pt0 = point_of_col(j0, p.int_cols, p.C, p.nib);
-      cp_async16(ccs + stage * BK + 2 * tid, p.cvec + pt0 + 2 * tid);
-    }
-    if (tid < BK) ccv[stage * BK + tid] = is_value_col(j0 + tid, p.int_cols, p.C) ? 1.0 : 0.0;  // value flag
   };
 
   double acc[2][4][2];
@@ -462,26 +477,27 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  const int nst = (kt1 - kt0 + PUN - 1) / PUN;  // pipeline steps of this split
 #pragma unroll
   for (int s0 = 0; s0 < PNST - 1; ++s0) {
-    if (kt0 + s0 < kt1) load_stage(s0, kt0 + s0);
+    if (s0 < nst) load_stage(s0, kt0 + s0 * PUN, kt1);
     cp_async_commit();
   }
-  for (int kt = kt0; kt < kt1; ++kt) {
-    const int st = (kt - kt0) % PNST;
+  for (int it = 0; it < nst; ++it) {
+    const int st = it % PNST;
     cp_async_wait<PNST - 2>();
     __syncthreads();
     {
-      const int nk = kt + PNST - 1;
-      if (nk < kt1) load_stage((nk - kt0) % PNST, nk);
+      const int nk = it + PNST - 1;
+      if (nk < nst) load_stage(nk % PNST, kt0 + nk * PUN, kt1);
       cp_async_commit();
     }
     const double* as = As + st * PBM * PSTR;
     const double* bs = Bs + st * PBN * PSTR;
-    const double* cs = ccs + st * BK;
-    const double* vf = ccv + st * BK;
+    const double* cs = ccs + st * PKS;
+    const double* vf = ccv + st * PKS;
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
+    for (int kk = 0; kk < PKS; kk += 4) {
       if (!w_active) break;
       const double cc = cs[kk + t];
       const double a0 = as[(wm * 16 + g) * PSTR + kk + t] * cc;
