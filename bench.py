@@ -228,7 +228,8 @@ def run_reference(args, rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded quadrature, reference init)",
         "config": config_dict(name, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": host_cores(), "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": host_cores(), "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -282,6 +283,17 @@ def roofline_entry(kind, widths, n_int, n_bnd, ell, p, sweeps, count, total_ms, 
             "avg_launch_us": avg_s * 1e6, "algorithmic_work_per_launch": work,
             "peak_source": "FP64: DMMA measured on this pool (tools/probe/fp64_peak.cu, profiles/r01_fp64_peak.txt); "
                            f"HBM: {peaks['hbm_gbs']} GB/s from {peaks['source']}"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def standalone_rooflines(ngd, _lib, lib, prob, quad, theta0, widths, n_int, n_bnd, ell, peaks, reps=5):
@@ -495,9 +507,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        t_cpu, sample, extra = cpu_step_sample(args.config)
+        t_cpu, sample, cpu_parts = cpu_step_sample(args.config)
         cpu = {"value": 1.0 / t_cpu, "unit": "steps/s", "cores": host_cores(), "kind": "port", "sample": sample,
-               **{k: round(v, 6) for k, v in extra.items()}}
+               "cpu_model": cpu_model(), **{k: round(v, 6) for k, v in cpu_parts.items()}}
 
     if rank == 0:
         line = {
