@@ -1310,10 +1310,10 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
   if (have_pre) {
     CK(precond_apply(static_cast<PrecondArgs*>(c->pargs.p), p, ell, r, z, c->ppart.d(), c->pcprime.d(),
                      c->counter(8), done, sp, 0, red, c->stream));
-    pcg_dir(z, dv, p, sp, c->stream);
+    pcg_dir(z, dv, p, sp, &c->h_flags[5], c->stream);
   } else {
     CK(precond_apply(nullptr, p, 0, r, z, nullptr, nullptr, c->counter(8), done, sp, 0, red, c->stream));
-    pcg_dir(z, dv, p, sp, c->stream);
+    pcg_dir(z, dv, p, sp, &c->h_flags[5], c->stream);
   }
   CK(cudaGetLastError());
   return NGD_OK;
@@ -1339,6 +1339,8 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
   }
   PcgState* sp = static_cast<PcgState*>(c->pcgs.p);
   const int* done = &sp->done;
+  // every earlier solve ended with a stream synchronisation: no kernel can still write the flag
+  *reinterpret_cast<volatile int*>(&c->h_flags[5]) = 0;
   // operands into stable, ctx-owned locations (graph replay needs fixed addresses)
   PrecondArgs hpa{U, eig, precond_mu};
   CK(cudaMemcpyAsync(c->pargs.p, &hpa, sizeof(hpa), cudaMemcpyHostToDevice, c->stream));
@@ -1390,14 +1392,9 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
       TRY(pcg_iteration(c, p, dense, mu, ell, have_pre, rec));
     }
     ++issued;
-    // non-blocking poll of the device 'done' flag (copied to pinned memory after each iteration)
-    const int slot = it & 3;
-    CK(cudaMemcpyAsync(&c->h_flags[slot], &sp->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaEventRecord(c->poll_ev[slot], c->stream));
-    if (it >= 3) {
-      const int old = (it - 2) & 3;
-      if (cudaEventQuery(c->poll_ev[old]) == cudaSuccess && c->h_flags[old] != 0) break;
-    }
+    // stop enqueueing once the device has published 'done' (pcg_dir writes the flag to pinned host
+    // memory at the end of every iteration; kernels of iterations after 'done' return at once)
+    if (*reinterpret_cast<volatile int*>(&c->h_flags[5]) != 0) break;
   }
   // final true residual (krylov.py:83-88)
   CK(cudaMemcpyAsync(&c->h_flags[4], &sp->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));

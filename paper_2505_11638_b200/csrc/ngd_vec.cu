@@ -513,7 +513,10 @@ __global__ void pcg_true_res_kernel(const double* b, const double* ax, double* r
 }
 
 // d = z + beta d  (krylov.py:79-81)
-__global__ void pcg_dir_kernel(const double* z, double* d, int64_t p, PcgState* s) {
+__global__ void pcg_dir_kernel(const double* z, double* d, int64_t p, PcgState* s, int* host_flag) {
+  // last kernel of an iteration: publish the done flag to pinned host memory (zero-copy, no memcpy
+  // or event between graph replays)
+  if (host_flag && blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<volatile int*>(host_flag) = s->done;
   if (s->done) return;
   const double beta = s->beta;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x)
@@ -556,9 +559,9 @@ void pcg_true_res(const double* b, const double* ax, double* r, int64_t p, PcgSt
   pcg_true_res_kernel<<<rgrid(p), kThreads, 0, st>>>(b, ax, r, p, s, count, final_pass, partials, counter);
   probe_after(K_VEC, st);
 }
-void pcg_dir(const double* z, double* d, int64_t p, PcgState* s, cudaStream_t st) {
+void pcg_dir(const double* z, double* d, int64_t p, PcgState* s, int* host_flag, cudaStream_t st) {
   probe_before(K_VEC, st);
-  pcg_dir_kernel<<<vgrid(p), 256, 0, st>>>(z, d, p, s);
+  pcg_dir_kernel<<<vgrid(p), 256, 0, st>>>(z, d, p, s, host_flag);
   probe_after(K_VEC, st);
 }
 
