@@ -201,11 +201,13 @@ class NystromNgdRunner:
             raise _lib.NonFiniteError(f"non-finite loss at iteration {k}")
         self.ctx.call("ngd_loss_grad", _lib.ptr(self.grad))
         grad = self.grad
-        grad_norm = float(np.sqrt(self._dot(grad, grad)))
         if timer:
             timer.mark("linearize+grad")
         factor = nystrom_approximate(gop, self.ell, seed=int(self.rng.integers(2**63)),
                                      omega_source=config.omega_source)
+        # |grad| is read after the sketch (same value as before it: deterministic kernels), so the
+        # host does not stall on the gradient while the sketch could already be queued
+        grad_norm = float(np.sqrt(self._dot(grad, grad)))
         if timer:
             timer.mark("sketch")
         mu = adapt_mu(factor.eig_host[0], self.gamma, loss, grad_norm, config.mu_floor_mode,
