@@ -144,6 +144,7 @@ struct ngd_ctx {
   Buf dseed, pre_last, zs0, zs1;
   Buf jets;  // arena behind zin / dbuf / dseed
   int force_comm = 0;  // "force_comm": build a communicator (and take the multi-rank paths) even for 1 rank
+  int phb_cs = 0;  // option "phb_cs": 0 auto (DSMEM cluster reduction when G >= 16), 1 never
   int use_fused = 0;  // opt-in: measured slower than the two-phase path at C1/C2
   bool fused_ok = false;
   int fgrid = 0;
@@ -827,7 +828,7 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
   CK(c->partA.ensure(sizeof(double) * (size_t)c->rows_A * npp));
   // phase-B split plan: every (layer, tile) gets the same number G of K splits (a tile costs the
   // same per k-tile whatever its fill).  G is the largest that keeps the whole launch in ONE
-  // wave of 3 CTAs/SM (no tail wave); when G >= 16 the splits are grouped into clusters of 8
+  // wave of 3 CTAs/SM (no tail wave); when G >= 64 the splits are grouped into clusters of 8
   // whose partial tiles are reduced through DSMEM (G/8 partials per parameter).
   {
     const int kt = (int)(gm.s_pad / 16);
@@ -836,8 +837,11 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
     const int slots = 3 * 148;
     int G = std::max(1, slots / tiles);
     G = std::min(G, std::max(1, kt / 8));
+    // DSMEM cluster reduction of the split partials pays only when there are many of them (C2:
+    // G = 104 -> 13 partials; measured PCG 3.9 -> 2.9 ms); at G ~ 32 (C3) the cluster
+    // co-scheduling costs more than reading 37 partials (PCG 104.8 -> 98.6 ms without clusters)
     int CS = 1;
-    if (G >= 16) {
+    if (G >= 64 && c->phb_cs != 1) {
       G = G / 8 * 8;
       CS = 8;
     }
@@ -1523,6 +1527,10 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_comm")) {
     c->force_comm = value ? 1 : 0;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "phb_cs")) {
+    c->phb_cs = value ? 1 : 0;
     return NGD_OK;
   }
   if (!strcmp(key, "fused")) {
