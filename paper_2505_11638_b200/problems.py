@@ -180,10 +180,12 @@ class PdeProblem:
         rank, nranks = self.shard
         xi, wmi, wri, oi = rows.x_int, rows.wm_int, rows.wr_int, rows.off_int
         xv, wmv, wrv, ov = rows.x_val, rows.wm_val, rows.wr_val, rows.off_val
+        ctx._int_slice = slice(0, len(xi))
         if nranks > 1:
             from .distributed import shard_slices
 
             si, sv = shard_slices(len(xi), len(xv), self.topology.input_dim + 2, rank, nranks)
+            ctx._int_slice = si
             xi, wmi, wri, oi = xi[si], wmi[si], wri[si], oi[si]
             xv, wmv, wrv, ov = xv[sv], wmv[sv], wrv[sv], ov[sv]
         d = self.topology.input_dim
@@ -266,14 +268,13 @@ class PdeProblem:
         return _lib.like_input(resid, theta)
 
     def h1_relative_error(self, theta, quad):
-        """Relative H1 error at the interior points (problems.py:104-119), on the device."""
-        if self.shard[1] > 1:
-            raise NotImplementedError("h1_relative_error on a sharded problem")
+        """Relative H1 error at the interior points (problems.py:104-119), on the device; on a
+        sharded problem each rank sums its interior shard and the C-ABI all-reduces both sums."""
         ctx = self.context(quad)
         key = "_h1_exact"
         ex = getattr(ctx, key, None)
         if ex is None or ex[0] is not quad:
-            x = quad.interior_points
+            x = quad.interior_points[ctx._int_slice]
             tab = np.concatenate([self.exact(x)[:, None], self.exact_grad(x).reshape(len(x), -1)], axis=1)
             ex = (quad, _lib.to_device(tab))
             setattr(ctx, key, ex)
