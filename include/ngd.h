@@ -121,8 +121,9 @@ int ngd_nystrom_prepare(ngd_ctx* ctx, double* d_omega, int64_t p, int32_t ell);
 int ngd_nystrom_finish(ngd_ctx* ctx, const double* d_omega, double* d_Y, int64_t p, int32_t ell,
                        double* d_U, double* d_eig, double* h_shift);
 /* small dense SVD A = U diag(sigma) V^T of an ell x ell column-major matrix (the step of
- * sketch.py:85 after B = QR); method 2 = cluster one-sided Jacobi, 1 = cuSOLVER polar SVD.
- * h_sweeps receives the Jacobi sweep count (negative if not converged). */
+ * sketch.py:85 after B = QR); method 2 = cluster one-sided Jacobi, 3 = block-exchange cluster Jacobi,
+ * 4 = FP32 pre-sweeps + FP64 block Jacobi, 1 = cuSOLVER polar SVD.  h_sweeps receives the Jacobi
+ * sweep count (negative if not converged; method 4: 1000 * FP32 sweeps + FP64 sweeps). */
 int ngd_small_svd(ngd_ctx* ctx, const double* d_A, int32_t ell, double* d_U, double* d_sigma, int32_t method,
                   int32_t* h_sweeps);
 /* dense operator helper (DenseOperator.matmat, gramian.py:101-120): Y = G V */
@@ -144,7 +145,8 @@ int ngd_pcg(ngd_ctx* ctx, const double* d_dense, int64_t p, const double* d_b, d
 int ngd_small_cholesky(ngd_ctx* ctx, double* d_A, int32_t n, int32_t method, int32_t* h_info);
 
 /* ---- tuning knobs: "svd" = 0 (Householder QR + cuSOLVER gesvdj) | 1 (shifted Cholesky-QR3 + cuSOLVER polar SVD)
- *      | 2 (shifted Cholesky-QR3 + in-house cluster one-sided Jacobi SVD; default, falls back to 1 above ell = 512);
+ *      | 2 (shifted Cholesky-QR3 + in-house cluster one-sided Jacobi SVD; default, falls back to 1 above ell = 512)
+ *      | 3 (as 2 with FP32 Jacobi pre-sweeps, FP64 finish);
  *      "graphs" = 1 (replay PCG iterations as a CUDA graph, default) | 0;
  *      "chol" = 1 (in-house: one-CTA Cholesky for ell <= 32, 8-CTA cluster Cholesky up to 512; default)
  *               | 2 (cluster Cholesky for every ell <= 512) | 0 (cuSOLVER potrf);

@@ -87,7 +87,7 @@ _RESTYPE = {"ngd_last_error": ctypes.c_char_p, "ngd_param_count": _I64, "ngd_lau
 
 _lib = None
 _contexts = []  # weak registry so option changes reach live contexts
-OPTIONS = {"svd": 2}
+OPTIONS = {"svd": 3}
 
 
 def set_option(key, value):

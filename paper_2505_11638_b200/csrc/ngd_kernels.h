@@ -214,6 +214,12 @@ bool chol_cluster_supported(int n);
 cudaError_t chol_upper_cluster(double* A, int n, int lda, int* info, int* flag, cudaStream_t st);
 cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
                              cudaStream_t st);
+// FP64 block Jacobi on X = A^T starting from V = V0 (orthonormal): sigma / U of A^T V0 rotated
+cudaError_t jacobi_svd_block_from(const double* A, int ell, int lda, const double* V0, int ldv, double* U, int ldu,
+                                  double* sigma, int* info, cudaStream_t st);
+// FP32 pre-sweeps of the block Jacobi on A^T: V (ell x ell, unsorted, only near-orthogonal) out
+cudaError_t jacobi_presweep_f32(const double* A, int ell, int lda, double* V, int ldv, double coupling, int* info,
+                                cudaStream_t st);
 void h1_terms(const double* pre_last, Geom gm, const double* exact, double* num, double* den, cudaStream_t st);
 void gather_points(const double* padded, double* compact, Geom gm, cudaStream_t st);
 void scatter_points(const double* compact, double* padded, Geom gm, cudaStream_t st);

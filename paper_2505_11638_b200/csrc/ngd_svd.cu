@@ -329,21 +329,49 @@ __device__ __forceinline__ void jacobi_cs(double al, double be, double ga, doubl
   s *= f;
 }
 
+// FP32 twin for the single-precision pre-sweeps (orthogonality is restored in FP64 afterwards)
+__device__ __forceinline__ void jacobi_cs(float al, float be, float ga, float& c, float& s) {
+  float d = be - al, g2 = 2.0f * ga;
+  const float m = fmaxf(fabsf(d), fabsf(g2));
+  if (m > 1e18f || m < 1e-18f) {
+    const float sc = 1.0f / m;
+    d *= sc;
+    g2 *= sc;
+  }
+  const float ri = rsqrtf(fmaf(d, d, g2 * g2));
+  const float cos2 = fabsf(d) * ri;
+  const float sin2 = (d < 0.0f ? -g2 : g2) * ri;
+  const float hh = fmaf(0.5f, cos2, 0.5f);
+  const float rh = rsqrtf(hh);
+  c = hh * rh;
+  s = 0.5f * sin2 * rh;
+  const float f = fmaf(-0.5f, fmaf(c, c, fmaf(s, s, -1.0f)), 1.0f);
+  c *= f;
+  s *= f;
+}
+
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+template <typename T> using vec2_t = typename Vec2<T>::type;
+
+__device__ __forceinline__ double fmx(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float fmx(float a, float b, float c) { return fmaf(a, b, c); }
+
 // warp-wide Gram entries of two register-resident columns
-template <int RPL>
-__device__ __forceinline__ void gram3(const double2 (&x)[RPL], const double2 (&y)[RPL], double& al, double& be,
-                                      double& ga) {
-  al = 0.0;
-  be = 0.0;
-  ga = 0.0;
+template <int RPL, typename T>
+__device__ __forceinline__ void gram3(const vec2_t<T> (&x)[RPL], const vec2_t<T> (&y)[RPL], T& al, T& be, T& ga) {
+  al = T(0);
+  be = T(0);
+  ga = T(0);
 #pragma unroll
   for (int u = 0; u < RPL; ++u) {
-    al = fma(x[u].x, x[u].x, al);
-    be = fma(y[u].x, y[u].x, be);
-    ga = fma(x[u].x, y[u].x, ga);
-    al = fma(x[u].y, x[u].y, al);
-    be = fma(y[u].y, y[u].y, be);
-    ga = fma(x[u].y, y[u].y, ga);
+    al = fmx(x[u].x, x[u].x, al);
+    be = fmx(y[u].x, y[u].x, be);
+    ga = fmx(x[u].x, y[u].x, ga);
+    al = fmx(x[u].y, x[u].y, al);
+    be = fmx(y[u].y, y[u].y, be);
+    ga = fmx(x[u].y, y[u].y, ga);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {  // three interleaved butterfly reductions
@@ -353,19 +381,19 @@ __device__ __forceinline__ void gram3(const double2 (&x)[RPL], const double2 (&y
   }
 }
 
-template <int RPL>
-__device__ __forceinline__ void load_col(double2 (&x)[RPL], const double* col, int nq, int lane) {
-  const double2* c2 = reinterpret_cast<const double2*>(col);
+template <int RPL, typename T>
+__device__ __forceinline__ void load_col(vec2_t<T> (&x)[RPL], const T* col, int nq, int lane) {
+  const vec2_t<T>* c2 = reinterpret_cast<const vec2_t<T>*>(col);
 #pragma unroll
   for (int u = 0; u < RPL; ++u) {
     const int q = lane + 32 * u;
-    x[u] = q < nq ? c2[q] : make_double2(0.0, 0.0);
+    x[u] = q < nq ? c2[q] : vec2_t<T>{T(0), T(0)};
   }
 }
 
-template <int RPL>
-__device__ __forceinline__ void store_col(double* col, const double2 (&x)[RPL], int nq, int lane) {
-  double2* c2 = reinterpret_cast<double2*>(col);
+template <int RPL, typename T>
+__device__ __forceinline__ void store_col(T* col, const vec2_t<T> (&x)[RPL], int nq, int lane) {
+  vec2_t<T>* c2 = reinterpret_cast<vec2_t<T>*>(col);
 #pragma unroll
   for (int u = 0; u < RPL; ++u) {
     const int q = lane + 32 * u;
@@ -373,84 +401,113 @@ __device__ __forceinline__ void store_col(double* col, const double2 (&x)[RPL], 
   }
 }
 
-template <int RPL>
-__device__ __forceinline__ void rot2(double2 (&x)[RPL], double2 (&y)[RPL], double c, double s) {
+template <int RPL, typename T>
+__device__ __forceinline__ void rot2(vec2_t<T> (&x)[RPL], vec2_t<T> (&y)[RPL], T c, T s) {
 #pragma unroll
   for (int u = 0; u < RPL; ++u) {
-    const double2 a = x[u], b = y[u];
-    x[u] = make_double2(c * a.x - s * b.x, c * a.y - s * b.y);
-    y[u] = make_double2(s * a.x + c * b.x, s * a.y + c * b.y);
+    const vec2_t<T> a = x[u], b = y[u];
+    x[u] = vec2_t<T>{c * a.x - s * b.x, c * a.y - s * b.y};
+    y[u] = vec2_t<T>{s * a.x + c * b.x, s * a.y + c * b.y};
   }
 }
 
-// rotate two shared-memory column pairs (X and V) in place; one warp
-template <int RPL>
-__device__ __forceinline__ bool rotate_pair(double* ci, double* cj, double* vi, double* vj, int ldc, int lane,
-                                            double tol, bool& big) {
+// rotate two shared-memory column pairs (X and V) in place; one warp.  Rotates when the relative
+// coupling |ga| / sqrt(al be) exceeds tol (tol2 = tol^2); 'big' records a coupling^2 >= tbig.
+template <int RPL, typename T>
+__device__ __forceinline__ bool rotate_pair(T* ci, T* cj, T* vi, T* vj, int ldc, int lane, T tol2, T tbig,
+                                            bool& big) {
   const int nq = ldc >> 1;
-  double2 x[RPL], y[RPL];
-  load_col<RPL>(x, ci, nq, lane);
-  load_col<RPL>(y, cj, nq, lane);
-  double al, be, ga;
-  gram3<RPL>(x, y, al, be, ga);
-  if (!(ga != 0.0 && ga * ga > tol * tol * al * be)) return false;
-  big |= ga * ga >= tol * (al * be);  // coupling >= sqrt(tol)
-  double c, s;
+  vec2_t<T> x[RPL], y[RPL];
+  load_col<RPL, T>(x, ci, nq, lane);
+  load_col<RPL, T>(y, cj, nq, lane);
+  T al, be, ga;
+  gram3<RPL, T>(x, y, al, be, ga);
+  if (!(ga != T(0) && ga * ga > tol2 * al * be)) return false;
+  big |= ga * ga >= tbig * (al * be);
+  T c, s;
   jacobi_cs(al, be, ga, c, s);
-  rot2<RPL>(x, y, c, s);
-  store_col<RPL>(ci, x, nq, lane);
-  store_col<RPL>(cj, y, nq, lane);
-  load_col<RPL>(x, vi, nq, lane);
-  load_col<RPL>(y, vj, nq, lane);
-  rot2<RPL>(x, y, c, s);
-  store_col<RPL>(vi, x, nq, lane);
-  store_col<RPL>(vj, y, nq, lane);
+  rot2<RPL, T>(x, y, c, s);
+  store_col<RPL, T>(ci, x, nq, lane);
+  store_col<RPL, T>(cj, y, nq, lane);
+  load_col<RPL, T>(x, vi, nq, lane);
+  load_col<RPL, T>(y, vj, nq, lane);
+  rot2<RPL, T>(x, y, c, s);
+  store_col<RPL, T>(vi, x, nq, lane);
+  store_col<RPL, T>(vj, y, nq, lane);
   return true;
 }
 
 // 16 warps: one column pair per warp and local round (h <= 16)
 constexpr int kBlockSvdThreads = 512;
 
-template <int RPL>
+// T = double: the FP64 Jacobi (outputs sigma descending and U = V sorted; V starts at V0 when given,
+// else I).  T = float: single-precision pre-sweeps on X = s A^T (s a power of two bringing max|A| to
+// [0.5, 1)); sigma == nullptr selects the raw output: V (unsorted, as double) into U[j * ldu + r].
+template <typename T, int RPL>
 __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const double* A, int ell, int lda,
-                                                                           double* U, int ldu, double* sigma,
-                                                                           double tol, int max_sweeps, int h,
+                                                                           const double* Vin, int ldv, double* U,
+                                                                           int ldu, double* sigma, double tol,
+                                                                           double tbig_d, int max_sweeps, int h,
                                                                            int* info) {
-  extern __shared__ __align__(16) double smem[];
-  constexpr int T = kBlockSvdThreads;
-  constexpr int NW = T / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  constexpr int NT = kBlockSvdThreads;
+  constexpr int NW = NT / 32;
   cg::cluster_group cl = cg::this_cluster();
   const int CL = (int)cl.num_blocks();
   const int k = (int)cl.block_rank();
   const int nb = 2 * CL;  // blocks
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ldc = ell + (ell & 1);  // even column stride: 16-B aligned double2 columns
+  const int ldc = ell + (ell & 1);  // even column stride: 8/16-B aligned vector columns
   const int nq = ldc >> 1;
   const size_t slot_sz = (size_t)h * ldc;  // one block of X (or V)
+  const T tol2 = (T)(tol * tol), tbig = (T)tbig_d;
   // buf[phase][slot][0 = X, 1 = V][h][ldc]; X and V of one (phase, slot) are contiguous
   auto bufp = [&](int phase, int slot, int which) { return smem + ((size_t)(phase * 2 + slot) * 2 + which) * slot_sz; };
-  double* norms = smem + 8 * slot_sz;                  // [2][h]
-  int* flags = reinterpret_cast<int*>(norms + 2 * h);  // [4]: rotated / large rotation, by sweep parity
-  __shared__ __align__(8) unsigned long long mbar;    // block arrivals of an exchange
+  double* norms = reinterpret_cast<double*>(smem + 8 * slot_sz);  // [2][h]
+  int* flags = reinterpret_cast<int*>(norms + 2 * h);             // [4]: rotated / large rotation, by sweep parity
+  __shared__ __align__(8) unsigned long long mbar;               // block arrivals of an exchange
   __shared__ int held[2];
+  __shared__ double red[NW];
   const unsigned mbar_a = smem_u32(&mbar);
-  const unsigned blk_bytes = (unsigned)(2 * slot_sz * sizeof(double));  // X + V of one block
+  const unsigned blk_bytes = (unsigned)(2 * slot_sz * sizeof(T));  // X + V of one block
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_a));
     asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  double scale = 1.0;
+  if constexpr (sizeof(T) == 4) {  // keep FP32 Gram entries far from overflow / underflow
+    double m = 0.0;
+    for (int64_t e = tid; e < (int64_t)ell * ell; e += NT) m = fmax(m, fabs(A[(e / ell) * lda + e % ell]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    m = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) m = fmax(m, red[w]);
+    if (m > 0.0) {
+      int ex;
+      frexp(m, &ex);
+      scale = ldexp(1.0, -ex);
+    }
   }
   int phase = 0;
   unsigned mb_parity = 0;
   int blk[2];
   circle_pair(nb, 0, k, blk[0], blk[1]);
   for (int sl = 0; sl < 2; ++sl) {
-    double* X = bufp(0, sl, 0);
-    double* V = bufp(0, sl, 1);
-    for (int64_t e = tid; e < (int64_t)slot_sz; e += T) {
+    T* X = bufp(0, sl, 0);
+    T* V = bufp(0, sl, 1);
+    for (int64_t e = tid; e < (int64_t)slot_sz; e += NT) {
       const int i = (int)(e / ldc), r = (int)(e % ldc);
       const int j = blk[sl] * h + i;  // global column id
-      X[e] = (j < ell && r < ell) ? A[(int64_t)r * lda + j] : 0.0;
-      V[e] = (j == r && r < ell) ? 1.0 : 0.0;
+      const bool in = j < ell && r < ell;
+      X[e] = in ? (T)(A[(int64_t)r * lda + j] * scale) : T(0);
+      if (Vin)
+        V[e] = in ? (T)Vin[(int64_t)j * ldv + r] : T(0);
+      else
+        V[e] = (j == r && r < ell) ? T(1) : T(0);
     }
   }
   if (tid < 4) flags[tid] = 0;
@@ -500,22 +557,22 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   for (; sweep < max_sweeps && !converged; ++sweep) {
     const int par = sweep & 1;
     bool rotated = false;
-    bool big = false;  // a rotation with relative coupling >= sqrt(tol) happened in this sweep
+    bool big = false;  // a rotation with coupling^2 >= tbig happened in this sweep
     for (int r = 0; r < nb - 1; ++r) {
-      double* X0 = bufp(phase, 0, 0);
-      double* V0 = bufp(phase, 0, 1);
-      double* X1 = bufp(phase, 1, 0);
-      double* V1 = bufp(phase, 1, 1);
+      T* X0 = bufp(phase, 0, 0);
+      T* V0 = bufp(phase, 0, 1);
+      T* X1 = bufp(phase, 1, 0);
+      T* V1 = bufp(phase, 1, 1);
       if (r == 0) {  // pairs inside each of the two blocks (circle method on h columns)
         for (int rr = 0; rr < h - 1; ++rr) {
           for (int q = warp; q < h; q += NW) {  // h/2 pairs per block, two blocks
             const int sl = q / (h / 2), kk = q % (h / 2);
             int i, j;
             circle_pair(h, rr, kk, i, j);
-            double* X = sl ? X1 : X0;
-            double* V = sl ? V1 : V0;
-            rotated |= rotate_pair<RPL>(X + (size_t)i * ldc, X + (size_t)j * ldc, V + (size_t)i * ldc,
-                                        V + (size_t)j * ldc, ldc, lane, tol, big);
+            T* X = sl ? X1 : X0;
+            T* V = sl ? V1 : V0;
+            rotated |= rotate_pair<RPL, T>(X + (size_t)i * ldc, X + (size_t)j * ldc, V + (size_t)i * ldc,
+                                           V + (size_t)j * ldc, ldc, lane, tol2, tbig, big);
           }
           __syncthreads();
         }
@@ -523,31 +580,31 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       // cross pairs of the two blocks: h rounds of h disjoint pairs (i, i + sft mod h).  Warp i keeps
       // column i of block 0 (X and V) in registers; the partner columns move through shared memory.
       {
-        double2 xr[RPL], vr[RPL];
+        vec2_t<T> xr[RPL], vr[RPL];
         const bool own = warp < h;
         if (own) {
-          load_col<RPL>(xr, X0 + (size_t)warp * ldc, nq, lane);
-          load_col<RPL>(vr, V0 + (size_t)warp * ldc, nq, lane);
+          load_col<RPL, T>(xr, X0 + (size_t)warp * ldc, nq, lane);
+          load_col<RPL, T>(vr, V0 + (size_t)warp * ldc, nq, lane);
         }
         for (int sft = 0; sft < h; ++sft) {
           TR_T(c0);
           if (own) {
             const int j = (warp + sft >= h) ? warp + sft - h : warp + sft;
-            double* yc = X1 + (size_t)j * ldc;
-            double2 y[RPL];
-            load_col<RPL>(y, yc, nq, lane);
-            double al, be, ga;
-            gram3<RPL>(xr, y, al, be, ga);
-            if (ga != 0.0 && ga * ga > tol * tol * al * be) {
-              big |= ga * ga >= tol * (al * be);
-              double c, s;
+            T* yc = X1 + (size_t)j * ldc;
+            vec2_t<T> y[RPL];
+            load_col<RPL, T>(y, yc, nq, lane);
+            T al, be, ga;
+            gram3<RPL, T>(xr, y, al, be, ga);
+            if (ga != T(0) && ga * ga > tol2 * al * be) {
+              big |= ga * ga >= tbig * (al * be);
+              T c, s;
               jacobi_cs(al, be, ga, c, s);
-              rot2<RPL>(xr, y, c, s);
-              store_col<RPL>(yc, y, nq, lane);
-              double* vc = V1 + (size_t)j * ldc;
-              load_col<RPL>(y, vc, nq, lane);
-              rot2<RPL>(vr, y, c, s);
-              store_col<RPL>(vc, y, nq, lane);
+              rot2<RPL, T>(xr, y, c, s);
+              store_col<RPL, T>(yc, y, nq, lane);
+              T* vc = V1 + (size_t)j * ldc;
+              load_col<RPL, T>(y, vc, nq, lane);
+              rot2<RPL, T>(vr, y, c, s);
+              store_col<RPL, T>(vc, y, nq, lane);
               rotated = true;
             }
           }
@@ -559,17 +616,17 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
           TR_ADD(5, 1);
         }
         if (own) {
-          store_col<RPL>(X0 + (size_t)warp * ldc, xr, nq, lane);
-          store_col<RPL>(V0 + (size_t)warp * ldc, vr, nq, lane);
+          store_col<RPL, T>(X0 + (size_t)warp * ldc, xr, nq, lane);
+          store_col<RPL, T>(V0 + (size_t)warp * ldc, vr, nq, lane);
         }
       }
       if (r == nb - 2) break;  // sweep ends; the exchange to round 0 happens after the convergence test
       exchange(r, r + 1);
     }
-    // Converged when no pair needed a rotation, or when every rotation of the sweep was already
-    // below sqrt(tol) in relative coupling: one-sided Jacobi converges quadratically at the end, so
-    // the following sweep would find every |ga| / sqrt(al be) ~ coupling^2 < tol and rotate nothing
-    // (measured on the C2 sketch's R: 1.7e-8 -> no rotation; tools/svd_timing.py, tests vs LAPACK).
+    // Converged when no pair needed a rotation, or when every rotation of the sweep was below
+    // sqrt(tbig) in relative coupling.  FP64 (tbig = tol): one-sided Jacobi converges quadratically
+    // at the end, so the following sweep would find every coupling ~ coupling^2 < tol and rotate
+    // nothing (measured on the C2 sketch's R: 1.7e-8 -> no rotation; tests vs LAPACK).
     if (rotated && lane == 0) flags[par] = 1;
     if (big && lane == 0) flags[2 + par] = 1;
     cl.sync();
@@ -586,13 +643,24 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
     if (!converged) exchange(nb - 2, 0);  // back to the round-0 placement
   }
   __syncthreads();
+  if (sigma == nullptr) {  // raw V, column j = global column id
+    for (int q = warp; q < 2 * h; q += NW) {
+      const int gid = blk[q / h] * h + (q % h);
+      if (gid >= ell) continue;
+      const T* v = bufp(phase, q / h, 1) + (size_t)(q % h) * ldc;
+      for (int r = lane; r < ell; r += 32) U[(int64_t)gid * ldu + r] = (double)v[r];
+    }
+    if (k == 0 && tid == 0) info[0] = converged ? sweep : -sweep;
+    cl.sync();
+    return;
+  }
   // norms of the held columns, ranks over the cluster, outputs
   for (int q = warp; q < 2 * h; q += NW) {
-    const double* c = bufp(phase, q / h, 0) + (size_t)(q % h) * ldc;
+    const T* c = bufp(phase, q / h, 0) + (size_t)(q % h) * ldc;
     double sacc = 0.0;
-    for (int r = lane; r < ell; r += 32) sacc = fma(c[r], c[r], sacc);
+    for (int r = lane; r < ell; r += 32) sacc = fma((double)c[r], (double)c[r], sacc);
     sacc = warp_sum(sacc);
-    if (lane == 0) norms[q] = sqrt(sacc);
+    if (lane == 0) norms[q] = sqrt(sacc) / scale;
   }
   if (tid == 0) {
     held[0] = blk[0];
@@ -613,22 +681,26 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
     for (int off = 16; off > 0; off >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
     if (rank < ell) {
       if (lane == 0) sigma[rank] = sj;
-      const double* v = bufp(phase, q / h, 1) + (size_t)(q % h) * ldc;
-      for (int r = lane; r < ell; r += 32) U[(int64_t)rank * ldu + r] = v[r];
+      const T* v = bufp(phase, q / h, 1) + (size_t)(q % h) * ldc;
+      for (int r = lane; r < ell; r += 32) U[(int64_t)rank * ldu + r] = (double)v[r];
     }
   }
   if (k == 0 && tid == 0) info[0] = converged ? sweep : -sweep;
   cl.sync();
 }
 
+static size_t jsvd_block_smem(int ell, int h, size_t elt) {
+  return elt * 8 * (size_t)h * (ell + (ell & 1)) + sizeof(double) * 2 * h + 64;
+}
+
 // cluster size / block size for the block-exchange Jacobi: h <= 16 columns per block
-// (one pair per warp and round), 8 blocks of X/V per CTA within 200 KB.
+// (one pair per warp and round), 8 blocks of X/V per CTA within 200 KB (FP64 sizing).
 static bool jsvd_block_plan(int ell, int& cl, int& h) {
   for (int c : {2, 4, 8, 16}) {
     int hh = (ell + 2 * c - 1) / (2 * c);
     hh += hh & 1;  // even (circle method inside a block)
     if (hh > 16 && c < 16) continue;
-    if (sizeof(double) * (8 * (size_t)hh * (ell + (ell & 1)) + 2 * hh) + 64 > 200 * 1024) continue;
+    if (jsvd_block_smem(ell, hh, sizeof(double)) > 200 * 1024) continue;
     cl = c;
     h = hh;
     return true;
@@ -641,11 +713,12 @@ int jsvd_block_supported(int ell) {
   return jsvd_block_plan(ell, c, h) ? c : 0;
 }
 
-template <int RPL>
-static cudaError_t launch_jsvd_block_r(const double* A, int ell, int lda, double* U, int ldu, double* sigma,
-                                       double tol, int max_sweeps, int cl, int h, int* info, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (8 * (size_t)h * (ell + (ell & 1)) + 2 * h) + 64;
-  auto kern = jsvd_block_kernel<RPL>;
+template <typename T, int RPL>
+static cudaError_t launch_jsvd_block_r(const double* A, int ell, int lda, const double* Vin, int ldv, double* U,
+                                       int ldu, double* sigma, double tol, double tbig, int max_sweeps, int cl, int h,
+                                       int* info, cudaStream_t st) {
+  const size_t smem = jsvd_block_smem(ell, h, sizeof(T));
+  auto kern = jsvd_block_kernel<T, RPL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (cl > 8) {
@@ -665,29 +738,52 @@ static cudaError_t launch_jsvd_block_r(const double* A, int ell, int lda, double
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   probe_before(K_SVD, st);
-  e = cudaLaunchKernelEx(&cfg, kern, A, ell, lda, U, ldu, sigma, tol, max_sweeps, h, info);
+  e = cudaLaunchKernelEx(&cfg, kern, A, ell, lda, Vin, ldv, U, ldu, sigma, tol, tbig, max_sweeps, h, info);
   probe_after(K_SVD, st);
   return e;
 }
 
-cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
-                             cudaStream_t st) {
+template <typename T>
+static cudaError_t launch_jsvd_block(const double* A, int ell, int lda, const double* Vin, int ldv, double* U,
+                                     int ldu, double* sigma, double tol, double tbig, int max_sweeps, int* info,
+                                     cudaStream_t st) {
   int cl, h;
   if (!jsvd_block_plan(ell, cl, h)) return cudaErrorInvalidValue;
-  const double tol = 2.220446049250313e-16 * (double)ell;
-  const int max_sweeps = 40;
-  const int rpl = (ell + 63) / 64;  // double2 per lane
-  switch (rpl) {
-    case 1: return launch_jsvd_block_r<1>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-    case 2: return launch_jsvd_block_r<2>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-    case 3: return launch_jsvd_block_r<3>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-    case 4: return launch_jsvd_block_r<4>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-    case 5: return launch_jsvd_block_r<5>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-    case 6: return launch_jsvd_block_r<6>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-    case 7: return launch_jsvd_block_r<7>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
-    case 8: return launch_jsvd_block_r<8>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, cl, h, info, st);
+  switch ((ell + 63) / 64) {  // vector pairs per lane
+#define NGD_JSVD_CASE(R)                                                                                       \
+  case R:                                                                                                      \
+    return launch_jsvd_block_r<T, R>(A, ell, lda, Vin, ldv, U, ldu, sigma, tol, tbig, max_sweeps, cl, h, info, \
+                                     st);
+    NGD_JSVD_CASE(1)
+    NGD_JSVD_CASE(2)
+    NGD_JSVD_CASE(3)
+    NGD_JSVD_CASE(4)
+    NGD_JSVD_CASE(5)
+    NGD_JSVD_CASE(6)
+    NGD_JSVD_CASE(7)
+    NGD_JSVD_CASE(8)
+#undef NGD_JSVD_CASE
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
+                             cudaStream_t st) {
+  const double tol = 2.220446049250313e-16 * (double)ell;
+  return launch_jsvd_block<double>(A, ell, lda, nullptr, 0, U, ldu, sigma, tol, tol, 40, info, st);
+}
+
+cudaError_t jacobi_svd_block_from(const double* A, int ell, int lda, const double* V0, int ldv, double* U, int ldu,
+                                  double* sigma, int* info, cudaStream_t st) {
+  const double tol = 2.220446049250313e-16 * (double)ell;
+  return launch_jsvd_block<double>(A, ell, lda, V0, ldv, U, ldu, sigma, tol, tol, 40, info, st);
+}
+
+cudaError_t jacobi_presweep_f32(const double* A, int ell, int lda, double* V, int ldv, double coupling, int* info,
+                                cudaStream_t st) {
+  // rotate above coupling^2 (near FP32 rounding), stop once no rotation of a sweep reached 'coupling'
+  return launch_jsvd_block<float>(A, ell, lda, nullptr, 0, V, ldv, nullptr, coupling * coupling,
+                                  coupling * coupling, 30, info, st);
 }
 
 }  // namespace ngd
