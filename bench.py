@@ -248,7 +248,7 @@ def config_dict(name, world):
 # ---------------------------------------------------------------------------
 
 
-def roofline_entry(kind, widths, n_int, n_bnd, ell, p, sweeps, count, total_ms, peaks):
+def roofline_entry(kind, widths, n_int, n_bnd, ell, p, sweeps, count, total_ms, peaks, sweeps_f32=0):
     """Algorithmic work per launch of kernel class `kind` / average duration."""
     d = widths[0]
     S = n_int * (d + 2) + n_bnd
@@ -260,8 +260,10 @@ def roofline_entry(kind, widths, n_int, n_bnd, ell, p, sweeps, count, total_ms, 
         work = 2.0 * pw * S
     elif kind in (1, 2):  # one launch = one layer, one point segment (average)
         work = 2.0 * pw * S / (2 * nl)
-    elif kind == 9:  # one-sided Jacobi on X = R^T with rotation accumulation: ~9 ell^2 (ell-1) per sweep
-        work = 9.0 * ell * ell * (ell - 1) * max(sweeps, 1)
+    elif kind == 9:  # one-sided Jacobi on X = R^T with rotation accumulation: ~9 ell^2 (ell-1) per sweep;
+        # svd=3 runs two launches per factorisation (FP32 pre-sweeps, FP64 finish): their average
+        launches = 2 if sweeps_f32 > 0 else 1
+        work = 9.0 * ell * ell * (ell - 1) * (max(sweeps, 1) + sweeps_f32) / launches
     elif kind == 10:
         work = ell ** 3 / 3.0
     elif kind == 14:  # fused narrow matvec: one launch = one full J^T diag(w) J v
@@ -470,8 +472,12 @@ def main():
     avg_ms = ktot.value / max(kcnt.value, 1)
     sweeps = _lib.ctypes.c_int64()
     runner.ctx.call("ngd_get_stat", b"jacobi_sweeps", _lib.ctypes.byref(sweeps))
+    sweeps_f32 = _lib.ctypes.c_int64()
+    runner.ctx.call("ngd_get_stat", b"jacobi_sweeps_f32", _lib.ctypes.byref(sweeps_f32))
     roof = roofline_entry(probe_kind, widths, n_int, n_bnd, ell, len(theta0), abs(sweeps.value), kcnt.value,
-                          ktot.value, peaks)
+                          ktot.value, peaks, sweeps_f32=abs(sweeps_f32.value))
+    if probe_kind == 9:
+        roof["sweeps"] = {"fp64": abs(sweeps.value), "fp32": abs(sweeps_f32.value)}
     try:  # measured DRAM traffic of this kernel at this config (one ncu --set full capture)
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_r01.json")) as fh:
             tr = json.load(fh).get(f"{args.config}/{roof['kernel']}")

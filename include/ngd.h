@@ -152,7 +152,8 @@ int ngd_small_cholesky(ngd_ctx* ctx, double* d_A, int32_t n, int32_t method, int
  *               | 2 (cluster Cholesky for every ell <= 512) | 0 (cuSOLVER potrf);
  *      "trsm" = 1 (in-house DMMA right triangular solve for ell <= 512, default) | 0 (cuBLAS DTRSM) */
 int ngd_set_option(ngd_ctx* ctx, const char* key, int64_t value);
-/* diagnostics: "jacobi_sweeps" (last Nystrom factorisation), "phase_b_splits" */
+/* diagnostics: "jacobi_sweeps" (FP64 sweeps of the last Nystrom factorisation), "jacobi_sweeps_f32"
+ * (its FP32 pre-sweeps, svd = 3), "phase_b_splits" */
 int ngd_get_stat(ngd_ctx* ctx, const char* key, int64_t* out);
 
 /* ---- vector helpers used by the host policy ------------------------------

@@ -176,6 +176,7 @@ struct ngd_ctx {
   Buf trsm_work;
   Buf chol_work;
   int last_sweeps = 0;
+  int last_sweeps_f32 = 0;
   int use_graphs = 1;
   int graph_gen = 0;
   cudaStream_t cap_stream = nullptr;
@@ -579,7 +580,11 @@ static int small_svd_mixed(ngd_ctx* c, int ell) {
   double* G = V0 + 2 * l2;
   double* A2 = V0 + 3 * l2;
   int* info = static_cast<int*>(c->nys_info.p);
-  CK(jacobi_presweep_f32(c->nys_r.d(), ell, ell, V0, ell, 1e-3, info + 3, c->stream));
+  static const double coupling = [] {  // NGD_SVD_F32_COUPLING: tuning override of the FP32 stopping coupling
+    const char* e = getenv("NGD_SVD_F32_COUPLING");
+    return e ? atof(e) : 1e-3;
+  }();
+  CK(jacobi_presweep_f32(c->nys_r.d(), ell, ell, V0, ell, coupling, info + 3, c->stream));
   for (int it = 0; it < 2; ++it) {
     CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, ell, &one, V0, ell, V0, ell, &zero, G, ell));
     CK(cudaMemcpyAsync(V1, V0, sizeof(double) * l2, cudaMemcpyDeviceToDevice, c->stream));
@@ -1251,7 +1256,7 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
                   U_row, (int)p));
   eig_from_sv(c->nys_s.d(), ell, c->S(SC_SHIFT), eig, c->stream);
   CK(cudaMemcpyAsync(&c->h_pin[0], c->S(SC_SHIFT), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(&c->h_pin[60], static_cast<int*>(c->nys_info.p) + 2, sizeof(int), cudaMemcpyDeviceToHost,
+  CK(cudaMemcpyAsync(&c->h_pin[60], static_cast<int*>(c->nys_info.p) + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost,
                      c->stream));
   CK(cudaStreamSynchronize(c->stream));
   {
@@ -1262,9 +1267,10 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
   }
   if (h_shift) *h_shift = c->h_pin[0];
   {
-    int sw = 0;
-    memcpy(&sw, &c->h_pin[60], sizeof(int));
-    c->last_sweeps = sw;
+    int sw[2] = {0, 0};  // FP64 sweeps, FP32 pre-sweeps
+    memcpy(sw, &c->h_pin[60], 2 * sizeof(int));
+    c->last_sweeps = sw[0];
+    c->last_sweeps_f32 = (c->svd_method == 3 && jsvd_block_supported(ell) > 0) ? sw[1] : 0;
   }
   CK(cudaGetLastError());
   return NGD_OK;
@@ -1548,6 +1554,10 @@ int ngd_get_stat(ngd_ctx* c, const char* key, int64_t* out) {
   if (!c || !key || !out) return fail(NGD_E_SHAPE, "bad stat query");
   if (!strcmp(key, "jacobi_sweeps")) {
     *out = c->last_sweeps;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "jacobi_sweeps_f32")) {
+    *out = c->last_sweeps_f32;
     return NGD_OK;
   }
   if (!strcmp(key, "phase_b_splits")) {

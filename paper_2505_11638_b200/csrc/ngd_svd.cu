@@ -16,6 +16,7 @@
 // accumulates the rotations V, which are then R's left singular vectors:
 // R^T V = U_X S  =>  R = V S U_X^T.
 #include <cooperative_groups.h>
+#include <cstring>
 
 #include "ngd_common.cuh"
 #include "ngd_kernels.h"
@@ -278,9 +279,9 @@ cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, do
 // accumulated rotation with DMMA was measured slower: at one SM's FP64 rate that
 // update costs as much as the direct rotations.)
 #ifdef NGD_SVD_TRACE
-__device__ unsigned long long g_tr[16];
+__device__ unsigned long long g_tr[16 * 16];  // [CTA][counter], thread 0 of each CTA
 #define TR_T(v) long long v = clock64()
-#define TR_ADD(k, d) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_tr[k] += (unsigned long long)(d); } while (0)
+#define TR_ADD(k, d) do { if (threadIdx.x == 0) g_tr[blockIdx.x * 16 + (k)] += (unsigned long long)(d); } while (0)
 #else
 #define TR_T(v)
 #define TR_ADD(k, d)
@@ -440,6 +441,87 @@ __device__ __forceinline__ bool rotate_pair(T* ci, T* cj, T* vi, T* vj, int ldc,
 // 16 warps: one column pair per warp and local round (h <= 16)
 constexpr int kBlockSvdThreads = 512;
 
+// Exchange schedule of the block tournament (circle method on nb = 2 CL blocks).  Consecutive rounds
+// share no pair, so the graph "CTA -- next-round pair containing one of its blocks" is 2-regular and
+// has a perfect matching: every CTA keeps one block in place and receives its new partner, which
+// lands in the other buffer phase of the outgoing slot (free since the previous barrier).  The
+// placement sequence repeats after 4 sweeps.  Word (t, c): bits 0-1 source buffer (phase * 2 + slot),
+// 2-5 destination CTA, 6-7 destination buffer, 8-12 / 13-17 blocks held after the move (slots 0, 1),
+// 18 / 19 their buffer phases.
+struct JsvdPlan {
+  int period;             // exchanges before the placement sequence repeats
+  unsigned w[4 * 31 * 16];
+};
+
+static bool jsvd_make_plan(int CL, JsvdPlan& P) {
+  const int nb = 2 * CL, m = nb - 1;
+  auto circle = [&](int r, int kk, int& a, int& b) {
+    if (kk == 0) {
+      a = 0;
+      b = 1 + r;
+    } else {
+      a = 1 + (r + kk) % m;
+      b = 1 + ((r - kk) % m + m) % m;
+    }
+  };
+  int blk[16][2], ph[16][2];
+  for (int c = 0; c < CL; ++c) {
+    circle(0, c, blk[c][0], blk[c][1]);
+    ph[c][0] = ph[c][1] = 0;
+  }
+  const int period = 4 * m;
+  if (period * CL > (int)(sizeof(P.w) / sizeof(P.w[0]))) return false;
+  P.period = period;
+  for (int t = 0; t < period; ++t) {
+    const int r_to = (t + 1) % m;
+    int pa[16][2], pair_of[32], hold_c[32], hold_s[32], assigned[16], keep[16], owner[16];
+    for (int j = 0; j < CL; ++j) {
+      circle(r_to, j, pa[j][0], pa[j][1]);
+      pair_of[pa[j][0]] = pair_of[pa[j][1]] = j;
+    }
+    for (int c = 0; c < CL; ++c) {
+      assigned[c] = -1;
+      for (int s = 0; s < 2; ++s) {
+        hold_c[blk[c][s]] = c;
+        hold_s[blk[c][s]] = s;
+      }
+    }
+    for (int c0 = 0; c0 < CL; ++c0) {  // walk each alternating cycle
+      if (assigned[c0] >= 0) continue;
+      int c = c0, x = blk[c0][0];
+      while (true) {
+        const int j = pair_of[x];
+        assigned[c] = j;
+        owner[j] = c;
+        keep[c] = hold_s[x];
+        const int z = pa[j][0] == x ? pa[j][1] : pa[j][0];
+        const int c2 = hold_c[z];
+        if (assigned[c2] >= 0) break;
+        c = c2;
+        x = blk[c2][hold_s[z] ^ 1];
+      }
+    }
+    int nblk[16][2], nph[16][2];
+    for (int c = 0; c < CL; ++c) {
+      const int os = keep[c] ^ 1, kept = blk[c][keep[c]], j = assigned[c];
+      nblk[c][keep[c]] = kept;
+      nph[c][keep[c]] = ph[c][keep[c]];
+      nblk[c][os] = pa[j][0] == kept ? pa[j][1] : pa[j][0];
+      nph[c][os] = ph[c][os] ^ 1;
+    }
+    for (int c = 0; c < CL; ++c) {
+      const int os = keep[c] ^ 1, y = blk[c][os];
+      const int d = owner[pair_of[y]], ds = keep[d] ^ 1;
+      const unsigned sb = (unsigned)(ph[c][os] * 2 + os), db = (unsigned)(nph[d][ds] * 2 + ds);
+      P.w[t * CL + c] = sb | ((unsigned)d << 2) | (db << 6) | ((unsigned)nblk[c][0] << 8) |
+                        ((unsigned)nblk[c][1] << 13) | ((unsigned)nph[c][0] << 18) | ((unsigned)nph[c][1] << 19);
+    }
+    memcpy(blk, nblk, sizeof(blk));
+    memcpy(ph, nph, sizeof(ph));
+  }
+  return true;
+}
+
 // T = double: the FP64 Jacobi (outputs sigma descending and U = V sorted; V starts at V0 when given,
 // else I).  T = float: single-precision pre-sweeps on X = s A^T (s a power of two bringing max|A| to
 // [0.5, 1)); sigma == nullptr selects the raw output: V (unsorted, as double) into U[j * ldu + r].
@@ -448,7 +530,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
                                                                            const double* Vin, int ldv, double* U,
                                                                            int ldu, double* sigma, double tol,
                                                                            double tbig_d, int max_sweeps, int h,
-                                                                           int* info) {
+                                                                           int* info, const __grid_constant__ JsvdPlan plan) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
   constexpr int NT = kBlockSvdThreads;
@@ -492,9 +574,8 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       scale = ldexp(1.0, -ex);
     }
   }
-  int phase = 0;
   unsigned mb_parity = 0;
-  int blk[2];
+  int blk[2], ph[2] = {0, 0};
   circle_pair(nb, 0, k, blk[0], blk[1]);
   for (int sl = 0; sl < 2; ++sl) {
     T* X = bufp(0, sl, 0);
@@ -513,38 +594,32 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   if (tid < 4) flags[tid] = 0;
   cl.sync();
 
-  // move the two held blocks from the placement of round r_from to that of round r_to
-  auto exchange = [&](int r_from, int r_to) {
+  // Move to the next round's placement (schedule precomputed on the host, see jsvd_plan): one block
+  // per CTA crosses DSMEM, the other stays in place (the exchange is DSMEM-bandwidth bound).
+  int xt = 0;  // exchanges so far
+  auto exchange = [&]() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async-proxy reads
+    const unsigned e = plan.w[(xt % plan.period) * CL + k];
+    ++xt;
     TR_T(e0);
-    cl.sync();  // all rotations of r_from done everywhere; all phase^1 buffers are free
+    cl.sync();  // all rotations done everywhere; every copy of the previous exchange has landed
     TR_T(e1);
     TR_ADD(0, e1 - e0);
     if (tid == 0) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_a), "r"(2 * blk_bytes)
-                   : "memory");
-      for (int sl = 0; sl < 2; ++sl) {
-        int dst_cta = 0, dst_slot = 0;
-        for (int k2 = 0; k2 < CL; ++k2) {
-          int a2, b2;
-          circle_pair(nb, r_to, k2, a2, b2);
-          if (a2 == blk[sl]) { dst_cta = k2; dst_slot = 0; }
-          if (b2 == blk[sl]) { dst_cta = k2; dst_slot = 1; }
-        }
-        const unsigned src = smem_u32(bufp(phase, sl, 0));
-        const unsigned dst = cluster_addr(smem_u32(bufp(phase ^ 1, dst_slot, 0)), dst_cta);
-        const unsigned mb = cluster_addr(mbar_a, dst_cta);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-            "r"(src), "r"(blk_bytes), "r"(mb)
-            : "memory");
-      }
+      const int sb = e & 3, dc = (e >> 2) & 15, db = (e >> 6) & 3;
+      const unsigned src = smem_u32(bufp(sb >> 1, sb & 1, 0));
+      const unsigned dst = cluster_addr(smem_u32(bufp(db >> 1, db & 1, 0)), dc);
+      const unsigned mb = cluster_addr(mbar_a, dc);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_a), "r"(blk_bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+          "r"(src), "r"(blk_bytes), "r"(mb)
+          : "memory");
     }
-    int want[2];
-    circle_pair(nb, r_to, k, want[0], want[1]);
-    blk[0] = want[0];
-    blk[1] = want[1];
-    phase ^= 1;
+    blk[0] = (e >> 8) & 31;
+    blk[1] = (e >> 13) & 31;
+    ph[0] = (e >> 18) & 1;
+    ph[1] = (e >> 19) & 1;
     mbar_wait(mbar_a, mb_parity);
     mb_parity ^= 1u;
     TR_T(e2);
@@ -559,10 +634,10 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
     bool rotated = false;
     bool big = false;  // a rotation with coupling^2 >= tbig happened in this sweep
     for (int r = 0; r < nb - 1; ++r) {
-      T* X0 = bufp(phase, 0, 0);
-      T* V0 = bufp(phase, 0, 1);
-      T* X1 = bufp(phase, 1, 0);
-      T* V1 = bufp(phase, 1, 1);
+      T* X0 = bufp(ph[0], 0, 0);
+      T* V0 = bufp(ph[0], 0, 1);
+      T* X1 = bufp(ph[1], 1, 0);
+      T* V1 = bufp(ph[1], 1, 1);
       if (r == 0) {  // pairs inside each of the two blocks (circle method on h columns)
         for (int rr = 0; rr < h - 1; ++rr) {
           for (int q = warp; q < h; q += NW) {  // h/2 pairs per block, two blocks
@@ -621,7 +696,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
         }
       }
       if (r == nb - 2) break;  // sweep ends; the exchange to round 0 happens after the convergence test
-      exchange(r, r + 1);
+      exchange();
     }
     // Converged when no pair needed a rotation, or when every rotation of the sweep was below
     // sqrt(tbig) in relative coupling.  FP64 (tbig = tol): one-sided Jacobi converges quadratically
@@ -640,14 +715,14 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       flags[par ^ 1] = 0;
       flags[2 + (par ^ 1)] = 0;
     }
-    if (!converged) exchange(nb - 2, 0);  // back to the round-0 placement
+    if (!converged) exchange();  // on to round 0 of the next sweep
   }
   __syncthreads();
   if (sigma == nullptr) {  // raw V, column j = global column id
     for (int q = warp; q < 2 * h; q += NW) {
       const int gid = blk[q / h] * h + (q % h);
       if (gid >= ell) continue;
-      const T* v = bufp(phase, q / h, 1) + (size_t)(q % h) * ldc;
+      const T* v = bufp(ph[q / h], q / h, 1) + (size_t)(q % h) * ldc;
       for (int r = lane; r < ell; r += 32) U[(int64_t)gid * ldu + r] = (double)v[r];
     }
     if (k == 0 && tid == 0) info[0] = converged ? sweep : -sweep;
@@ -656,7 +731,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   }
   // norms of the held columns, ranks over the cluster, outputs
   for (int q = warp; q < 2 * h; q += NW) {
-    const T* c = bufp(phase, q / h, 0) + (size_t)(q % h) * ldc;
+    const T* c = bufp(ph[q / h], q / h, 0) + (size_t)(q % h) * ldc;
     double sacc = 0.0;
     for (int r = lane; r < ell; r += 32) sacc = fma((double)c[r], (double)c[r], sacc);
     sacc = warp_sum(sacc);
@@ -681,7 +756,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
     for (int off = 16; off > 0; off >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
     if (rank < ell) {
       if (lane == 0) sigma[rank] = sj;
-      const T* v = bufp(phase, q / h, 1) + (size_t)(q % h) * ldc;
+      const T* v = bufp(ph[q / h], q / h, 1) + (size_t)(q % h) * ldc;
       for (int r = lane; r < ell; r += 32) U[(int64_t)rank * ldu + r] = (double)v[r];
     }
   }
@@ -737,8 +812,17 @@ static cudaError_t launch_jsvd_block_r(const double* A, int ell, int lda, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static JsvdPlan plans[5];  // CL = 1 << i
+  static bool have[5] = {false, false, false, false, false};
+  int li = 0;
+  while ((1 << li) < cl) ++li;
+  if (!have[li]) {
+    if (!jsvd_make_plan(cl, plans[li])) return cudaErrorInvalidValue;
+    have[li] = true;
+  }
   probe_before(K_SVD, st);
-  e = cudaLaunchKernelEx(&cfg, kern, A, ell, lda, Vin, ldv, U, ldu, sigma, tol, tbig, max_sweeps, h, info);
+  e = cudaLaunchKernelEx(&cfg, kern, A, ell, lda, Vin, ldv, U, ldu, sigma, tol, tbig, max_sweeps, h, info,
+                         plans[li]);
   probe_after(K_SVD, st);
   return e;
 }

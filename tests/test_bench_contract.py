@@ -42,3 +42,6 @@ def test_roofline_work_model():
     # Jacobi SVD: 9 ell^2 (ell - 1) FLOP per sweep
     r = bench.roofline_entry(9, widths, n_int, n_bnd, ell, 8577, 12, 1, 5.0, peaks)
     assert r["algorithmic_work_per_launch"] == pytest.approx(9.0 * ell * ell * (ell - 1) * 12)
+    # mixed precision (svd = 3): 9 FP32 + 2 FP64 sweeps over two launches
+    r = bench.roofline_entry(9, widths, n_int, n_bnd, ell, 8577, 2, 2, 5.0, peaks, sweeps_f32=9)
+    assert r["algorithmic_work_per_launch"] == pytest.approx(9.0 * ell * ell * (ell - 1) * 11 / 2)
