@@ -685,7 +685,7 @@ int ngd_ctx_create(const int32_t* widths, int32_t n_widths, int32_t device, ngd_
     ck(c->vp[l].ensure(nf));
     if (l + 1 < c->NL) ck(c->apr[l].ensure(sizeof(double) * (size_t)c->Mp_r[l] * c->Kp_r[l]));
   }
-  ck(c->redp.ensure(sizeof(double) * 4096));
+  ck(c->redp.ensure(sizeof(double) * 65536));  // block partials of the last-block reductions (grid <= 65536)
   ck(c->counters.ensure(sizeof(unsigned) * 64));
   ck(c->scal.ensure(sizeof(double) * SC_N));
   ck(c->pcgs.ensure(sizeof(PcgState)));

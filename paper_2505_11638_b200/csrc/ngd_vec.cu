@@ -73,7 +73,7 @@ void init_point_data(double* zin1, double* dlast, Geom gm, const double* x_int, 
 // ----------------------- deterministic two-stage sums ------------------------
 // Each launch uses grid = nblocks_for(n) blocks; block b sums a fixed strided set,
 // the last block to finish sums the block partials in index order.
-int nblocks_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 511) / 512, 1184)); }
+int nblocks_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1184)); }
 
 template <typename T, typename F>
 __device__ __forceinline__ void finish_sum(double v, double* partials, unsigned int* counter, T* out, F&& post) {
@@ -323,14 +323,21 @@ __global__ void __launch_bounds__(kThreads) utv_kernel(const PrecondArgs* pa, in
   __shared__ double sh[kThreads / 32];
   const int j = blockIdx.x;
   const double* u = pa->U + (int64_t)j * p;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int64_t i = threadIdx.x;
-  for (; i + 3 * kThreads < p; i += 4 * kThreads) {
+  for (; i + 7 * kThreads < p; i += 8 * kThreads) {  // 16 loads in flight per thread
+    double uu[8], vv[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] = fma(u[i + q * kThreads], v[i + q * kThreads], acc[q]);
+    for (int q = 0; q < 8; ++q) {
+      uu[q] = u[i + q * kThreads];
+      vv[q] = v[i + q * kThreads];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = fma(uu[q], vv[q], acc[q]);
   }
-  for (; i < p; i += kThreads) acc[0] = fma(u[i], v[i], acc[0]);
-  const double tot = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), sh);
+  for (int q = 0; i < p; i += kThreads, ++q) acc[q & 7] = fma(u[i], v[i], acc[q & 7]);
+  const double tot =
+      block_sum(((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7])), sh);
   if (threadIdx.x == 0) {
     const double mu = pa->mu;
     const double* eig = pa->eig;
@@ -345,31 +352,41 @@ __global__ void __launch_bounds__(kThreads) uc_kernel(const PrecondArgs* pa, int
                                                       const double* v, double* out, const int* done, PcgState* pcg,
                                                       int first, double* partials, unsigned* counter) {
   if (done && *done) return;
-  extern __shared__ double cs[];  // [ell] c' then [4][64] partial rows
+  extern __shared__ double cs[];  // [ell] c' then [8][32] partial rows
   double* part = cs + ell;
   for (int j = threadIdx.x; j < ell; j += blockDim.x) cs[j] = cprime[j];
   __syncthreads();
-  const int rl = threadIdx.x & 63, grp = threadIdx.x >> 6;
-  const int64_t i = (int64_t)blockIdx.x * 64 + rl;
+  constexpr int kRows = 32, kGroups = kThreads / kRows;
+  const int rl = threadIdx.x & (kRows - 1), grp = threadIdx.x / kRows;
+  const int64_t i = (int64_t)blockIdx.x * kRows + rl;
   double s = 0.0;
   if (i < p && ell > 0) {
     const double* U = pa->U;
-    const int j0 = grp * ((ell + 3) / 4), j1 = min(ell, j0 + (ell + 3) / 4);
+    const int per = (ell + kGroups - 1) / kGroups;
+    const int j0 = grp * per, j1 = min(ell, j0 + per);
     int j = j0;
-    for (; j + 8 <= j1; j += 8) {
-      double u[8];
+    double s2 = 0.0;
+    for (; j + 16 <= j1; j += 16) {  // 16 loads in flight, two interleaved chains
+      double u[16];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) u[q] = U[(int64_t)(j + q) * p + i];
+      for (int q = 0; q < 16; ++q) u[q] = U[(int64_t)(j + q) * p + i];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) s = fma(u[q], cs[j + q], s);
+      for (int q = 0; q < 16; q += 2) {
+        s = fma(u[q], cs[j + q], s);
+        s2 = fma(u[q + 1], cs[j + q + 1], s2);
+      }
     }
     for (; j < j1; ++j) s = fma(U[(int64_t)j * p + i], cs[j], s);
+    s += s2;
   }
-  part[grp * 64 + rl] = s;
+  part[grp * kRows + rl] = s;
   __syncthreads();
   double rz = 0.0;
   if (grp == 0 && i < p) {
-    const double z = v[i] + (((part[rl] + part[64 + rl]) + part[128 + rl]) + part[192 + rl]);
+    double t = 0.0;
+#pragma unroll
+    for (int g2 = 0; g2 < kGroups; ++g2) t += part[g2 * kRows + rl];
+    const double z = v[i] + t;
     out[i] = z;
     rz = v[i] * z;
   }
@@ -385,7 +402,7 @@ __global__ void __launch_bounds__(kThreads) uc_kernel(const PrecondArgs* pa, int
   });
 }
 
-int precond_blocks(int64_t p) { return (int)std::max<int64_t>(1, (p + 63) / 64); }
+int precond_blocks(int64_t p) { return (int)std::max<int64_t>(1, (p + 31) / 32); }
 
 cudaError_t precond_apply(const PrecondArgs* pa, int64_t p, int ell, const double* v, double* out, double* part,
                           double* cprime, unsigned* counters, const int* done, PcgState* pcg, int first,
@@ -398,7 +415,7 @@ cudaError_t precond_apply(const PrecondArgs* pa, int64_t p, int ell, const doubl
   }
   const int grid = precond_blocks(p);
   probe_before(K_PRECOND, st);
-  uc_kernel<<<grid, kThreads, sizeof(double) * (std::max(ell, 1) + 256), st>>>(pa, p, ell, cprime, v, out, done, pcg,
+  uc_kernel<<<grid, kThreads, sizeof(double) * (std::max(ell, 1) + kThreads), st>>>(pa, p, ell, cprime, v, out, done, pcg,
                                                                               first, partials, counters + 1);
   probe_after(K_PRECOND, st);
   return cudaGetLastError();
@@ -434,22 +451,44 @@ __global__ void pcg_first_dir_kernel(const double* z, double* d, int64_t p, PcgS
     d[i] = z[i];
 }
 
-// ad = sum_g part[g] + mu d ; dad = d.ad ; breakdown test and alpha (krylov.py:59-66)
+// ad = sum_g part[g] + mu d ; dad = d.ad ; breakdown test and alpha (krylov.py:59-66).  Four lanes per
+// element split the split-K partial sum (lane q takes g = q, q+4, ...; combined in fixed order), so
+// the dependent L2 loads of the G partials are spread over 4x more threads.
+constexpr int kAdPerBlock = kThreads / 4;
 __global__ void pcg_ad_kernel(const double* part, RedPlan rp, int64_t p, const double* mu_p, const double* d,
                               double* ad, PcgState* s, int ad_ready, double* partials, unsigned* counter) {
   if (s->done) return;
   const double mu = *mu_p;
+  const int q = threadIdx.x & 3;
   double v = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
-    double a;
+  for (int64_t i0 = (int64_t)blockIdx.x * kAdPerBlock; i0 < p; i0 += (int64_t)gridDim.x * kAdPerBlock) {
+    const int64_t i = i0 + (threadIdx.x >> 2);
     if (ad_ready) {
-      a = ad[i];
-    } else {
-      a = sum_partials(part, plan_G(rp, i), p, i);
-      a = fma(mu, d[i], a);
-      ad[i] = a;
+      if (q == 0 && i < p) v = fma(d[i], ad[i], v);
+      continue;
     }
-    v = fma(d[i], a, v);
+    double a = 0.0;
+    if (i < p) {
+      const int G = plan_G(rp, i);
+      int g = q;
+      for (; g + 12 < G; g += 16) {
+        const double x0 = __ldcg(&part[(int64_t)g * p + i]), x1 = __ldcg(&part[(int64_t)(g + 4) * p + i]);
+        const double x2 = __ldcg(&part[(int64_t)(g + 8) * p + i]), x3 = __ldcg(&part[(int64_t)(g + 12) * p + i]);
+        a += x0;
+        a += x1;
+        a += x2;
+        a += x3;
+      }
+      for (; g < G; g += 4) a += __ldcg(&part[(int64_t)g * p + i]);
+    }
+    const double a1 = __shfl_xor_sync(0xffffffffu, a, 1);
+    const double a2 = __shfl_xor_sync(0xffffffffu, a, 2);
+    const double a3 = __shfl_xor_sync(0xffffffffu, a, 3);
+    if (q == 0 && i < p) {  // (s0 + s1) + (s2 + s3), fixed order
+      const double tot = fma(mu, d[i], (a + a1) + (a2 + a3));
+      ad[i] = tot;
+      v = fma(d[i], tot, v);
+    }
   }
   finish_sum(v, partials, counter, s, [](double sum, PcgState* st) {
     st->dad = sum;
@@ -544,7 +583,8 @@ void pcg_first_dir(const double* z, double* d, int64_t p, PcgState* s, cudaStrea
 void pcg_ad(const double* part, const RedPlan& rp, int64_t p, const double* mu_p, const double* d, double* ad,
             PcgState* s, int ad_ready, double* partials, unsigned* counter, cudaStream_t st) {
   probe_before(K_VEC, st);
-  pcg_ad_kernel<<<rgrid(p), kThreads, 0, st>>>(part, rp, p, mu_p, d, ad, s, ad_ready, partials, counter);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((p + kAdPerBlock - 1) / kAdPerBlock, 1184));
+  pcg_ad_kernel<<<grid, kThreads, 0, st>>>(part, rp, p, mu_p, d, ad, s, ad_ready, partials, counter);
   probe_after(K_VEC, st);
 }
 void pcg_update(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s, int recompute,
