@@ -8,6 +8,7 @@ library's sm_100a kernels, cuBLAS/cuSOLVER calls and NCCL collectives.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -15,6 +16,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libngd_b200.so")
+LIB_PATH = os.environ.get("NGD_LIB_PATH", LIB_PATH)  # tuning experiments: an alternative build of the library
 
 NGD_OK, NGD_E_SHAPE, NGD_E_NONFINITE, NGD_E_CHOL, NGD_E_CUDA, NGD_E_NCCL, NGD_E_STATE = range(7)
 
@@ -88,6 +90,25 @@ _RESTYPE = {"ngd_last_error": ctypes.c_char_p, "ngd_param_count": _I64, "ngd_lau
 _lib = None
 _contexts = []  # weak registry so option changes reach live contexts
 OPTIONS = {"svd": 3}
+
+
+# library defaults of the ngd_set_option knobs (include/ngd.h), for restoring a temporary change
+DEFAULTS = {"svd": 3, "graphs": 1, "chol": 1, "trsm": 1, "syrk": 0, "l2window": 0, "fused": 0, "force_comm": 0,
+            "phb_cs": 0, "phb_g": 0, "phb_plan": 2}
+
+
+@contextlib.contextmanager
+def option(key, value):
+    """Temporarily set a library knob (restores the previous or default value on exit)."""
+    prev = OPTIONS.get(key, DEFAULTS.get(key))
+    set_option(key, value)
+    try:
+        yield
+    finally:
+        if prev is None:
+            OPTIONS.pop(key, None)
+        else:
+            set_option(key, prev)
 
 
 def set_option(key, value):

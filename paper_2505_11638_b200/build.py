@@ -50,15 +50,20 @@ def _stale():
     return any(os.path.getmtime(f) > t for f in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile every csrc/*.cu for sm_100a and link LIB (or `out`, with extra -D defines: tuning
+    variants for experiments, loaded through NGD_LIB_PATH)."""
+    lib_path = out or LIB
+    if not force and out is None and not defines and not _stale():
         return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    build_dir = BUILD if out is None else out + ".objs"
+    os.makedirs(build_dir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src,
+               "-o", obj]
         if verbose:
             print(" ".join(cmd))
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), src))
@@ -70,7 +75,7 @@ def build(force=False, verbose=False):
         if verbose and out.strip():
             print(out)
     nccl = _nccl_libdir()
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64", "-lcublas", "-lcusolver",
            f"-L{nccl}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nccl}:/usr/local/cuda/lib64"]
     if verbose:
@@ -78,9 +83,13 @@ def build(force=False, verbose=False):
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout.decode())
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--variant" in sys.argv:  # python -m paper_2505_11638_b200.build --variant OUT.so DEF=1 ...
+        k = sys.argv.index("--variant")
+        print(build(force=True, out=os.path.abspath(sys.argv[k + 1]), defines=sys.argv[k + 2:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

@@ -145,6 +145,11 @@ struct ngd_ctx {
   Buf jets;  // arena behind zin / dbuf / dseed
   int force_comm = 0;  // "force_comm": build a communicator (and take the multi-rank paths) even for 1 rank
   int phb_cs = 0;  // option "phb_cs": 0 auto (DSMEM cluster reduction when G >= 16), 1 never
+  int phb_g = 0;   // option "phb_g": force the phase-B split count (tuning; 0 = plan)
+  int phb_plan = 2;  // option "phb_plan": 0 uniform splits (3 CTAs/SM), 1 work-weighted (6 stages),
+                     // 2 pipelined producer/consumer kernel (ngd_phb2.cu)
+  int phb_deep = 0;  // kernel chosen by the plan: 0/1 phb_all_kernel depth, 2 phb2_kernel
+  int phb_thin[kMaxLayers] = {};  // phb2: thin layers (N <= 16 or M <= 16)
   int use_fused = 0;  // opt-in: measured slower than the two-phase path at C1/C2
   bool fused_ok = false;
   int fgrid = 0;
@@ -378,6 +383,7 @@ static void fill_phb(ngd_ctx* c, const double* cot, const int* skip, PhbAll& pb)
   }
   pb.tile_start[c->NL] = tiles;
   pb.cluster = c->phb_cluster;
+  for (int l = 0; l < c->NL; ++l) pb.thin[l] = c->phb_thin[l];
 }
 
 // out = J^T cot (+ mu v), all-reduced over ranks
@@ -385,7 +391,7 @@ static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* m
                        const int* skip) {
   PhbAll pb{};
   fill_phb(c, cot, skip, pb);
-  CK(phase_b_all_layers(pb, c->G, c->stream));
+  CK(c->phb_deep == 2 ? phase_b2_all_layers(pb, c->stream) : phase_b_all_layers(pb, c->phb_deep, c->stream));
   const bool shifted = v && (mu_p || mu != 0.0);
   if (c->comm) {
     reduce_splits(c->partB.d(), c->rplan, c->p, 0.0, nullptr, nullptr, out, skip, c->stream);
@@ -876,15 +882,22 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
     // DSMEM cluster reduction of the split partials pays only when there are many of them (C2:
     // G = 104 -> 13 partials; measured PCG 3.9 -> 2.9 ms); at G ~ 32 (C3) the cluster
     // co-scheduling costs more than reading 37 partials (PCG 104.8 -> 98.6 ms without clusters)
+    if (c->phb_g > 0) G = c->phb_g;
     int CS = 1;
     if (G >= 64 && c->phb_cs != 1) {
-      G = G / 8 * 8;
+      // whole clusters of 8 in one wave: clusters are placed per GPC, so fewer than slots / 8 fit
+      // (C2: 48 co-resident clusters; G = 104 gave 52 clusters and a 4-cluster tail wave)
+      static int max_clusters = -1;
+      if (max_clusters < 0) max_clusters = phb_max_active_clusters(8);
+      const int gc = max_clusters > 0 ? std::max(8, max_clusters / tiles * 8) : G / 8 * 8;
+      G = std::min(G / 8 * 8, gc);
       CS = 8;
     }
     const int kps = (kt + G - 1) / G;
     c->G = G;
     c->kps = kps;
     c->phb_cluster = CS;
+    c->phb_deep = 0;
     c->rplan.n_layers = c->NL;
     for (int l = 0; l < c->NL; ++l) {
       c->Gl[l] = G;
@@ -893,6 +906,72 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
       c->rplan.G[l] = G / CS;  // one partial per cluster
     }
     c->rplan.start[c->NL] = c->p;
+    if (c->phb_plan == 1 && c->phb_g == 0) {
+      // Work-weighted plan: one wave of CTAs with a 6-stage pipeline, per-layer split counts in
+      // proportion to each tile's DMMA work (a 64 x 64 tile whose rows or columns are mostly
+      // padding -- the input layer's N = d, the output layer's M = 1 -- runs only its active
+      // 16 x 32 warp tiles), so every CTA streams the same amount of tensor-core work.
+      const int slots = phb_ctas_per_sm(1) * 148;
+      double cost[kMaxLayers], total = 0.0;
+      int nt[kMaxLayers];
+      for (int l = 0; l < c->NL; ++l) {
+        const int M = c->w[l + 1], N = c->w[l];
+        const int tm = (M + 63) / 64, tn = (N + 63) / 64;
+        nt[l] = tm * tn;
+        double cl = 0.0;
+        for (int bm = 0; bm < tm; ++bm)
+          for (int bn = 0; bn < tn; ++bn) {
+            int act = 0;
+            for (int wm = 0; wm < 4; ++wm)
+              for (int wn = 0; wn < 2; ++wn) act += (bm * 64 + wm * 16 < M && bn * 64 + wn * 32 < N) ? 1 : 0;
+            cl += act / 8.0;
+          }
+        cost[l] = cl;
+        total += cl;
+      }
+      int Gl[kMaxLayers], used = 0;
+      for (int l = 0; l < c->NL; ++l) {
+        Gl[l] = std::max(1, std::min(kt, (int)(slots * cost[l] / total / nt[l])));
+        used += Gl[l] * nt[l];
+      }
+      int maxg = 0;
+      for (int l = 0; l < c->NL; ++l) {
+        c->Gl[l] = Gl[l];
+        c->kpsl[l] = (kt + Gl[l] - 1) / Gl[l];
+        c->rplan.G[l] = Gl[l];
+        maxg = std::max(maxg, Gl[l]);
+      }
+      (void)used;
+      c->G = maxg;
+      c->kps = c->kpsl[0];
+      c->phb_cluster = 1;
+      c->phb_deep = 1;
+    }
+    if (c->phb_plan == 2 && c->phb_g == 0) {
+      // Pipelined kernel (ngd_phb2.cu), one CTA per SM: heavy tiles (both sides > 16) share 148
+      // K-split items, thin tiles (input layer N = d, output layer M = 1) another 148; CTA i
+      // streams heavy item i and thin item i interleaved.
+      int heavy = 0, thin = 0;
+      for (int l = 0; l < c->NL; ++l) {
+        const int M = c->w[l + 1], N = c->w[l];
+        c->phb_thin[l] = (M <= 16 || N <= 16) ? 1 : 0;
+        (c->phb_thin[l] ? thin : heavy) += ((M + 63) / 64) * ((N + 63) / 64);
+      }
+      const int gh = heavy ? std::max(1, std::min(kt, 148 / heavy)) : 1;
+      const int gt = thin ? std::max(1, std::min(kt, 148 / thin)) : 1;
+      int maxg = 0;
+      for (int l = 0; l < c->NL; ++l) {
+        const int Gl = c->phb_thin[l] ? gt : gh;
+        c->Gl[l] = Gl;
+        c->kpsl[l] = (kt + Gl - 1) / Gl;
+        c->rplan.G[l] = Gl;
+        maxg = std::max(maxg, Gl);
+      }
+      c->G = maxg;
+      c->kps = c->kpsl[0];
+      c->phb_cluster = 1;
+      c->phb_deep = 2;
+    }
   }
   CK(c->partB.ensure(sizeof(double) * (size_t)(c->G / c->phb_cluster) * c->p));
   // fused narrow-network matvec: persistent CTAs over point blocks, one partial each
@@ -1327,7 +1406,7 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
       TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done));
       PhbAll pb{};
       fill_phb(c, c->cot.d(), done, pb);
-      CK(phase_b_all_layers(pb, c->G, c->stream));
+      CK(c->phb_deep == 2 ? phase_b2_all_layers(pb, c->stream) : phase_b_all_layers(pb, c->phb_deep, c->stream));
     }
     if (c->comm) {
       reduce_splits(part, *rp, p, 0.0, nullptr, nullptr, ad, done, c->stream);
@@ -1580,6 +1659,15 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_comm")) {
     c->force_comm = value ? 1 : 0;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "phb_plan")) {
+    if (value < 0 || value > 2) return fail(NGD_E_SHAPE, "phb_plan must be 0, 1 or 2");
+    c->phb_plan = (int)value;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "phb_g")) {
+    c->phb_g = (int)std::max<int64_t>(0, value);
     return NGD_OK;
   }
   if (!strcmp(key, "phb_cs")) {

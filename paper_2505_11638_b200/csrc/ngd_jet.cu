@@ -407,10 +407,16 @@ __device__ __forceinline__ bool is_value_col(int64_t j64, int64_t int_cols, int 
   return j64 >= int_cols || (((int)j64 % (PB * C)) < PB);
 }
 
-constexpr int PNST = PUN == 1 ? 3 : 2;  // cp.async pipeline depth of phase B (3 CTAs / SM either way)
-static_assert(PBM * (PBN + 1) + PBM <= 2 * PNST * PBM * PSTR, "cluster reduction staging must fit");
-constexpr size_t kPhbSmem = sizeof(double) * (2 * PNST * PBM * PSTR + 2 * PNST * PKS + PBM);
+// cp.async pipeline depth of phase B: 3 stages at 3 CTAs / SM (uniform split plan), or 6 stages at
+// one CTA / SM (work-weighted plan, phb_plan = 1)
+constexpr int PNST_DEFAULT = PUN == 1 ? 3 : 2;
+constexpr int PNST_DEEP = 6;
+static_assert(PBM * (PBN + 1) + PBM <= 2 * 2 * PBM * PSTR, "cluster reduction staging must fit");
+template <int NST>
+constexpr size_t phb_smem() { return sizeof(double) * (2 * NST * PBM * PSTR + 2 * NST * PKS + PBM); }
+constexpr size_t kPhbSmem = phb_smem<PNST_DEFAULT>();
 
+template <int PNST>
 __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const int by, const int kt0, const int kt1,
                                          const int split) {
   extern __shared__ __align__(16) double smem[];
@@ -489,13 +495,18 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
     __syncthreads();
     {
       const int nk = it + PNST - 1;
+#ifndef NGD_PHB_NOLOAD
       if (nk < nst) load_stage(nk % PNST, kt0 + nk * PUN, kt1);
+#endif
       cp_async_commit();
     }
     const double* as = As + st * PBM * PSTR;
     const double* bs = Bs + st * PBN * PSTR;
     const double* cs = ccs + st * PKS;
     const double* vf = ccv + st * PKS;
+#ifdef NGD_PHB_NOCOMPUTE
+    if (w_active && as[0] == 12345.0) acc[0][0][0] += 1.0;
+#else
 #pragma unroll
     for (int kk = 0; kk < PKS; kk += 4) {
       if (!w_active) break;
@@ -514,6 +525,7 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
         bsum1 = fma(f, a1, bsum1);
       }
     }
+#endif
   }
   // combine the 4 column phases t of each bias row (fixed order)
   bsum0 += __shfl_xor_sync(0xffffffffu, bsum0, 1);
@@ -566,6 +578,7 @@ __device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const i
 
 // Phase B over ALL layers in one launch: blockIdx.x enumerates (layer, split, m-tile, n-tile)
 // with a per-layer split count proportional to the layer's work.
+template <int NST>
 __global__ void __launch_bounds__(kThreads) phb_all_kernel(PhbAll a) {
   const int t = blockIdx.x;
   int l = 0;
@@ -574,14 +587,45 @@ __global__ void __launch_bounds__(kThreads) phb_all_kernel(PhbAll a) {
   const int G = a.G[l];
   const int split = local % G, tile = local / G;  // consecutive CTAs = consecutive splits of one tile
   const PhbArgs& p = a.L[l];
+#ifdef NGD_PHB_SKIPTHIN
+  if (p.M < 16 || p.N < 16) return;
+#endif
   const int kt0 = split * p.ktiles_per_split;
-  phb_tile(p, tile % a.tiles_n[l], tile / a.tiles_n[l], kt0, min(p.ktiles_total, kt0 + p.ktiles_per_split), split);
+  phb_tile<NST>(p, tile % a.tiles_n[l], tile / a.tiles_n[l], kt0, min(p.ktiles_total, kt0 + p.ktiles_per_split),
+                split);
 }
 
-cudaError_t phase_b_all_layers(const PhbAll& a, int splits, cudaStream_t st) {
+// clusters of `cs` phase-B CTAs that can be co-resident on the device (one wave)
+int phb_max_active_clusters(int cs) {
+  cudaFuncSetAttribute(phb_all_kernel<PNST_DEFAULT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPhbSmem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = kPhbSmem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, phb_all_kernel<PNST_DEFAULT>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// CTAs per SM of the phase-B kernel at pipeline depth `deep` (0: 3 stages, 1: 6 stages)
+int phb_ctas_per_sm(int deep) { return deep ? (int)(227 * 1024 / phb_smem<PNST_DEEP>()) : 3; }
+
+cudaError_t phase_b_all_layers(const PhbAll& a, int deep, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(phb_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPhbSmem);
+    cudaFuncSetAttribute(phb_all_kernel<PNST_DEFAULT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPhbSmem);
+    cudaFuncSetAttribute(phb_all_kernel<PNST_DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)phb_smem<PNST_DEEP>());
     attr_set = true;
   }
   const int tiles = a.tile_start[a.n_layers];
@@ -589,7 +633,7 @@ cudaError_t phase_b_all_layers(const PhbAll& a, int splits, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = kPhbSmem;
+  cfg.dynamicSmemBytes = deep ? phb_smem<PNST_DEEP>() : kPhbSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -599,9 +643,9 @@ cudaError_t phase_b_all_layers(const PhbAll& a, int splits, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   probe_before(K_PHB, st);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, phb_all_kernel, a);
+  cudaError_t e = deep ? cudaLaunchKernelEx(&cfg, phb_all_kernel<PNST_DEEP>, a)
+                       : cudaLaunchKernelEx(&cfg, phb_all_kernel<PNST_DEFAULT>, a);
   probe_after(K_PHB, st);
-  (void)splits;
   return e;
 }
 

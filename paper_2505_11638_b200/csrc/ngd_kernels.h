@@ -110,6 +110,7 @@ struct PhbAll {
   int tiles_n[kMaxLayers], tiles_m[kMaxLayers], G[kMaxLayers];
   int n_layers;
   int cluster;  // split-K CTAs reduced per cluster through DSMEM (divides G)
+  int thin[kMaxLayers];  // phb2: layer whose tiles are thin (N <= 16 or M <= 16): paired with heavy work
 };
 // fixed-order reduction plan of the phase-B partials: param range of layer l uses G[l] splits
 struct RedPlan {
@@ -150,7 +151,12 @@ cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles,
 cudaError_t jet_gemm_both(int C, int mode, const JetArgs& a, int nib, int nbb, int64_t int_cols, int mtiles,
                           cudaStream_t st);
 cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st);
-cudaError_t phase_b_all_layers(const PhbAll& a, int splits, cudaStream_t st);
+int phb_max_active_clusters(int cs);
+cudaError_t phase_b_all_layers(const PhbAll& a, int deep, cudaStream_t st);
+int phb_ctas_per_sm(int deep);
+// pipelined phase B (ngd_phb2.cu): producer warp + bulk copies, 32x32 warp tiles, thin-block skip
+cudaError_t phase_b2_all_layers(const PhbAll& a, cudaStream_t st);
+int phb2_ctas_per_sm();
 void pack_all(const PackAll& a, const double* src, const int* skip, cudaStream_t st);
 cudaError_t form_j(const FormJArgs& a, int nblocks, int n_layers, int max_nin, int max_nout, cudaStream_t st);
 

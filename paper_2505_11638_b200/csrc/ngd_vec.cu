@@ -231,16 +231,38 @@ __global__ void reduce_splits_kernel(const double* part, RedPlan rp, int64_t p, 
                                      const double* v, double* out, const int* done) {
   if (done && *done) return;
   if (mu_p) mu = *mu_p;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
-    double s = sum_partials(part, plan_G(rp, i), p, i);
-    if (v) s = fma(mu, v[i], s);
-    out[i] = s;
+  // four lanes per element (lane q sums g = q, q+4, ...; fixed-order combine), as pcg_ad_kernel
+  const int q = threadIdx.x & 3;
+  for (int64_t i0 = (int64_t)blockIdx.x * (blockDim.x / 4); i0 < p; i0 += (int64_t)gridDim.x * (blockDim.x / 4)) {
+    const int64_t i = i0 + (threadIdx.x >> 2);
+    double a = 0.0;
+    if (i < p) {
+      const int G = plan_G(rp, i);
+      int g = q;
+      for (; g + 12 < G; g += 16) {
+        const double x0 = __ldcg(&part[(int64_t)g * p + i]), x1 = __ldcg(&part[(int64_t)(g + 4) * p + i]);
+        const double x2 = __ldcg(&part[(int64_t)(g + 8) * p + i]), x3 = __ldcg(&part[(int64_t)(g + 12) * p + i]);
+        a += x0;
+        a += x1;
+        a += x2;
+        a += x3;
+      }
+      for (; g < G; g += 4) a += __ldcg(&part[(int64_t)g * p + i]);
+    }
+    const double a1 = __shfl_xor_sync(0xffffffffu, a, 1);
+    const double a2 = __shfl_xor_sync(0xffffffffu, a, 2);
+    const double a3 = __shfl_xor_sync(0xffffffffu, a, 3);
+    if (q == 0 && i < p) {
+      double s = (a + a1) + (a2 + a3);
+      if (v) s = fma(mu, v[i], s);
+      out[i] = s;
+    }
   }
 }
 
 void reduce_splits(const double* part, const RedPlan& rp, int64_t p, double mu, const double* mu_p, const double* v,
                    double* out, const int* done, cudaStream_t st) {
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((p + 255) / 256, 148 * 8));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((p + 63) / 64, 148 * 8));
   probe_before(K_VEC, st);
   reduce_splits_kernel<<<grid, 256, 0, st>>>(part, rp, p, mu, mu_p, v, out, done);
   probe_after(K_VEC, st);

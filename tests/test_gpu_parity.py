@@ -37,12 +37,16 @@ def test_c1_loss_metric_grad_matvec(c1):
     assert gop.matvec_count == 9
 
 
-@pytest.mark.parametrize("svd", [2, 1, 0])
+@pytest.mark.parametrize("svd", [3, 2, 1, 0])
 def test_c1_nystrom_preconditioner_pcg(c1, svd):
     G, prob, quad, theta = c1
     from paper_2505_11638_b200 import _lib
 
-    _lib.set_option("svd", svd)
+    with _lib.option("svd", svd):
+        _check_c1_pcg(G, prob, quad, theta)
+
+
+def _check_c1_pcg(G, prob, quad, theta):
     gop = ngd.GramianOperator.from_problem(prob, theta, quad)
     fac = ngd.nystrom_approximate(gop, 100, seed=7, omega_source="host")
     assert gop.matvec_count == 100
@@ -56,7 +60,6 @@ def test_c1_nystrom_preconditioner_pcg(c1, svd):
         meta = G[f"pcg{k}_meta"]
         assert rel(rep.solution, G[f"pcg{k}_x"]) <= 1e-8, k
         assert (rep.iterations, rep.matvecs, rep.breakdown) == (int(meta[0]), int(meta[1]), bool(meta[4]))
-    _lib.set_option("svd", 2)
 
 
 def test_c1_device_omega_sketch_statistics(c1):

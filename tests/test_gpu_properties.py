@@ -230,6 +230,7 @@ def test_fused_matvec_matches_factored(name, widths, nint, nbnd):
 
     top = ngd.MlpTopology(widths)
     res = {}
+    prev = _lib.OPTIONS.get("fused", _lib.DEFAULTS["fused"])
     try:
         for fused in (1, 0):
             _lib.set_option("fused", fused)  # applies to contexts created below
@@ -246,7 +247,7 @@ def test_fused_matvec_matches_factored(name, widths, nint, nbnd):
             rep = ngd.pcg(ngd.ShiftedOperator(gop, 1e-3), g, 1e-300, 3)  # few its: CG amplifies 1e-16 differences
             res[fused] = (gop.matvec(v), rep.solution, rep.iterations)
     finally:
-        _lib.set_option("fused", 1)
+        _lib.set_option("fused", prev)
     np.testing.assert_allclose(res[1][0], res[0][0], rtol=1e-12, atol=1e-12 * np.abs(res[0][0]).max())
     assert res[1][2] == res[0][2]
     np.testing.assert_allclose(res[1][1], res[0][1], rtol=1e-9, atol=1e-9 * np.abs(res[0][1]).max())

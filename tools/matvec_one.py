@@ -9,9 +9,10 @@ import paper_2505_11638_b200 as ngd
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-if len(sys.argv) > 3:
-    from paper_2505_11638_b200 import _lib
-    _lib.set_option("l2window", int(sys.argv[3]))
+from paper_2505_11638_b200 import _lib
+for kv in sys.argv[3:]:  # key=value library options, e.g. phb_cs=1
+    k, v = kv.split("=") if "=" in kv else ("l2window", kv)
+    _lib.set_option(k, int(v))
 side = torch.cuda.Stream()
 torch.cuda.set_stream(side)  # a non-default stream can carry the L2 access-policy window
 prob, quad, theta0, _ = bench.make_problem(ngd, cfg, 1, 0)
