@@ -150,6 +150,8 @@ struct ngd_ctx {
                      // 2 pipelined producer/consumer kernel (ngd_phb2.cu)
   int phb_deep = 0;  // kernel chosen by the plan: 0/1 phb_all_kernel depth, 2 phb2_kernel
   int phb_thin[kMaxLayers] = {};  // phb2: thin layers (N <= 16 or M <= 16)
+  int pha_plan = 0;  // option "pha_plan": 0 one CTA per unit (ngd_jet.cu, default), 1 persistent TMA
+                     // pipeline (ngd_pha2.cu: measured slower, see its header)
   int use_fused = 0;  // opt-in: measured slower than the two-phase path at C1/C2
   bool fused_ok = false;
   int fgrid = 0;
@@ -348,7 +350,33 @@ static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double*
     tiles += c->mtiles[l] * (gm.nib + gm.nbb);
   }
   pa.tile_start[c->NL] = tiles;
-  CK(pha_all(gm.C, pa, c->stream));
+  if (c->pha_plan == 1 && pha2_supported(gm.C)) {
+    static Pha2Args a2;  // large (tensor maps): not on the stack
+    a2.n_layers = c->NL;
+    a2.nib = gm.nib;
+    a2.nbb = gm.nbb;
+    a2.n_pts_pad = gm.n_pts_pad();
+    a2.int_cols = gm.int_cols();
+    a2.s_pad = gm.s_pad;
+    a2.skip = skip;
+    const double* vps[kMaxLayers];
+    const double* zs[kMaxLayers];
+    int kps[kMaxLayers], mps[kMaxLayers];
+    for (int l = 0; l < c->NL; ++l) {
+      a2.D[l] = pa.L[l].Dk;
+      a2.vb[l] = pa.L[l].bias;
+      a2.partA[l] = pa.L[l].partA;
+      a2.M[l] = c->w[l + 1];
+      a2.mtiles[l] = c->mtiles[l];
+      vps[l] = c->vp[l].d();
+      zs[l] = c->zin[l].d();
+      kps[l] = c->Kp_f[l];
+      mps[l] = c->Mp_f[l];
+    }
+    CK(pha2_all_layers(a2, vps, zs, kps, mps, gm.C, c->stream));
+  } else {
+    CK(pha_all(gm.C, pa, c->stream));
+  }
   reduce_pha(c->partA.d(), c->rows_A, gm.n_pts_pad(), w_or_null, cot_out, skip, c->stream);
   CK(cudaGetLastError());
   return NGD_OK;
@@ -1659,6 +1687,10 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_comm")) {
     c->force_comm = value ? 1 : 0;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "pha_plan")) {
+    c->pha_plan = value ? 1 : 0;
     return NGD_OK;
   }
   if (!strcmp(key, "phb_plan")) {

@@ -1,6 +1,7 @@
 // Internal launch interface of the CUDA kernels (not part of the C-ABI).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "ngd_common.cuh"
@@ -104,6 +105,23 @@ struct PhaAll {
   int n_layers, nib, nbb;
   int64_t int_cols;
 };
+// pipelined phase A (ngd_pha2.cu): persistent CTAs over cost-balanced (layer, m-tile, point block) units
+struct Pha2Args {
+  CUtensorMap vmap[kMaxLayers];  // packed V_l [Mp][Kp], box 64 x 16
+  CUtensorMap zmap[kMaxLayers];  // Zin_l [Kp][s_pad], box 16 x 16
+  const double* D[kMaxLayers];   // adjoints of layer l [>= M rows][s_pad]
+  const double* vb[kMaxLayers];  // value-channel bias rows of V_l
+  double* partA[kMaxLayers];     // [mtiles][n_pts_pad] partials of layer l
+  int M[kMaxLayers], mtiles[kMaxLayers], kchunk[kMaxLayers], kchunks[kMaxLayers];
+  int n_layers, nib, nbb, n_pts_pad, n_ctas;
+  int64_t int_cols, s_pad;
+  const int* skip;
+  int cta_start[149];  // unit range of CTA i: [cta_start[i], cta_start[i + 1])
+};
+bool pha2_supported(int C);
+cudaError_t pha2_all_layers(Pha2Args& a, const double* const* vp, const double* const* zin, const int* kp,
+                            const int* mp, int C, cudaStream_t st);
+
 struct PhbAll {
   PhbArgs L[kMaxLayers];          // per layer (ktiles_per_split set per layer)
   int tile_start[kMaxLayers + 1];  // flat CTA offsets: layer l owns tiles_m*tiles_n*G_l CTAs

@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) utv_kernel(const PrecondArgs* pa, in
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = fma(uu[q], vv[q], acc[q]);
   }
-  for (int q = 0; i < p; i += kThreads, ++q) acc[q & 7] = fma(u[i], v[i], acc[q & 7]);
+  for (; i < p; i += kThreads) acc[0] = fma(u[i], v[i], acc[0]);  // (a runtime acc index would go to local memory)
   const double tot =
       block_sum(((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7])), sh);
   if (threadIdx.x == 0) {
