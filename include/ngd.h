@@ -145,12 +145,14 @@ int ngd_pcg(ngd_ctx* ctx, const double* d_dense, int64_t p, const double* d_b, d
 int ngd_small_cholesky(ngd_ctx* ctx, double* d_A, int32_t n, int32_t method, int32_t* h_info);
 
 /* ---- tuning knobs: "svd" = 0 (Householder QR + cuSOLVER gesvdj) | 1 (shifted Cholesky-QR3 + cuSOLVER polar SVD)
- *      | 2 (shifted Cholesky-QR3 + in-house cluster one-sided Jacobi SVD; default, falls back to 1 above ell = 512)
- *      | 3 (as 2 with FP32 Jacobi pre-sweeps, FP64 finish);
+ *      | 2 (shifted Cholesky-QR3 + in-house cluster one-sided Jacobi SVD; falls back to 1 above ell = 310)
+ *      | 3 (as 2 with FP32 Jacobi pre-sweeps and an FP64 finish; default);
  *      "graphs" = 1 (replay PCG iterations as a CUDA graph, default) | 0;
  *      "chol" = 1 (in-house: one-CTA Cholesky for ell <= 32, 8-CTA cluster Cholesky up to 512; default)
  *               | 2 (cluster Cholesky for every ell <= 512) | 0 (cuSOLVER potrf);
- *      "trsm" = 1 (in-house DMMA right triangular solve for ell <= 512, default) | 0 (cuBLAS DTRSM) */
+ *      "trsm" = 1 (in-house DMMA right triangular solve for ell <= 512, default) | 0 (cuBLAS DTRSM);
+ *      "phb_plan" = 2 (phase B: TMA-fed warp-specialised kernel, default) | 1 | 0 (first form, 3 stages);
+ *      "pha_plan" = 0 (phase A: one CTA per unit, default) | 1 (persistent TMA pipeline, slower at C2) */
 int ngd_set_option(ngd_ctx* ctx, const char* key, int64_t value);
 /* diagnostics: "jacobi_sweeps" (FP64 sweeps of the last Nystrom factorisation), "jacobi_sweeps_f32"
  * (its FP32 pre-sweeps, svd = 3), "phase_b_splits" */
