@@ -306,8 +306,8 @@ static int loss_finish(ngd_ctx* c, double* h_loss, double* F, double* cot, doubl
 }
 
 // ------------------------------ phase A / B ---------------------------------
-static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double* cot_out, const int* skip) {
-  const Geom& gm = c->gm;
+// forward packing plan of a parameter-layout vector into the phase-A layer matrices (vp)
+static PackAll vp_plan(ngd_ctx* c) {
   PackAll pk{};
   pk.n_layers = c->NL;
   int64_t off = 0;
@@ -323,7 +323,14 @@ static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double*
     off += (int64_t)c->Mp_f[l] * c->Kp_f[l] + c->Mp_f[l];
   }
   pk.start[c->NL] = off;
-  pack_all(pk, v, skip, c->stream);
+  return pk;
+}
+
+// J v: pack v (unless prepacked: PCG's direction is packed by pcg_dir_pack), phase A, reduction
+static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double* cot_out, const int* skip,
+                   bool prepacked = false) {
+  const Geom& gm = c->gm;
+  if (!prepacked) pack_all(vp_plan(c), v, skip, c->stream);
   PhaAll pa{};
   pa.n_layers = c->NL;
   pa.nib = gm.nib;
@@ -1431,7 +1438,7 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
       part = c->partF.d();
       rp = &c->rplan_f;
     } else {
-      TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done));
+      TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done, /*prepacked=*/true));
       PhbAll pb{};
       fill_phb(c, c->cot.d(), done, pb);
       CK(c->phb_deep == 2 ? phase_b2_all_layers(pb, c->stream) : phase_b_all_layers(pb, c->phb_deep, c->stream));
@@ -1457,14 +1464,17 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
     pcg_true_res(b, tmp, r, p, sp, 1, 0, red, c->counter(6), c->stream);
   }
   // z = P^{-1} r ; beta = r.z / rz ; d = z + beta d   (krylov.py:75-81)
-  if (have_pre) {
+  // the direction update also packs d for the next iteration's phase A (matrix-free path)
+  const bool pack_next = !dense && !c->fused_ok;
+  if (have_pre)
     CK(precond_apply(static_cast<PrecondArgs*>(c->pargs.p), p, ell, r, z, c->ppart.d(), c->pcprime.d(),
                      c->counter(8), done, sp, 0, red, c->stream));
-    pcg_dir(z, dv, p, sp, &c->h_flags[5], c->stream);
-  } else {
+  else
     CK(precond_apply(nullptr, p, 0, r, z, nullptr, nullptr, c->counter(8), done, sp, 0, red, c->stream));
+  if (pack_next)
+    pcg_dir_pack(z, dv, vp_plan(c), sp, &c->h_flags[5], c->stream);
+  else
     pcg_dir(z, dv, p, sp, &c->h_flags[5], c->stream);
-  }
   CK(cudaGetLastError());
   return NGD_OK;
 }
@@ -1505,6 +1515,7 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
   CK(precond_apply(have_pre ? static_cast<PrecondArgs*>(c->pargs.p) : nullptr, p, have_pre ? ell : 0, r, z,
                    c->ppart.d(), c->pcprime.d(), c->counter(8), done, sp, 1, c->redp.d(), c->stream));
   pcg_first_dir(z, dv, p, sp, c->stream);
+  if (!dense && !c->fused_ok) pack_all(vp_plan(c), dv, &sp->done, c->stream);  // iterations use d prepacked
 
   // iterations: replay a captured CUDA graph of one iteration (Gram operator), or launch directly
   const bool use_graph = !dense && c->use_graphs;

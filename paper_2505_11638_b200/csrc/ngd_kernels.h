@@ -211,6 +211,7 @@ void pcg_update(double* x, double* r, const double* d, const double* ad, int64_t
                 double* partials, unsigned* counter, cudaStream_t st);
 void pcg_true_res(const double* b, const double* ax, double* r, int64_t p, PcgState* s, int count, int final_pass,
                   double* partials, unsigned* counter, cudaStream_t st);
+void pcg_dir_pack(const double* z, double* d, const PackAll& pk, PcgState* s, int* host_flag, cudaStream_t st);
 void pcg_dir(const double* z, double* d, int64_t p, PcgState* s, int* host_flag, cudaStream_t st);
 void theta_minus(const double* a, double alpha, const double* b, double* out, int64_t n, cudaStream_t st);
 void scale_rows(double* S, int64_t R, int ell, const double* w, cudaStream_t st);

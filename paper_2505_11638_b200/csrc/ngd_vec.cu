@@ -584,6 +584,35 @@ __global__ void pcg_dir_kernel(const double* z, double* d, int64_t p, PcgState* 
     d[i] = z[i] + beta * d[i];
 }
 
+// d = z + beta d fused with the packing of d into the forward layer matrices of the next matvec
+// (pack_all_kernel's index space: every parameter is read and written by exactly one thread)
+__global__ void pcg_dir_pack_kernel(const double* z, double* d, PackAll a, PcgState* s, int* host_flag) {
+  if (host_flag && blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<volatile int*>(host_flag) = s->done;
+  if (s->done) return;
+  const double beta = s->beta;
+  const int64_t n = a.start[a.n_layers];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    int l = 0;
+    while (l + 1 < a.n_layers && k >= a.start[l + 1]) ++l;
+    const int64_t kk = k - a.start[l];
+    const int64_t mat = (int64_t)a.Mp[l] * a.Kp[l];
+    int64_t i = -1;
+    if (kk < mat) {
+      const int m = (int)(kk / a.Kp[l]), c = (int)(kk % a.Kp[l]);
+      if (m < a.n_out[l] && c < a.n_in[l]) i = a.woff[l] + (int64_t)m * a.n_in[l] + c;
+    } else {
+      const int m = (int)(kk - mat);
+      if (m < a.n_out[l]) i = a.boff[l] + m;
+    }
+    double v = 0.0;
+    if (i >= 0) {
+      v = z[i] + beta * d[i];
+      d[i] = v;
+    }
+    a.dst[l][kk] = v;
+  }
+}
+
 static int vgrid(int64_t p) { return (int)std::max<int64_t>(1, std::min<int64_t>((p + 255) / 256, 148 * 8)); }
 static int rgrid(int64_t p) { return nblocks_for(p); }
 
@@ -619,6 +648,12 @@ void pcg_true_res(const double* b, const double* ax, double* r, int64_t p, PcgSt
                   double* partials, unsigned* counter, cudaStream_t st) {
   probe_before(K_VEC, st);
   pcg_true_res_kernel<<<rgrid(p), kThreads, 0, st>>>(b, ax, r, p, s, count, final_pass, partials, counter);
+  probe_after(K_VEC, st);
+}
+void pcg_dir_pack(const double* z, double* d, const PackAll& pk, PcgState* s, int* host_flag, cudaStream_t st) {
+  const int64_t n = pk.start[pk.n_layers];
+  probe_before(K_VEC, st);
+  pcg_dir_pack_kernel<<<vgrid(n), 256, 0, st>>>(z, d, pk, s, host_flag);
   probe_after(K_VEC, st);
 }
 void pcg_dir(const double* z, double* d, int64_t p, PcgState* s, int* host_flag, cudaStream_t st) {
