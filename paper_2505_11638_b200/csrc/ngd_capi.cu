@@ -150,6 +150,8 @@ struct ngd_ctx {
                      // 2 pipelined producer/consumer kernel (ngd_phb2.cu)
   int phb_deep = 0;  // kernel chosen by the plan: 0/1 phb_all_kernel depth, 2 phb2_kernel
   int phb_thin[kMaxLayers] = {};  // phb2: thin layers (N <= 16 or M <= 16)
+  int pcg_fuse = 0;  // option "pcg_fuse": PCG update fused with the preconditioner's first pass (measured
+                    // slower at C2: 93 vs 84 us per iteration, tools/pcg_periter.py)
   int pha_plan = 0;  // option "pha_plan": 0 one CTA per unit (ngd_jet.cu, default), 1 persistent TMA
                      // pipeline (ngd_pha2.cu: measured slower, see its header)
   int use_fused = 0;  // opt-in: measured slower than the two-phase path at C1/C2
@@ -1452,8 +1454,14 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
       pcg_ad(part, *rp, p, mu_p, dv, ad, sp, 0, red, c->counter(4), c->stream);
     }
   }
-  // x += alpha d ; r -= alpha ad (or r = b - A x) ; ||r|| test   (krylov.py:66-74)
-  pcg_update(x, r, dv, ad, p, sp, recompute, red, c->counter(5), c->stream);
+  // x += alpha d ; r -= alpha ad (or r = b - A x) ; ||r|| test   (krylov.py:66-74); with a
+  // preconditioner and no recompute, the same kernel also runs the preconditioner's U^T r pass
+  const bool fuse_pre = have_pre && !recompute && c->pcg_fuse;
+  if (fuse_pre)
+    CK(pcg_update_precond1(x, r, dv, ad, p, sp, static_cast<PrecondArgs*>(c->pargs.p), ell, c->ppart.d(),
+                           c->pcprime.d(), red, c->counter(5), c->stream));
+  else
+    pcg_update(x, r, dv, ad, p, sp, recompute, red, c->counter(5), c->stream);
   if (recompute) {
     if (dense) {
       CKB(cublasDgemv(c->blas, CUBLAS_OP_T, (int)p, (int)p, &one, dense, (int)p, x, 1, &zero, tmp, 1));
@@ -1466,7 +1474,10 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
   // z = P^{-1} r ; beta = r.z / rz ; d = z + beta d   (krylov.py:75-81)
   // the direction update also packs d for the next iteration's phase A (matrix-free path)
   const bool pack_next = !dense && !c->fused_ok;
-  if (have_pre)
+  if (fuse_pre)
+    CK(precond_apply2(static_cast<PrecondArgs*>(c->pargs.p), p, ell, c->pcprime.d(), r, z, done, sp, 0, red,
+                      c->counter(8) + 1, c->stream));
+  else if (have_pre)
     CK(precond_apply(static_cast<PrecondArgs*>(c->pargs.p), p, ell, r, z, c->ppart.d(), c->pcprime.d(),
                      c->counter(8), done, sp, 0, red, c->stream));
   else
@@ -1698,6 +1709,11 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_comm")) {
     c->force_comm = value ? 1 : 0;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "pcg_fuse")) {
+    c->pcg_fuse = value ? 1 : 0;
+    c->graph_gen++;  // captured PCG graphs bake the choice in
     return NGD_OK;
   }
   if (!strcmp(key, "pha_plan")) {

@@ -199,6 +199,13 @@ void add_scaled(double* out, double mu, const double* mu_p, const double* v, int
                 cudaStream_t st);
 int precond_blocks(int64_t p);
 // counters: two consecutive unsigned counters (utv combine, uc dot)
+int utv_chunks(int64_t p);
+cudaError_t pcg_update_precond1(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s,
+                                const PrecondArgs* pa, int ell, double* part, double* cprime, double* partials,
+                                unsigned* counter, cudaStream_t st);
+cudaError_t precond_apply2(const PrecondArgs* pa, int64_t p, int ell, const double* cprime, const double* v,
+                           double* out, const int* done, PcgState* pcg, int first, double* partials,
+                           unsigned* counter, cudaStream_t st);
 cudaError_t precond_apply(const PrecondArgs* pa, int64_t p, int ell, const double* v, double* out, double* part,
                           double* cprime, unsigned* counters, const int* done, PcgState* pcg, int first,
                           double* partials, cudaStream_t st);
