@@ -16,7 +16,9 @@
 // accumulates the rotations V, which are then R's left singular vectors:
 // R^T V = U_X S  =>  R = V S U_X^T.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "ngd_common.cuh"
 #include "ngd_kernels.h"
@@ -450,7 +452,16 @@ constexpr int kBlockSvdThreads = 512;
 // 18 / 19 their buffer phases.
 struct JsvdPlan {
   int period;             // exchanges before the placement sequence repeats
+  int p2p;                // 1: point-to-point exchange (below), 0: one cluster barrier per exchange
   unsigned w[4 * 31 * 16];
+  // Point-to-point exchange: a CTA may write its outgoing block into buffer b of CTA d as soon as
+  // every earlier copy OUT of that buffer has landed -- counted in d's gen[b], incremented by the
+  // receiver of each copy.  Word (t, c): bits 0-7 the count required at the first period, 8-15
+  // its increase per period, 16-19 the CTA that sends to c at t, 20-21 that sender's source buffer.
+  // Data of consecutive exchanges lands on alternating mbarriers (exchange t + 2 cannot reach a CTA
+  // before it consumed t).  Verified on random asynchronous schedules (no write into an in-flight
+  // source or a held block, no stall): tools/probe/jsvd_p2p_check.py.
+  unsigned w2[4 * 31 * 16];
 };
 
 static bool jsvd_make_plan(int CL, JsvdPlan& P) {
@@ -519,6 +530,46 @@ static bool jsvd_make_plan(int CL, JsvdPlan& P) {
     memcpy(blk, nblk, sizeof(blk));
     memcpy(ph, nph, sizeof(ph));
   }
+  // point-to-point permissions from three periods of the (periodic) schedule
+  {
+    const int T = 3 * period;
+    auto dec = [&](int t, int c, int& sb, int& dc, int& db) {
+      const unsigned w = P.w[(t % period) * CL + c];
+      sb = w & 3;
+      dc = (w >> 2) & 15;
+      db = (w >> 6) & 3;
+    };
+    std::vector<int> uses[16][4];  // source-use exchanges per (cta, buffer)
+    for (int t = 0; t < T; ++t)
+      for (int c = 0; c < CL; ++c) {
+        int sb, dc, db;
+        dec(t, c, sb, dc, db);
+        uses[c][sb].push_back(t);
+      }
+    auto req = [&](int t, int c) {
+      int sb, dc, db;
+      dec(t, c, sb, dc, db);
+      int n = 0;
+      for (int u : uses[dc][db]) n += (u < t) ? 1 : 0;
+      return n;
+    };
+    for (int t = 0; t < period; ++t)
+      for (int c = 0; c < CL; ++c) {
+        const int base = req(t, c), upp = req(t + period, c) - base;
+        if (base > 255 || upp > 255 || req(t + 2 * period, c) - req(t + period, c) != upp) return false;
+        int snd = -1, ssb = 0;
+        for (int e = 0; e < CL; ++e) {
+          int sb, dc, db;
+          dec(t, e, sb, dc, db);
+          if (dc == c) {
+            snd = e;
+            ssb = sb;
+          }
+        }
+        if (snd < 0) return false;
+        P.w2[t * CL + c] = (unsigned)base | ((unsigned)upp << 8) | ((unsigned)snd << 16) | ((unsigned)ssb << 20);
+      }
+  }
   return true;
 }
 
@@ -548,14 +599,19 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   auto bufp = [&](int phase, int slot, int which) { return smem + ((size_t)(phase * 2 + slot) * 2 + which) * slot_sz; };
   double* norms = reinterpret_cast<double*>(smem + 8 * slot_sz);  // [2][h]
   int* flags = reinterpret_cast<int*>(norms + 2 * h);             // [4]: rotated / large rotation, by sweep parity
-  __shared__ __align__(8) unsigned long long mbar;               // block arrivals of an exchange
+  __shared__ __align__(8) unsigned long long mbars[2];           // block arrivals, by exchange parity
+  __shared__ unsigned gen[4];                                    // copies out of each buffer that landed
+  __shared__ int p2p_err;
   __shared__ int held[2];
   __shared__ double red[NW];
-  const unsigned mbar_a = smem_u32(&mbar);
+  const unsigned mbar_a = smem_u32(&mbars[0]);
   const unsigned blk_bytes = (unsigned)(2 * slot_sz * sizeof(T));  // X + V of one block
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_a));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_a + 8));
     asm volatile("fence.mbarrier_init.release.cluster;");
+    for (int b = 0; b < 4; ++b) gen[b] = 0;
+    p2p_err = 0;
   }
   double scale = 1.0;
   if constexpr (sizeof(T) == 4) {  // keep FP32 Gram entries far from overflow / underflow
@@ -574,7 +630,6 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       scale = ldexp(1.0, -ex);
     }
   }
-  unsigned mb_parity = 0;
   int blk[2], ph[2] = {0, 0};
   circle_pair(nb, 0, k, blk[0], blk[1]);
   for (int sl = 0; sl < 2; ++sl) {
@@ -599,29 +654,61 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
   int xt = 0;  // exchanges so far
   auto exchange = [&]() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async-proxy reads
-    const unsigned e = plan.w[(xt % plan.period) * CL + k];
+    const int tp = xt % plan.period, xi = xt;
+    const unsigned e = plan.w[tp * CL + k];
     ++xt;
+    const int sb = e & 3, dc = (e >> 2) & 15, db = (e >> 6) & 3;
+    const unsigned mb_own = mbar_a + 8u * (unsigned)(xi & 1);
     TR_T(e0);
-    cl.sync();  // all rotations done everywhere; every copy of the previous exchange has landed
+    if (plan.p2p) {
+      __syncthreads();  // this CTA's rotations are done: the outgoing block is final
+      if (tid == 0) {
+        const unsigned w2 = plan.w2[tp * CL + k];
+        const unsigned need = (w2 & 255u) + (unsigned)(xi / plan.period) * ((w2 >> 8) & 255u);
+        const unsigned ga = cluster_addr(smem_u32(&gen[db]), dc);
+        unsigned have = 0;
+        for (long long spin = 0;; ++spin) {  // the destination buffer's earlier copies out have landed
+          asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(have) : "r"(ga) : "memory");
+          if (have >= need) break;
+          if (spin > (1ll << 28)) {  // protocol error: never hang the device
+            p2p_err = 1;
+            break;
+          }
+        }
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb_own), "r"(blk_bytes) : "memory");
+        const unsigned src = smem_u32(bufp(sb >> 1, sb & 1, 0));
+        const unsigned dst = cluster_addr(smem_u32(bufp(db >> 1, db & 1, 0)), dc);
+        const unsigned mb = cluster_addr(mbar_a + 8u * (unsigned)(xi & 1), dc);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "r"(src), "r"(blk_bytes), "r"(mb)
+            : "memory");
+      }
+    } else {
+      cl.sync();  // all rotations done everywhere; every copy of the previous exchange has landed
+      if (tid == 0) {
+        const unsigned src = smem_u32(bufp(sb >> 1, sb & 1, 0));
+        const unsigned dst = cluster_addr(smem_u32(bufp(db >> 1, db & 1, 0)), dc);
+        const unsigned mb = cluster_addr(mbar_a + 8u * (unsigned)(xi & 1), dc);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb_own), "r"(blk_bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "r"(src), "r"(blk_bytes), "r"(mb)
+            : "memory");
+      }
+    }
     TR_T(e1);
     TR_ADD(0, e1 - e0);
-    if (tid == 0) {
-      const int sb = e & 3, dc = (e >> 2) & 15, db = (e >> 6) & 3;
-      const unsigned src = smem_u32(bufp(sb >> 1, sb & 1, 0));
-      const unsigned dst = cluster_addr(smem_u32(bufp(db >> 1, db & 1, 0)), dc);
-      const unsigned mb = cluster_addr(mbar_a, dc);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_a), "r"(blk_bytes) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-          "r"(src), "r"(blk_bytes), "r"(mb)
-          : "memory");
-    }
     blk[0] = (e >> 8) & 31;
     blk[1] = (e >> 13) & 31;
     ph[0] = (e >> 18) & 1;
     ph[1] = (e >> 19) & 1;
-    mbar_wait(mbar_a, mb_parity);
-    mb_parity ^= 1u;
+    mbar_wait(mb_own, (unsigned)(xi >> 1) & 1u);
+    if (plan.p2p && tid == 0) {  // the sender's source buffer is free again: count it at its owner
+      const unsigned w2 = plan.w2[tp * CL + k];
+      const unsigned ga = cluster_addr(smem_u32(&gen[(w2 >> 20) & 3u]), (int)((w2 >> 16) & 15u));
+      asm volatile("red.release.cluster.shared::cluster.add.u32 [%0], 1;" ::"r"(ga) : "memory");
+    }
     TR_T(e2);
     TR_ADD(1, e2 - e1);
     TR_ADD(2, 1);
@@ -725,7 +812,8 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       const T* v = bufp(ph[q / h], q / h, 1) + (size_t)(q % h) * ldc;
       for (int r = lane; r < ell; r += 32) U[(int64_t)gid * ldu + r] = (double)v[r];
     }
-    if (k == 0 && tid == 0) info[0] = converged ? sweep : -sweep;
+    if (tid == 0 && p2p_err) info[0] = -1000;
+    if (k == 0 && tid == 0 && !p2p_err) info[0] = converged ? sweep : -sweep;
     cl.sync();
     return;
   }
@@ -760,7 +848,8 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       for (int r = lane; r < ell; r += 32) U[(int64_t)rank * ldu + r] = (double)v[r];
     }
   }
-  if (k == 0 && tid == 0) info[0] = converged ? sweep : -sweep;
+  if (tid == 0 && p2p_err) info[0] = -1000;  // exchange protocol timed out (results invalid)
+  if (k == 0 && tid == 0 && !p2p_err) info[0] = converged ? sweep : -sweep;
   cl.sync();
 }
 
@@ -818,6 +907,8 @@ static cudaError_t launch_jsvd_block_r(const double* A, int ell, int lda, const 
   while ((1 << li) < cl) ++li;
   if (!have[li]) {
     if (!jsvd_make_plan(cl, plans[li])) return cudaErrorInvalidValue;
+    const char* env = getenv("NGD_SVD_P2P");  // tuning / A-B: 0 = one cluster barrier per exchange
+    plans[li].p2p = env ? atoi(env) : 1;
     have[li] = true;
   }
   probe_before(K_SVD, st);
