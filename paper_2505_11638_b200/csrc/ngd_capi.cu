@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -150,6 +151,9 @@ struct ngd_ctx {
                      // 2 pipelined producer/consumer kernel (ngd_phb2.cu)
   int phb_deep = 0;  // kernel chosen by the plan: 0/1 phb_all_kernel depth, 2 phb2_kernel
   int phb_thin[kMaxLayers] = {};  // phb2: thin layers (N <= 16 or M <= 16)
+  Phb2Cache phb2_cache;           // phb2: tensor maps of this context's jets
+  Pha2Cache pha2_cache;
+  std::unique_ptr<Pha2Args> pha2_args{new Pha2Args()};
   int pcg_fuse = 0;  // option "pcg_fuse": PCG update fused with the preconditioner's first pass (measured
                     // slower at C2: 93 vs 84 us per iteration, tools/pcg_periter.py)
   int pha_plan = 0;  // option "pha_plan": 0 one CTA per unit (ngd_jet.cu, default), 1 persistent TMA
@@ -360,7 +364,7 @@ static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double*
   }
   pa.tile_start[c->NL] = tiles;
   if (c->pha_plan == 1 && pha2_supported(gm.C)) {
-    static Pha2Args a2;  // large (tensor maps): not on the stack
+    Pha2Args& a2 = *c->pha2_args;  // large (tensor maps): owned by the context, not on the stack
     a2.n_layers = c->NL;
     a2.nib = gm.nib;
     a2.nbb = gm.nbb;
@@ -382,7 +386,7 @@ static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double*
       kps[l] = c->Kp_f[l];
       mps[l] = c->Mp_f[l];
     }
-    CK(pha2_all_layers(a2, vps, zs, kps, mps, gm.C, c->stream));
+    CK(pha2_all_layers(a2, c->pha2_cache, vps, zs, kps, mps, gm.C, c->stream));
   } else {
     CK(pha_all(gm.C, pa, c->stream));
   }
@@ -428,7 +432,7 @@ static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* m
                        const int* skip) {
   PhbAll pb{};
   fill_phb(c, cot, skip, pb);
-  CK(c->phb_deep == 2 ? phase_b2_all_layers(pb, c->stream) : phase_b_all_layers(pb, c->phb_deep, c->stream));
+  CK(c->phb_deep == 2 ? phase_b2_all_layers(pb, c->phb2_cache, c->stream) : phase_b_all_layers(pb, c->phb_deep, c->stream));
   const bool shifted = v && (mu_p || mu != 0.0);
   if (c->comm) {
     reduce_splits(c->partB.d(), c->rplan, c->p, 0.0, nullptr, nullptr, out, skip, c->stream);
@@ -1443,7 +1447,7 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
       TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done, /*prepacked=*/true));
       PhbAll pb{};
       fill_phb(c, c->cot.d(), done, pb);
-      CK(c->phb_deep == 2 ? phase_b2_all_layers(pb, c->stream) : phase_b_all_layers(pb, c->phb_deep, c->stream));
+      CK(c->phb_deep == 2 ? phase_b2_all_layers(pb, c->phb2_cache, c->stream) : phase_b_all_layers(pb, c->phb_deep, c->stream));
     }
     if (c->comm) {
       reduce_splits(part, *rp, p, 0.0, nullptr, nullptr, ad, done, c->stream);

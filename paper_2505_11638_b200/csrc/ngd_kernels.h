@@ -119,8 +119,14 @@ struct Pha2Args {
   int cta_start[149];  // unit range of CTA i: [cta_start[i], cta_start[i + 1])
 };
 bool pha2_supported(int C);
-cudaError_t pha2_all_layers(Pha2Args& a, const double* const* vp, const double* const* zin, const int* kp,
-                            const int* mp, int C, cudaStream_t st);
+struct Pha2Cache {  // host-side tensor-map keys of pha2_all_layers (maps live in Pha2Args)
+  const double* kv[kMaxLayers] = {};
+  const double* kz[kMaxLayers] = {};
+  int kkp[kMaxLayers] = {}, kmp[kMaxLayers] = {}, kc[kMaxLayers] = {};
+  int64_t ks[kMaxLayers] = {};
+};
+cudaError_t pha2_all_layers(Pha2Args& a, Pha2Cache& cache, const double* const* vp, const double* const* zin,
+                            const int* kp, const int* mp, int C, cudaStream_t st);
 
 struct PhbAll {
   PhbArgs L[kMaxLayers];          // per layer (ktiles_per_split set per layer)
@@ -172,8 +178,19 @@ cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st);
 int phb_max_active_clusters(int cs);
 cudaError_t phase_b_all_layers(const PhbAll& a, int deep, cudaStream_t st);
 int phb_ctas_per_sm(int deep);
-// pipelined phase B (ngd_phb2.cu): producer warp + bulk copies, 32x32 warp tiles, thin-block skip
-cudaError_t phase_b2_all_layers(const PhbAll& a, cudaStream_t st);
+// pipelined phase B (ngd_phb2.cu): TMA producer + MMA warps; tensor maps cached per context
+struct Phb2Maps {
+  CUtensorMap d[kMaxLayers];  // D_l: [M rows][s_pad], box 64 x 16
+  CUtensorMap z[kMaxLayers];  // Zin_l: [N rows][s_pad]
+};
+struct Phb2Cache {  // host-side: re-encoded when a layer's buffers or shape change
+  Phb2Maps maps;
+  const double* kd[kMaxLayers] = {};
+  const double* kz[kMaxLayers] = {};
+  int km[kMaxLayers] = {}, kn[kMaxLayers] = {};
+  int64_t ks[kMaxLayers] = {};
+};
+cudaError_t phase_b2_all_layers(const PhbAll& a, Phb2Cache& cache, cudaStream_t st);
 int phb2_ctas_per_sm();
 void pack_all(const PackAll& a, const double* src, const int* skip, cudaStream_t st);
 cudaError_t form_j(const FormJArgs& a, int nblocks, int n_layers, int max_nin, int max_nout, cudaStream_t st);

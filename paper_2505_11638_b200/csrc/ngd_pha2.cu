@@ -395,29 +395,22 @@ bool pha2_supported(int C) { return C == 3 || C == 4 || C == 5 || C == 6 || C ==
 // Fills the tensor maps (cached per layer while the buffers stay put) and the cost-balanced unit
 // ranges, then launches.  Units cost ~ k-chunks x (channel boxes + V box) (interior) or x 2
 // (boundary).
-cudaError_t pha2_all_layers(Pha2Args& a, const double* const* vp, const double* const* zin, const int* kp,
-                            const int* mp, int C, cudaStream_t st) {
-  static const double* kv[kMaxLayers] = {};
-  static const double* kz[kMaxLayers] = {};
-  static int kkp[kMaxLayers] = {}, kmp[kMaxLayers] = {};
-  static int64_t ks[kMaxLayers] = {};
-  static int kc_[kMaxLayers] = {};
-  static CUtensorMap vmaps[kMaxLayers], zmaps[kMaxLayers];
+cudaError_t pha2_all_layers(Pha2Args& a, Pha2Cache& cache, const double* const* vp, const double* const* zin,
+                            const int* kp, const int* mp, int C, cudaStream_t st) {
   for (int l = 0; l < a.n_layers; ++l) {
     const int kc = std::min(kp[l], kc_max_rt(C));
-    if (kv[l] != vp[l] || kz[l] != zin[l] || kkp[l] != kp[l] || kmp[l] != mp[l] || ks[l] != a.s_pad || kc_[l] != C) {
-      if (!encode3_rows_inner(&vmaps[l], vp[l], kp[l], mp[l], AB, kc / AK) ||
-          !encode3(&zmaps[l], zin[l], a.s_pad, kp[l], C, kc))
+    if (cache.kv[l] != vp[l] || cache.kz[l] != zin[l] || cache.kkp[l] != kp[l] || cache.kmp[l] != mp[l] ||
+        cache.ks[l] != a.s_pad || cache.kc[l] != C) {  // a.vmap / a.zmap persist with the context's args
+      if (!encode3_rows_inner(&a.vmap[l], vp[l], kp[l], mp[l], AB, kc / AK) ||
+          !encode3(&a.zmap[l], zin[l], a.s_pad, kp[l], C, kc))
         return cudaErrorInvalidValue;
-      kc_[l] = C;
-      kv[l] = vp[l];
-      kz[l] = zin[l];
-      kkp[l] = kp[l];
-      kmp[l] = mp[l];
-      ks[l] = a.s_pad;
+      cache.kc[l] = C;
+      cache.kv[l] = vp[l];
+      cache.kz[l] = zin[l];
+      cache.kkp[l] = kp[l];
+      cache.kmp[l] = mp[l];
+      cache.ks[l] = a.s_pad;
     }
-    a.vmap[l] = vmaps[l];
-    a.zmap[l] = zmaps[l];
     a.kchunk[l] = std::min(kp[l], kc_max_rt(C));
     a.kchunks[l] = kp[l] / a.kchunk[l];
   }

@@ -209,11 +209,6 @@ __device__ __forceinline__ void epilogue(const PhbArgs& p, const Item& it, doubl
 }
 }  // namespace
 
-struct Phb2Maps {
-  CUtensorMap d[kMaxLayers];  // D_l: [M rows][s_pad], box 64 x 16
-  CUtensorMap z[kMaxLayers];  // Zin_l: [N rows][s_pad]
-};
-
 namespace {
 // one thread streams an item's units through an NS-deep ring (TMA boxes + cotangent run)
 template <int NS>
@@ -372,7 +367,7 @@ bool encode_rows(CUtensorMap* m, const double* base, int rows, int64_t s_pad) {
 }
 }  // namespace
 
-cudaError_t phase_b2_all_layers(const PhbAll& a, cudaStream_t st) {
+cudaError_t phase_b2_all_layers(const PhbAll& a, Phb2Cache& cache, cudaStream_t st) {
   const size_t smem = kPhb2Smem + kStaging;
   static bool attr_set = false;
   if (!attr_set) {
@@ -384,26 +379,23 @@ cudaError_t phase_b2_all_layers(const PhbAll& a, cudaStream_t st) {
   for (int l = 0; l < a.n_layers; ++l) (a.thin[l] ? nt : nh) += a.tiles_n[l] * a.tiles_m[l] * a.G[l];
   const int ctas = std::max(nh, nt);
   if (ctas <= 0) return cudaSuccess;
-  // tensor maps of every layer's operands (host-side encode, cached while the buffers stay put)
-  static Phb2Maps maps;
-  static const double* key_d[kMaxLayers] = {};
-  static const double* key_z[kMaxLayers] = {};
-  static int key_m[kMaxLayers] = {}, key_n[kMaxLayers] = {};
-  static int64_t key_s[kMaxLayers] = {};
+  // tensor maps of every layer's operands (host-side encode, cached in the context while the
+  // buffers stay put)
   for (int l = 0; l < a.n_layers; ++l) {
     const PhbArgs& p = a.L[l];
-    if (key_d[l] != p.D || key_z[l] != p.Z || key_m[l] != p.M || key_n[l] != p.N || key_s[l] != p.s_pad) {
-      if (!encode_rows(&maps.d[l], p.D, p.M, p.s_pad) || !encode_rows(&maps.z[l], p.Z, p.N, p.s_pad))
+    if (cache.kd[l] != p.D || cache.kz[l] != p.Z || cache.km[l] != p.M || cache.kn[l] != p.N ||
+        cache.ks[l] != p.s_pad) {
+      if (!encode_rows(&cache.maps.d[l], p.D, p.M, p.s_pad) || !encode_rows(&cache.maps.z[l], p.Z, p.N, p.s_pad))
         return cudaErrorInvalidValue;
-      key_d[l] = p.D;
-      key_z[l] = p.Z;
-      key_m[l] = p.M;
-      key_n[l] = p.N;
-      key_s[l] = p.s_pad;
+      cache.kd[l] = p.D;
+      cache.kz[l] = p.Z;
+      cache.km[l] = p.M;
+      cache.kn[l] = p.N;
+      cache.ks[l] = p.s_pad;
     }
   }
   probe_before(K_PHB, st);
-  phb2_kernel<<<ctas, kPhb2Threads, smem, st>>>(a, maps);
+  phb2_kernel<<<ctas, kPhb2Threads, smem, st>>>(a, cache.maps);
   probe_after(K_PHB, st);
   return cudaGetLastError();
 }

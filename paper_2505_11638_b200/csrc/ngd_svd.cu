@@ -901,19 +901,26 @@ static cudaError_t launch_jsvd_block_r(const double* A, int ell, int lda, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static JsvdPlan plans[5];  // CL = 1 << i
-  static bool have[5] = {false, false, false, false, false};
+  // exchange schedules for CL = 1, 2, 4, 8, 16 (built once, thread-safe static initialisation)
+  struct Plans {
+    JsvdPlan p[5];
+    bool ok[5];
+  };
+  static const Plans* plans = [] {
+    auto* ps = new Plans();
+    const char* env = getenv("NGD_SVD_P2P");  // tuning / A-B: 0 = one cluster barrier per exchange
+    for (int i = 0; i < 5; ++i) {
+      ps->ok[i] = jsvd_make_plan(1 << i, ps->p[i]);
+      ps->p[i].p2p = env ? atoi(env) : 1;
+    }
+    return ps;
+  }();
   int li = 0;
   while ((1 << li) < cl) ++li;
-  if (!have[li]) {
-    if (!jsvd_make_plan(cl, plans[li])) return cudaErrorInvalidValue;
-    const char* env = getenv("NGD_SVD_P2P");  // tuning / A-B: 0 = one cluster barrier per exchange
-    plans[li].p2p = env ? atoi(env) : 1;
-    have[li] = true;
-  }
+  if (li > 4 || !plans->ok[li]) return cudaErrorInvalidValue;
   probe_before(K_SVD, st);
   e = cudaLaunchKernelEx(&cfg, kern, A, ell, lda, Vin, ldv, U, ldu, sigma, tol, tbig, max_sweeps, h, info,
-                         plans[li]);
+                         plans->p[li]);
   probe_after(K_SVD, st);
   return e;
 }
