@@ -580,15 +580,16 @@ __global__ void pcg_first_dir_kernel(const double* z, double* d, int64_t p, PcgS
 // ad = sum_g part[g] + mu d ; dad = d.ad ; breakdown test and alpha (krylov.py:59-66).  Four lanes per
 // element split the split-K partial sum (lane q takes g = q, q+4, ...; combined in fixed order), so
 // the dependent L2 loads of the G partials are spread over 4x more threads.
-constexpr int kAdPerBlock = kThreads / 4;
+constexpr int kAdLanes = 8;  // lanes per element: G = 74 split partials (C2) -> <= 10 loads per lane
+constexpr int kAdPerBlock = kThreads / kAdLanes;
 __global__ void pcg_ad_kernel(const double* part, RedPlan rp, int64_t p, const double* mu_p, const double* d,
                               double* ad, PcgState* s, int ad_ready, double* partials, unsigned* counter) {
   if (s->done) return;
   const double mu = *mu_p;
-  const int q = threadIdx.x & 3;
+  const int q = threadIdx.x & (kAdLanes - 1);
   double v = 0.0;
   for (int64_t i0 = (int64_t)blockIdx.x * kAdPerBlock; i0 < p; i0 += (int64_t)gridDim.x * kAdPerBlock) {
-    const int64_t i = i0 + (threadIdx.x >> 2);
+    const int64_t i = i0 + (threadIdx.x / kAdLanes);
     if (ad_ready) {
       if (q == 0 && i < p) v = fma(d[i], ad[i], v);
       continue;
@@ -597,21 +598,22 @@ __global__ void pcg_ad_kernel(const double* part, RedPlan rp, int64_t p, const d
     if (i < p) {
       const int G = plan_G(rp, i);
       int g = q;
-      for (; g + 12 < G; g += 16) {
-        const double x0 = __ldcg(&part[(int64_t)g * p + i]), x1 = __ldcg(&part[(int64_t)(g + 4) * p + i]);
-        const double x2 = __ldcg(&part[(int64_t)(g + 8) * p + i]), x3 = __ldcg(&part[(int64_t)(g + 12) * p + i]);
+      for (; g + 3 * kAdLanes < G; g += 4 * kAdLanes) {
+        const double x0 = __ldcg(&part[(int64_t)g * p + i]);
+        const double x1 = __ldcg(&part[(int64_t)(g + kAdLanes) * p + i]);
+        const double x2 = __ldcg(&part[(int64_t)(g + 2 * kAdLanes) * p + i]);
+        const double x3 = __ldcg(&part[(int64_t)(g + 3 * kAdLanes) * p + i]);
         a += x0;
         a += x1;
         a += x2;
         a += x3;
       }
-      for (; g < G; g += 4) a += __ldcg(&part[(int64_t)g * p + i]);
+      for (; g < G; g += kAdLanes) a += __ldcg(&part[(int64_t)g * p + i]);
     }
-    const double a1 = __shfl_xor_sync(0xffffffffu, a, 1);
-    const double a2 = __shfl_xor_sync(0xffffffffu, a, 2);
-    const double a3 = __shfl_xor_sync(0xffffffffu, a, 3);
-    if (q == 0 && i < p) {  // (s0 + s1) + (s2 + s3), fixed order
-      const double tot = fma(mu, d[i], (a + a1) + (a2 + a3));
+#pragma unroll
+    for (int o = 1; o < kAdLanes; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);  // fixed xor tree
+    if (q == 0 && i < p) {
+      const double tot = fma(mu, d[i], a);
       ad[i] = tot;
       v = fma(d[i], tot, v);
     }
