@@ -1,0 +1,57 @@
+"""Phase B (J^T c, ngd_phb2.cu) on topologies that exercise its tile plan: partial 64x64 tiles,
+several m/n tiles per layer, 'heavy' layers just above the thin threshold (17 x 33), thin
+input layers with N = d up to 10 (two 8-column blocks) and the M = 1 output layer.  Each
+Gramian matvec is checked against the CPU oracle and against the first phase-B form
+(phb_plan 0): same math, different split / summation order."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ngd = pytest.importorskip("paper_2505_11638_b200")
+
+from oracle import ngd_oracle as O  # noqa: E402
+
+CASES = [
+    ("sin2d", (2, 50, 100, 1), 256, 64),
+    ("sin2d", (2, 17, 33, 1), 200, 40),
+    ("sin2d", (2, 64, 130, 1), 256, 64),
+    ("sin2d", (2, 8, 16, 8, 1), 160, 32),
+    ("sinsum", (10, 40, 24, 1), 192, 48),
+    ("gauss", (5, 70, 1), 192, 48),
+]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def build(kind, widths, nint, nbnd):
+    top = ngd.MlpTopology(widths)
+    prob = ngd.Poisson2D(top) if kind == "sin2d" else ngd.PoissonND(top, kind)
+    quad = prob.sample_quadrature(nint, nbnd, 0)
+    theta = ngd.init(top, 0).values + 0.05 * np.random.default_rng(1).standard_normal(top.param_count)
+    return prob, quad, theta
+
+
+@pytest.mark.parametrize("kind,widths,nint,nbnd", CASES)
+def test_phase_b_tile_plans(kind, widths, nint, nbnd):
+    from paper_2505_11638_b200 import _lib
+
+    prob, quad, theta = build(kind, widths, nint, nbnd)
+    v = np.random.default_rng(2).standard_normal(prob.topology.param_count)
+    oprob = O.PoissonProblem(widths, kind=kind)
+    oq = oprob.sample_quadrature(nint, nbnd, 0)
+    ref = O.GramianOracle(oprob, theta, oq).matvec(v)
+    out = {}
+    for plan in (2, 0):
+        with _lib.option("phb_plan", plan):
+            p2, q2, _ = build(kind, widths, nint, nbnd)
+            gop = ngd.GramianOperator.from_problem(p2, theta, q2)
+            out[plan] = gop.matvec(v)
+            # the gradient runs phase B with the residual cotangent
+            g = p2.loss_grad(theta, q2)
+            assert rel(g, oprob.loss_grad(theta, oq)) <= 1e-10
+    assert rel(out[2], ref) <= 1e-10
+    assert rel(out[2], out[0]) <= 1e-12
