@@ -1389,8 +1389,13 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
   {
     int sw[2] = {0, 0};  // FP64 sweeps, FP32 pre-sweeps
     memcpy(sw, &c->h_pin[60], 2 * sizeof(int));
+    const bool jacobi = (c->svd_method == 2 || c->svd_method == 3) && jsvd_block_supported(ell) > 0;
     c->last_sweeps = sw[0];
-    c->last_sweeps_f32 = (c->svd_method == 3 && jsvd_block_supported(ell) > 0) ? sw[1] : 0;
+    c->last_sweeps_f32 = (c->svd_method == 3 && jacobi) ? sw[1] : 0;
+    // a non-converged FP64 Jacobi (or a timed-out block exchange) must not hand back a factor
+    // (the FP32 pre-sweeps may stop at their sweep cap: the FP64 phase finishes the job)
+    if (jacobi && (sw[0] <= 0 || (c->svd_method == 3 && sw[1] == -1000)))
+      return fail(NGD_E_CUDA, "small SVD: block Jacobi failed (FP64 sweeps %d, FP32 status %d)", sw[0], sw[1]);
   }
   CK(cudaGetLastError());
   return NGD_OK;

@@ -714,6 +714,16 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
     TR_ADD(2, 1);
   };
 
+  // info[0]: sweeps (negative: not converged), or -1000 if any CTA's exchange protocol timed out
+  auto report = [&](bool conv, int sweeps) {
+    cl.sync();  // every CTA's p2p_err is final
+    if (k == 0 && tid == 0) {
+      int err = 0;
+      for (int o = 0; o < CL; ++o) err |= *cl.map_shared_rank(&p2p_err, o);
+      info[0] = err ? -1000 : (conv ? sweeps : -sweeps);
+    }
+    cl.sync();  // keep every CTA's shared memory alive until CTA 0 has read it
+  };
   int sweep = 0;
   bool converged = false;
   for (; sweep < max_sweeps && !converged; ++sweep) {
@@ -812,9 +822,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       const T* v = bufp(ph[q / h], q / h, 1) + (size_t)(q % h) * ldc;
       for (int r = lane; r < ell; r += 32) U[(int64_t)gid * ldu + r] = (double)v[r];
     }
-    if (tid == 0 && p2p_err) info[0] = -1000;
-    if (k == 0 && tid == 0 && !p2p_err) info[0] = converged ? sweep : -sweep;
-    cl.sync();
+    report(converged, sweep);
     return;
   }
   // norms of the held columns, ranks over the cluster, outputs
@@ -848,9 +856,7 @@ __global__ void __launch_bounds__(kBlockSvdThreads, 1) jsvd_block_kernel(const d
       for (int r = lane; r < ell; r += 32) U[(int64_t)rank * ldu + r] = (double)v[r];
     }
   }
-  if (tid == 0 && p2p_err) info[0] = -1000;  // exchange protocol timed out (results invalid)
-  if (k == 0 && tid == 0 && !p2p_err) info[0] = converged ? sweep : -sweep;
-  cl.sync();
+  report(converged, sweep);
 }
 
 static size_t jsvd_block_smem(int ell, int h, size_t elt) {
