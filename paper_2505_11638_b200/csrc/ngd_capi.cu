@@ -154,6 +154,9 @@ struct ngd_ctx {
   Phb2Cache phb2_cache;           // phb2: tensor maps of this context's jets
   Pha2Cache pha2_cache;
   std::unique_ptr<Pha2Args> pha2_args{new Pha2Args()};
+  int l2u = 1;      // option "l2u": keep the preconditioner basis U L2-persisting during PCG
+  Buf u_persist;     // PCG's copy of U at a fixed address (the captured graph carries its L2 window)
+  size_t jets_arena = 0;
   int pcg_fuse = 0;  // option "pcg_fuse": PCG update fused with the preconditioner's first pass (measured
                     // slower at C2: 93 vs 84 us per iteration, tools/pcg_periter.py)
   int pha_plan = 0;  // option "pha_plan": 0 one CTA per unit (ngd_jet.cu, default), 1 persistent TMA
@@ -780,7 +783,7 @@ int ngd_ctx_destroy(ngd_ctx* c) {
   for (auto& e : c->poll_ev)
     if (e) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->rinv, &c->tsq, &c->jets, &c->partF, &c->wr_pad, &c->R_pad, &c->alpha_bar})
+  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->rinv, &c->tsq, &c->jets, &c->partF, &c->wr_pad, &c->R_pad, &c->alpha_bar, &c->u_persist})
     b->release();
   if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
   if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
@@ -877,6 +880,7 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
     if (l + 1 < c->NL) c->dbuf[l].set_view(jb + doff[l], col_b * rup(c->w[l + 1], 16));
   }
   c->dseed.set_view(jb + soff, col_b * 16);
+  c->jets_arena = arena;
   TRY(set_l2_window(c, c->jets.p, arena));
   CK(c->pre_last.ensure(col_b * 16));
   CK(c->zs0.ensure(col_b * maxw));
@@ -1521,7 +1525,17 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
   const int* done = &sp->done;
   // every earlier solve ended with a stream synchronisation: no kernel can still write the flag
   *reinterpret_cast<volatile int*>(&c->h_flags[5]) = 0;
-  // operands into stable, ctx-owned locations (graph replay needs fixed addresses)
+  // operands into stable, ctx-owned locations (graph replay needs fixed addresses).  With "l2u",
+  // U is copied to a context buffer that carries an L2 persisting window for the solve: the two
+  // passes over U per iteration otherwise lose it to the jets streamed by phase A and B.
+  const bool l2u = have_pre && c->l2u && c->use_l2_window;
+  if (l2u) {
+    const size_t ub = sizeof(double) * (size_t)p * ell;
+    CK(c->u_persist.ensure(ub));
+    CK(cudaMemcpyAsync(c->u_persist.p, U, ub, cudaMemcpyDeviceToDevice, c->stream));
+    U = c->u_persist.d();
+    TRY(set_l2_window(c, c->u_persist.p, ub));
+  }
   PrecondArgs hpa{U, eig, precond_mu};
   CK(cudaMemcpyAsync(c->pargs.p, &hpa, sizeof(hpa), cudaMemcpyHostToDevice, c->stream));
   c->h_pin[48] = mu;
@@ -1613,6 +1627,7 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
     }
   }
   (void)issued;
+  if (l2u && c->jets_arena) TRY(set_l2_window(c, c->jets.p, c->jets_arena));  // back to the jets
   return NGD_OK;
 }
 
@@ -1718,6 +1733,11 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_comm")) {
     c->force_comm = value ? 1 : 0;
+    return NGD_OK;
+  }
+  if (!strcmp(key, "l2u")) {
+    c->l2u = value ? 1 : 0;
+    c->graph_gen++;
     return NGD_OK;
   }
   if (!strcmp(key, "pcg_fuse")) {
