@@ -122,7 +122,8 @@ int ngd_nystrom_finish(ngd_ctx* ctx, const double* d_omega, double* d_Y, int64_t
                        double* d_U, double* d_eig, double* h_shift);
 /* small dense SVD A = U diag(sigma) V^T of an ell x ell column-major matrix (the step of
  * sketch.py:85 after B = QR); method 2 = cluster one-sided Jacobi, 3 = block-exchange cluster Jacobi,
- * 4 = FP32 pre-sweeps + FP64 block Jacobi, 1 = cuSOLVER polar SVD.  h_sweeps receives the Jacobi
+ * 4 = FP32 pre-sweeps + FP64 block Jacobi (ell <= 512; V in global memory above ~310), 1 = cuSOLVER
+ * polar SVD.  h_sweeps receives the Jacobi
  * sweep count (negative if not converged; method 4: 1000 * FP32 sweeps + FP64 sweeps). */
 int ngd_small_svd(ngd_ctx* ctx, const double* d_A, int32_t ell, double* d_U, double* d_sigma, int32_t method,
                   int32_t* h_sweeps);

@@ -622,7 +622,8 @@ static int small_svd_polar(ngd_ctx* c, int ell) {
 // errors ~eps ||R||, the level Cholesky-QR already leaves in R.
 static int small_svd_mixed(ngd_ctx* c, int ell) {
   const double one = 1.0, zero = 0.0, mhalf = -0.5, three_half = 1.5;
-  const size_t l2 = (size_t)ell * ell;
+  const int ld = ell + (ell & 1);  // even: V0 may be the FP64 phase's in-place V (vector columns)
+  const size_t l2 = (size_t)ld * ell;
   CK(c->svd_mix.ensure(sizeof(double) * 4 * l2));
   CK(c->nys_info.ensure(sizeof(int) * 8));
   double* V0 = c->svd_mix.d();
@@ -634,16 +635,17 @@ static int small_svd_mixed(ngd_ctx* c, int ell) {
     const char* e = getenv("NGD_SVD_F32_COUPLING");
     return e ? atof(e) : 1e-3;
   }();
-  CK(jacobi_presweep_f32(c->nys_r.d(), ell, ell, V0, ell, coupling, info + 3, c->stream));
-  for (int it = 0; it < 2; ++it) {
-    CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, ell, &one, V0, ell, V0, ell, &zero, G, ell));
+  if (ld != ell) CK(cudaMemsetAsync(V0, 0, sizeof(double) * 2 * l2, c->stream));  // padding rows
+  CK(jacobi_presweep_f32(c->nys_r.d(), ell, ell, V0, ld, coupling, info + 3, c->stream));
+  for (int it = 0; it < 2; ++it) {  // two Newton-Schulz steps: V0 <- V0 (3 I - V0^T V0) / 2
+    CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, ell, &one, V0, ld, V0, ld, &zero, G, ell));
     CK(cudaMemcpyAsync(V1, V0, sizeof(double) * l2, cudaMemcpyDeviceToDevice, c->stream));
-    CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, ell, ell, ell, &mhalf, V0, ell, G, ell, &three_half, V1, ell));
+    CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, ell, ell, ell, &mhalf, V0, ld, G, ell, &three_half, V1, ld));
     std::swap(V0, V1);
   }
   // X = R^T V0 enters the kernel as A2^T, A2 = V0^T R
-  CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, ell, &one, V0, ell, c->nys_r.d(), ell, &zero, A2, ell));
-  CK(jacobi_svd_block_from(A2, ell, ell, V0, ell, c->nys_ur.d(), ell, c->nys_s.d(), info + 2, c->stream));
+  CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, ell, &one, V0, ld, c->nys_r.d(), ell, &zero, A2, ell));
+  CK(jacobi_svd_block_from(A2, ell, ell, V0, ld, c->nys_ur.d(), ell, c->nys_s.d(), info + 2, c->stream));
   return NGD_OK;
 }
 
@@ -1366,7 +1368,7 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
     // 5. R = U_R diag(s) V^T, descending: cluster one-sided Jacobi (method 2) or polar SVD
     // in-house block-exchange cluster Jacobi (all rotations in local shared memory) where the
     // factor fits a cluster (ell <~ 310); cuSOLVER's polar SVD above
-    if (c->svd_method == 3 && jsvd_block_supported(ell) > 0) {
+    if (c->svd_method == 3 && jsvd_mixed_supported(ell) > 0) {
       TRY(small_svd_mixed(c, ell));
     } else if (c->svd_method == 2 && jsvd_block_supported(ell) > 0) {
       CK(jacobi_svd_block(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(),
@@ -1393,7 +1395,8 @@ int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, in
   {
     int sw[2] = {0, 0};  // FP64 sweeps, FP32 pre-sweeps
     memcpy(sw, &c->h_pin[60], 2 * sizeof(int));
-    const bool jacobi = (c->svd_method == 2 || c->svd_method == 3) && jsvd_block_supported(ell) > 0;
+    const bool jacobi = (c->svd_method == 2 && jsvd_block_supported(ell) > 0) ||
+                        (c->svd_method == 3 && jsvd_mixed_supported(ell) > 0);
     c->last_sweeps = sw[0];
     c->last_sweeps_f32 = (c->svd_method == 3 && jacobi) ? sw[1] : 0;
     // a non-converged FP64 Jacobi (or a timed-out block exchange) must not hand back a factor
@@ -1643,7 +1646,8 @@ int ngd_small_svd(ngd_ctx* c, const double* A, int32_t ell, double* U, double* s
   CK(cudaMemcpyAsync(c->nys_r.d(), A, sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
   int sweeps = 0;
   if (method == 4) {
-    if (jsvd_block_supported(ell) == 0) return fail(NGD_E_SHAPE, "ell = %d too large for the block-exchange Jacobi SVD", ell);
+    if (jsvd_mixed_supported(ell) == 0)
+      return fail(NGD_E_SHAPE, "ell = %d too large for the mixed-precision Jacobi SVD", ell);
     TRY(small_svd_mixed(c, ell));
     CK(cudaMemcpyAsync(&c->h_pin[56], static_cast<int*>(c->nys_info.p) + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost,
                        c->stream));

@@ -251,6 +251,8 @@ int jsvd_cluster_size(int ell);
 cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
                        cudaStream_t st);
 int jsvd_block_supported(int ell);
+// FP32 pre-sweeps + FP64 finish (V in place in global memory for ell > ~310): cluster size, 0 if unsupported
+int jsvd_mixed_supported(int ell);
 bool chol_supported(int n);
 // X R = A in place (A p x n col-major, R n x n upper col-major); work: trsm_work(n) bytes
 size_t trsm_work(int n);
@@ -264,7 +266,7 @@ cudaError_t chol_upper_cluster(double* A, int n, int lda, int* info, int* flag, 
 cudaError_t jacobi_svd_block(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
                              cudaStream_t st);
 // FP64 block Jacobi on X = A^T starting from V = V0 (orthonormal): sigma / U of A^T V0 rotated
-cudaError_t jacobi_svd_block_from(const double* A, int ell, int lda, const double* V0, int ldv, double* U, int ldu,
+cudaError_t jacobi_svd_block_from(const double* A, int ell, int lda, double* V0, int ldv, double* U, int ldu,
                                   double* sigma, int* info, cudaStream_t st);
 // FP32 pre-sweeps of the block Jacobi on A^T: V (ell x ell, unsorted, only near-orthogonal) out
 cudaError_t jacobi_presweep_f32(const double* A, int ell, int lda, double* V, int ldv, double coupling, int* info,

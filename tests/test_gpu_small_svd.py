@@ -24,7 +24,8 @@ def graded(n, seed):
 
 @pytest.mark.parametrize("method,n", [(2, 7), (2, 100), (2, 101), (2, 160), (2, 300), (2, 301), (2, 400),
                                       (3, 7), (3, 100), (3, 101), (3, 160), (3, 300), (3, 301), (3, 310),
-                                      (4, 7), (4, 100), (4, 101), (4, 160), (4, 300), (4, 301), (4, 310)])
+                                      (4, 7), (4, 100), (4, 101), (4, 160), (4, 300), (4, 301), (4, 310),
+                                      (4, 311), (4, 400), (4, 401), (4, 500), (4, 512)])
 def test_jacobi_svd_matches_lapack(method, n):
     a = graded(n, n)
     ctx = utility_context()

@@ -46,13 +46,18 @@ def run(r, method, reps=10):
     return U.cpu().numpy().T, S.cpu().numpy(), sw.value, float(np.median(ts))
 
 
-for name, r in (("c2", load_c2()), ("graded300", graded(300)), ("graded160", graded(160))):
+cases = (("c2", load_c2()), ("graded300", graded(300)), ("graded160", graded(160)))
+methods = (3, 4)
+if "big" in sys.argv[1:]:  # ell above the FP64 shared-memory limit: polar SVD vs mixed (V in global)
+    cases = tuple((f"graded{n}", graded(n)) for n in (320, 400, 500, 512))
+    methods = (1, 4)
+for name, r in cases:
     n = r.shape[0]
     u0, s0, _ = np.linalg.svd(r)
     nu = 2.2e-16 * s0[0] ** 2 * 10
     eig0 = np.maximum(s0 ** 2 - nu, 0)
     v = np.random.default_rng(0).standard_normal(n)
-    for m in (3, 4):
+    for m in methods:
         u, s, sw, ms = run(r, m)
         eig = np.maximum(s ** 2 - nu, 0)
         line = f"{name} method {m}: {ms:.3f} ms sweeps {sw} sig_abs {np.max(np.abs(s - s0)) / s0[0]:.1e}"
