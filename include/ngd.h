@@ -153,7 +153,8 @@ int ngd_small_cholesky(ngd_ctx* ctx, double* d_A, int32_t n, int32_t method, int
  *               | 2 (cluster Cholesky for every ell <= 512) | 0 (cuSOLVER potrf);
  *      "trsm" = 1 (in-house DMMA right triangular solve for ell <= 512, default) | 0 (cuBLAS DTRSM);
  *      "phb_plan" = 2 (phase B: TMA-fed warp-specialised kernel, default) | 1 | 0 (first form, 3 stages);
- *      "pha_plan" = 0 (phase A: one CTA per unit, default) | 1 (persistent TMA pipeline, slower at C2) */
+ *      "pha_plan" = 0 (phase A: one CTA per unit, default) | 1 (persistent TMA pipeline, slower at C2);
+ *      "pdl" = 1 (programmatic dependent launch along the PCG kernel chain, default; process-wide) | 0 */
 int ngd_set_option(ngd_ctx* ctx, const char* key, int64_t value);
 /* diagnostics: "jacobi_sweeps" (FP64 sweeps of the last Nystrom factorisation), "jacobi_sweeps_f32"
  * (its FP32 pre-sweeps, svd = 3), "phase_b_splits" */

@@ -94,7 +94,7 @@ OPTIONS = {"svd": 3}
 
 # library defaults of the ngd_set_option knobs (include/ngd.h), for restoring a temporary change
 DEFAULTS = {"svd": 3, "graphs": 1, "chol": 1, "trsm": 1, "syrk": 0, "l2window": 0, "fused": 0, "force_comm": 0,
-            "phb_cs": 0, "phb_g": 0, "phb_plan": 2}
+            "phb_cs": 0, "phb_g": 0, "phb_plan": 2, "pdl": 1, "l2u": 1, "pcg_fuse": 0}
 
 
 @contextlib.contextmanager

@@ -1744,6 +1744,11 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
     c->graph_gen++;
     return NGD_OK;
   }
+  if (!strcmp(key, "pdl")) {  // programmatic dependent launch along the PCG kernel chain (process-wide)
+    g_pdl = value ? 1 : 0;
+    c->graph_gen++;
+    return NGD_OK;
+  }
   if (!strcmp(key, "pcg_fuse")) {
     c->pcg_fuse = value ? 1 : 0;
     c->graph_gen++;  // captured PCG graphs bake the choice in

@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(kThreads) jet_gemm_kernel(JetArgs p) {
 // Phase A over ALL layers and both point segments in one launch (tile table).
 template <int C>
 __global__ void __launch_bounds__(kThreads) pha_all_kernel(PhaAll a) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   const int t = blockIdx.x;
   int l = 0;
   while (l + 1 < a.n_layers && t >= a.tile_start[l + 1]) ++l;
@@ -286,9 +287,9 @@ static cudaError_t launch_pha_all(const PhaAll& a, cudaStream_t st) {
   const int tiles = a.tile_start[a.n_layers];
   if (tiles <= 0) return cudaSuccess;
   probe_before(K_PHA, st);
-  kern<<<tiles, kThreads, smem, st>>>(a);
+  const cudaError_t e = launch_pdl(kern, dim3(tiles), dim3(kThreads), smem, st, a);
   probe_after(K_PHA, st);
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st) {

@@ -252,6 +252,7 @@ __device__ __forceinline__ void consume(const PhbArgs& p, const Item& it, const 
 // heavy tiles' MMAs on the same SM.
 __global__ void __maxnreg__(144) phb2_kernel(const __grid_constant__ PhbAll a,
                                               const __grid_constant__ Phb2Maps maps) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   extern __shared__ unsigned char phb2_smem[];
   // 1024-byte aligned rings (128-byte swizzle atoms); offsetting the extern array keeps the
   // accesses in the shared window (LDS) -- an integer round trip through uintptr_t made them generic
@@ -395,9 +396,9 @@ cudaError_t phase_b2_all_layers(const PhbAll& a, Phb2Cache& cache, cudaStream_t 
     }
   }
   probe_before(K_PHB, st);
-  phb2_kernel<<<ctas, kPhb2Threads, smem, st>>>(a, cache.maps);
+  const cudaError_t e = launch_pdl(phb2_kernel, dim3(ctas), dim3(kPhb2Threads), smem, st, a, cache.maps);
   probe_after(K_PHB, st);
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace ngd

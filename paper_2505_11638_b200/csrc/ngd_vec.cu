@@ -2,10 +2,16 @@
 // Nystrom preconditioner apply, fused PCG vector updates, Philox Gaussians.
 // All reductions use a fixed work assignment and a fixed combination order, so
 // results are bitwise reproducible run to run.
+#include <cstdlib>
 #include "ngd_common.cuh"
 #include "ngd_kernels.h"
 
 namespace ngd {
+
+int g_pdl = [] {  // NGD_PDL=0: plain stream-ordered launches (A/B); option "pdl" at run time
+  const char* e = getenv("NGD_PDL");
+  return e ? atoi(e) : 1;
+}();
 
 // ------------------------------- packing -----------------------------------
 // dst[m][k] (Mp x Kp, zero padded) = W[m][k] (trans=0) or W[k][m] (trans=1),
@@ -205,6 +211,7 @@ void frozen_alpha(const double* pre_last, Geom gm, double kappa, double* alpha, 
 // phase A reduction: s[pt] = sum over (layer, mtile) partials in fixed order; cot = w * s
 __global__ void reduce_pha_kernel(const double* partA, int rows, int n_pts_pad, const double* w, double* cot,
                                   const int* done) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (done && *done) return;
   for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < n_pts_pad; pt += gridDim.x * blockDim.x) {
     const double s = sum_partials(partA, rows, n_pts_pad, pt);
@@ -216,7 +223,7 @@ void reduce_pha(const double* partA, int rows, int n_pts_pad, const double* w, d
                 cudaStream_t st) {
   const int grid = std::max(1, std::min((n_pts_pad + 255) / 256, 148 * 8));
   probe_before(K_VEC, st);
-  reduce_pha_kernel<<<grid, 256, 0, st>>>(partA, rows, n_pts_pad, w, cot, done);
+  launch_pdl(reduce_pha_kernel, dim3(grid), dim3(256), 0, st, partA, rows, n_pts_pad, w, cot, done);
   probe_after(K_VEC, st);
 }
 
@@ -229,6 +236,7 @@ __device__ __forceinline__ int plan_G(const RedPlan& rp, int64_t i) {
 
 __global__ void reduce_splits_kernel(const double* part, RedPlan rp, int64_t p, double mu, const double* mu_p,
                                      const double* v, double* out, const int* done) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (done && *done) return;
   if (mu_p) mu = *mu_p;
   // four lanes per element (lane q sums g = q, q+4, ...; fixed-order combine), as pcg_ad_kernel
@@ -264,13 +272,14 @@ void reduce_splits(const double* part, const RedPlan& rp, int64_t p, double mu, 
                    double* out, const int* done, cudaStream_t st) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((p + 63) / 64, 148 * 8));
   probe_before(K_VEC, st);
-  reduce_splits_kernel<<<grid, 256, 0, st>>>(part, rp, p, mu, mu_p, v, out, done);
+  launch_pdl(reduce_splits_kernel, dim3(grid), dim3(256), 0, st, part, rp, p, mu, mu_p, v, out, done);
   probe_after(K_VEC, st);
 }
 
 // out += mu * v
 __global__ void add_scaled_kernel(double* out, double mu, const double* mu_p, const double* v, int64_t n,
                                   const int* done) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (done && *done) return;
   if (mu_p) mu = *mu_p;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -280,7 +289,7 @@ void add_scaled(double* out, double mu, const double* mu_p, const double* v, int
                 cudaStream_t st) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
   probe_before(K_VEC, st);
-  add_scaled_kernel<<<grid, 256, 0, st>>>(out, mu, mu_p, v, n, done);
+  launch_pdl(add_scaled_kernel, dim3(grid), dim3(256), 0, st, out, mu, mu_p, v, n, done);
   probe_after(K_VEC, st);
 }
 
@@ -341,6 +350,7 @@ void scatter_points(const double* compact, double* padded, Geom gm, cudaStream_t
 // Pass 2 (uc_kernel): out = v + U c', optionally with the PCG dot r.z fused in.
 __global__ void __launch_bounds__(kThreads) utv_kernel(const PrecondArgs* pa, int64_t p, int ell, const double* v,
                                                        double* cprime, const int* done) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (done && *done) return;
   __shared__ double sh[kThreads / 32];
   const int j = blockIdx.x;
@@ -373,6 +383,7 @@ __global__ void __launch_bounds__(kThreads) utv_kernel(const PrecondArgs* pa, in
 __global__ void __launch_bounds__(kThreads) uc_kernel(const PrecondArgs* pa, int64_t p, int ell, const double* cprime,
                                                       const double* v, double* out, const int* done, PcgState* pcg,
                                                       int first, double* partials, unsigned* counter) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (done && *done) return;
   extern __shared__ double cs[];  // [ell] c' then [8][32] partial rows
   double* part = cs + ell;
@@ -524,7 +535,7 @@ cudaError_t precond_apply2(const PrecondArgs* pa, int64_t p, int ell, const doub
                            unsigned* counter, cudaStream_t st) {
   const int grid = precond_blocks(p);
   probe_before(K_PRECOND, st);
-  uc_kernel<<<grid, kThreads, sizeof(double) * (std::max(ell, 1) + kThreads), st>>>(pa, p, ell, cprime, v, out, done,
+  launch_pdl(uc_kernel, dim3(grid), dim3(kThreads), sizeof(double) * (std::max(ell, 1) + kThreads), st, pa, p, ell, cprime, v, out, done,
                                                                                 pcg, first, partials, counter);
   probe_after(K_PRECOND, st);
   return cudaGetLastError();
@@ -536,12 +547,12 @@ cudaError_t precond_apply(const PrecondArgs* pa, int64_t p, int ell, const doubl
   (void)part;
   if (ell > 0) {
     probe_before(K_PRECOND, st);
-    utv_kernel<<<ell, kThreads, 0, st>>>(pa, p, ell, v, cprime, done);
+    launch_pdl(utv_kernel, dim3(ell), dim3(kThreads), 0, st, pa, p, ell, v, cprime, done);
     probe_after(K_PRECOND, st);
   }
   const int grid = precond_blocks(p);
   probe_before(K_PRECOND, st);
-  uc_kernel<<<grid, kThreads, sizeof(double) * (std::max(ell, 1) + kThreads), st>>>(pa, p, ell, cprime, v, out, done, pcg,
+  launch_pdl(uc_kernel, dim3(grid), dim3(kThreads), sizeof(double) * (std::max(ell, 1) + kThreads), st, pa, p, ell, cprime, v, out, done, pcg,
                                                                               first, partials, counters + 1);
   probe_after(K_PRECOND, st);
   return cudaGetLastError();
@@ -584,6 +595,7 @@ constexpr int kAdLanes = 8;  // lanes per element: G = 74 split partials (C2) ->
 constexpr int kAdPerBlock = kThreads / kAdLanes;
 __global__ void pcg_ad_kernel(const double* part, RedPlan rp, int64_t p, const double* mu_p, const double* d,
                               double* ad, PcgState* s, int ad_ready, double* partials, unsigned* counter) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (s->done) return;
   const double mu = *mu_p;
   const int q = threadIdx.x & (kAdLanes - 1);
@@ -635,6 +647,7 @@ __global__ void pcg_ad_kernel(const double* part, RedPlan rp, int64_t p, const d
 // x += alpha d ; r -= alpha ad ; rr = r.r ; convergence test (krylov.py:66-74)
 __global__ void pcg_update_kernel(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s,
                                   int recompute, double* partials, unsigned* counter) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (s->done) return;
   const double a = s->alpha;
   double v = 0.0;
@@ -657,6 +670,7 @@ __global__ void pcg_update_kernel(double* x, double* r, const double* d, const d
 // r = b - Ax (true residual, krylov.py:69-71 and 83-85) ; rr ; test
 __global__ void pcg_true_res_kernel(const double* b, const double* ax, double* r, int64_t p, PcgState* s,
                                     int count_matvec, int final_pass, double* partials, unsigned* counter) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (!final_pass && s->done) return;
   double v = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x) {
@@ -681,6 +695,7 @@ __global__ void pcg_true_res_kernel(const double* b, const double* ax, double* r
 
 // d = z + beta d  (krylov.py:79-81)
 __global__ void pcg_dir_kernel(const double* z, double* d, int64_t p, PcgState* s, int* host_flag) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   // last kernel of an iteration: publish the done flag to pinned host memory (zero-copy, no memcpy
   // or event between graph replays)
   if (host_flag && blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<volatile int*>(host_flag) = s->done;
@@ -693,6 +708,7 @@ __global__ void pcg_dir_kernel(const double* z, double* d, int64_t p, PcgState* 
 // d = z + beta d fused with the packing of d into the forward layer matrices of the next matvec
 // (pack_all_kernel's index space: every parameter is read and written by exactly one thread)
 __global__ void pcg_dir_pack_kernel(const double* z, double* d, PackAll a, PcgState* s, int* host_flag) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (host_flag && blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<volatile int*>(host_flag) = s->done;
   if (s->done) return;
   const double beta = s->beta;
@@ -741,30 +757,30 @@ void pcg_ad(const double* part, const RedPlan& rp, int64_t p, const double* mu_p
             PcgState* s, int ad_ready, double* partials, unsigned* counter, cudaStream_t st) {
   probe_before(K_VEC, st);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((p + kAdPerBlock - 1) / kAdPerBlock, 1184));
-  pcg_ad_kernel<<<grid, kThreads, 0, st>>>(part, rp, p, mu_p, d, ad, s, ad_ready, partials, counter);
+  launch_pdl(pcg_ad_kernel, dim3(grid), dim3(kThreads), 0, st, part, rp, p, mu_p, d, ad, s, ad_ready, partials, counter);
   probe_after(K_VEC, st);
 }
 void pcg_update(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s, int recompute,
                 double* partials, unsigned* counter, cudaStream_t st) {
   probe_before(K_VEC, st);
-  pcg_update_kernel<<<rgrid(p), kThreads, 0, st>>>(x, r, d, ad, p, s, recompute, partials, counter);
+  launch_pdl(pcg_update_kernel, dim3(rgrid(p)), dim3(kThreads), 0, st, x, r, d, ad, p, s, recompute, partials, counter);
   probe_after(K_VEC, st);
 }
 void pcg_true_res(const double* b, const double* ax, double* r, int64_t p, PcgState* s, int count, int final_pass,
                   double* partials, unsigned* counter, cudaStream_t st) {
   probe_before(K_VEC, st);
-  pcg_true_res_kernel<<<rgrid(p), kThreads, 0, st>>>(b, ax, r, p, s, count, final_pass, partials, counter);
+  launch_pdl(pcg_true_res_kernel, dim3(rgrid(p)), dim3(kThreads), 0, st, b, ax, r, p, s, count, final_pass, partials, counter);
   probe_after(K_VEC, st);
 }
 void pcg_dir_pack(const double* z, double* d, const PackAll& pk, PcgState* s, int* host_flag, cudaStream_t st) {
   const int64_t n = pk.start[pk.n_layers];
   probe_before(K_VEC, st);
-  pcg_dir_pack_kernel<<<vgrid(n), 256, 0, st>>>(z, d, pk, s, host_flag);
+  launch_pdl(pcg_dir_pack_kernel, dim3(vgrid(n)), dim3(256), 0, st, z, d, pk, s, host_flag);
   probe_after(K_VEC, st);
 }
 void pcg_dir(const double* z, double* d, int64_t p, PcgState* s, int* host_flag, cudaStream_t st) {
   probe_before(K_VEC, st);
-  pcg_dir_kernel<<<vgrid(p), 256, 0, st>>>(z, d, p, s, host_flag);
+  launch_pdl(pcg_dir_kernel, dim3(vgrid(p)), dim3(256), 0, st, z, d, p, s, host_flag);
   probe_after(K_VEC, st);
 }
 
