@@ -86,6 +86,11 @@ __device__ __forceinline__ void finish_sum(double v, double* partials, unsigned 
   __shared__ double sh[kThreads / 32];
   __shared__ bool last;
   const double bs = block_sum(v, sh);
+#ifndef NGD_PDL_NO_TAIL_TRIGGER
+  // this block's streaming work is done: once every block got here, the next kernel of the chain
+  // may launch (it still waits for this grid's completion) and overlaps the last-block combine
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = bs;
     __threadfence();
