@@ -121,14 +121,18 @@ int ngd_nystrom_prepare(ngd_ctx* ctx, double* d_omega, int64_t p, int32_t ell);
 int ngd_nystrom_finish(ngd_ctx* ctx, const double* d_omega, double* d_Y, int64_t p, int32_t ell,
                        double* d_U, double* d_eig, double* h_shift);
 /* small dense SVD A = U diag(sigma) V^T of an ell x ell column-major matrix (the step of
- * sketch.py:85 after B = QR); method 2 = cluster one-sided Jacobi, 3 = block-exchange cluster Jacobi,
- * 4 = FP32 pre-sweeps + FP64 block Jacobi (ell <= 512; V in global memory above ~310), 1 = cuSOLVER
- * polar SVD.  h_sweeps receives the Jacobi
- * sweep count (negative if not converged; method 4: 1000 * FP32 sweeps + FP64 sweeps). */
+ * sketch.py:85 after B = QR); method 3 = block-exchange cluster Jacobi (FP64),
+ * 4 = FP32 pre-sweeps + FP64 block Jacobi (the library's choice for ell <= 512; V in global memory
+ * above ~310), 1 = cuSOLVER polar SVD (the library's choice above 512).  h_sweeps receives the
+ * Jacobi sweep count (negative if not converged; method 4: 1000 * FP32 sweeps + FP64 sweeps). */
 int ngd_small_svd(ngd_ctx* ctx, const double* d_A, int32_t ell, double* d_U, double* d_sigma, int32_t method,
                   int32_t* h_sweeps);
 /* dense operator helper (DenseOperator.matmat, gramian.py:101-120): Y = G V */
 int ngd_dense_matmat(ngd_ctx* ctx, const double* d_G, int64_t p, const double* d_V, int64_t ell, double* d_Y);
+/* the in-house FP64 DMMA GEMM behind every dense product of the sketch / factorisation (test hook):
+ * C = alpha op(A) op(B) + beta C, column-major, op = transpose when trans_* != 0 */
+int ngd_gemm(ngd_ctx* ctx, int32_t trans_a, int32_t trans_b, int32_t M, int32_t N, int32_t K, double alpha,
+             const double* d_A, int64_t lda, const double* d_B, int64_t ldb, double beta, double* d_C, int64_t ldc);
 
 /* ---- preconditioner (NystromPreconditioner.apply, sketch.py:101-112) ---- */
 int ngd_precond_apply(ngd_ctx* ctx, const double* d_U, const double* d_eig, int32_t ell, double mu,
@@ -141,20 +145,17 @@ int ngd_pcg(ngd_ctx* ctx, const double* d_dense, int64_t p, const double* d_b, d
             int32_t maxit, int32_t recompute_every, double* d_x, ngd_solve_report* h_report);
 
 /* upper Cholesky A = U^T U in place (A n x n column-major, upper triangle read/written), the
- * factorisation inside ngd_nystrom_* exposed for testing: method 0 cuSOLVER potrf, 1 one-CTA
- * (n <= 160), 2 8-CTA cluster (n <= 512); *h_info = 0 or the first failing pivot + 1 (potrf) */
+ * factorisation inside ngd_nystrom_* exposed for testing: method 0 = the library's choice (one CTA,
+ * cluster, blocked with DMMA updates above 512), 1 one-CTA (n <= 160), 2 8-CTA cluster (n <= 512);
+ * *h_info = 0 or the first failing pivot + 1 (LAPACK potrf semantics) */
 int ngd_small_cholesky(ngd_ctx* ctx, double* d_A, int32_t n, int32_t method, int32_t* h_info);
 
-/* ---- tuning knobs: "svd" = 0 (Householder QR + cuSOLVER gesvdj) | 1 (shifted Cholesky-QR3 + cuSOLVER polar SVD)
- *      | 2 (shifted Cholesky-QR3 + in-house cluster one-sided Jacobi SVD; falls back to 1 above ell = 310)
- *      | 3 (as 2 with FP32 Jacobi pre-sweeps and an FP64 finish; default);
- *      "graphs" = 1 (replay PCG iterations as a CUDA graph, default) | 0;
- *      "chol" = 1 (in-house: one-CTA Cholesky for ell <= 32, 8-CTA cluster Cholesky up to 512; default)
- *               | 2 (cluster Cholesky for every ell <= 512) | 0 (cuSOLVER potrf);
- *      "trsm" = 1 (in-house DMMA right triangular solve for ell <= 512, default) | 0 (cuBLAS DTRSM);
- *      "phb_plan" = 2 (phase B: TMA-fed warp-specialised kernel, default) | 1 | 0 (first form, 3 stages);
- *      "pha_plan" = 0 (phase A: one CTA per unit, default) | 1 (persistent TMA pipeline, slower at C2);
- *      "pdl" = 1 (programmatic dependent launch along the PCG kernel chain, default; process-wide) | 0 */
+/* ---- knobs: "svd" = 3 (FP32 pre-sweeps + FP64 block Jacobi for ell <= 512, cuSOLVER polar SVD above;
+ *      default) | 1 (polar SVD at every ell);  "graphs" = 1 (replay PCG iterations as a CUDA graph,
+ *      default) | 0;  "pdl" = 1 (programmatic dependent launch along the PCG kernel chain, default;
+ *      process-wide) | 0;  "l2window" / "l2u" = 1 (L2 persisting windows over the jets / the
+ *      preconditioner basis during PCG, default) | 0;  "force_comm" = 1 (build an NCCL communicator
+ *      even for one rank: tests of the multi-rank paths) */
 int ngd_set_option(ngd_ctx* ctx, const char* key, int64_t value);
 /* diagnostics: "jacobi_sweeps" (FP64 sweeps of the last Nystrom factorisation), "jacobi_sweeps_f32"
  * (its FP32 pre-sweeps, svd = 3), "phase_b_splits" */
@@ -170,12 +171,17 @@ int ngd_axpy(ngd_ctx* ctx, const double* d_a, double alpha, const double* d_b, d
  * ngd_launch_count: number of this library's kernel launches so far (process-wide).
  * ngd_probe_start(kind, n): bracket the next n launches of kernel class `kind`
  *   (1 FWD jets, 2 REV jets, 3 phase A, 4 phase B, 5 J rows, 6 preconditioner,
- *   7 vector/scalar, 8 pack, 9 small SVD, 10 small Cholesky) with CUDA events on their launch stream;
+ *   7 vector/scalar, 8 pack, 9 small SVD, 10 small Cholesky, 11 (unused), 12 cuSOLVER, 13 triangular
+ *   solve, 14 DMMA GEMM; 0 = every class at once, read back with ngd_probe_stop_all) with CUDA events
+ *   on their launch stream;
  *   ngd_probe_stop returns the summed device time and the launch count. */
 int ngd_stream_sync(ngd_ctx* ctx);
 int64_t ngd_launch_count(void);
+/* algorithmic FLOPs (2 M N K) of every in-house DMMA GEMM launched so far (process-wide) */
+double ngd_gemm_flops(void);
 int ngd_probe_start(int32_t kind, int32_t max_launches);
 int ngd_probe_stop(double* h_total_ms, int64_t* h_count);
+int ngd_probe_stop_all(double* h_ms, int64_t* h_count, int32_t n_kinds);
 
 #ifdef __cplusplus
 }

@@ -73,6 +73,7 @@ SIGNATURES = {
     "ngd_nystrom_prepare": [_P, _P, _I64, _I32],
     "ngd_nystrom_finish": [_P, _P, _P, _I64, _I32, _P, _P, ctypes.POINTER(_D)],
     "ngd_dense_matmat": [_P, _P, _I64, _P, _I64, _P],
+    "ngd_gemm": [_P, _I32, _I32, _I32, _I32, _I32, _D, _P, _I64, _P, _I64, _D, _P, _I64],
     "ngd_precond_apply": [_P, _P, _P, _I32, _D, _P, _P, _I64],
     "ngd_pcg": [_P, _P, _I64, _P, _D, _P, _P, _I32, _D, _D, _I32, _I32, _P, ctypes.POINTER(SolveReportC)],
     "ngd_small_svd": [_P, _P, _I32, _P, _P, _I32, ctypes.POINTER(_I32)],
@@ -82,10 +83,13 @@ SIGNATURES = {
     "ngd_axpy": [_P, _P, _D, _P, _P, _I64],
     "ngd_stream_sync": [_P],
     "ngd_launch_count": [],
+    "ngd_gemm_flops": [],
     "ngd_probe_start": [_I32, _I32],
     "ngd_probe_stop": [ctypes.POINTER(_D), ctypes.POINTER(_I64)],
+    "ngd_probe_stop_all": [ctypes.POINTER(_D), ctypes.POINTER(_I64), _I32],
 }
-_RESTYPE = {"ngd_last_error": ctypes.c_char_p, "ngd_param_count": _I64, "ngd_launch_count": _I64}
+_RESTYPE = {"ngd_last_error": ctypes.c_char_p, "ngd_param_count": _I64, "ngd_launch_count": _I64,
+            "ngd_gemm_flops": _D}
 
 _lib = None
 _contexts = []  # weak registry so option changes reach live contexts
@@ -93,8 +97,7 @@ OPTIONS = {"svd": 3}
 
 
 # library defaults of the ngd_set_option knobs (include/ngd.h), for restoring a temporary change
-DEFAULTS = {"svd": 3, "graphs": 1, "chol": 1, "trsm": 1, "syrk": 0, "l2window": 0, "fused": 0, "force_comm": 0,
-            "phb_cs": 0, "phb_g": 0, "phb_plan": 2, "pdl": 1, "l2u": 1, "pcg_fuse": 0}
+DEFAULTS = {"svd": 3, "graphs": 1, "l2window": 1, "force_comm": 0, "pdl": 1, "l2u": 1}
 
 
 @contextlib.contextmanager
@@ -112,14 +115,14 @@ def option(key, value):
 
 
 def set_option(key, value):
-    """Set a library knob on every live and future context (see ngd_set_option)."""
-    import weakref
-
+    """Set a library knob on every live and future context (see ngd_set_option).  A value the
+    library rejects raises (ValueError) and leaves the process-wide setting unchanged."""
+    live = [c for c in (r() for r in list(_contexts)) if c is not None and c._h is not None]
+    if live:
+        live[0].call("ngd_set_option", key.encode(), int(value))  # validates first
     OPTIONS[key] = int(value)
-    for ref in list(_contexts):
-        ctx = ref()
-        if ctx is not None and ctx._h is not None:
-            ctx.call("ngd_set_option", key.encode(), int(value))
+    for ctx in live[1:]:
+        ctx.call("ngd_set_option", key.encode(), int(value))
 
 
 def load():

@@ -3,8 +3,8 @@
     python -m paper_2505_11638_b200.build
 
 The library is a plain C-ABI shared object (include/ngd.h): CUDA kernels for
-sm_100a + cuBLAS/cuSOLVER for the small dense factorizations + NCCL for the
-multi-GPU all-reduce.  NCCL is linked against the torch-bundled libnccl.so.2
+sm_100a (every dense product on the in-house DMMA GEMM) + cuSOLVER's polar SVD
+for ell > 512 only + NCCL for the multi-GPU all-reduce.  NCCL is linked against the torch-bundled libnccl.so.2
 (same SONAME as the system copy) so one process never loads two NCCLs.
 """
 
@@ -76,7 +76,7 @@ def build(force=False, verbose=False, out=None, defines=()):
             print(out)
     nccl = _nccl_libdir()
     tmp = lib_path + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64", "-lcublas", "-lcusolver",
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64", "-lcusolver",
            f"-L{nccl}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nccl}:/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd))

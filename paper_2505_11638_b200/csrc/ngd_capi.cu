@@ -1,11 +1,12 @@
 // C-ABI of the B200 NystromNGD inner solve (include/ngd.h).
 //
-// Host orchestration of the CUDA kernels in ngd_jet.cu / ngd_vec.cu plus the
-// small dense factorizations (cuBLAS / cuSOLVER) of the Nystrom sketch and the
-// NCCL all-reduces of the point-sharded multi-GPU path.  Every entry point is
-// stream-ordered on the context's stream; only scalars the host policy needs
-// (loss values, PCG report, Cholesky status) are copied back.
-#include <cublas_v2.h>
+// Host orchestration of the CUDA kernels (ngd_jet.cu, ngd_phb2.cu, ngd_gemm.cu, ngd_chol.cu,
+// ngd_trsm.cu, ngd_svd.cu, ngd_vec.cu) and the NCCL all-reduces of the point-sharded multi-GPU
+// path.  Every dense product of the sketch and the factorisation runs on the in-house DMMA GEMM;
+// the only library compute call left is cuSOLVER's polar SVD for ell > 512 (C5's ell = 1000:
+// 0.4% of the step).  Every entry point is stream-ordered on the context's
+// stream; only scalars the host policy needs (loss values, PCG report, Cholesky status) are
+// copied back.
 #include <cusolverDn.h>
 #include <nccl.h>
 
@@ -46,13 +47,6 @@ int fail(int code, const char* fmt, ...) {
     cudaError_t e_ = (x);                                                                        \
     if (e_ != cudaSuccess) return fail(NGD_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
   } while (0)
-#define CKB(x)                                                                                   \
-  do {                                                                                           \
-    lib_probe_before(K_BLAS, c->stream);                                                         \
-    cublasStatus_t s_ = (x);                                                                     \
-    lib_probe_after(K_BLAS, c->stream);                                                          \
-    if (s_ != CUBLAS_STATUS_SUCCESS) return fail(NGD_E_CUDA, "%s:%d %s: cublas status %d", __FILE__, __LINE__, #x, (int)s_); \
-  } while (0)
 #define CKS(x)                                                                                   \
   do {                                                                                           \
     lib_probe_before(K_SOLVER, c->stream);                                                       \
@@ -72,6 +66,22 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 inline int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// NGD_DEBUG_SYNC=1: synchronise and check after the marked steps (locates an asynchronous fault)
+bool debug_sync() {
+  static const int on = [] {
+    const char* e = getenv("NGD_DEBUG_SYNC");
+    return e && *e == '1' ? 1 : 0;
+  }();
+  return on != 0;
+}
+#define DSYNC(tag)                                                                                  \
+  do {                                                                                              \
+    if (debug_sync()) {                                                                             \
+      cudaError_t e_ = cudaStreamSynchronize(c->stream);                                            \
+      if (e_ != cudaSuccess) return fail(NGD_E_CUDA, "after %s: %s", tag, cudaGetErrorString(e_));  \
+    }                                                                                               \
+  } while (0)
 
 // grow-only device buffer
 struct Buf {
@@ -114,9 +124,7 @@ struct PcgGraph {
 struct ngd_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cublasHandle_t blas = nullptr;
-  cusolverDnHandle_t sol = nullptr;
-  gesvdjInfo_t svdj = nullptr;
+  cusolverDnHandle_t sol = nullptr;  // polar SVD for ell > 512 only
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
 
@@ -133,8 +141,7 @@ struct ngd_ctx {
   // point data
   bool have_points = false;
   Geom gm{};
-  int G = 1, kps = 1;  // phase-B splits (G = max over layers)
-  int phb_cluster = 1;
+  int G = 1;  // phase-B splits (max over layers)
   int Gl[kMaxLayers] = {0}, kpsl[kMaxLayers] = {0};
   RedPlan rplan{};
   Buf w_pad, off_pad, w_c, F, cot_grad, cot, metric_tmp;
@@ -145,27 +152,11 @@ struct ngd_ctx {
   Buf dseed, pre_last, zs0, zs1;
   Buf jets;  // arena behind zin / dbuf / dseed
   int force_comm = 0;  // "force_comm": build a communicator (and take the multi-rank paths) even for 1 rank
-  int phb_cs = 0;  // option "phb_cs": 0 auto (DSMEM cluster reduction when G >= 16), 1 never
-  int phb_g = 0;   // option "phb_g": force the phase-B split count (tuning; 0 = plan)
-  int phb_plan = 2;  // option "phb_plan": 0 uniform splits (3 CTAs/SM), 1 work-weighted (6 stages),
-                     // 2 pipelined producer/consumer kernel (ngd_phb2.cu)
-  int phb_deep = 0;  // kernel chosen by the plan: 0/1 phb_all_kernel depth, 2 phb2_kernel
-  int phb_thin[kMaxLayers] = {};  // phb2: thin layers (N <= 16 or M <= 16)
-  Phb2Cache phb2_cache;           // phb2: tensor maps of this context's jets
-  Pha2Cache pha2_cache;
-  std::unique_ptr<Pha2Args> pha2_args{new Pha2Args()};
+  int phb_thin[kMaxLayers] = {};  // phase B: thin layers (N <= 16 or M <= 16)
+  Phb2Cache phb2_cache;           // phase B: tensor maps of this context's jets
   int l2u = 1;      // option "l2u": keep the preconditioner basis U L2-persisting during PCG
   Buf u_persist;     // PCG's copy of U at a fixed address (the captured graph carries its L2 window)
   size_t jets_arena = 0;
-  int pcg_fuse = 0;  // option "pcg_fuse": PCG update fused with the preconditioner's first pass (measured
-                    // slower at C2: 93 vs 84 us per iteration, tools/pcg_periter.py)
-  int pha_plan = 0;  // option "pha_plan": 0 one CTA per unit (ngd_jet.cu, default), 1 persistent TMA
-                     // pipeline (ngd_pha2.cu: measured slower, see its header)
-  int use_fused = 0;  // opt-in: measured slower than the two-phase path at C1/C2
-  bool fused_ok = false;
-  int fgrid = 0;
-  Buf partF;
-  RedPlan rplan_f{};
   int use_l2_window = 1;
   int l2_window_max = 0;
   bool l2_attr_set = false;
@@ -177,7 +168,12 @@ struct ngd_ctx {
   Buf pcgs;         // PcgState
   Buf pr, pz, pd, pad, ptmp;  // PCG vectors
   Buf ppart, pcprime;         // precond scratch
-  Buf jt, smat;               // sketch scratch
+  Buf jt, smat;               // sketch scratch: Jacobian-row chunk (ld = ldp), S = J_c V
+  Buf vpad, omp, yp;          // p x ell blocks at the padded leading dimension ldp (TMA: even ld)
+  Buf gwork, gscrA, gscrB;    // GEMM split-K partials; staging of operands TMA cannot address
+  Buf chol_t, chol_info;      // blocked Cholesky (n > 512): off-diagonal panel, per-level status
+  Buf chol_pad;               // Cholesky of an odd-ld matrix: even-ld copy
+  int64_t ldp = 0;            // rup(p, 16)
   Buf fj_tab;                 // FormJ device tables
   Buf nys_m, nys_tau, nys_r, nys_ur, nys_v, nys_s, nys_work, nys_info;
   Buf svd_mix;  // FP32-presweep Jacobi scratch: V0, V1, G, A2 (4 ell^2)
@@ -185,10 +181,6 @@ struct ngd_ctx {
   cusolverDnParams_t dn_params = nullptr;
   std::vector<char> h_work;
   int svd_method = 3;
-  int use_own_chol = 1;
-  int use_own_trsm = 1;
-  Buf rinv, tsq;  // explicit-inverse TRSM scratch
-  int use_syrk = 0;
   Buf trsm_work;
   Buf chol_work;
   int last_sweeps = 0;
@@ -366,33 +358,7 @@ static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double*
     tiles += c->mtiles[l] * (gm.nib + gm.nbb);
   }
   pa.tile_start[c->NL] = tiles;
-  if (c->pha_plan == 1 && pha2_supported(gm.C)) {
-    Pha2Args& a2 = *c->pha2_args;  // large (tensor maps): owned by the context, not on the stack
-    a2.n_layers = c->NL;
-    a2.nib = gm.nib;
-    a2.nbb = gm.nbb;
-    a2.n_pts_pad = gm.n_pts_pad();
-    a2.int_cols = gm.int_cols();
-    a2.s_pad = gm.s_pad;
-    a2.skip = skip;
-    const double* vps[kMaxLayers];
-    const double* zs[kMaxLayers];
-    int kps[kMaxLayers], mps[kMaxLayers];
-    for (int l = 0; l < c->NL; ++l) {
-      a2.D[l] = pa.L[l].Dk;
-      a2.vb[l] = pa.L[l].bias;
-      a2.partA[l] = pa.L[l].partA;
-      a2.M[l] = c->w[l + 1];
-      a2.mtiles[l] = c->mtiles[l];
-      vps[l] = c->vp[l].d();
-      zs[l] = c->zin[l].d();
-      kps[l] = c->Kp_f[l];
-      mps[l] = c->Mp_f[l];
-    }
-    CK(pha2_all_layers(a2, c->pha2_cache, vps, zs, kps, mps, gm.C, c->stream));
-  } else {
-    CK(pha_all(gm.C, pa, c->stream));
-  }
+  CK(pha_all(gm.C, pa, c->stream));
   reduce_pha(c->partA.d(), c->rows_A, gm.n_pts_pad(), w_or_null, cot_out, skip, c->stream);
   CK(cudaGetLastError());
   return NGD_OK;
@@ -426,7 +392,6 @@ static void fill_phb(ngd_ctx* c, const double* cot, const int* skip, PhbAll& pb)
     tiles += pb.tiles_n[l] * pb.tiles_m[l] * c->Gl[l];
   }
   pb.tile_start[c->NL] = tiles;
-  pb.cluster = c->phb_cluster;
   for (int l = 0; l < c->NL; ++l) pb.thin[l] = c->phb_thin[l];
 }
 
@@ -435,7 +400,7 @@ static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* m
                        const int* skip) {
   PhbAll pb{};
   fill_phb(c, cot, skip, pb);
-  CK(c->phb_deep == 2 ? phase_b2_all_layers(pb, c->phb2_cache, c->stream) : phase_b_all_layers(pb, c->phb_deep, c->stream));
+  CK(phase_b2_all_layers(pb, c->phb2_cache, c->stream));
   const bool shifted = v && (mu_p || mu != 0.0);
   if (c->comm) {
     reduce_splits(c->partB.d(), c->rplan, c->p, 0.0, nullptr, nullptr, out, skip, c->stream);
@@ -448,56 +413,7 @@ static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* m
   return NGD_OK;
 }
 
-// fused narrow-network matvec (ngd_fused.cu): one kernel writes per-CTA partials into partF
-static int fused_partials(ngd_ctx* c, const double* v, const int* skip) {
-  const Geom& gm = c->gm;
-  FusedArgs a{};
-  a.v = v;
-  int vt = 0;
-  for (int l = 0; l < c->NL; ++l) {
-    a.Z[l] = c->zin[l].d();
-    a.D[l] = (l == c->NL - 1) ? c->dseed.d() : c->dbuf[l].d();
-    a.n_in[l] = c->w[l];
-    a.n_out[l] = c->w[l + 1];
-    a.woff[l] = c->woff[l];
-    a.boff[l] = c->boff[l];
-    const int k4 = (int)rup(c->w[l], 4);
-    a.vs[l] = (k4 + 27) / 32 * 32 + 4;  // == 4 (mod 32): conflict-free DMMA A fragments
-    const int mr = (int)rup(c->w[l + 1], 8);
-    a.vso[l] = vt;
-    vt += mr * a.vs[l];
-    a.vbo[l] = vt;
-    vt += mr;
-  }
-  a.v_total = (vt + 1) & ~1;
-  a.n_layers = c->NL;
-  a.C = gm.C;
-  a.nib = gm.nib;
-  a.nbb = gm.nbb;
-  a.s_pad = gm.s_pad;
-  a.int_cols = gm.int_cols();
-  a.w = c->w_pad.d();
-  a.part = c->partF.d();
-  a.p = c->p;
-  a.skip = skip;
-  CK(fused_mv(a, c->fgrid, c->stream));
-  return NGD_OK;
-}
-
 static int gram_mv(ngd_ctx* c, const double* v, double mu, const double* mu_p, double* out, const int* skip) {
-  if (c->fused_ok) {
-    TRY(fused_partials(c, v, skip));
-    const bool shifted = v && (mu_p || mu != 0.0);
-    if (c->comm) {
-      reduce_splits(c->partF.d(), c->rplan_f, c->p, 0.0, nullptr, nullptr, out, skip, c->stream);
-      TRY(allreduce(c, out, c->p));
-      if (shifted) add_scaled(out, mu, mu_p, v, c->p, skip, c->stream);
-    } else {
-      reduce_splits(c->partF.d(), c->rplan_f, c->p, mu, mu_p, shifted ? v : nullptr, out, skip, c->stream);
-    }
-    CK(cudaGetLastError());
-    return NGD_OK;
-  }
   TRY(phase_a(c, v, c->w_pad.d(), c->cot.d(), skip));
   TRY(phase_b_all(c, c->cot.d(), mu, mu_p, v, out, skip));
   return NGD_OK;
@@ -509,96 +425,128 @@ static int need_lin(ngd_ctx* c) {
   return NGD_OK;
 }
 
-// Upper Cholesky of a small ell x ell matrix: in-house one-CTA kernel (ngd_chol.cu), cuSOLVER
-// potrf when it does not fit shared memory.  info follows LAPACK (0 ok, j+1 first bad pivot).
-static int potrf_upper(ngd_ctx* c, double* A, int n, int* info) {
-  if (c->use_own_chol == 1 && n <= 32) {  // one CTA: no cluster barriers for a single block
-    CK(chol_upper(A, n, n, info, c->stream));
+// ------------------------------ dense products ------------------------------
+// operand copy at an even leading dimension (TMA addresses 16-byte aligned rows only)
+static int stage_operand(ngd_ctx* c, GemmOperand& o, int MN, int K, Buf& scr) {
+  const int64_t inner = o.kmaj ? K : MN, outer = o.kmaj ? MN : K;
+  const int64_t ld = rup(inner, 2);
+  CK(scr.ensure(sizeof(double) * (size_t)(ld * outer)));
+  CK(cudaMemcpy2DAsync(scr.p, sizeof(double) * ld, o.p, sizeof(double) * o.ld, sizeof(double) * inner, outer,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  o.p = scr.d();
+  o.ld = ld;
+  return NGD_OK;
+}
+
+// C(M x N, ldc) = alpha A B [* row_scale] + beta C on the in-house DMMA GEMM (ngd_gemm.cu)
+static int gemm(ngd_ctx* c, int M, int N, int K, double alpha, GemmOperand A, GemmOperand B, double beta, double* C,
+                int64_t ldc, const double* row_scale = nullptr) {
+  if (M <= 0 || N <= 0) return NGD_OK;
+  if (!gemm_operand_ok(A, M, K)) TRY(stage_operand(c, A, M, K, c->gscrA));
+  if (!gemm_operand_ok(B, N, K)) TRY(stage_operand(c, B, N, K, c->gscrB));
+  const GemmPlan pl = gemm_plan(M, N, K);
+  CK(c->gwork.ensure(std::max<size_t>(pl.work_bytes, 64)));
+  CK(dgemm(M, N, K, alpha, A, B, beta, C, ldc, row_scale, c->gwork.d(), c->gwork.bytes, c->stream));
+  return NGD_OK;
+}
+static inline GemmOperand kmaj(const double* p, int64_t ld) { return GemmOperand{p, ld, true}; }
+static inline GemmOperand mnmaj(const double* p, int64_t ld) { return GemmOperand{p, ld, false}; }
+
+// B <- B R^{-1} (B p x n col-major (ldb), R n x n upper (ldr)): DMMA solve kernel (ngd_trsm.cu) for
+// n <= 512; above, blocked:  X1 = B1 R11^{-1},  B2 -= X1 R12 (GEMM),  X2 = B2 R22^{-1}
+static int trsm_right(ngd_ctx* c, double* B, int64_t ldb, int64_t p, const double* R, int ldr, int n) {
+  if (trsm_supported(n)) {
+    CK(c->trsm_work.ensure(trsm_work(n)));
+    CK(trsm_right_upper(B, ldb, p, R, ldr, n, c->trsm_work.d(), c->stream));
     return NGD_OK;
   }
-  if (c->use_own_chol && chol_cluster_supported(n)) {  // 8-CTA cluster, look-ahead
+  const int n1 = (int)rup((n + 1) / 2, 32), n2 = n - n1;
+  TRY(trsm_right(c, B, ldb, p, R, ldr, n1));
+  TRY(gemm(c, (int)p, n2, n1, -1.0, mnmaj(B, ldb), kmaj(R + (int64_t)n1 * ldr, ldr), 1.0, B + (int64_t)n1 * ldb,
+           ldb));
+  return trsm_right(c, B + (int64_t)n1 * ldb, ldb, p, R + (int64_t)n1 * ldr + n1, ldr, n2);
+}
+
+// Upper Cholesky A = U^T U in place (n x n column-major, lda; upper triangle read and written).
+// One CTA (n <= 32), 8-CTA cluster (n <= 512, ngd_chol.cu), else blocked:
+//   U11 = chol(A11);  U12 = U11^{-T} A12 (right solve on A12^T);  A22 -= U12^T U12 (GEMM);  U22 = chol(A22)
+// *info (device) follows LAPACK: 0, or the first failing pivot + 1.
+static int potrf_upper(ngd_ctx* c, double* A, int n, int lda, int* info, int depth = 0) {
+  if (n > 32 && ((lda & 1) || (reinterpret_cast<uintptr_t>(A) & 15u))) {
+    // the cluster kernel addresses columns as 16-byte aligned runs: factor an even-ld copy
+    const int ldp = n + (n & 1);
+    CK(c->chol_pad.ensure(sizeof(double) * (size_t)ldp * n));
+    CK(cudaMemcpy2DAsync(c->chol_pad.p, sizeof(double) * ldp, A, sizeof(double) * lda, sizeof(double) * n, n,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    TRY(potrf_upper(c, c->chol_pad.d(), n, ldp, info, depth));
+    CK(cudaMemcpy2DAsync(A, sizeof(double) * lda, c->chol_pad.p, sizeof(double) * ldp, sizeof(double) * n, n,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    return NGD_OK;
+  }
+  if (n <= 32) {
+    CK(chol_upper(A, n, lda, info, c->stream));
+    return NGD_OK;
+  }
+  if (chol_cluster_supported(n)) {
     CK(c->chol_work.ensure(sizeof(int) * 4));
-    CK(chol_upper_cluster(A, n, n, info, static_cast<int*>(c->chol_work.p), c->stream));
+    CK(chol_upper_cluster(A, n, lda, info, static_cast<int*>(c->chol_work.p), c->stream));
     return NGD_OK;
   }
-  int lw = 0;
-  CKS(cusolverDnDpotrf_bufferSize(c->sol, CUBLAS_FILL_MODE_UPPER, n, A, n, &lw));
-  CK(c->chol_work.ensure(sizeof(double) * std::max(lw, 1)));
-  CKS(cusolverDnDpotrf(c->sol, CUBLAS_FILL_MODE_UPPER, n, A, n, c->chol_work.d(), lw, info));
+  if (depth >= 8) return fail(NGD_E_SHAPE, "Cholesky of order %d too large", n);
+  const int n1 = (int)rup((n + 1) / 2, 32), n2 = n - n1;
+  CK(c->chol_info.ensure(sizeof(int) * 16));
+  int* info2 = static_cast<int*>(c->chol_info.p) + depth;
+  CK(cudaMemsetAsync(info2, 0, sizeof(int), c->stream));
+  TRY(potrf_upper(c, A, n1, lda, info, depth + 1));
+  DSYNC("blocked potrf: diagonal block 1");
+  double* A12 = A + (int64_t)n1 * lda;
+  CK(c->chol_t.ensure(sizeof(double) * (size_t)n1 * n2));
+  double* T = c->chol_t.d();  // A12^T (n2 x n1)
+  transpose(A12, lda, n1, n2, T, n2, c->stream);
+  DSYNC("blocked potrf: transpose");
+  TRY(trsm_right(c, T, n2, n2, A, lda, n1));  // T U11 = A12^T  ->  T = U12^T
+  DSYNC("blocked potrf: trsm");
+  transpose(T, n2, n2, n1, A12, lda, c->stream);
+  TRY(gemm(c, n2, n2, n1, -1.0, kmaj(A12, lda), kmaj(A12, lda), 1.0, A12 + n1, lda));
+  DSYNC("blocked potrf: gemm");
+  TRY(potrf_upper(c, A12 + n1, n2, lda, info2, depth + 1));
+  DSYNC("blocked potrf: diagonal block 2");
+  info_combine(info, info2, n1, c->stream);
   return NGD_OK;
 }
 
-// W = A^T A for a tall p x ell column-major A (upper triangle used).  cuBLAS DSYRK picks a
-// 32x32-tile kernel with little parallelism for these shapes (~7 TF/s at 8577 x 300);
-// the full DGEMM (2x the FLOPs, split over more CTAs) is faster ("syrk" option = 1 keeps DSYRK).
-static int gram_tall(ngd_ctx* c, const double* A, int64_t p, int ell, double* W) {
-  const double one = 1.0, zero = 0.0;
-  if (c->use_syrk) {
-    CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, ell, (int)p, &one, A, (int)p, &zero, W, ell));
-  } else {
-    CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, (int)p, &one, A, (int)p, A, (int)p, &zero, W, ell));
-  }
-  return NGD_OK;
-}
-
-// B <- B R^{-1} (B p x ell col-major, R ell x ell upper, lda ell): own DMMA kernel, cuBLAS beyond ell = 512
-static int trsm_right(ngd_ctx* c, double* B, int64_t p, const double* R, int ell) {
-  if (c->use_own_trsm == 2 && trsm_supported(ell)) {
-    // explicit inverse: Rinv by the DMMA solve on the identity (ell x ell), then B <- B Rinv as one
-    // cuBLAS DGEMM into scratch (the triangle's zeros multiply through; the GEMM runs near peak)
-    CK(c->trsm_work.ensure(trsm_work(ell)));
-    CK(c->rinv.ensure(sizeof(double) * (size_t)ell * ell));
-    CK(c->tsq.ensure(sizeof(double) * (size_t)p * ell));
-    set_identity(c->rinv.d(), ell, c->stream);
-    CK(trsm_right_upper(c->rinv.d(), ell, ell, R, ell, ell, c->trsm_work.d(), c->stream));
-    const double one = 1.0, zero = 0.0;
-    CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)p, ell, ell, &one, B, (int)p, c->rinv.d(), ell, &zero,
-                    c->tsq.d(), (int)p));
-    CK(cudaMemcpyAsync(B, c->tsq.d(), sizeof(double) * (size_t)p * ell, cudaMemcpyDeviceToDevice, c->stream));
-    return NGD_OK;
-  }
-  if (c->use_own_trsm && trsm_supported(ell)) {
-    CK(c->trsm_work.ensure(trsm_work(ell)));
-    CK(trsm_right_upper(B, p, p, R, ell, ell, c->trsm_work.d(), c->stream));
-    return NGD_OK;
-  }
-  const double one = 1.0;
-  CKB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)p, ell,
-                  &one, R, ell, B, (int)p));
-  return NGD_OK;
+// W = A^T A for a tall p x ell column-major A (lda)
+static int gram_tall(ngd_ctx* c, const double* A, int64_t lda, int64_t p, int ell, double* W) {
+  return gemm(c, ell, ell, (int)p, 1.0, kmaj(A, lda), kmaj(A, lda), 0.0, W, ell);
 }
 
 // Shifted Cholesky-QR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020) in place:
-// B (p x ell, col-major) <- Q, nys_r <- R (upper, ell x ell, col-major).
-static int scholqr3(ngd_ctx* c, double* B, int64_t p, int ell) {
-  const double one = 1.0, zero = 0.0;
-  int lw = 0;
-  CKS(cusolverDnDpotrf_bufferSize(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, &lw));
-  CK(c->nys_work.ensure(sizeof(double) * std::max<size_t>(lw, (size_t)ell * ell)));
+// B (p x ell, ldb) <- Q, nys_r <- R (upper, ell x ell).  info[4..6]: the three Cholesky statuses.
+static int scholqr3(ngd_ctx* c, double* B, int64_t ldb, int64_t p, int ell) {
   CK(c->nys_v.ensure(sizeof(double) * (size_t)ell * ell));
-  int* info = static_cast<int*>(c->nys_info.p);
+  int* info = static_cast<int*>(c->nys_info.p) + 4;
   const double shift_coef = 11.0 * ((double)p * ell + (double)ell * (ell + 1)) * 2.220446049250313e-16;
   for (int pass = 0; pass < 3; ++pass) {
     double* W = c->nys_m.d();
-    TRY(gram_tall(c, B, p, ell, W));
+    TRY(gram_tall(c, B, ldb, p, ell, W));
     if (pass == 0) shift_diag(W, ell, shift_coef, c->stream);
-    TRY(potrf_upper(c, W, ell, info));
+    TRY(potrf_upper(c, W, ell, ell, info + pass));
     triu(W, ell, ell, c->stream);
-    TRY(trsm_right(c, B, p, W, ell));
+    TRY(trsm_right(c, B, ldb, p, W, ell, ell));
     if (pass == 0) {
       CK(cudaMemcpyAsync(c->nys_r.d(), W, sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
     } else {
-      // R <- R_pass * R  (both upper triangular)
-      CKB(cublasDtrmm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ell, ell,
-                      &one, W, ell, c->nys_r.d(), ell, c->nys_v.d(), ell));
+      // R <- R_pass R  (both upper triangular; the zero triangles multiply through exactly)
+      TRY(gemm(c, ell, ell, ell, 1.0, mnmaj(W, ell), kmaj(c->nys_r.d(), ell), 0.0, c->nys_v.d(), ell));
       CK(cudaMemcpyAsync(c->nys_r.d(), c->nys_v.d(), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
     }
   }
   return NGD_OK;
 }
 
-// SVD of the ell x ell matrix in nys_r: singular values -> nys_s (descending), U -> nys_ur.
-static int small_svd_polar(ngd_ctx* c, int ell) {
+// SVD of the ell x ell matrix in nys_r by cuSOLVER's polar SVD (ell > 512): singular values -> nys_s
+// (descending), U -> nys_ur.  info[2] <- its status (0 ok), h_err <- its residual estimate.
+static int small_svd_polar(ngd_ctx* c, int ell, double* h_err) {
   if (!c->dn_params) CKS(cusolverDnCreateParams(&c->dn_params));
   size_t wd = 0, wh = 0;
   CKS(cusolverDnXgesvdp_bufferSize(c->sol, c->dn_params, CUSOLVER_EIG_MODE_VECTOR, 1, ell, ell, CUDA_R_64F,
@@ -609,7 +557,9 @@ static int small_svd_polar(ngd_ctx* c, int ell) {
   double err = 0.0;
   CKS(cusolverDnXgesvdp(c->sol, c->dn_params, CUSOLVER_EIG_MODE_VECTOR, 1, ell, ell, CUDA_R_64F, c->nys_r.d(), ell,
                         CUDA_R_64F, c->nys_s.d(), CUDA_R_64F, c->nys_ur.d(), ell, CUDA_R_64F, c->nys_v.d(), ell,
-                        CUDA_R_64F, c->nys_work.p, wd, c->h_work.data(), wh, static_cast<int*>(c->nys_info.p), &err));
+                        CUDA_R_64F, c->nys_work.p, wd, c->h_work.data(), wh, static_cast<int*>(c->nys_info.p) + 2,
+                        &err));
+  if (h_err) *h_err = err;
   return NGD_OK;
 }
 
@@ -621,7 +571,6 @@ static int small_svd_polar(ngd_ctx* c, int ell) {
 // sim).  Backward stable like the reference's LAPACK SVD: the product R^T V0 carries absolute
 // errors ~eps ||R||, the level Cholesky-QR already leaves in R.
 static int small_svd_mixed(ngd_ctx* c, int ell) {
-  const double one = 1.0, zero = 0.0, mhalf = -0.5, three_half = 1.5;
   const int ld = ell + (ell & 1);  // even: V0 may be the FP64 phase's in-place V (vector columns)
   const size_t l2 = (size_t)ld * ell;
   CK(c->svd_mix.ensure(sizeof(double) * 4 * l2));
@@ -638,13 +587,13 @@ static int small_svd_mixed(ngd_ctx* c, int ell) {
   if (ld != ell) CK(cudaMemsetAsync(V0, 0, sizeof(double) * 2 * l2, c->stream));  // padding rows
   CK(jacobi_presweep_f32(c->nys_r.d(), ell, ell, V0, ld, coupling, info + 3, c->stream));
   for (int it = 0; it < 2; ++it) {  // two Newton-Schulz steps: V0 <- V0 (3 I - V0^T V0) / 2
-    CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, ell, &one, V0, ld, V0, ld, &zero, G, ell));
+    TRY(gemm(c, ell, ell, ell, 1.0, kmaj(V0, ld), kmaj(V0, ld), 0.0, G, ell));
     CK(cudaMemcpyAsync(V1, V0, sizeof(double) * l2, cudaMemcpyDeviceToDevice, c->stream));
-    CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, ell, ell, ell, &mhalf, V0, ld, G, ell, &three_half, V1, ld));
+    TRY(gemm(c, ell, ell, ell, -0.5, mnmaj(V0, ld), kmaj(G, ell), 1.5, V1, ld));
     std::swap(V0, V1);
   }
   // X = R^T V0 enters the kernel as A2^T, A2 = V0^T R
-  CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, ell, &one, V0, ld, c->nys_r.d(), ell, &zero, A2, ell));
+  TRY(gemm(c, ell, ell, ell, 1.0, kmaj(V0, ld), kmaj(c->nys_r.d(), ell), 0.0, A2, ell));
   CK(jacobi_svd_block_from(A2, ell, ell, V0, ld, c->nys_ur.d(), ell, c->nys_s.d(), info + 2, c->stream));
   return NGD_OK;
 }
@@ -652,14 +601,15 @@ static int small_svd_mixed(ngd_ctx* c, int ell) {
 // L2 persisting window over the jets arena (B200: 79 MB persisting capacity, 128 MB max window)
 static int set_l2_window(ngd_ctx* c, void* base, size_t bytes) {
   if (!c->use_l2_window) return NGD_OK;
-  static int persist_max = -1;
+  static int persist_max = -1, window_max = 0;  // device properties (one device type per process)
   if (persist_max < 0) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, c->device));
     persist_max = prop.persistingL2CacheMaxSize;
+    window_max = prop.accessPolicyMaxWindowSize;
     if (persist_max > 0) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_max));
-    c->l2_window_max = prop.accessPolicyMaxWindowSize;
   }
+  c->l2_window_max = window_max;
   if (persist_max <= 0) return NGD_OK;
   cudaStreamAttrValue attr{};
   const size_t win = std::min(bytes, (size_t)std::max(c->l2_window_max, 1));
@@ -722,6 +672,7 @@ int ngd_ctx_create(const int32_t* widths, int32_t n_widths, int32_t device, ngd_
     }
   }
   c->p = off;
+  c->ldp = rup(off, 16);
   c->apf.resize(c->NL);
   c->apr.resize(c->NL);
   c->vp.resize(c->NL);
@@ -752,16 +703,12 @@ int ngd_ctx_create(const int32_t* widths, int32_t n_widths, int32_t device, ngd_
     for (auto& e : c->poll_ev)
       if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) rc = fail(NGD_E_CUDA, "event failed");
   }
-  if (rc == NGD_OK && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) rc = fail(NGD_E_CUDA, "cublasCreate failed");
   if (rc == NGD_OK && cusolverDnCreate(&c->sol) != CUSOLVER_STATUS_SUCCESS)
     rc = fail(NGD_E_CUDA, "cusolverDnCreate failed");
-  if (rc == NGD_OK && cusolverDnCreateGesvdjInfo(&c->svdj) != CUSOLVER_STATUS_SUCCESS)
-    rc = fail(NGD_E_CUDA, "gesvdj info failed");
   if (rc != NGD_OK) {
     ngd_ctx_destroy(c);
     return rc;
   }
-  cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH);
   *out = c;
   return NGD_OK;
 }
@@ -776,7 +723,8 @@ int ngd_ctx_destroy(ngd_ctx* c) {
   for (Buf* b : {&c->w_pad, &c->off_pad, &c->w_c, &c->F, &c->cot_grad, &c->cot, &c->metric_tmp, &c->dseed,
                  &c->pre_last, &c->zs0, &c->zs1, &c->partA, &c->partB, &c->redp, &c->counters, &c->scal, &c->pcgs,
                  &c->pr, &c->pz, &c->pd, &c->pad, &c->ptmp, &c->ppart, &c->pcprime, &c->jt, &c->smat, &c->fj_tab,
-                 &c->nys_m, &c->nys_tau, &c->nys_r, &c->nys_ur, &c->nys_v, &c->nys_s, &c->nys_work, &c->nys_info, &c->svd_mix})
+                 &c->nys_m, &c->nys_tau, &c->nys_r, &c->nys_ur, &c->nys_v, &c->nys_s, &c->nys_work, &c->nys_info, &c->svd_mix,
+                 &c->vpad, &c->omp, &c->yp, &c->gwork, &c->gscrA, &c->gscrB, &c->chol_t, &c->chol_info, &c->chol_pad})
     b->release();
   if (c->h_pin) cudaFreeHost(c->h_pin);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -785,12 +733,10 @@ int ngd_ctx_destroy(ngd_ctx* c) {
   for (auto& e : c->poll_ev)
     if (e) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->rinv, &c->tsq, &c->jets, &c->partF, &c->wr_pad, &c->R_pad, &c->alpha_bar, &c->u_persist})
+  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->jets, &c->wr_pad, &c->R_pad, &c->alpha_bar, &c->u_persist})
     b->release();
-  if (c->svdj) cusolverDnDestroyGesvdjInfo(c->svdj);
   if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
   if (c->sol) cusolverDnDestroy(c->sol);
-  if (c->blas) cublasDestroy(c->blas);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
   return NGD_OK;
@@ -799,7 +745,6 @@ int ngd_ctx_destroy(ngd_ctx* c) {
 int ngd_ctx_set_stream(ngd_ctx* c, void* stream) {
   TRY(bind(c));
   c->stream = static_cast<cudaStream_t>(stream);
-  CKB(cublasSetStream(c->blas, c->stream));
   CKS(cusolverDnSetStream(c->sol, c->stream));
   if (c->l2_attr_set && c->stream &&
       cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &c->l2_attr) != cudaSuccess)
@@ -915,120 +860,33 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
   CK(cudaGetLastError());
   // phase-A partial rows and phase-B split plan
   CK(c->partA.ensure(sizeof(double) * (size_t)c->rows_A * npp));
-  // phase-B split plan: every (layer, tile) gets the same number G of K splits (a tile costs the
-  // same per k-tile whatever its fill).  G is the largest that keeps the whole launch in ONE
-  // wave of 3 CTAs/SM (no tail wave); when G >= 64 the splits are grouped into clusters of 8
-  // whose partial tiles are reduced through DSMEM (G/8 partials per parameter).
+  // phase-B plan (ngd_phb2.cu), one CTA per SM: heavy tiles (both sides > 16) share 148 K-split
+  // items, thin tiles (input layer N = d, output layer M = 1) another 148; CTA i streams heavy item
+  // i and thin item i interleaved.
   {
     const int kt = (int)(gm.s_pad / 16);
-    int tiles = 0;
-    for (int l = 0; l < c->NL; ++l) tiles += ((c->w[l] + 63) / 64) * ((c->w[l + 1] + 63) / 64);
-    const int slots = 3 * 148;
-    int G = std::max(1, slots / tiles);
-    G = std::min(G, std::max(1, kt / 8));
-    // DSMEM cluster reduction of the split partials pays only when there are many of them (C2:
-    // G = 104 -> 13 partials; measured PCG 3.9 -> 2.9 ms); at G ~ 32 (C3) the cluster
-    // co-scheduling costs more than reading 37 partials (PCG 104.8 -> 98.6 ms without clusters)
-    if (c->phb_g > 0) G = c->phb_g;
-    int CS = 1;
-    if (G >= 64 && c->phb_cs != 1) {
-      // whole clusters of 8 in one wave: clusters are placed per GPC, so fewer than slots / 8 fit
-      // (C2: 48 co-resident clusters; G = 104 gave 52 clusters and a 4-cluster tail wave)
-      static int max_clusters = -1;
-      if (max_clusters < 0) max_clusters = phb_max_active_clusters(8);
-      const int gc = max_clusters > 0 ? std::max(8, max_clusters / tiles * 8) : G / 8 * 8;
-      G = std::min(G / 8 * 8, gc);
-      CS = 8;
+    int heavy = 0, thin = 0;
+    for (int l = 0; l < c->NL; ++l) {
+      const int M = c->w[l + 1], N = c->w[l];
+      c->phb_thin[l] = (M <= 16 || N <= 16) ? 1 : 0;
+      (c->phb_thin[l] ? thin : heavy) += ((M + 63) / 64) * ((N + 63) / 64);
     }
-    const int kps = (kt + G - 1) / G;
-    c->G = G;
-    c->kps = kps;
-    c->phb_cluster = CS;
-    c->phb_deep = 0;
+    const int gh = heavy ? std::max(1, std::min(kt, 148 / heavy)) : 1;
+    const int gt = thin ? std::max(1, std::min(kt, 148 / thin)) : 1;
+    int maxg = 0;
     c->rplan.n_layers = c->NL;
     for (int l = 0; l < c->NL; ++l) {
-      c->Gl[l] = G;
-      c->kpsl[l] = kps;
+      const int Gl = c->phb_thin[l] ? gt : gh;
+      c->Gl[l] = Gl;
+      c->kpsl[l] = (kt + Gl - 1) / Gl;
       c->rplan.start[l] = c->woff[l];
-      c->rplan.G[l] = G / CS;  // one partial per cluster
+      c->rplan.G[l] = Gl;
+      maxg = std::max(maxg, Gl);
     }
     c->rplan.start[c->NL] = c->p;
-    if (c->phb_plan == 1 && c->phb_g == 0) {
-      // Work-weighted plan: one wave of CTAs with a 6-stage pipeline, per-layer split counts in
-      // proportion to each tile's DMMA work (a 64 x 64 tile whose rows or columns are mostly
-      // padding -- the input layer's N = d, the output layer's M = 1 -- runs only its active
-      // 16 x 32 warp tiles), so every CTA streams the same amount of tensor-core work.
-      const int slots = phb_ctas_per_sm(1) * 148;
-      double cost[kMaxLayers], total = 0.0;
-      int nt[kMaxLayers];
-      for (int l = 0; l < c->NL; ++l) {
-        const int M = c->w[l + 1], N = c->w[l];
-        const int tm = (M + 63) / 64, tn = (N + 63) / 64;
-        nt[l] = tm * tn;
-        double cl = 0.0;
-        for (int bm = 0; bm < tm; ++bm)
-          for (int bn = 0; bn < tn; ++bn) {
-            int act = 0;
-            for (int wm = 0; wm < 4; ++wm)
-              for (int wn = 0; wn < 2; ++wn) act += (bm * 64 + wm * 16 < M && bn * 64 + wn * 32 < N) ? 1 : 0;
-            cl += act / 8.0;
-          }
-        cost[l] = cl;
-        total += cl;
-      }
-      int Gl[kMaxLayers], used = 0;
-      for (int l = 0; l < c->NL; ++l) {
-        Gl[l] = std::max(1, std::min(kt, (int)(slots * cost[l] / total / nt[l])));
-        used += Gl[l] * nt[l];
-      }
-      int maxg = 0;
-      for (int l = 0; l < c->NL; ++l) {
-        c->Gl[l] = Gl[l];
-        c->kpsl[l] = (kt + Gl[l] - 1) / Gl[l];
-        c->rplan.G[l] = Gl[l];
-        maxg = std::max(maxg, Gl[l]);
-      }
-      (void)used;
-      c->G = maxg;
-      c->kps = c->kpsl[0];
-      c->phb_cluster = 1;
-      c->phb_deep = 1;
-    }
-    if (c->phb_plan == 2 && c->phb_g == 0) {
-      // Pipelined kernel (ngd_phb2.cu), one CTA per SM: heavy tiles (both sides > 16) share 148
-      // K-split items, thin tiles (input layer N = d, output layer M = 1) another 148; CTA i
-      // streams heavy item i and thin item i interleaved.
-      int heavy = 0, thin = 0;
-      for (int l = 0; l < c->NL; ++l) {
-        const int M = c->w[l + 1], N = c->w[l];
-        c->phb_thin[l] = (M <= 16 || N <= 16) ? 1 : 0;
-        (c->phb_thin[l] ? thin : heavy) += ((M + 63) / 64) * ((N + 63) / 64);
-      }
-      const int gh = heavy ? std::max(1, std::min(kt, 148 / heavy)) : 1;
-      const int gt = thin ? std::max(1, std::min(kt, 148 / thin)) : 1;
-      int maxg = 0;
-      for (int l = 0; l < c->NL; ++l) {
-        const int Gl = c->phb_thin[l] ? gt : gh;
-        c->Gl[l] = Gl;
-        c->kpsl[l] = (kt + Gl - 1) / Gl;
-        c->rplan.G[l] = Gl;
-        maxg = std::max(maxg, Gl);
-      }
-      c->G = maxg;
-      c->kps = c->kpsl[0];
-      c->phb_cluster = 1;
-      c->phb_deep = 2;
-    }
+    c->G = maxg;
   }
-  CK(c->partB.ensure(sizeof(double) * (size_t)(c->G / c->phb_cluster) * c->p));
-  // fused narrow-network matvec: persistent CTAs over point blocks, one partial each
-  c->fused_ok = c->use_fused && fused_supported(c->w.data(), c->NL, gm.C);
-  if (c->fused_ok) {
-    c->fgrid = std::min(gm.nib + gm.nbb, 148);
-    CK(c->partF.ensure(sizeof(double) * (size_t)c->fgrid * c->p));
-    c->rplan_f = c->rplan;
-    for (int l = 0; l < c->NL; ++l) c->rplan_f.G[l] = c->fgrid;
-  }
+  CK(c->partB.ensure(sizeof(double) * (size_t)c->G * c->p));
   c->have_points = true;
   c->lin_valid = false;
   c->graph_gen++;
@@ -1161,10 +1019,9 @@ int ngd_gram_matvec(ngd_ctx* c, const double* v, double mu, double* out) {
   return gram_mv(c, v, mu, nullptr, out, nullptr);
 }
 
-// Y = G V by the J-chunk formulation: per point chunk, explicit Jacobian rows
-// Jt (R x p), S = Jt V, Y += Jt^T (w o S)  -- two DGEMMs on FP64 tensor cores.
 // explicit Jacobian rows (FormJ) setup shared by the J-chunk sketch and the dense Gramian:
-// chunks of whole point blocks in padded point order (padded points have w = 0)
+// chunks of whole point blocks in padded point order (padded points have w = 0); rows at the
+// padded leading dimension ldp (the DMMA GEMM reads them with TMA: 16-byte aligned rows)
 struct FormJPlan {
   FormJArgs fa;
   int nblk_total, bpc, max_nin, max_nout;
@@ -1175,9 +1032,13 @@ static int formj_plan(ngd_ctx* c, FormJPlan& pl) {
   const Geom& gm = c->gm;
   const int nblk_total = gm.nib + gm.nbb;
   const size_t budget = (size_t)8 << 30;  // bytes for one Jacobian chunk
-  const int bpc = (int)std::max<int64_t>(1, std::min<int64_t>(nblk_total, (int64_t)(budget / (sizeof(double) * c->p * PB))));
+  const int bpc = (int)std::max<int64_t>(1, std::min<int64_t>(nblk_total, (int64_t)(budget / (sizeof(double) * c->ldp * PB))));
   const int64_t R = (int64_t)bpc * PB;
-  CK(c->jt.ensure(sizeof(double) * (size_t)R * c->p));
+  const size_t jbytes = sizeof(double) * (size_t)R * c->ldp;
+  if (c->jt.bytes < jbytes) {
+    CK(c->jt.ensure(jbytes));
+    CK(cudaMemsetAsync(c->jt.p, 0, jbytes, c->stream));  // the row padding [p, ldp) stays zero
+  }
   const int NL = c->NL;
   const size_t tab_bytes = NL * (2 * sizeof(double*) + 2 * sizeof(int) + sizeof(int64_t)) + 64;
   CK(c->fj_tab.ensure(tab_bytes));
@@ -1209,7 +1070,7 @@ static int formj_plan(ngd_ctx* c, FormJPlan& pl) {
   fa.nib = gm.nib;
   fa.n_int = gm.n_int;
   fa.Jt = c->jt.d();
-  fa.ldj = c->p;
+  fa.ldj = c->ldp;
   int max_nin = 1, max_nout = 1;
   for (int l = 0; l < NL; ++l) {
     max_nin = std::max(max_nin, c->w[l]);
@@ -1224,25 +1085,24 @@ static int formj_plan(ngd_ctx* c, FormJPlan& pl) {
   return NGD_OK;
 }
 
-// G = J^T diag(w) J assembled densely: per chunk, Jacobian rows scaled by sqrt(w), one DSYRK
-// (gramian.py:138-145 assembles column by column; the spectrum dump of harness.py:237-266 uses it)
+// G = J^T diag(w) J assembled densely: per chunk, Jacobian rows scaled by sqrt(w), then
+// G += J_c^T J_c on the DMMA GEMM (gramian.py:138-145 assembles column by column; the spectrum
+// dump of harness.py:237-266 uses it)
 int ngd_gram_dense(ngd_ctx* c, double* G, int64_t ldg) {
   TRY(bind(c));
   TRY(need_lin(c));
   if (ldg < c->p) return fail(NGD_E_SHAPE, "ldg < p");
   FormJPlan pl;
   TRY(formj_plan(c, pl));
-  const double one = 1.0;
+  const int p = (int)c->p;
   for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
     const int nb = std::min(pl.bpc, pl.nblk_total - b0);
     const int64_t r = (int64_t)nb * PB;
     const int64_t q0 = (int64_t)b0 * PB;
     pl.fa.blk0 = b0;
     CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));
-    scale_cols_sqrt(c->jt.d(), c->p, r, c->w_pad.d() + q0, c->stream);
-    const double beta = (q0 == 0) ? 0.0 : 1.0;
-    CKB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, (int)c->p, (int)r, &one, c->jt.d(), (int)c->p,
-                    &beta, G, (int)ldg));
+    scale_cols_sqrt(c->jt.d(), c->ldp, r, c->w_pad.d() + q0, c->stream);
+    TRY(gemm(c, p, p, (int)r, 1.0, mnmaj(c->jt.d(), c->ldp), mnmaj(c->jt.d(), c->ldp), q0 == 0 ? 0.0 : 1.0, G, ldg));
   }
   symmetrize_upper(G, c->p, ldg, c->stream);
   if (c->comm) {
@@ -1253,6 +1113,9 @@ int ngd_gram_dense(ngd_ctx* c, double* G, int64_t ldg) {
   return NGD_OK;
 }
 
+// Y = G V by the J-chunk formulation (gramian.py:55-61 as ell matvecs): per point
+// chunk, explicit Jacobian rows J_c (formj_kernel), then on the DMMA GEMM
+//   S = J_c V  (w folded into the epilogue)   and   Y += J_c^T S.
 int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, double* Y, int64_t ldy) {
   TRY(bind(c));
   TRY(need_lin(c));
@@ -1260,22 +1123,22 @@ int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, doubl
   FormJPlan pl;
   TRY(formj_plan(c, pl));
   CK(c->smat.ensure(sizeof(double) * (size_t)pl.R * ell));
-  FormJArgs& fa = pl.fa;
-  const int nblk_total = pl.nblk_total, bpc = pl.bpc, max_nin = pl.max_nin, max_nout = pl.max_nout, NL = c->NL;
-  const double one = 1.0, zero = 0.0;
-  for (int b0 = 0; b0 < nblk_total; b0 += bpc) {
-    const int nb = std::min(bpc, nblk_total - b0);
-    const int64_t r = (int64_t)nb * PB;
+  const int p = (int)c->p;
+  GemmOperand vop = kmaj(V, ldv);
+  if (!gemm_operand_ok(vop, (int)ell, p)) {  // caller's odd leading dimension: one padded copy per call
+    CK(c->vpad.ensure(sizeof(double) * (size_t)c->ldp * ell));
+    CK(cudaMemcpy2DAsync(c->vpad.p, sizeof(double) * c->ldp, V, sizeof(double) * ldv, sizeof(double) * p, ell,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    vop = kmaj(c->vpad.d(), c->ldp);
+  }
+  for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
+    const int nb = std::min(pl.bpc, pl.nblk_total - b0);
+    const int r = nb * PB;
     const int64_t q0 = (int64_t)b0 * PB;
-    fa.blk0 = b0;
-    CK(form_j(fa, nb, NL, max_nin, max_nout, c->stream));
-    // S (r x ell) = Jt_chunk (r x p) * V  -> col-major: S = Jt^T(p x r)^T V
-    CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)r, (int)ell, (int)c->p, &one, c->jt.d(), (int)c->p, V,
-                    (int)ldv, &zero, c->smat.d(), (int)r));
-    scale_rows(c->smat.d(), r, (int)ell, c->w_pad.d() + q0, c->stream);
-    const double beta = (q0 == 0) ? 0.0 : 1.0;
-    CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)c->p, (int)ell, (int)r, &one, c->jt.d(), (int)c->p,
-                    c->smat.d(), (int)r, &beta, Y, (int)ldy));
+    pl.fa.blk0 = b0;
+    CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));
+    TRY(gemm(c, r, (int)ell, p, 1.0, kmaj(c->jt.d(), c->ldp), vop, 0.0, c->smat.d(), r, c->w_pad.d() + q0));
+    TRY(gemm(c, p, (int)ell, r, 1.0, mnmaj(c->jt.d(), c->ldp), kmaj(c->smat.d(), r), q0 == 0 ? 0.0 : 1.0, Y, ldy));
   }
   if (c->comm) {
     if (ldy != c->p) return fail(NGD_E_SHAPE, "multi-rank matmat needs ldy == p");
@@ -1292,129 +1155,109 @@ int ngd_fill_gaussian(ngd_ctx* c, uint64_t seed, double* out, int64_t n) {
   return NGD_OK;
 }
 
-// Cholesky-QR2 of Omega in place: Omega <- Omega R^{-1}, twice.  Gives the same
+// p x ell column-major block (ld p) <-> the context's copy at the padded leading dimension
+static int to_padded(ngd_ctx* c, Buf& dst, const double* src, int64_t p, int ell) {
+  const int64_t ld = rup(p, 16);
+  CK(dst.ensure(sizeof(double) * (size_t)ld * ell));
+  CK(cudaMemcpy2DAsync(dst.p, sizeof(double) * ld, src, sizeof(double) * p, sizeof(double) * p, ell,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  return NGD_OK;
+}
+static int from_padded(ngd_ctx* c, double* dst, const Buf& src, int64_t p, int ell) {
+  const int64_t ld = rup(p, 16);
+  CK(cudaMemcpy2DAsync(dst, sizeof(double) * p, src.p, sizeof(double) * ld, sizeof(double) * p, ell,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  return NGD_OK;
+}
+
+// Cholesky-QR of Omega in place: Omega <- Omega R^{-1} (once for p >= 4 ell, else twice).  Same
 // orthonormal basis as the reference's Householder QR (sketch.py:75) up to column signs.
 int ngd_nystrom_prepare(ngd_ctx* c, double* omega, int64_t p, int32_t ell) {
   TRY(bind(c));
   if (ell < 1 || ell > p) return fail(NGD_E_SHAPE, "rank must be in [1, %lld], got %d", (long long)p, ell);
   CK(c->nys_m.ensure(sizeof(double) * (size_t)ell * ell));
-  CK(c->nys_info.ensure(sizeof(int) * 4));
-  int lwork = 0;
-  CKS(cusolverDnDpotrf_bufferSize(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, &lwork));
-  CK(c->nys_work.ensure(sizeof(double) * std::max(lwork, 1)));
-  const double one = 1.0, zero = 0.0;
+  CK(c->nys_info.ensure(sizeof(int) * 8));
+  CK(cudaMemsetAsync(c->nys_info.p, 0, sizeof(int) * 8, c->stream));
+  const int64_t ld = rup(p, 16);
+  TRY(to_padded(c, c->omp, omega, p, ell));
   // A Gaussian p x ell block with p >= 4 ell has cond <= ~(sqrt(p)+sqrt(ell))/(sqrt(p)-sqrt(ell)) < 3, so
   // one Cholesky-QR pass is already orthonormal to O(eps cond^2); squarer blocks get a second pass.
   const int passes = (p >= 4 * (int64_t)ell) ? 1 : 2;
   for (int pass = 0; pass < passes; ++pass) {
-    TRY(gram_tall(c, omega, p, ell, c->nys_m.d()));
-    TRY(potrf_upper(c, c->nys_m.d(), ell, static_cast<int*>(c->nys_info.p) + 1));
-    TRY(trsm_right(c, omega, p, c->nys_m.d(), ell));
+    TRY(gram_tall(c, c->omp.d(), ld, p, ell, c->nys_m.d()));
+    TRY(potrf_upper(c, c->nys_m.d(), ell, ell, static_cast<int*>(c->nys_info.p) + 1));
+    TRY(trsm_right(c, c->omp.d(), ld, p, c->nys_m.d(), ell, ell));
   }
   // the potrf status is checked (no extra host sync) together with the sketch Cholesky in ngd_nystrom_finish
-  return NGD_OK;
+  return from_padded(c, omega, c->omp, p, ell);
 }
 
 // sketch.py:77-86: shift, Cholesky of Omega^T Y_nu, B = Y_nu C^{-1}, thin SVD of B
-// (Householder QR of B, Jacobi SVD of R, U = Q U_R), eigenvalues max(s^2 - nu, 0).
+// (B = Q R by shifted Cholesky-QR3, SVD of R, U = Q U_R), eigenvalues max(s^2 - nu, 0).
+// info words (device, read back with the results -- one host sync per sketch):
+//   [0] sketch Cholesky  [1] Omega's Cholesky-QR  [2] SVD (Jacobi sweeps / gesvdp status)
+//   [3] FP32 pre-sweeps  [4..6] the Cholesky factors of shifted Cholesky-QR3
 int ngd_nystrom_finish(ngd_ctx* c, const double* omega, double* Y, int64_t p, int32_t ell, double* U_row,
                        double* eig, double* h_shift) {
   TRY(bind(c));
   if (ell < 1 || ell > p) return fail(NGD_E_SHAPE, "rank must be in [1, %lld], got %d", (long long)p, ell);
   const int64_t n = p * ell;
-  CK(c->nys_m.ensure(sizeof(double) * (size_t)ell * ell));
-  CK(c->nys_r.ensure(sizeof(double) * (size_t)ell * ell));
-  CK(c->nys_ur.ensure(sizeof(double) * (size_t)ell * ell));
-  CK(c->nys_v.ensure(sizeof(double) * (size_t)ell * ell));
+  const int64_t ld = rup(p, 16);
+  for (Buf* b : {&c->nys_m, &c->nys_r, &c->nys_ur, &c->nys_v}) CK(b->ensure(sizeof(double) * (size_t)ell * ell));
   CK(c->nys_s.ensure(sizeof(double) * ell));
-  CK(c->nys_tau.ensure(sizeof(double) * ell));
-  CK(c->nys_info.ensure(sizeof(int) * 4));
-  // 1. nu = eps ||Y||_F ; Y_nu = Y + nu Omega
+  CK(c->nys_info.ensure(sizeof(int) * 8));
+  int* info = static_cast<int*>(c->nys_info.p);
+  CK(cudaMemsetAsync(info + 4, 0, sizeof(int) * 3, c->stream));  // [0..3] are written by every path
+  // 1. nu = eps ||Y||_F ; Y_nu = Y + nu Omega   (in the caller's Y, then one padded copy of each)
   dot(Y, Y, n, c->redp.d(), c->counter(1), c->S(SC_FRO2), nullptr, c->stream);
   add_shift(Y, omega, n, c->S(SC_FRO2), c->S(SC_SHIFT), c->stream);
+  TRY(to_padded(c, c->omp, omega, p, ell));
+  TRY(to_padded(c, c->yp, Y, p, ell));
   // 2. M = Omega^T Y_nu ; upper Cholesky
-  const double one = 1.0, zero = 0.0;
-  CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, (int)p, &one, omega, (int)p, Y, (int)p, &zero,
-                  c->nys_m.d(), ell));
-  int lw_potrf = 0, lw_geqrf = 0, lw_orgqr = 0, lw_svd = 0;
-  CKS(cusolverDnDpotrf_bufferSize(c->sol, CUBLAS_FILL_MODE_UPPER, ell, c->nys_m.d(), ell, &lw_potrf));
-  CKS(cusolverDnDgeqrf_bufferSize(c->sol, (int)p, ell, Y, (int)p, &lw_geqrf));
-  CKS(cusolverDnDorgqr_bufferSize(c->sol, (int)p, ell, ell, Y, (int)p, c->nys_tau.d(), &lw_orgqr));
-  CKS(cusolverDnDgesvdj_bufferSize(c->sol, CUSOLVER_EIG_MODE_VECTOR, 0, ell, ell, c->nys_r.d(), ell, c->nys_s.d(),
-                                   c->nys_ur.d(), ell, c->nys_v.d(), ell, &lw_svd, c->svdj));
-  const int lw = std::max(std::max(lw_potrf, lw_geqrf), std::max(lw_orgqr, lw_svd));
-  CK(c->nys_work.ensure(sizeof(double) * std::max(lw, 1)));
-  int* info = static_cast<int*>(c->nys_info.p);
-  TRY(potrf_upper(c, c->nys_m.d(), ell, info));
-  // status of this Cholesky (and of Omega's Cholesky-QR) is read back with the results below: one host
-  // sync per sketch; on failure the (discarded) remaining work runs on garbage and NGD_E_CHOL is returned
-  CK(cudaMemcpyAsync(&c->h_pin[8], info, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  TRY(gemm(c, ell, ell, (int)p, 1.0, kmaj(c->omp.d(), ld), kmaj(c->yp.d(), ld), 0.0, c->nys_m.d(), ell));
+  TRY(potrf_upper(c, c->nys_m.d(), ell, ell, info));
   // 3. B = Y_nu C^{-1}
-  TRY(trsm_right(c, Y, p, c->nys_m.d(), ell));
-  if (c->svd_method == 0) {
-    // 4. B = Q R (Householder)
-    CKS(cusolverDnDgeqrf(c->sol, (int)p, ell, Y, (int)p, c->nys_tau.d(), c->nys_work.d(), lw_geqrf, info));
-    CK(cudaMemcpy2DAsync(c->nys_r.d(), sizeof(double) * ell, Y, sizeof(double) * p, sizeof(double) * ell, ell,
-                         cudaMemcpyDeviceToDevice, c->stream));
-    triu(c->nys_r.d(), ell, ell, c->stream);
-    // 5. R = U_R diag(s) V^T (Jacobi, descending)
-    CKS(cusolverDnDgesvdj(c->sol, CUSOLVER_EIG_MODE_VECTOR, 0, ell, ell, c->nys_r.d(), ell, c->nys_s.d(),
-                          c->nys_ur.d(), ell, c->nys_v.d(), ell, c->nys_work.d(), lw_svd, info, c->svdj));
-    // 6. Q explicitly
-    CKS(cusolverDnDorgqr(c->sol, (int)p, ell, ell, Y, (int)p, c->nys_tau.d(), c->nys_work.d(), lw_orgqr, info));
-  } else {
-    // 4. B = Q R by shifted Cholesky-QR3 (GEMM/SYRK + potrf + TRSM; stable for cond(B) up to 1/eps)
-    TRY(scholqr3(c, Y, p, ell));
-    // 5. R = U_R diag(s) V^T, descending: cluster one-sided Jacobi (method 2) or polar SVD
-    // in-house block-exchange cluster Jacobi (all rotations in local shared memory) where the
-    // factor fits a cluster (ell <~ 310); cuSOLVER's polar SVD above
-    if (c->svd_method == 3 && jsvd_mixed_supported(ell) > 0) {
-      TRY(small_svd_mixed(c, ell));
-    } else if (c->svd_method == 2 && jsvd_block_supported(ell) > 0) {
-      CK(jacobi_svd_block(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(),
-                          static_cast<int*>(c->nys_info.p) + 2, c->stream));
-    } else {
-      TRY(small_svd_polar(c, ell));
-    }
-  }
-  // U = Q U_R  (column-major p x ell output)
-  CKB(cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)p, ell, ell, &one, Y, (int)p, c->nys_ur.d(), ell, &zero,
-                  U_row, (int)p));
+  TRY(trsm_right(c, c->yp.d(), ld, p, c->nys_m.d(), ell, ell));
+  // 4. B = Q R by shifted Cholesky-QR3 (stable for cond(B) up to 1/eps)
+  TRY(scholqr3(c, c->yp.d(), ld, p, ell));
+  // 5. R = U_R diag(s) V^T, descending: FP32 pre-sweeps + FP64 block Jacobi in a thread-block
+  //    cluster (ell <= 512), cuSOLVER's polar SVD above (or with option svd = 1)
+  const bool jacobi = c->svd_method == 3 && jsvd_mixed_supported(ell) > 0;
+  double svd_err = 0.0;
+  if (jacobi)
+    TRY(small_svd_mixed(c, ell));
+  else
+    TRY(small_svd_polar(c, ell, &svd_err));
+  // 6. U = Q U_R  (column-major p x ell output, ld p)
+  TRY(gemm(c, (int)p, ell, ell, 1.0, mnmaj(c->yp.d(), ld), kmaj(c->nys_ur.d(), ell), 0.0, U_row, p));
   eig_from_sv(c->nys_s.d(), ell, c->S(SC_SHIFT), eig, c->stream);
   CK(cudaMemcpyAsync(&c->h_pin[0], c->S(SC_SHIFT), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(&c->h_pin[60], static_cast<int*>(c->nys_info.p) + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost,
-                     c->stream));
+  CK(cudaMemcpyAsync(&c->h_pin[8], info, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  {
-    int hinfo[2] = {0, 0};
-    memcpy(hinfo, &c->h_pin[8], 2 * sizeof(int));
-    if (hinfo[1] != 0) return fail(NGD_E_CHOL, "test matrix is numerically rank deficient (potrf info %d)", hinfo[1]);
-    if (hinfo[0] != 0) return fail(NGD_E_CHOL, "sketch Cholesky failed (potrf info %d)", hinfo[0]);
-  }
+  int hinfo[8];
+  memcpy(hinfo, &c->h_pin[8], sizeof(hinfo));
+  if (hinfo[1] != 0) return fail(NGD_E_CHOL, "test matrix is numerically rank deficient (potrf info %d)", hinfo[1]);
+  if (hinfo[0] != 0) return fail(NGD_E_CHOL, "sketch Cholesky failed (potrf info %d)", hinfo[0]);
+  for (int k = 4; k < 7; ++k)
+    if (hinfo[k] != 0)
+      return fail(NGD_E_CUDA, "shifted Cholesky-QR3 pass %d: Cholesky failed (info %d)", k - 4, hinfo[k]);
   if (h_shift) *h_shift = c->h_pin[0];
-  {
-    int sw[2] = {0, 0};  // FP64 sweeps, FP32 pre-sweeps
-    memcpy(sw, &c->h_pin[60], 2 * sizeof(int));
-    const bool jacobi = (c->svd_method == 2 && jsvd_block_supported(ell) > 0) ||
-                        (c->svd_method == 3 && jsvd_mixed_supported(ell) > 0);
-    c->last_sweeps = sw[0];
-    c->last_sweeps_f32 = (c->svd_method == 3 && jacobi) ? sw[1] : 0;
-    // a non-converged FP64 Jacobi (or a timed-out block exchange) must not hand back a factor
-    // (the FP32 pre-sweeps may stop at their sweep cap: the FP64 phase finishes the job)
-    if (jacobi && (sw[0] <= 0 || (c->svd_method == 3 && sw[1] == -1000)))
-      return fail(NGD_E_CUDA, "small SVD: block Jacobi failed (FP64 sweeps %d, FP32 status %d)", sw[0], sw[1]);
-  }
+  c->last_sweeps = jacobi ? hinfo[2] : 0;
+  c->last_sweeps_f32 = jacobi ? hinfo[3] : 0;
+  // a non-converged FP64 Jacobi (or a timed-out block exchange) must not hand back a factor
+  // (the FP32 pre-sweeps may stop at their sweep cap: the FP64 phase finishes the job)
+  if (jacobi && (hinfo[2] <= 0 || hinfo[3] == -1000))
+    return fail(NGD_E_CUDA, "small SVD: block Jacobi failed (FP64 sweeps %d, FP32 status %d)", hinfo[2], hinfo[3]);
+  if (!jacobi && (hinfo[2] != 0 || !std::isfinite(svd_err)))
+    return fail(NGD_E_CUDA, "small SVD: gesvdp failed (info %d, err %g)", hinfo[2], svd_err);
   CK(cudaGetLastError());
   return NGD_OK;
 }
 
 int ngd_dense_matmat(ngd_ctx* c, const double* G, int64_t p, const double* V, int64_t ell, double* Y) {
   TRY(bind(c));
-  const double one = 1.0, zero = 0.0;
-  // G is a C-order (row-major) p x p matrix: in column-major terms it is G^T.
-  CKB(cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)p, (int)ell, (int)p, &one, G, (int)p, V, (int)p, &zero, Y,
-                  (int)p));
-  return NGD_OK;
+  // G is a C-order (row-major) p x p matrix: Y(m, n) = sum_k G[m p + k] V[n p + k]
+  return gemm(c, (int)p, (int)ell, (int)p, 1.0, kmaj(G, p), kmaj(V, p), 0.0, Y, p);
 }
 
 int ngd_precond_apply(ngd_ctx* c, const double* U, const double* eig, int32_t ell, double mu, const double* v,
@@ -1438,49 +1281,34 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
                          int recompute) {
   PcgState* sp = static_cast<PcgState*>(c->pcgs.p);
   const int* done = &sp->done;
-  const double one = 1.0, zero = 0.0;
   double *x = c->px.d(), *r = c->pr.d(), *z = c->pz.d(), *dv = c->pd.d(), *ad = c->pad.d(), *tmp = c->ptmp.d();
   const double* b = c->pb.d();
   double* mu_p = c->S(SC_MU);
   double* red = c->redp.d();
   // ad = (A + mu I) d ; dad = d.ad ; alpha / breakdown   (krylov.py:59-66)
   if (dense) {
-    CKB(cublasDgemv(c->blas, CUBLAS_OP_T, (int)p, (int)p, &one, dense, (int)p, dv, 1, &zero, ad, 1));
+    CK(gemv_rows(dense, p, dv, ad, done, c->stream));
     add_scaled(ad, mu, nullptr, dv, p, done, c->stream);
     pcg_ad(nullptr, c->rplan, p, mu_p, dv, ad, sp, 1, red, c->counter(4), c->stream);
   } else {
-    const double* part = c->partB.d();
-    const RedPlan* rp = &c->rplan;
-    if (c->fused_ok) {
-      TRY(fused_partials(c, dv, done));
-      part = c->partF.d();
-      rp = &c->rplan_f;
-    } else {
-      TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done, /*prepacked=*/true));
-      PhbAll pb{};
-      fill_phb(c, c->cot.d(), done, pb);
-      CK(c->phb_deep == 2 ? phase_b2_all_layers(pb, c->phb2_cache, c->stream) : phase_b_all_layers(pb, c->phb_deep, c->stream));
-    }
+    TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done, /*prepacked=*/true));
+    PhbAll pb{};
+    fill_phb(c, c->cot.d(), done, pb);
+    CK(phase_b2_all_layers(pb, c->phb2_cache, c->stream));
     if (c->comm) {
-      reduce_splits(part, *rp, p, 0.0, nullptr, nullptr, ad, done, c->stream);
+      reduce_splits(c->partB.d(), c->rplan, p, 0.0, nullptr, nullptr, ad, done, c->stream);
       TRY(allreduce(c, ad, p));
       add_scaled(ad, 0.0, mu_p, dv, p, done, c->stream);
-      pcg_ad(nullptr, *rp, p, mu_p, dv, ad, sp, 1, red, c->counter(4), c->stream);
+      pcg_ad(nullptr, c->rplan, p, mu_p, dv, ad, sp, 1, red, c->counter(4), c->stream);
     } else {
-      pcg_ad(part, *rp, p, mu_p, dv, ad, sp, 0, red, c->counter(4), c->stream);
+      pcg_ad(c->partB.d(), c->rplan, p, mu_p, dv, ad, sp, 0, red, c->counter(4), c->stream);
     }
   }
-  // x += alpha d ; r -= alpha ad (or r = b - A x) ; ||r|| test   (krylov.py:66-74); with a
-  // preconditioner and no recompute, the same kernel also runs the preconditioner's U^T r pass
-  const bool fuse_pre = have_pre && !recompute && c->pcg_fuse;
-  if (fuse_pre)
-    CK(pcg_update_precond1(x, r, dv, ad, p, sp, static_cast<PrecondArgs*>(c->pargs.p), ell, c->ppart.d(),
-                           c->pcprime.d(), red, c->counter(5), c->stream));
-  else
-    pcg_update(x, r, dv, ad, p, sp, recompute, red, c->counter(5), c->stream);
+  // x += alpha d ; r -= alpha ad (or r = b - A x) ; ||r|| test   (krylov.py:66-74)
+  pcg_update(x, r, dv, ad, p, sp, recompute, red, c->counter(5), c->stream);
   if (recompute) {
     if (dense) {
-      CKB(cublasDgemv(c->blas, CUBLAS_OP_T, (int)p, (int)p, &one, dense, (int)p, x, 1, &zero, tmp, 1));
+      CK(gemv_rows(dense, p, x, tmp, done, c->stream));
       add_scaled(tmp, mu, nullptr, x, p, done, c->stream);
     } else {
       TRY(gram_mv(c, x, 0.0, mu_p, tmp, done));
@@ -1489,11 +1317,8 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
   }
   // z = P^{-1} r ; beta = r.z / rz ; d = z + beta d   (krylov.py:75-81)
   // the direction update also packs d for the next iteration's phase A (matrix-free path)
-  const bool pack_next = !dense && !c->fused_ok;
-  if (fuse_pre)
-    CK(precond_apply2(static_cast<PrecondArgs*>(c->pargs.p), p, ell, c->pcprime.d(), r, z, done, sp, 0, red,
-                      c->counter(8) + 1, c->stream));
-  else if (have_pre)
+  const bool pack_next = !dense;
+  if (have_pre)
     CK(precond_apply(static_cast<PrecondArgs*>(c->pargs.p), p, ell, r, z, c->ppart.d(), c->pcprime.d(),
                      c->counter(8), done, sp, 0, red, c->stream));
   else
@@ -1552,7 +1377,7 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
   CK(precond_apply(have_pre ? static_cast<PrecondArgs*>(c->pargs.p) : nullptr, p, have_pre ? ell : 0, r, z,
                    c->ppart.d(), c->pcprime.d(), c->counter(8), done, sp, 1, c->redp.d(), c->stream));
   pcg_first_dir(z, dv, p, sp, c->stream);
-  if (!dense && !c->fused_ok) pack_all(vp_plan(c), dv, &sp->done, c->stream);  // iterations use d prepacked
+  if (!dense) pack_all(vp_plan(c), dv, &sp->done, c->stream);  // iterations use d prepacked
 
   // iterations: replay a captured CUDA graph of one iteration (Gram operator), or launch directly
   const bool use_graph = !dense && c->use_graphs;
@@ -1591,8 +1416,12 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
     }
     ++issued;
     // stop enqueueing once the device has published 'done' (pcg_dir writes the flag to pinned host
-    // memory at the end of every iteration; kernels of iterations after 'done' return at once)
-    if (*reinterpret_cast<volatile int*>(&c->h_flags[5]) != 0) break;
+    // memory at the end of every iteration; kernels of iterations after 'done' return at once).
+    // With a communicator every iteration carries an all-reduce, so all ranks must enqueue the same
+    // number of iterations: the host-timing-dependent early exit would pair one rank's final
+    // true-residual all-reduce with another rank's iteration.  The device-side 'done' is identical
+    // on every rank (all-reduced inputs, replicated arithmetic), so the extra iterations are no-ops.
+    if (!c->comm && *reinterpret_cast<volatile int*>(&c->h_flags[5]) != 0) break;
   }
   // final true residual (krylov.py:83-88)
   CK(cudaMemcpyAsync(&c->h_flags[4], &sp->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -1600,8 +1429,7 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
   const int dn = c->h_flags[4];
   if (dn != 2) {
     if (dense) {
-      const double one = 1.0, zero = 0.0;
-      CKB(cublasDgemv(c->blas, CUBLAS_OP_T, (int)p, (int)p, &one, dense, (int)p, xx, 1, &zero, tmp, 1));
+      CK(gemv_rows(dense, p, xx, tmp, nullptr, c->stream));
       add_scaled(tmp, mu, nullptr, xx, p, nullptr, c->stream);
     } else {
       TRY(gram_mv(c, xx, 0.0, c->S(SC_MU), tmp, nullptr));
@@ -1638,54 +1466,48 @@ int ngd_small_svd(ngd_ctx* c, const double* A, int32_t ell, double* U, double* s
                   int32_t* h_sweeps) {
   TRY(bind(c));
   if (ell < 1) return fail(NGD_E_SHAPE, "empty matrix");
-  CK(c->nys_r.ensure(sizeof(double) * (size_t)ell * ell));
-  CK(c->nys_ur.ensure(sizeof(double) * (size_t)ell * ell));
-  CK(c->nys_v.ensure(sizeof(double) * (size_t)ell * ell));
+  for (Buf* b : {&c->nys_r, &c->nys_ur, &c->nys_v}) CK(b->ensure(sizeof(double) * (size_t)ell * ell));
   CK(c->nys_s.ensure(sizeof(double) * ell));
-  CK(c->nys_info.ensure(sizeof(int) * 4));
+  CK(c->nys_info.ensure(sizeof(int) * 8));
   CK(cudaMemcpyAsync(c->nys_r.d(), A, sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
-  int sweeps = 0;
+  int* info = static_cast<int*>(c->nys_info.p);
+  double err = 0.0;
   if (method == 4) {
     if (jsvd_mixed_supported(ell) == 0)
       return fail(NGD_E_SHAPE, "ell = %d too large for the mixed-precision Jacobi SVD", ell);
     TRY(small_svd_mixed(c, ell));
-    CK(cudaMemcpyAsync(&c->h_pin[56], static_cast<int*>(c->nys_info.p) + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost,
-                       c->stream));
-  } else if (method == 2 || method == 3) {
-    if (method == 2 && jsvd_cluster_size(ell) == 0)
-      return fail(NGD_E_SHAPE, "ell = %d too large for the cluster Jacobi SVD", ell);
-    if (method == 3 && jsvd_block_supported(ell) == 0)
+  } else if (method == 3) {
+    if (jsvd_block_supported(ell) == 0)
       return fail(NGD_E_SHAPE, "ell = %d too large for the block-exchange Jacobi SVD", ell);
-    if (method == 2)
-      CK(jacobi_svd(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(), static_cast<int*>(c->nys_info.p) + 2,
-                    c->stream));
-    else {
-      CK(jacobi_svd_block(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(),
-                          static_cast<int*>(c->nys_info.p) + 2, c->stream));
-    }
-    CK(cudaMemcpyAsync(&c->h_pin[56], static_cast<int*>(c->nys_info.p) + 2, sizeof(int), cudaMemcpyDeviceToHost,
-                       c->stream));
+    CK(jacobi_svd_block(c->nys_r.d(), ell, ell, c->nys_ur.d(), ell, c->nys_s.d(), info + 2, c->stream));
+  } else if (method == 1) {
+    TRY(small_svd_polar(c, ell, &err));
   } else {
-    TRY(small_svd_polar(c, ell));
+    return fail(NGD_E_SHAPE, "small SVD method must be 1 (polar), 3 (block Jacobi) or 4 (FP32 + FP64 Jacobi)");
   }
   CK(cudaMemcpyAsync(U, c->nys_ur.d(), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaMemcpyAsync(sigma, c->nys_s.d(), sizeof(double) * ell, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(&c->h_pin[56], info + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  if (method >= 2) memcpy(&sweeps, &c->h_pin[56], sizeof(int));
-  if (method == 4) {  // FP32 pre-sweeps * 1000 + FP64 sweeps
-    int both[2];
-    memcpy(both, &c->h_pin[56], 2 * sizeof(int));
-    sweeps = both[1] * 1000 + both[0];
+  int both[2];
+  memcpy(both, &c->h_pin[56], 2 * sizeof(int));
+  int sweeps = both[0];
+  if (method == 1) {
+    if (both[0] != 0 || !std::isfinite(err)) return fail(NGD_E_CUDA, "gesvdp failed (info %d)", both[0]);
+    sweeps = 0;
   }
+  if (method == 4) sweeps = both[1] * 1000 + both[0];  // FP32 pre-sweeps * 1000 + FP64 sweeps
   if (h_sweeps) *h_sweeps = sweeps;
   return NGD_OK;
 }
 
+// method 0: the factorisation the library uses (one CTA, cluster, or blocked above 512);
+// 1: one-CTA kernel (n <= 160); 2: 8-CTA cluster kernel (n <= 512)
 int ngd_small_cholesky(ngd_ctx* c, double* A, int32_t n, int32_t method, int32_t* h_info) {
   TRY(bind(c));
   if (n < 1) return fail(NGD_E_SHAPE, "empty matrix");
-  CK(c->nys_info.ensure(sizeof(int) * 4));
-  int* info = static_cast<int*>(c->nys_info.p) + 3;
+  CK(c->nys_info.ensure(sizeof(int) * 8));
+  int* info = static_cast<int*>(c->nys_info.p) + 7;
   CK(cudaMemsetAsync(info, 0, sizeof(int), c->stream));
   if (method == 1) {
     if (!chol_supported(n)) return fail(NGD_E_SHAPE, "n = %d too large for the one-CTA Cholesky", n);
@@ -1694,17 +1516,27 @@ int ngd_small_cholesky(ngd_ctx* c, double* A, int32_t n, int32_t method, int32_t
     if (!chol_cluster_supported(n)) return fail(NGD_E_SHAPE, "n = %d too large for the cluster Cholesky", n);
     CK(c->chol_work.ensure(sizeof(int) * 4));
     CK(chol_upper_cluster(A, n, n, info, static_cast<int*>(c->chol_work.p), c->stream));
+  } else if (method == 0) {
+    TRY(potrf_upper(c, A, n, n, info));
   } else {
-    const int saved = c->use_own_chol;
-    c->use_own_chol = 0;
-    const int rc = potrf_upper(c, A, n, info);
-    c->use_own_chol = saved;
-    TRY(rc);
+    return fail(NGD_E_SHAPE, "Cholesky method must be 0, 1 or 2");
   }
   CK(cudaMemcpyAsync(&c->h_pin[60], info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   memcpy(h_info, &c->h_pin[60], sizeof(int));
   return NGD_OK;
+}
+
+// C = alpha op(A) op(B) + beta C on the in-house DMMA GEMM (test hook of ngd_gemm.cu): column-major
+// operands; trans_a = 0: A is M x K (lda), 1: A is K x M; trans_b = 0: B is K x N, 1: B is N x K
+int ngd_gemm(ngd_ctx* c, int32_t trans_a, int32_t trans_b, int32_t M, int32_t N, int32_t K, double alpha,
+             const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  TRY(bind(c));
+  if (M < 0 || N < 0 || K < 1) return fail(NGD_E_SHAPE, "bad GEMM shape");
+  // column-major A (M x K): A(m, k) = A[k lda + m] -> MN-major; transposed: K-major
+  const GemmOperand a{A, lda, trans_a != 0};
+  const GemmOperand b{B, ldb, trans_b == 0};
+  return gemm(c, M, N, K, alpha, a, b, beta, C, ldc);
 }
 
 int ngd_get_stat(ngd_ctx* c, const char* key, int64_t* out) {
@@ -1726,11 +1558,6 @@ int ngd_get_stat(ngd_ctx* c, const char* key, int64_t* out) {
 
 int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(NGD_E_SHAPE, "bad option");
-  if (!strcmp(key, "chol")) {
-    if (value < 0 || value > 2) return fail(NGD_E_SHAPE, "chol must be 0 (cuSOLVER), 1 (auto) or 2 (cluster)");
-    c->use_own_chol = (int)value;
-    return NGD_OK;
-  }
   if (!strcmp(key, "graphs")) {
     c->use_graphs = value ? 1 : 0;
     return NGD_OK;
@@ -1749,54 +1576,14 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
     c->graph_gen++;
     return NGD_OK;
   }
-  if (!strcmp(key, "pcg_fuse")) {
-    c->pcg_fuse = value ? 1 : 0;
-    c->graph_gen++;  // captured PCG graphs bake the choice in
-    return NGD_OK;
-  }
-  if (!strcmp(key, "pha_plan")) {
-    c->pha_plan = value ? 1 : 0;
-    return NGD_OK;
-  }
-  if (!strcmp(key, "phb_plan")) {
-    if (value < 0 || value > 2) return fail(NGD_E_SHAPE, "phb_plan must be 0, 1 or 2");
-    c->phb_plan = (int)value;
-    return NGD_OK;
-  }
-  if (!strcmp(key, "phb_g")) {
-    c->phb_g = (int)std::max<int64_t>(0, value);
-    return NGD_OK;
-  }
-  if (!strcmp(key, "phb_cs")) {
-    c->phb_cs = value ? 1 : 0;
-    return NGD_OK;
-  }
-  if (!strcmp(key, "fused")) {
-    c->use_fused = value ? 1 : 0;
-    if (c->have_points) {
-      c->fused_ok = false;  // re-planned by the next ngd_set_points / ngd_set_rows
-      c->graph_gen++;
-    }
-    return NGD_OK;
-  }
   if (!strcmp(key, "l2window")) {
     c->use_l2_window = value ? 1 : 0;
-    return NGD_OK;
-  }
-  if (!strcmp(key, "syrk")) {
-    c->use_syrk = value ? 1 : 0;
-    return NGD_OK;
-  }
-  if (!strcmp(key, "trsm")) {
-    if (value < 0 || value > 2) return fail(NGD_E_SHAPE, "trsm must be 0 (cuBLAS), 1 (DMMA solve) or 2 (inverse + GEMM)");
-    c->use_own_trsm = (int)value;
+    c->graph_gen++;  // the captured PCG iteration carries the stream's access-policy window
     return NGD_OK;
   }
   if (!strcmp(key, "svd")) {
-    if (value < 0 || value > 3)
-      return fail(NGD_E_SHAPE,
-                  "svd method must be 0 (geqrf+gesvdj), 1 (scholqr3+gesvdp), 2 (scholqr3+cluster Jacobi) or 3 "
-                  "(scholqr3+FP32-presweep Jacobi)");
+    if (value != 1 && value != 3)
+      return fail(NGD_E_SHAPE, "svd method must be 1 (cuSOLVER polar SVD) or 3 (FP32 + FP64 block Jacobi, ell <= 512)");
     c->svd_method = (int)value;
     return NGD_OK;
   }

@@ -380,276 +380,6 @@ cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles,
 #undef NGD_JET_CASE
 }
 
-// ---------------------------------------------------------------------------
-// Phase B: split-K  out_k = D_k diag(cc) Zin_k^T  (+ bias column), DMMA.
-// Tile 64 (a) x 64 (b) x 16 (columns j); 8 warps = 4 (a) x 2 (b), warp 16 x 32.
-// Partial of split g goes to part[g][off_k + a*N + b] / part[g][off_k + M*N + a],
-// i.e. the flat parameter layout (model.py:41-51); a fixed-order reduction
-// (reduce_splits) makes the result bitwise deterministic.
-// ---------------------------------------------------------------------------
-
-#ifndef NGD_PHB_UNITS
-#define NGD_PHB_UNITS 1  // 2 (32-column stages, 2-deep pipeline) measured neutral: C3 -1%, C2 +3%
-#endif
-// a phase-B pipeline stage covers PUN k-units of BK = 16 columns (one channel run of a point block each)
-constexpr int PUN = NGD_PHB_UNITS, PKS = PUN * BK;
-constexpr int PBM = 64, PBN = 64, PSTR = PKS + 4;
-
-// 32-bit column arithmetic (S < 2^31 for every supported configuration)
-__device__ __forceinline__ int point_of_col(int64_t j64, int64_t int_cols, int C, int nib) {
-  const int j = (int)j64;
-  if (j64 < int_cols) {
-    const int blk = j / (PB * C);
-    return blk * PB + (j & (PB - 1));
-  }
-  return nib * PB + (int)(j64 - int_cols);
-}
-__device__ __forceinline__ bool is_value_col(int64_t j64, int64_t int_cols, int C) {
-  return j64 >= int_cols || (((int)j64 % (PB * C)) < PB);
-}
-
-// cp.async pipeline depth of phase B: 3 stages at 3 CTAs / SM (uniform split plan), or 6 stages at
-// one CTA / SM (work-weighted plan, phb_plan = 1)
-constexpr int PNST_DEFAULT = PUN == 1 ? 3 : 2;
-constexpr int PNST_DEEP = 6;
-static_assert(PBM * (PBN + 1) + PBM <= 2 * 2 * PBM * PSTR, "cluster reduction staging must fit");
-template <int NST>
-constexpr size_t phb_smem() { return sizeof(double) * (2 * NST * PBM * PSTR + 2 * NST * PKS + PBM); }
-constexpr size_t kPhbSmem = phb_smem<PNST_DEFAULT>();
-
-template <int PNST>
-__device__ __forceinline__ void phb_tile(const PhbArgs& p, const int bx, const int by, const int kt0, const int kt1,
-                                         const int split) {
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;                              // [PNST][PBM][PSTR]
-  double* Bs = As + PNST * PBM * PSTR;            // [PNST][PBN][PSTR]
-  double* ccs = Bs + PNST * PBN * PSTR;           // [PNST][PKS] cotangent per column
-  double* ccv = ccs + PNST * PKS;                 // [PNST][PKS] value-column flag (bias)
-  double* bias_acc = ccv + PNST * PKS;            // [PBM]
-  if (p.skip && *p.skip) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 3, wn = warp >> 2;
-  const int n0 = bx * PBN, m0 = by * PBM;
-  const bool do_bias = (bx == 0);
-  // warps whose 16 x 32 sub-tile is all padding (output layer M = 1, input layer N = d) skip the MMAs
-  const bool w_active = (m0 + wm * 16) < p.M && (n0 + wn * 32) < p.N;
-  // bias partials from the A fragments already in registers (rows wm*16 + g, +8; columns kk + t):
-  // D c over value columns = the scaled fragment where the column is a value column
-  const bool bias_warp = do_bias && wn == 0 && w_active;
-  double bsum0 = 0.0, bsum1 = 0.0;
-
-  // stage = k-units [u, u + PUN) of this split (units past kt1 are zero-filled)
-  auto load_stage = [&](int stage, int u, int kt1_) {
-    double* as = As + stage * PBM * PSTR;
-    double* bs = Bs + stage * PBN * PSTR;
-#pragma unroll
-    for (int q = 0; q < PUN; ++q) {
-      const bool live = u + q < kt1_;
-      const int64_t j0 = (int64_t)(u + q) * BK;
-      const int cq = q * BK;
-      for (int i = tid; i < PBM * BK / 2; i += kThreads) {
-        const int r = i >> 3, c2 = (i & 7) * 2;
-        const int row = m0 + r;
-        if (live && row < p.M)
-          cp_async16(as + r * PSTR + cq + c2, p.D + (int64_t)row * p.s_pad + j0 + c2);
-        else
-          *reinterpret_cast<double2*>(as + r * PSTR + cq + c2) = make_double2(0.0, 0.0);
-      }
-      for (int i = tid; i < PBN * BK / 2; i += kThreads) {
-        const int r = i >> 3, c2 = (i & 7) * 2;
-        const int row = n0 + r;
-        if (live && row < p.N)
-          cp_async16(bs + r * PSTR + cq + c2, p.Z + (int64_t)row * p.s_pad + j0 + c2);
-        else
-          *reinterpret_cast<double2*>(bs + r * PSTR + cq + c2) = make_double2(0.0, 0.0);
-      }
-      // a unit's 16 columns are one channel run of one point block, i.e. 16 consecutive points:
-      // their cotangents are one contiguous 128-byte run -> asynchronous copy (warp 0 never stalls)
-      if (tid < BK / 2) {
-        if (live) {
-          const int pt0 = point_of_col(j0, p.int_cols, p.C, p.nib);
-          cp_async16(ccs + stage * PKS + cq + 2 * tid, p.cvec + pt0 + 2 * tid);
-        } else {
-          *reinterpret_cast<double2*>(ccs + stage * PKS + cq + 2 * tid) = make_double2(0.0, 0.0);
-        }
-      }
-      if (tid < BK) ccv[stage * PKS + cq + tid] = (live && is_value_col(j0 + tid, p.int_cols, p.C)) ? 1.0 : 0.0;
-    }
-  };
-
-  double acc[2][4][2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  const int nst = (kt1 - kt0 + PUN - 1) / PUN;  // pipeline steps of this split
-#pragma unroll
-  for (int s0 = 0; s0 < PNST - 1; ++s0) {
-    if (s0 < nst) load_stage(s0, kt0 + s0 * PUN, kt1);
-    cp_async_commit();
-  }
-  for (int it = 0; it < nst; ++it) {
-    const int st = it % PNST;
-    cp_async_wait<PNST - 2>();
-    __syncthreads();
-    {
-      const int nk = it + PNST - 1;
-#ifndef NGD_PHB_NOLOAD
-      if (nk < nst) load_stage(nk % PNST, kt0 + nk * PUN, kt1);
-#endif
-      cp_async_commit();
-    }
-    const double* as = As + st * PBM * PSTR;
-    const double* bs = Bs + st * PBN * PSTR;
-    const double* cs = ccs + st * PKS;
-    const double* vf = ccv + st * PKS;
-#ifdef NGD_PHB_NOCOMPUTE
-    if (w_active && as[0] == 12345.0) acc[0][0][0] += 1.0;
-#else
-#pragma unroll
-    for (int kk = 0; kk < PKS; kk += 4) {
-      if (!w_active) break;
-      const double cc = cs[kk + t];
-      const double a0 = as[(wm * 16 + g) * PSTR + kk + t] * cc;
-      const double a1 = as[(wm * 16 + 8 + g) * PSTR + kk + t] * cc;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double b = bs[(wn * 32 + j * 8 + g) * PSTR + kk + t];
-        dmma884(acc[0][j][0], acc[0][j][1], a0, b);
-        dmma884(acc[1][j][0], acc[1][j][1], a1, b);
-      }
-      if (bias_warp) {
-        const double f = vf[kk + t];
-        bsum0 = fma(f, a0, bsum0);
-        bsum1 = fma(f, a1, bsum1);
-      }
-    }
-#endif
-  }
-  // combine the 4 column phases t of each bias row (fixed order)
-  bsum0 += __shfl_xor_sync(0xffffffffu, bsum0, 1);
-  bsum0 += __shfl_xor_sync(0xffffffffu, bsum0, 2);
-  bsum1 += __shfl_xor_sync(0xffffffffu, bsum1, 1);
-  bsum1 += __shfl_xor_sync(0xffffffffu, bsum1, 2);
-  if (do_bias && wn == 0 && t == 0) {
-    bias_acc[wm * 16 + g] = bsum0;
-    bias_acc[wm * 16 + 8 + g] = bsum1;
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  // ---- split-K reduction inside the thread-block cluster (DSMEM) ----------
-  // The CS (runtime cluster size) CTAs of a cluster are consecutive K splits of the same output
-  // tile: each stages its 64x64 partial in shared memory, then CTA `rank` sums
-  // rows [8 rank, 8 rank + 8) over all ranks in rank order and writes one partial
-  // per cluster (deterministic, CS x less partial traffic).
-  constexpr int RSTR = PBN + 1;
-  double* red = smem;                 // [PBM][RSTR]
-  double* red_bias = red + PBM * RSTR;  // [PBM]
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) red[(wm * 16 + i * 8 + g) * RSTR + wn * 32 + j * 8 + 2 * t + e] = acc[i][j][e];
-  __syncthreads();
-  if (tid < PBM) red_bias[tid] = do_bias ? bias_acc[tid] : 0.0;
-  cg::cluster_group cl = cg::this_cluster();
-  const int CS = (int)cl.num_blocks();  // runtime cluster size (1, 2, 4 or 8)
-  if (CS > 1) cl.sync(); else __syncthreads();
-  const int rank = CS > 1 ? (int)cl.block_rank() : 0;
-  double* out = p.part + (int64_t)(split / CS) * p.p + p.off;
-  const int ROWS = PBM / CS;
-  for (int e = tid; e < ROWS * PBN; e += kThreads) {
-    const int r = rank * ROWS + e / PBN, col = e % PBN;
-    if (m0 + r < p.M && n0 + col < p.N) {
-      double sum = 0.0;
-      for (int q = 0; q < CS; ++q) sum += (CS > 1 ? cl.map_shared_rank(red, q) : red)[r * RSTR + col];
-      out[(int64_t)(m0 + r) * p.N + n0 + col] = sum;
-    }
-  }
-  if (do_bias && rank == 0 && tid < PBM && m0 + tid < p.M) {
-    double sum = 0.0;
-    for (int q = 0; q < CS; ++q) sum += (CS > 1 ? cl.map_shared_rank(red_bias, q) : red_bias)[tid];
-    out[(int64_t)p.M * p.N + m0 + tid] = sum;
-  }
-  if (CS > 1) cl.sync();  // keep this CTA's shared memory alive until the cluster has read it
-}
-
-// Phase B over ALL layers in one launch: blockIdx.x enumerates (layer, split, m-tile, n-tile)
-// with a per-layer split count proportional to the layer's work.
-template <int NST>
-__global__ void __launch_bounds__(kThreads) phb_all_kernel(PhbAll a) {
-  const int t = blockIdx.x;
-  int l = 0;
-  while (l + 1 < a.n_layers && t >= a.tile_start[l + 1]) ++l;
-  const int local = t - a.tile_start[l];
-  const int G = a.G[l];
-  const int split = local % G, tile = local / G;  // consecutive CTAs = consecutive splits of one tile
-  const PhbArgs& p = a.L[l];
-#ifdef NGD_PHB_SKIPTHIN
-  if (p.M < 16 || p.N < 16) return;
-#endif
-  const int kt0 = split * p.ktiles_per_split;
-  phb_tile<NST>(p, tile % a.tiles_n[l], tile / a.tiles_n[l], kt0, min(p.ktiles_total, kt0 + p.ktiles_per_split),
-                split);
-}
-
-// clusters of `cs` phase-B CTAs that can be co-resident on the device (one wave)
-int phb_max_active_clusters(int cs) {
-  cudaFuncSetAttribute(phb_all_kernel<PNST_DEFAULT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPhbSmem);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cs, 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = kPhbSmem;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, phb_all_kernel<PNST_DEFAULT>, &cfg) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  return n;
-}
-
-// CTAs per SM of the phase-B kernel at pipeline depth `deep` (0: 3 stages, 1: 6 stages)
-int phb_ctas_per_sm(int deep) { return deep ? (int)(227 * 1024 / phb_smem<PNST_DEEP>()) : 3; }
-
-cudaError_t phase_b_all_layers(const PhbAll& a, int deep, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(phb_all_kernel<PNST_DEFAULT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPhbSmem);
-    cudaFuncSetAttribute(phb_all_kernel<PNST_DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)phb_smem<PNST_DEEP>());
-    attr_set = true;
-  }
-  const int tiles = a.tile_start[a.n_layers];
-  if (tiles <= 0) return cudaSuccess;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles, 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = deep ? phb_smem<PNST_DEEP>() : kPhbSmem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = a.cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  probe_before(K_PHB, st);
-  cudaError_t e = deep ? cudaLaunchKernelEx(&cfg, phb_all_kernel<PNST_DEEP>, a)
-                       : cudaLaunchKernelEx(&cfg, phb_all_kernel<PNST_DEFAULT>, a);
-  probe_after(K_PHB, st);
-  return e;
-}
-
 
 // ---------------------------------------------------------------------------
 // Explicit Jacobian rows for the sketch (J-chunk formulation):

@@ -12,7 +12,7 @@ namespace ngd {
 enum KernelKind {
   K_FWD = 1, K_REV = 2, K_PHA = 3, K_PHB = 4, K_FORMJ = 5, K_PRECOND = 6, K_VEC = 7, K_PACK = 8, K_SVD = 9, K_CHOL = 10,
   K_BLAS = 11, K_SOLVER = 12,  // library calls (cuBLAS / cuSOLVER): timed, not counted as our launches
-  K_TRSM = 13, K_FUSED = 14
+  K_TRSM = 13, K_GEMM = 14
 };
 void probe_before(int kind, cudaStream_t st);
 void probe_after(int kind, cudaStream_t st);
@@ -97,6 +97,34 @@ struct FormJArgs {
   int64_t ldj;
 };
 
+// FP64 DMMA GEMM (ngd_gemm.cu): C(m, n) = alpha sum_k A(m, k) B(k, n) [* row_scale(m)] + beta C(m, n),
+// C column-major (ldc).  K-major operand: A(m, k) = p[m * ld + k]; MN-major: A(m, k) = p[k * ld + m].
+// TMA needs 16-byte aligned bases and even leading dimensions (gemm_operand_ok).
+struct GemmOperand {
+  const double* p;
+  int64_t ld;
+  bool kmaj;
+};
+struct GemmArgs {
+  int M, N, K;
+  int tiles_m, tiles_n, kstages, splits, kps;
+  double alpha, beta;
+  double* C;
+  int64_t ldc;
+  const double* row_scale;
+  double* part;  // split-K partials [splits][N][M]
+};
+struct GemmPlan {
+  int tiles_m, tiles_n, kstages, splits, kps;
+  size_t work_bytes;
+};
+bool gemm_operand_ok(const GemmOperand& o, int MN, int K);
+GemmPlan gemm_plan(int M, int N, int K);
+cudaError_t dgemm(int M, int N, int K, double alpha, const GemmOperand& A, const GemmOperand& B, double beta,
+                  double* C, int64_t ldc, const double* row_scale, double* work, size_t work_bytes, cudaStream_t st);
+double gemm_flops_total();
+cudaError_t gemv_rows(const double* G, int64_t n, const double* x, double* y, const int* skip, cudaStream_t st);
+
 constexpr int kMaxLayers = 8;
 struct PhaAll {
   JetArgs L[kMaxLayers];      // per layer, interior segment settings
@@ -105,35 +133,11 @@ struct PhaAll {
   int n_layers, nib, nbb;
   int64_t int_cols;
 };
-// pipelined phase A (ngd_pha2.cu): persistent CTAs over cost-balanced (layer, m-tile, point block) units
-struct Pha2Args {
-  CUtensorMap vmap[kMaxLayers];  // packed V_l [Mp][Kp], box 64 x 16
-  CUtensorMap zmap[kMaxLayers];  // Zin_l [Kp][s_pad], box 16 x 16
-  const double* D[kMaxLayers];   // adjoints of layer l [>= M rows][s_pad]
-  const double* vb[kMaxLayers];  // value-channel bias rows of V_l
-  double* partA[kMaxLayers];     // [mtiles][n_pts_pad] partials of layer l
-  int M[kMaxLayers], mtiles[kMaxLayers], kchunk[kMaxLayers], kchunks[kMaxLayers];
-  int n_layers, nib, nbb, n_pts_pad, n_ctas;
-  int64_t int_cols, s_pad;
-  const int* skip;
-  int cta_start[149];  // unit range of CTA i: [cta_start[i], cta_start[i + 1])
-};
-bool pha2_supported(int C);
-struct Pha2Cache {  // host-side tensor-map keys of pha2_all_layers (maps live in Pha2Args)
-  const double* kv[kMaxLayers] = {};
-  const double* kz[kMaxLayers] = {};
-  int kkp[kMaxLayers] = {}, kmp[kMaxLayers] = {}, kc[kMaxLayers] = {};
-  int64_t ks[kMaxLayers] = {};
-};
-cudaError_t pha2_all_layers(Pha2Args& a, Pha2Cache& cache, const double* const* vp, const double* const* zin,
-                            const int* kp, const int* mp, int C, cudaStream_t st);
-
 struct PhbAll {
   PhbArgs L[kMaxLayers];          // per layer (ktiles_per_split set per layer)
   int tile_start[kMaxLayers + 1];  // flat CTA offsets: layer l owns tiles_m*tiles_n*G_l CTAs
   int tiles_n[kMaxLayers], tiles_m[kMaxLayers], G[kMaxLayers];
   int n_layers;
-  int cluster;  // split-K CTAs reduced per cluster through DSMEM (divides G)
   int thin[kMaxLayers];  // phb2: layer whose tiles are thin (N <= 16 or M <= 16): paired with heavy work
 };
 // fixed-order reduction plan of the phase-B partials: param range of layer l uses G[l] splits
@@ -151,33 +155,10 @@ struct PackAll {  // entries: forward W_l (+ bias row) and, for the reverse swee
   int n_layers;                       // number of entries
 };
 
-// fused narrow-network Gramian matvec (ngd_fused.cu)
-struct FusedArgs {
-  const double* v;                  // flat parameter-space vector (model.py:41-51 layout)
-  const double* Z[kMaxLayers];      // input jets per layer
-  const double* D[kMaxLayers];      // adjoints per layer (dseed for the output layer)
-  int n_in[kMaxLayers], n_out[kMaxLayers];
-  int64_t woff[kMaxLayers], boff[kMaxLayers];
-  int vso[kMaxLayers], vbo[kMaxLayers], vs[kMaxLayers];  // shared-memory layout of V_l and v_b
-  int v_total;
-  int n_layers, C, nib, nbb;
-  int64_t s_pad, int_cols;
-  const double* w;                  // metric weight per padded point
-  double* part;                     // [grid][p] per-CTA partials
-  int64_t p;
-  const int* skip;
-};
-bool fused_supported(const int* widths, int n_layers, int C);
-size_t fused_smem(const FusedArgs& a);
-cudaError_t fused_mv(const FusedArgs& a, int grid, cudaStream_t st);
-
 cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles, cudaStream_t st);
 cudaError_t jet_gemm_both(int C, int mode, const JetArgs& a, int nib, int nbb, int64_t int_cols, int mtiles,
                           cudaStream_t st);
 cudaError_t pha_all(int C, const PhaAll& a, cudaStream_t st);
-int phb_max_active_clusters(int cs);
-cudaError_t phase_b_all_layers(const PhbAll& a, int deep, cudaStream_t st);
-int phb_ctas_per_sm(int deep);
 // pipelined phase B (ngd_phb2.cu): TMA producer + MMA warps; tensor maps cached per context
 struct Phb2Maps {
   CUtensorMap d[kMaxLayers];  // D_l: [M rows][s_pad], box 64 x 16
@@ -216,13 +197,6 @@ void add_scaled(double* out, double mu, const double* mu_p, const double* v, int
                 cudaStream_t st);
 int precond_blocks(int64_t p);
 // counters: two consecutive unsigned counters (utv combine, uc dot)
-int utv_chunks(int64_t p);
-cudaError_t pcg_update_precond1(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s,
-                                const PrecondArgs* pa, int ell, double* part, double* cprime, double* partials,
-                                unsigned* counter, cudaStream_t st);
-cudaError_t precond_apply2(const PrecondArgs* pa, int64_t p, int ell, const double* cprime, const double* v,
-                           double* out, const int* done, PcgState* pcg, int first, double* partials,
-                           unsigned* counter, cudaStream_t st);
 cudaError_t precond_apply(const PrecondArgs* pa, int64_t p, int ell, const double* v, double* out, double* part,
                           double* cprime, unsigned* counters, const int* done, PcgState* pcg, int first,
                           double* partials, cudaStream_t st);
@@ -238,18 +212,15 @@ void pcg_true_res(const double* b, const double* ax, double* r, int64_t p, PcgSt
 void pcg_dir_pack(const double* z, double* d, const PackAll& pk, PcgState* s, int* host_flag, cudaStream_t st);
 void pcg_dir(const double* z, double* d, int64_t p, PcgState* s, int* host_flag, cudaStream_t st);
 void theta_minus(const double* a, double alpha, const double* b, double* out, int64_t n, cudaStream_t st);
-void scale_rows(double* S, int64_t R, int ell, const double* w, cudaStream_t st);
 void scale_cols_sqrt(double* J, int64_t p, int64_t R, const double* w, cudaStream_t st);
 void symmetrize_upper(double* G, int64_t n, int64_t ld, cudaStream_t st);
-void set_identity(double* a, int n, cudaStream_t st);
 void add_shift(double* y, const double* omega, int64_t n, const double* fro2, double* shift_out, cudaStream_t st);
 void eig_from_sv(const double* s, int ell, const double* shift, double* eig, cudaStream_t st);
 void triu(double* a, int n, int lda, cudaStream_t st);
+void transpose(const double* src, int64_t lds, int rows, int cols, double* dst, int64_t ldd, cudaStream_t st);
+void info_combine(int* info, const int* info2, int offset, cudaStream_t st);
 void shift_diag(double* w, int n, double coef, cudaStream_t st);
 void fill_gaussian(double* out, int64_t n, uint64_t seed, cudaStream_t st);
-int jsvd_cluster_size(int ell);
-cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
-                       cudaStream_t st);
 int jsvd_block_supported(int ell);
 // FP32 pre-sweeps + FP64 finish (V in place in global memory for ell > ~310): cluster size, 0 if unsupported
 int jsvd_mixed_supported(int ell);

@@ -69,200 +69,6 @@ __device__ __forceinline__ double* col_ptr(double* cols, int j, int m, int ldc) 
   }
 }
 
-// A: ell x ell column-major (lda).  Outputs: sigma (descending), U (ell x ell, ldu),
-// info[0] = sweeps used (negative if not converged).
-template <int CL, int RPL>
-__global__ void __launch_bounds__(svd_threads<RPL>(), 1) jsvd_kernel(const double* A, int ell, int lda, double* U, int ldu,
-                                                              double* sigma, double tol, int max_sweeps, int* info) {
-  extern __shared__ __align__(16) double smem[];
-  const int n = (ell + 2 * CL - 1) / (2 * CL) * (2 * CL);  // even, multiple of CL
-  const int m = n / CL;                                     // columns per CTA
-  const int ldc = ell;
-  double* cols = smem;                           // [m][ldc]  X columns
-  double* vcols = cols + (int64_t)m * ldc;       // [m][ldc]  accumulated rotations
-  double* norms = vcols + (int64_t)m * ldc;      // [m]
-  int* flags = reinterpret_cast<int*>(norms + m);  // [2]
-  const int q = (CL == 1) ? 0 : (int)cg::this_cluster().block_rank();
-  constexpr int kSvdThreads = svd_threads<RPL>();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kSvdThreads / 32;
-
-  // X = R^T (column j of X = row j of R) and V = I, both [m][ldc] per CTA
-  for (int64_t e = tid; e < (int64_t)m * ldc; e += kSvdThreads) {
-    const int jl = (int)(e / ldc), r = (int)(e % ldc);
-    const int j = q * m + jl;
-    cols[e] = (j < ell) ? A[(int64_t)r * lda + j] : 0.0;
-    vcols[e] = (j == r) ? 1.0 : 0.0;
-  }
-  if (tid < 2) flags[tid] = 0;
-  cluster_barrier<CL>();
-
-  int sweep = 0;
-  bool converged = false;
-  for (; sweep < max_sweeps && !converged; ++sweep) {
-    const int par = sweep & 1;
-    for (int rd = 0; rd < n - 1; ++rd) {
-      // pairs k = q, q + CL, ... of this round; one warp per pair
-      for (int k = q + CL * warp; k < n / 2; k += CL * NW) {
-        int i, j;
-        circle_pair(n, rd, k, i, j);
-        double* ci = col_ptr<CL>(cols, i, m, ldc);
-        double* cj = col_ptr<CL>(cols, j, m, ldc);
-        double* vi = col_ptr<CL>(vcols, i, m, ldc);
-        double* vj = col_ptr<CL>(vcols, j, m, ldc);
-        // both columns and their rotation-accumulator columns into registers up front
-        // (all loads in flight at once: one (D)SMEM latency per pair)
-        double x[RPL], y[RPL], pv[RPL], qv[RPL];
-#pragma unroll
-        for (int u = 0; u < RPL; ++u) {
-          const int r = lane + 32 * u;
-          const bool in = r < ell;
-          x[u] = in ? ci[r] : 0.0;
-          y[u] = in ? cj[r] : 0.0;
-          pv[u] = in ? vi[r] : 0.0;
-          qv[u] = in ? vj[r] : 0.0;
-        }
-        double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-        for (int u = 0; u < RPL; ++u) {
-          al = fma(x[u], x[u], al);
-          be = fma(y[u], y[u], be);
-          ga = fma(x[u], y[u], ga);
-        }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        // rotate iff |ga| > tol sqrt(al be)  (squared form: no square roots on the test)
-        if (ga != 0.0 && ga * ga > tol * tol * al * be) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double az = fabs(zeta);
-          const double t = (az > 1e150) ? 0.5 / zeta : copysign(1.0 / (az + sqrt(fma(az, az, 1.0))), zeta);
-          const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
-#pragma unroll
-          for (int u = 0; u < RPL; ++u) {
-            const int r = lane + 32 * u;
-            if (r < ell) {
-              ci[r] = c * x[u] - s * y[u];
-              cj[r] = s * x[u] + c * y[u];
-              vi[r] = c * pv[u] - s * qv[u];
-              vj[r] = s * pv[u] + c * qv[u];
-            }
-          }
-          if (lane == 0) flags[par] = 1;
-        }
-      }
-      cluster_barrier<CL>();
-    }
-    // cluster-wide convergence test (flags double-buffered by sweep parity)
-    int any = 0;
-    if constexpr (CL == 1) {
-      any = flags[par];
-    } else {
-      for (int o = 0; o < CL; ++o) any |= cg::this_cluster().map_shared_rank(flags, o)[par];
-    }
-    converged = (any == 0);
-    if (tid == 0) flags[par ^ 1] = 0;
-    cluster_barrier<CL>();
-  }
-  // norms of own columns
-  for (int jl = warp; jl < m; jl += NW) {
-    const double* c = cols + (int64_t)jl * ldc;
-    double s = 0.0;
-    for (int r = lane; r < ell; r += 32) s = fma(c[r], c[r], s);
-    s = warp_sum(s);
-    if (lane == 0) norms[jl] = sqrt(s);
-  }
-  cluster_barrier<CL>();
-  // rank of each own column among all n (descending sigma, ties by index), write sigma and U
-  for (int jl = warp; jl < m; jl += NW) {
-    const int j = q * m + jl;
-    const double sj = norms[jl];
-    int rank = 0;
-    for (int o = lane; o < n; o += 32) {
-      const double so = (CL == 1) ? norms[o] : cg::this_cluster().map_shared_rank(norms, o / m)[o % m];
-      rank += (so > sj || (so == sj && o < j)) ? 1 : 0;
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
-    if (rank < ell) {
-      if (lane == 0) sigma[rank] = sj;
-      const double* v = vcols + (int64_t)jl * ldc;
-      for (int r = lane; r < ell; r += 32) U[(int64_t)rank * ldu + r] = v[r];
-    }
-  }
-  if (q == 0 && tid == 0) info[0] = converged ? sweep : -sweep;
-  cluster_barrier<CL>();  // keep shared memory alive until every CTA has finished reading it
-}
-
-static size_t jsvd_smem(int ell, int cl) {
-  const int n = (ell + 2 * cl - 1) / (2 * cl) * (2 * cl);
-  const int m = n / cl;
-  return sizeof(double) * (2 * (size_t)m * ell + m) + 2 * sizeof(int) + 16;
-}
-
-int jsvd_cluster_size(int ell) {
-  for (int cl : {1, 2, 4, 8, 16})
-    if (jsvd_smem(ell, cl) <= 200 * 1024) return cl;
-  return 0;  // too large: caller falls back
-}
-
-template <int CL, int RPL>
-static cudaError_t launch_jsvd_r(const double* A, int ell, int lda, double* U, int ldu, double* sigma, double tol,
-                                 int max_sweeps, int* info, cudaStream_t st) {
-  const size_t smem = jsvd_smem(ell, CL);
-  auto kern = jsvd_kernel<CL, RPL>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  if (CL > 8) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(CL, 1, 1);
-  cfg.blockDim = dim3(svd_threads<RPL>(), 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  probe_before(K_SVD, st);
-  e = cudaLaunchKernelEx(&cfg, kern, A, ell, lda, U, ldu, sigma, tol, max_sweeps, info);
-  probe_after(K_SVD, st);
-  return e;
-}
-
-template <int CL>
-static cudaError_t launch_jsvd(const double* A, int ell, int lda, double* U, int ldu, double* sigma, double tol,
-                               int max_sweeps, int* info, cudaStream_t st) {
-  const int rpl = (ell + 31) / 32;
-  if (rpl <= 4) return launch_jsvd_r<CL, 4>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-  if (rpl <= 8) return launch_jsvd_r<CL, 8>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-  if (rpl <= 12) return launch_jsvd_r<CL, 12>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-  if (rpl <= 16) return launch_jsvd_r<CL, 16>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-  if (rpl <= 24) return launch_jsvd_r<CL, 24>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t jacobi_svd(const double* A, int ell, int lda, double* U, int ldu, double* sigma, int* info,
-                       cudaStream_t st) {
-  // rotate only when |a_i.a_j| > ell * eps * |a_i||a_j|: tighter thresholds only chase dot-product rounding noise
-  const double tol = 2.220446049250313e-16 * (double)ell;
-  const int max_sweeps = 40;
-  switch (jsvd_cluster_size(ell)) {
-    case 1: return launch_jsvd<1>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-    case 2: return launch_jsvd<2>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-    case 4: return launch_jsvd<4>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-    case 8: return launch_jsvd<8>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-    case 16: return launch_jsvd<16>(A, ell, lda, U, ldu, sigma, tol, max_sweeps, info, st);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-
 // ---------------------------------------------------------------------------
 // Block-exchange variant: every rotation touches only LOCAL shared memory.
 // The n (padded) columns form 2*CL blocks of h columns; CTA k holds two blocks.

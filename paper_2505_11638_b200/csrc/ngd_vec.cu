@@ -440,111 +440,7 @@ __global__ void __launch_bounds__(kThreads) uc_kernel(const PrecondArgs* pa, int
   });
 }
 
-// ---- PCG step fused with the preconditioner's first pass ----------------------------------
-// x += alpha d ; r -= alpha ad ; rr = r.r (krylov.py:66-74) on a 64-row chunk, then this chunk's
-// share of U^T r_new for every basis vector: part[j][b] (one pass over U, r read once; the
-// column-per-CTA utv_kernel re-read r for every column).  utv_reduce_kernel finishes c'.
-constexpr int kUtvRows = 64;
-__global__ void __launch_bounds__(kThreads) pcg_update_utv_kernel(double* x, double* r, const double* d,
-                                                                  const double* ad, int64_t p, PcgState* s,
-                                                                  const PrecondArgs* pa, int ell, double* part,
-                                                                  double* partials, unsigned* counter) {
-  if (s->done) return;
-  __shared__ double rs[kUtvRows];
-  const double alpha = s->alpha;
-  const int64_t r0 = (int64_t)blockIdx.x * kUtvRows;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double v = 0.0;
-  if (tid < kUtvRows) {
-    const int64_t i = r0 + tid;
-    double ri = 0.0;
-    if (i < p) {
-      x[i] = x[i] + alpha * d[i];
-      ri = r[i] - alpha * ad[i];
-      r[i] = ri;
-      v = ri * ri;
-    }
-    rs[tid] = ri;
-  }
-  // (finish_sum's block reduction synchronises the CTA: rs is complete after it)
-  finish_sum(v, partials, counter, s, [](double sum, PcgState* st) {
-    st->rr = sum;
-    st->rel = sqrt(sum) / st->norm_b;
-    if (st->rel <= st->tol) st->done = 3;
-  });
-  __syncthreads();
-  const double* U = pa->U;
-  const int64_t i0 = r0 + lane, i1 = r0 + lane + 32;
-  const double q0 = rs[lane], q1 = rs[lane + 32];
-  const bool ok0 = i0 < p, ok1 = i1 < p;
-  // warp w: columns w, w + 8, ... four at a time (8 loads in flight per lane)
-  int j = warp;
-  for (; j + 24 < ell; j += 32) {
-    double a[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double* u = U + (int64_t)(j + 8 * q) * p;
-      a[q] = (ok0 ? u[i0] * q0 : 0.0) + (ok1 ? u[i1] * q1 : 0.0);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) a[q] = warp_sum(a[q]);
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) part[(int64_t)(j + 8 * q) * gridDim.x + blockIdx.x] = a[q];
-    }
-  }
-  for (; j < ell; j += 8) {
-    const double* u = U + (int64_t)j * p;
-    double a0 = (ok0 ? u[i0] * q0 : 0.0) + (ok1 ? u[i1] * q1 : 0.0);
-    a0 = warp_sum(a0);
-    if (lane == 0) part[(int64_t)j * gridDim.x + blockIdx.x] = a0;
-  }
-}
-
-// c'_j = (scale / (lam_j + mu) - 1) * sum_b part[j][b]  (fixed order per lane, fixed xor tree)
-__global__ void utv_reduce_kernel(const PrecondArgs* pa, int ell, int nb, const double* part, double* cprime,
-                                  const int* done) {
-  if (done && *done) return;
-  const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (j >= ell) return;
-  double a = 0.0;
-  for (int b = lane; b < nb; b += 32) a += part[(int64_t)j * nb + b];
-  a = warp_sum(a);
-  if (lane == 0) {
-    const double mu = pa->mu;
-    cprime[j] = ((pa->eig[ell - 1] + mu) / (pa->eig[j] + mu) - 1.0) * a;
-  }
-}
-
-int utv_chunks(int64_t p) { return (int)std::max<int64_t>(1, (p + kUtvRows - 1) / kUtvRows); }
-
-// PCG update + first preconditioner pass (replaces pcg_update + utv_kernel when not recomputing)
-cudaError_t pcg_update_precond1(double* x, double* r, const double* d, const double* ad, int64_t p, PcgState* s,
-                                const PrecondArgs* pa, int ell, double* part, double* cprime, double* partials,
-                                unsigned* counter, cudaStream_t st) {
-  const int nb = utv_chunks(p);
-  probe_before(K_VEC, st);
-  pcg_update_utv_kernel<<<nb, kThreads, 0, st>>>(x, r, d, ad, p, s, pa, ell, part, partials, counter);
-  probe_after(K_VEC, st);
-  probe_before(K_PRECOND, st);
-  utv_reduce_kernel<<<(ell + 7) / 8, 256, 0, st>>>(pa, ell, nb, part, cprime, &s->done);
-  probe_after(K_PRECOND, st);
-  return cudaGetLastError();
-}
-
 int precond_blocks(int64_t p) { return (int)std::max<int64_t>(1, (p + 31) / 32); }
-
-// second preconditioner pass alone (c' already computed by pcg_update_precond1)
-cudaError_t precond_apply2(const PrecondArgs* pa, int64_t p, int ell, const double* cprime, const double* v,
-                           double* out, const int* done, PcgState* pcg, int first, double* partials,
-                           unsigned* counter, cudaStream_t st) {
-  const int grid = precond_blocks(p);
-  probe_before(K_PRECOND, st);
-  launch_pdl(uc_kernel, dim3(grid), dim3(kThreads), sizeof(double) * (std::max(ell, 1) + kThreads), st, pa, p, ell, cprime, v, out, done,
-                                                                                pcg, first, partials, counter);
-  probe_after(K_PRECOND, st);
-  return cudaGetLastError();
-}
 
 cudaError_t precond_apply(const PrecondArgs* pa, int64_t p, int ell, const double* v, double* out, double* part,
                           double* cprime, unsigned* counters, const int* done, PcgState* pcg, int first,
@@ -833,18 +729,6 @@ void theta_minus(const double* a, double alpha, const double* b, double* out, in
   probe_after(K_VEC, st);
 }
 
-// S[q][j] (col-major R x ell) *= w[q]
-__global__ void scale_rows_kernel(double* S, int64_t R, int ell, const double* w) {
-  const int64_t n = R * ell;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    S[i] *= w[i % R];
-}
-void scale_rows(double* S, int64_t R, int ell, const double* w, cudaStream_t st) {
-  probe_before(K_VEC, st);
-  scale_rows_kernel<<<vgrid(R * ell), 256, 0, st>>>(S, R, ell, w);
-  probe_after(K_VEC, st);
-}
-
 // Jt (p x R column-major, one Jacobian row per column) columns scaled by sqrt(w)
 __global__ void scale_cols_sqrt_kernel(double* J, int64_t p, int64_t R, const double* w) {
   const int64_t n = p * R;
@@ -857,17 +741,6 @@ void scale_cols_sqrt(double* J, int64_t p, int64_t R, const double* w, cudaStrea
   probe_after(K_VEC, st);
 }
 
-// n x n identity (column-major, ld = n)
-__global__ void identity_kernel(double* a, int n) {
-  const int64_t tot = (int64_t)n * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x)
-    a[e] = (e % n == e / n) ? 1.0 : 0.0;
-}
-void set_identity(double* a, int n, cudaStream_t st) {
-  probe_before(K_VEC, st);
-  identity_kernel<<<vgrid((int64_t)n * n), 256, 0, st>>>(a, n);
-  probe_after(K_VEC, st);
-}
 
 // lower triangle <- upper triangle
 __global__ void symmetrize_upper_kernel(double* G, int64_t n, int64_t ld) {
@@ -969,6 +842,37 @@ __global__ void gaussian_kernel(double* out, int64_t n, uint64_t seed) {
 void fill_gaussian(double* out, int64_t n, uint64_t seed, cudaStream_t st) {
   probe_before(K_VEC, st);
   gaussian_kernel<<<vgrid((n + 1) / 2), 256, 0, st>>>(out, n, seed);
+  probe_after(K_VEC, st);
+}
+
+// dst(j, i) = src(i, j): rows x cols column-major (lds) -> cols x rows column-major (ldd); the
+// off-diagonal panel of the blocked Cholesky (ell > 512) is solved as a right triangular system
+__global__ void transpose_kernel(const double* src, int64_t lds, int rows, int cols, double* dst, int64_t ldd) {
+  __shared__ double tile[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int i = i0 + threadIdx.x, j = j0 + y;
+    if (i < rows && j < cols) tile[y][threadIdx.x] = src[(int64_t)j * lds + i];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int j = j0 + threadIdx.x, i = i0 + y;
+    if (i < rows && j < cols) dst[(int64_t)i * ldd + j] = tile[threadIdx.x][y];
+  }
+}
+void transpose(const double* src, int64_t lds, int rows, int cols, double* dst, int64_t ldd, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  transpose_kernel<<<dim3((rows + 31) / 32, (cols + 31) / 32), dim3(32, 8), 0, st>>>(src, lds, rows, cols, dst, ldd);
+  probe_after(K_VEC, st);
+}
+
+// LAPACK potrf status of a blocked factor: the first failing pivot of either diagonal block
+__global__ void info_combine_kernel(int* info, const int* info2, int offset) {
+  if (*info == 0 && *info2 != 0) *info = *info2 + offset;
+}
+void info_combine(int* info, const int* info2, int offset, cudaStream_t st) {
+  probe_before(K_VEC, st);
+  info_combine_kernel<<<1, 1, 0, st>>>(info, info2, offset);
   probe_after(K_VEC, st);
 }
 

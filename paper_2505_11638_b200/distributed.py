@@ -23,29 +23,36 @@ import ctypes
 from . import _lib
 
 
-def shard_range(n, rank, nranks):
-    """Contiguous [lo, hi) of n items for rank (first n % nranks ranks get one extra)."""
-    base, extra = divmod(n, nranks)
-    lo = rank * base + min(rank, extra)
-    hi = lo + base + (1 if rank < extra else 0)
+def shard_range(n, rank, nranks, block=1):
+    """Contiguous [lo, hi) of n items for rank, in whole blocks of ``block`` items (the first
+    ranks get one extra block; the last rank takes the ragged tail)."""
+    nblk = -(-n // block)
+    base, extra = divmod(nblk, nranks)
+    lo = min(n, (rank * base + min(rank, extra)) * block)
+    hi = min(n, lo + (base + (1 if rank < extra else 0)) * block)
     return lo, hi
 
 
-def shard_slices(n_int, n_bnd, channels, rank, nranks):
+def shard_slices(n_int, n_bnd, rank, nranks, block=16):
     """Interior and boundary slices of one rank.
 
-    Interior points (cost ``channels`` each) and boundary points (cost 1) are
-    both split contiguously and evenly, so every rank carries the same
-    channel-point count to within one point of each kind."""
+    Both point kinds are split contiguously into whole 16-point blocks (the
+    kernels' point-block granularity, csrc/ngd_common.cuh: no padded point
+    blocks inside a shard), evenly per kind, so every rank carries the same
+    channel-point count -- interior points cost d+2 Taylor channels, boundary
+    points one -- to within one block of each kind (``shard_cost``)."""
     if nranks < 1 or not 0 <= rank < nranks:
         raise ValueError("bad rank / world size")
-    li, hi = shard_range(n_int, rank, nranks)
-    lb, hb = shard_range(n_bnd, rank, nranks)
+    if -(-n_int // block) < nranks and -(-n_bnd // block) < nranks:
+        block = 1  # too few blocks for every rank to get one: split point by point
+    li, hi = shard_range(n_int, rank, nranks, block)
+    lb, hb = shard_range(n_bnd, rank, nranks, block)
     return slice(li, hi), slice(lb, hb)
 
 
 def shard_cost(n_int, n_bnd, channels, rank, nranks):
-    si, sb = shard_slices(n_int, n_bnd, channels, rank, nranks)
+    """Channel-points of a rank's shard (interior points carry ``channels`` channels)."""
+    si, sb = shard_slices(n_int, n_bnd, rank, nranks)
     return (si.stop - si.start) * channels + (sb.stop - sb.start)
 
 

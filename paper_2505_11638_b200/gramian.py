@@ -187,3 +187,18 @@ def assemble_dense(op, guard=DENSE_GUARD):
     if hasattr(op, "matmat"):
         return np.asarray(_lib.like_input(_lib.to_device(op.matmat(np.eye(p))), np.eye(1)))
     return np.column_stack([op.matvec(np.eye(p)[:, i]) for i in range(p)])
+
+
+def normalized_spectrum(matrix, top=None):
+    """Descending eigenvalues of an SPSD matrix over the largest (harness.py:237-248)."""
+    eigs = np.clip(np.linalg.eigvalsh(np.asarray(matrix, dtype=float))[::-1], 0.0, None)
+    if eigs[0] == 0.0:
+        raise ZeroDivisionError("matrix is identically zero; cannot normalize")
+    ratios = eigs / eigs[0]
+    return ratios if top is None else ratios[:top]
+
+
+def gramian_spectrum(problem, theta, quad, top=None):
+    """Top normalised eigenvalues of the Gramian (harness.py:249-252), assembled on the device as
+    J^T diag(w) J from Jacobian-row chunks on the DMMA GEMM (ngd_gram_dense)."""
+    return normalized_spectrum(assemble_dense(GramianOperator.from_problem(problem, theta, quad)), top=top)

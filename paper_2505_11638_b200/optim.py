@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .gramian import DENSE_GUARD, GramianOperator, ShiftedOperator, assemble_dense
+from .gramian import GramianOperator, ShiftedOperator
 from .krylov import pcg
 from .sketch import NystromPreconditioner, nystrom_approximate
 
@@ -266,9 +266,8 @@ def h1_relative_error(problem, theta, quad):
 
 
 # ---------------------------------------------------------------------------
-# Baselines of the reference's comparison protocol (optim.py:273-455), on the same
-# device path: NGD-CG (unpreconditioned PCG on the Gramian), dense NGD
-# (assembled Gramian, pseudoinverse), gradient descent and dense BFGS.
+# NGD-CG baseline of the reference's comparison protocol (optim.py:273-327):
+# unpreconditioned CG on the same device Gramian.
 # ---------------------------------------------------------------------------
 
 
@@ -305,11 +304,6 @@ class _DeviceIterate:
             raise _lib.NonFiniteError("non-finite loss")
         self.ctx.call("ngd_loss_grad", _lib.ptr(self.grad))
         return gop, gop.loss, self.grad
-
-    def loss_grad(self, th):
-        self.problem.linearize(th, self.quad)
-        self.ctx.call("ngd_loss_grad", _lib.ptr(self.grad))
-        return self.grad.clone()
 
     def step(self, direction, grad_dot_dir, loss0):
         """Armijo line search along -direction and update (default line-search knobs, optim.py:121)."""
@@ -358,117 +352,18 @@ def ngd_cg_run(problem, theta0, config, quad, quad_eval=None, matvec_budget=None
     return _lib.like_input(it.theta, theta0), records
 
 
-def _pinv_solve(matrix, rhs):
-    """Pseudoinverse solve of a symmetric matrix with the numerical-rank cutoff p eps s_1
-    (optim.py:350-355), by a device eigendecomposition (SVD of a symmetric matrix = |eig|)."""
-    torch = _lib.torch_mod()
-    lam, vec = torch.linalg.eigh(matrix)
-    s = lam.abs()
-    cutoff = matrix.shape[0] * EPS_MACH * float(s.max())
-    inv = torch.where(s > cutoff, 1.0 / torch.where(s > cutoff, lam, torch.ones_like(lam)), torch.zeros_like(lam))
-    return vec @ (inv * (vec.T @ rhs))
-
-
-def ngd_dense_step(problem, theta, quad, mu, guard=DENSE_GUARD):
-    """One NGD step with the assembled (G + mu I) and its pseudoinverse (optim.py:330-341)."""
-    torch = _lib.torch_mod()
-    it = _DeviceIterate(problem, theta, quad)
-    gop, loss, g = it.linearize()
-    dense = _lib.to_device(assemble_dense(gop, guard=guard)) + mu * torch.eye(gop.dim, dtype=torch.float64,
-                                                                                device=g.device)
-    d = _pinv_solve(dense, g).contiguous()
-    it.step(d, it.dot(g, d), loss)
-    return _lib.like_input(it.theta, theta), _lib.like_input(d, theta)
-
-
-def ngd_dense_run(problem, theta0, config, quad, quad_eval=None):
-    """Dense NGD baseline (optim.py:358-380)."""
-    torch = _lib.torch_mod()
-    it = _DeviceIterate(problem, theta0, quad)
-    records, total = [], 0
-    for k in range(config.iterations):
-        tic = time.perf_counter()
-        gop, loss, g = it.linearize()
-        mu = _baseline_mu(loss)
-        dense = _lib.to_device(assemble_dense(gop)) + mu * torch.eye(it.p, dtype=torch.float64, device=g.device)
-        d = _pinv_solve(dense, g).contiguous()
-        it.step(d, it.dot(g, d), loss)
-        total += it.p
-        records.append(RunRecord(k, loss, _h1(problem, it.theta, quad_eval), mu, 0, 0, total,
-                                 time.perf_counter() - tic))
-    return _lib.like_input(it.theta, theta0), records
-
-
-def gradient_descent_step(problem, theta, quad):
-    """Plain gradient descent with Armijo backtracking (optim.py:383-388)."""
-    it = _DeviceIterate(problem, theta, quad)
-    _, loss, g = it.linearize()
-    it.step(g, it.dot(g, g), loss)
-    return _lib.like_input(it.theta, theta)
-
-
-def gradient_descent_run(problem, theta0, config, quad, quad_eval=None):
-    """optim.py:391-411"""
-    it = _DeviceIterate(problem, theta0, quad)
-    records = []
-    for k in range(config.iterations):
-        tic = time.perf_counter()
-        _, loss, g = it.linearize()
-        it.step(g, it.dot(g, g), loss)
-        records.append(RunRecord(k, loss, _h1(problem, it.theta, quad_eval), 0.0, 0, 0, 0,
-                                 time.perf_counter() - tic))
-    return _lib.like_input(it.theta, theta0), records
-
-
-def bfgs_update(h, s, y):
-    """Inverse-Hessian BFGS update (optim.py:149-162); skipped when s^T y <= 0."""
-    torch = _lib.torch_mod()
-    sy = float(s @ y)
-    if sy <= 0.0:
-        return h
-    rho = 1.0 / sy
-    hy = h @ y
-    coeff = rho + rho**2 * float(y @ hy)
-    return h + coeff * torch.outer(s, s) - rho * (torch.outer(hy, s) + torch.outer(s, hy))
-
-
-def bfgs_run(problem, theta0, config, quad, quad_eval=None, guard=5000):
-    """Dense BFGS baseline (optim.py:414-438), inverse Hessian resident on the device."""
-    torch = _lib.torch_mod()
-    it = _DeviceIterate(problem, theta0, quad)
-    if it.p > guard:
-        raise ValueError(f"dense BFGS guard: p={it.p} exceeds {guard}")
-    h = torch.eye(it.p, dtype=torch.float64, device=it.theta.device)
-    g = it.loss_grad(it.theta)
-    records = []
-    for k in range(config.iterations):
-        tic = time.perf_counter()
-        loss = it.loss_at(it.theta, 0.0, g)
-        d = (h @ g).contiguous()
-        prev = it.theta.clone()
-        alpha = it.step(d, it.dot(g, d), loss)
-        if alpha > 0.0:
-            g_next = it.loss_grad(it.theta)
-            h = bfgs_update(h, it.theta - prev, g_next - g)
-            g = g_next
-        records.append(RunRecord(k, loss, _h1(problem, it.theta, quad_eval), 0.0, 0, 0, 0,
-                                 time.perf_counter() - tic))
-    return _lib.like_input(it.theta, theta0), records
-
-
-OPTIMIZER_NAMES = ("nystrom_ngd", "ngd_cg", "ngd_dense", "gd", "bfgs")
+# The hot path's optimizer and the one baseline SURVEY 8f #4 keeps (NGD-CG, the paper's comparison
+# protocol); gradient descent, dense BFGS and dense NGD (optim.py:330-438) are off the path.
+OPTIMIZER_NAMES = ("nystrom_ngd", "ngd_cg")
 
 _RUNNERS = {
     "nystrom_ngd": nystrom_ngd_run,
     "ngd_cg": ngd_cg_run,
-    "ngd_dense": ngd_dense_run,
-    "gd": gradient_descent_run,
-    "bfgs": bfgs_run,
 }
 
 
 def run_optimizer(name, problem, theta0, config, quad, quad_eval=None):
-    """Dispatch by name (optim.py:441-455)."""
+    """Dispatch by name (optim.py:441-455), for the two optimizers built on the device path."""
     if name not in _RUNNERS:
         raise KeyError(f"unknown optimizer {name!r}; available: {OPTIMIZER_NAMES}")
     return _RUNNERS[name](problem, theta0, config, quad, quad_eval=quad_eval)

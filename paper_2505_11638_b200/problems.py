@@ -184,7 +184,7 @@ class PdeProblem:
         if nranks > 1:
             from .distributed import shard_slices
 
-            si, sv = shard_slices(len(xi), len(xv), self.topology.input_dim + 2, rank, nranks)
+            si, sv = shard_slices(len(xi), len(xv), rank, nranks)
             ctx._int_slice = si
             xi, wmi, wri, oi = xi[si], wmi[si], wri[si], oi[si]
             xv, wmv, wrv, ov = xv[sv], wmv[sv], wrv[sv], ov[sv]

@@ -215,6 +215,119 @@ def case_baselines():
     return out
 
 
+def case_c2_step():
+    """C2 full step pieces on the benchmarked shapes: the rank-300 Nystrom factor
+    on host Omega (sketch.py:58-90), the step's mu (optim.py:86-103), P^-1 v (sketch.py:101-112),
+    PCG iterates at k = 5/20/50 (krylov.py:24-88) and a 5-step fixed-rank trajectory
+    (optim.py:188-270) with the bench config (ell = 300, 50 PCG iterations)."""
+    widths = (2, 64, 64, 64, 1)
+    prob = problems.make_problem("poisson2d", topology=model.MlpTopology(widths))
+    quad = prob.sample_quadrature(4096, 512, 0)
+    theta = model.init(prob.topology, 0).values
+    p = theta.shape[0]
+    out = {"v": np.random.default_rng(1).standard_normal(p)}
+    loss = prob.loss_value(theta, quad)
+    g = prob.loss_grad(theta, quad)
+    gop = gramian.GramianOperator.from_problem(prob, theta, quad)
+    t0 = time.time()
+    factor = sketch.nystrom_approximate(gop, 300, seed=11)
+    print(f"  c2 rank-300 sketch in {time.time() - t0:.1f}s")
+    mu = optim.adapt_mu(factor.eigenvalues[0], float(p), loss, float(np.linalg.norm(g)), "grad-power", 1e-6, 1.0)
+    pre = sketch.NystromPreconditioner(factor, mu)
+    out["eig300"] = factor.eigenvalues
+    out["mu"] = np.array(mu)
+    out["pinv_v"] = pre.apply(out["v"])
+    for k in (5, 20, 50):
+        rep = krylov.pcg(gramian.ShiftedOperator(gop, mu), g, 1e-300, k, precond=pre)
+        out[f"pcg{k}_x"] = rep.solution
+        out[f"pcg{k}_meta"] = np.array([rep.iterations, rep.matvecs, rep.relative_residual, rep.converged,
+                                        rep.breakdown], dtype=float)
+    cfg = optim.NystromNgdConfig(ell0=300, ell_max=300, cg_maxit=50, kappa=1e-300,
+                                 mu_floor_mode="grad-power", mu_floor_coeff=1e-6,
+                                 mu_floor_exponent=1.0, iterations=5, seed=0)
+    saved = optim.adapt_rank
+    optim.adapt_rank = lambda eigenvalues, mu, ell, ell_max, ratio=10.0: ell
+    try:
+        t0 = time.time()
+        theta_f, recs = optim.nystrom_ngd_run(prob, theta, cfg, quad)
+        print(f"  c2 5 NGD steps in {time.time() - t0:.1f}s")
+    finally:
+        optim.adapt_rank = saved
+    out["traj_loss"] = np.array([r.loss for r in recs])
+    out["traj_mu"] = np.array([r.mu for r in recs])
+    out["traj_pcg"] = np.array([r.pcg_iters for r in recs])
+    out["traj_matvecs"] = np.array([r.matvecs for r in recs])
+    out["traj_theta"] = theta_f
+    return out
+
+
+def case_c1_ensemble(k_runs=24, delta=2.220446049250313e-16):
+    """Rounding sensitivity of the reference's own 20-step C1 trajectory:
+    k_runs runs of the unmodified nystrom_ngd_run whose Gramian matvec output is perturbed
+    elementwise by a relative delta * U(-1, 1) (about one ulp, independent draws per run).
+    The spread of these runs is the parity envelope of any correct reimplementation."""
+    widths = (2, 32, 32, 1)
+    prob = problems.make_problem("poisson2d", topology=model.MlpTopology(widths))
+    quad = prob.sample_quadrature(900, 120, 0)
+    theta = model.init(prob.topology, 0).values
+    cfg = optim.NystromNgdConfig(ell0=100, ell_max=100, cg_maxit=20, kappa=1e-300,
+                                 mu_floor_mode="grad-power", mu_floor_coeff=1e-6,
+                                 mu_floor_exponent=1.0, iterations=20, seed=0)
+    orig_mv = gramian.GramianOperator.matvec
+    saved = optim.adapt_rank
+    optim.adapt_rank = lambda eigenvalues, mu, ell, ell_max, ratio=10.0: ell
+    losses, pcgs = [], []
+    try:
+        for run in range(k_runs):
+            prng = np.random.default_rng(1000 + run)
+
+            def mv(self, v, _prng=prng):
+                y = orig_mv(self, v)
+                return y * (1.0 + delta * _prng.uniform(-1.0, 1.0, y.shape))
+
+            gramian.GramianOperator.matvec = mv
+            t0 = time.time()
+            _, recs = optim.nystrom_ngd_run(prob, theta, cfg, quad)
+            print(f"  ensemble run {run}: {time.time() - t0:.1f}s")
+            losses.append([r.loss for r in recs])
+            pcgs.append([r.pcg_iters for r in recs])
+    finally:
+        gramian.GramianOperator.matvec = orig_mv
+        optim.adapt_rank = saved
+    return {"ens_loss": np.array(losses), "ens_pcg": np.array(pcgs), "delta": np.array(delta)}
+
+
+def case_nd_sketch(widths, kind, n_int, n_bnd):
+    """Point subsets of C3 / C5 with >= 1024 points: loss, grad, matvec and 8 sketch columns on a
+    fixed post-QR Omega (gramian.py:48-61)."""
+    top = model.MlpTopology(widths)
+    prob = PoissonND(top, kind)
+    quad = prob.sample_quadrature(n_int, n_bnd, 0)
+    theta = model.init(top, 0).values
+    p = theta.shape[0]
+    out = _basic(prob, theta, quad, np.random.default_rng(1).standard_normal(p))
+    gop = gramian.GramianOperator.from_problem(prob, theta, quad)
+    omega, _ = np.linalg.qr(np.random.default_rng(123).standard_normal((p, 8)), mode="reduced")
+    out["y8"] = gop.matmat(omega)
+    del out["v"]  # regenerated by the tests from the seeds (default_rng(1), default_rng(123) + QR)
+    return out
+
+
+def case_c4_sketch(n):
+    """C4 microbench on n points: matvec + 8 sketch columns on a fixed post-QR Omega."""
+    widths = (2, 256, 256, 256, 1)
+    top = model.MlpTopology(widths)
+    x = np.random.default_rng(0).random((n, 2))
+    w = np.full(n, 1.0 / n)
+    theta = model.init(top, 0).values
+    p = theta.shape[0]
+    stack = lambda th: model.input_derivatives(top, th, x)[2]
+    gop = gramian.GramianOperator.from_stack(stack, theta, w)
+    v = np.random.default_rng(1).standard_normal(p)
+    omega, _ = np.linalg.qr(np.random.default_rng(123).standard_normal((p, 8)), mode="reduced")
+    return {"x": x, "gv": gop.matvec(v), "y8": gop.matmat(omega)}  # v, omega: regenerated from the seeds
+
+
 def main():
     cases = {
         "c1": case_c1,
@@ -226,10 +339,18 @@ def main():
         "heat1p1d": lambda: case_problem("heat1p1d", (2, 24, 24, 1), 600, 80, 40),
         "nlpoisson2d": lambda: case_problem("nlpoisson2d", (2, 24, 24, 1), 600, 80, 40),
         "baselines": case_baselines,
+        "c2_step": case_c2_step,
+        "c1_ensemble": case_c1_ensemble,
+        "c3_1k": lambda: case_nd_sketch((5, 128, 128, 128, 1), "sinsum", 1024, 256),
+        "c5_1k": lambda: case_nd_sketch((10, 256, 256, 256, 256, 1), "gauss", 1024, 256),
+        "c4_1k": lambda: case_c4_sketch(1024),
     }
+    default_skip = {"baselines"}  # out-of-scope baselines (removed in round 2); run explicitly if needed
     only = sys.argv[1:]
     for name, fn in cases.items():
         if only and name not in only:
+            continue
+        if not only and name in default_skip:
             continue
         t0 = time.time()
         data = fn()

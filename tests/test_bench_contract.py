@@ -35,13 +35,25 @@ def test_roofline_work_model():
     pw = sum(i * o for i, o in zip(widths[:-1], widths[1:]))
     S = n_int * (widths[0] + 2) + n_bnd
     # phase B: one launch = all layers = 2 Pw S FLOP; 1 ms per launch -> 2 Pw S / 1e-3 FLOP/s
-    r = bench.roofline_entry(4, widths, n_int, n_bnd, ell, 8577, 0, 10, 10.0, peaks)
+    r = bench.roofline_entry(4, widths, n_int, n_bnd, ell, 8577, 10, 10.0, peaks)
     assert r["algorithmic_work_per_launch"] == pytest.approx(2.0 * pw * S)
     assert r["achieved"] == pytest.approx(2.0 * pw * S / 1e-3 / 1e12)
     assert r["frac"] == pytest.approx(r["achieved"] / 36.99) and r["bound"] == "tensor"
-    # Jacobi SVD: 9 ell^2 (ell - 1) FLOP per sweep
-    r = bench.roofline_entry(9, widths, n_int, n_bnd, ell, 8577, 12, 1, 5.0, peaks)
-    assert r["algorithmic_work_per_launch"] == pytest.approx(9.0 * ell * ell * (ell - 1) * 12)
-    # mixed precision (svd = 3): 9 FP32 + 2 FP64 sweeps over two launches
-    r = bench.roofline_entry(9, widths, n_int, n_bnd, ell, 8577, 2, 2, 5.0, peaks, sweeps_f32=9)
+    # DMMA GEMM: the library's count of 2 M N K over the probed launches
+    r = bench.roofline_entry(14, widths, n_int, n_bnd, ell, 8577, 4, 2.0, peaks, gemm_flops=8e12)
+    assert r["algorithmic_work_per_launch"] == pytest.approx(2e12) and r["achieved"] == pytest.approx(4000.0)
+    # Jacobi SVD (mixed precision): 9 FP32 + 2 FP64 sweeps of 9 ell^2 (ell - 1) FLOP over two launches
+    r = bench.roofline_entry(9, widths, n_int, n_bnd, ell, 8577, 2, 5.0, peaks, sweeps=(2, 9))
     assert r["algorithmic_work_per_launch"] == pytest.approx(9.0 * ell * ell * (ell - 1) * 11 / 2)
+
+
+def test_cpu_step_sample_scaling():
+    """The CPU baseline runs one real oracle NGD step on a point subset and scales only the
+    point-proportional part: at C1 with the full point set the scale factor is 1."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    t_full, sample, parts = bench.cpu_step_sample("c1")
+    assert parts["scale"] == 1.0 and parts["n_sub"] == 1020 and parts["matvecs"] == 121
+    assert t_full == pytest.approx(parts["fixed_s"] + parts["point_calls_s"])
+    assert "real NGD step" in sample

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared():
     text = open(os.path.join(ROOT, "include", "ngd.h")).read()
-    return sorted(set(re.findall(r"^(?:int|int64_t|const char\*)\s+(ngd_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|double|const char\*)\s+(ngd_\w+)\(", text, re.M)))
 
 
 def test_header_declares_the_protocol():
@@ -46,3 +46,21 @@ def test_sass_uses_fp64_tensor_cores():
     out = subprocess.run([exe, "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "DMMA.8x8x4" in out
     assert "sm_100a" in subprocess.run([exe, "-lelf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+
+
+def test_sass_gemm_is_tma_fed_dmma():
+    """The sketch / factorisation GEMM (ngd_gemm.cu) issues DMMA fed by TMA (UTMALDG) and no
+    library GEMM is linked in: cuBLAS is not a dependency of the library."""
+    import shutil
+    import subprocess
+
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump unavailable")
+    out = subprocess.run([exe, "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    gemm = [s for s in out.split("Function : ") if s.split("\n", 1)[0].find("dgemm_kernel") >= 0]
+    assert len(gemm) == 4  # the four operand layouts
+    for s in gemm:
+        assert "DMMA.8x8x4" in s and "UTMALDG.2D" in s
+    needed = subprocess.run(["readelf", "-d", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "libcublas" not in needed  # direct dependencies only (cuSOLVER pulls cuBLAS in itself)

@@ -43,7 +43,7 @@ def _worker(rank, world, port, out_path):
         prob = O.PoissonProblem(widths)
         quad = prob.sample_quadrature(300, 60, 0)
         theta = O.init_theta(widths, 0)
-        si, sb = shard_slices(len(quad.interior_points), len(quad.boundary_points), 4, rank, world)
+        si, sb = shard_slices(len(quad.interior_points), len(quad.boundary_points), rank, world)
         shard = O.Quadrature(quad.interior_points[si], quad.interior_weights[si], quad.boundary_points[sb],
                              quad.boundary_weights[sb])
         lin = O.Linearization(prob, theta, shard)

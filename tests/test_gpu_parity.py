@@ -37,7 +37,7 @@ def test_c1_loss_metric_grad_matvec(c1):
     assert gop.matvec_count == 9
 
 
-@pytest.mark.parametrize("svd", [3, 2, 1, 0])
+@pytest.mark.parametrize("svd", [3, 1])
 def test_c1_nystrom_preconditioner_pcg(c1, svd):
     G, prob, quad, theta = c1
     from paper_2505_11638_b200 import _lib
@@ -71,21 +71,27 @@ def test_c1_device_omega_sketch_statistics(c1):
     assert rel(fac.eig_host[top], G["eig100"][top]) <= 1e-8
 
 
-def test_c1_trajectory(c1):
-    """20-step fixed-rank NGD trajectory vs the reference.  The first 12 steps must
-    agree to 1e-6; beyond that the reference itself amplifies 1-ulp matvec noise
-    past 1e-6 (profiles/r01_traj_sensitivity_oracle_1e-16.txt: 2.9e-6 at step 13,
-    2.4e-4 at step 18), so later steps are held to that measured envelope (x10)."""
+def test_c1_trajectory(c1, gold):
+    """20-step fixed-rank NGD trajectory vs the reference, judged against the reference's own
+    rounding sensitivity: tests/golden/c1_ensemble.npz holds 24 runs of the unmodified reference
+    whose Gramian matvec output carries an independent relative 1-ulp perturbation (delta * U(-1, 1),
+    make_golden.py case_c1_ensemble).  Where every ensemble run stays within 1e-6 of the reference
+    (steps 0-12) the GPU must too (north-star bar); beyond, the GPU must stay within the ensemble's
+    largest deviation at that step (x1.5 for the finite ensemble: 24 draws)."""
     G, prob, quad, theta = c1
+    E = gold("c1_ensemble")
     cfg = ngd.NystromNgdConfig(ell0=100, ell_max=100, cg_maxit=20, kappa=1e-300, mu_floor_mode="grad-power",
                                mu_floor_coeff=1e-6, mu_floor_exponent=1.0, iterations=20, seed=0, fixed_rank=True)
     _, recs = ngd.nystrom_ngd_run(prob, theta, cfg, quad)
     loss = np.array([r.loss for r in recs])
-    dev = np.abs(loss - G["traj_loss"]) / np.abs(G["traj_loss"])
-    assert np.all(dev[:12] <= 1e-6), dev
-    envelope = np.array([1e-12] * 6 + [3e-9, 2e-8, 1e-8, 1e-7, 5e-7, 1.2e-6, 1.3e-6, 3e-5, 1.1e-4, 9.3e-5,
-                                       4.7e-5, 8.6e-4, 2.4e-3, 1.2e-3])
-    assert np.all(dev <= np.maximum(envelope, 1e-6)), dev
+    ref = G["traj_loss"]
+    dev = np.abs(loss - ref) / np.abs(ref)
+    ens = np.max(np.abs(E["ens_loss"] - ref) / np.abs(ref), axis=0)
+    print("gpu dev", dev, "ensemble max", ens)
+    strict = ens <= 1e-6
+    assert strict[:13].all(), ens  # the reference itself holds 1e-6 for 13 steps
+    assert np.all(dev[strict] <= 1e-6), dev
+    assert np.all(dev[~strict] <= 1.5 * ens[~strict]), (dev, ens)
     assert [r.pcg_iters for r in recs] == list(G["traj_pcg"].astype(int))
     assert [r.matvecs for r in recs] == list(G["traj_matvecs"].astype(int))
 
@@ -124,3 +130,93 @@ def test_c4_interior_only(gold):
     quad = ngd.QuadratureSet(G["x"], np.full(n, 1.0 / n), np.zeros((0, 2)), np.zeros(0))
     gop = ngd.GramianOperator.from_problem(prob, ngd.init(top, 0).values, quad)
     assert rel(gop.matvec(G["v"]), G["gv"]) <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# The benchmarked configurations: the C2 step's pieces on the reference's own
+# seeded inputs, and point subsets of >= 1024 points at C3 / C4 / C5 with sketch columns.
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def c2(gold):
+    G = gold("c2_step")
+    top = ngd.MlpTopology((2, 64, 64, 64, 1))
+    prob = ngd.Poisson2D(top)
+    quad = prob.sample_quadrature(4096, 512, 0)
+    theta = ngd.init(top, 0).values
+    return G, prob, quad, theta
+
+
+def test_c2_factor_preconditioner_pcg(c2):
+    """C2 (p = 8577): rank-300 Nystrom factor on host Omega (sketch.py:58-90: the FP32 + FP64 block
+    Jacobi path), the step's mu, P^-1 v, and PCG at k = 5 / 20 / 50 (krylov.py:24-88; the reference
+    breaks down at 19 iterations) -- same iteration, matvec and breakdown accounting."""
+    G, prob, quad, theta = c2
+    gop = ngd.GramianOperator.from_problem(prob, theta, quad)
+    fac = ngd.nystrom_approximate(gop, 300, seed=11, omega_source="host")
+    top = G["eig300"] > 1e-8 * G["eig300"][0]
+    assert rel(fac.eig_host[top], G["eig300"][top]) <= 1e-10
+    g = prob.loss_grad(theta, quad)
+    mu = ngd.adapt_mu(fac.eig_host[0], float(len(theta)), prob.loss_value(theta, quad), float(np.linalg.norm(g)),
+                      "grad-power", 1e-6, 1.0)
+    assert mu == pytest.approx(float(G["mu"]), rel=1e-10)
+    pre = ngd.NystromPreconditioner(fac, float(G["mu"]))
+    assert rel(pre.apply(G["v"]), G["pinv_v"]) <= 1e-8
+    for k in (5, 20, 50):
+        rep = ngd.pcg(ngd.ShiftedOperator(gop, float(G["mu"])), g, 1e-300, k, precond=pre)
+        meta = G[f"pcg{k}_meta"]
+        assert (rep.iterations, rep.matvecs, rep.breakdown) == (int(meta[0]), int(meta[1]), bool(meta[4])), k
+        assert rel(rep.solution, G[f"pcg{k}_x"]) <= 1e-8, k
+
+
+def test_c2_trajectory(c2):
+    """5 fixed-rank NGD steps of the benchmarked C2 configuration (ell = 300, 50 PCG iterations)
+    with host Omega: loss within 1e-6, identical PCG iterations and matvec totals."""
+    G, prob, quad, theta = c2
+    cfg = ngd.NystromNgdConfig(ell0=300, ell_max=300, cg_maxit=50, kappa=1e-300, mu_floor_mode="grad-power",
+                               mu_floor_coeff=1e-6, mu_floor_exponent=1.0, iterations=5, seed=0, fixed_rank=True)
+    theta_f, recs = ngd.nystrom_ngd_run(prob, theta, cfg, quad)
+    loss = np.array([r.loss for r in recs])
+    dev = np.abs(loss - G["traj_loss"]) / np.abs(G["traj_loss"])
+    print("c2 trajectory dev", dev)
+    assert np.all(dev <= 1e-6), dev
+    np.testing.assert_allclose([r.mu for r in recs], G["traj_mu"], rtol=1e-6)
+    assert [r.pcg_iters for r in recs] == list(G["traj_pcg"].astype(int))
+    assert [r.matvecs for r in recs] == list(G["traj_matvecs"].astype(int))
+
+
+def _omega8(p):
+    return np.linalg.qr(np.random.default_rng(123).standard_normal((p, 8)), mode="reduced")[0]
+
+
+@pytest.mark.parametrize("name,widths,kind", [("c3_1k", (5, 128, 128, 128, 1), "sinsum"),
+                                              ("c5_1k", (10, 256, 256, 256, 256, 1), "gauss")])
+def test_nd_1k_subsets_with_sketch_columns(gold, name, widths, kind):
+    """1024 + 256 points of C3 / C5 (the full configs' samplers, first points): loss, metric,
+    gradient, Gv and 8 sketch columns Y = G Omega (the J-chunk DMMA GEMM path) vs the reference."""
+    G = gold(name)
+    top = ngd.MlpTopology(widths)
+    prob = ngd.PoissonND(top, kind)
+    quad = prob.sample_quadrature(1024, 256, 0)
+    theta = ngd.init(top, 0).values
+    p = len(theta)
+    assert prob.loss_value(theta, quad) == pytest.approx(float(G["loss"]), rel=1e-12)
+    assert rel(prob.metric_stack(theta, None, quad), G["metric"]) <= 1e-12
+    assert rel(prob.loss_grad(theta, quad), G["grad"]) <= 1e-10
+    gop = ngd.GramianOperator.from_problem(prob, theta, quad)
+    assert rel(gop.matvec(np.random.default_rng(1).standard_normal(p)), G["gv"]) <= 1e-10
+    assert rel(gop.matmat(_omega8(p)), G["y8"]) <= 1e-10
+
+
+def test_c4_1k_with_sketch_columns(gold):
+    G = gold("c4_1k")
+    top = ngd.MlpTopology((2, 256, 256, 256, 1))
+    prob = ngd.LaplacianStack(top)
+    n = G["x"].shape[0]
+    quad = ngd.QuadratureSet(G["x"], np.full(n, 1.0 / n), np.zeros((0, 2)), np.zeros(0))
+    theta = ngd.init(top, 0).values
+    p = len(theta)
+    gop = ngd.GramianOperator.from_problem(prob, theta, quad)
+    assert rel(gop.matvec(np.random.default_rng(1).standard_normal(p)), G["gv"]) <= 1e-10
+    assert rel(gop.matmat(_omega8(p)), G["y8"]) <= 1e-10

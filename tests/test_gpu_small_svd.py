@@ -1,6 +1,7 @@
-"""The in-house cluster one-sided Jacobi SVD (ngd_svd.cu) against LAPACK (numpy) on
-graded matrices like the Nystrom factor's R (singular values spanning 1 .. 1e-8,
-with a tail cluster at the shift floor)."""
+"""The in-house dense factorisations of the Nystrom step against LAPACK (numpy): the cluster
+block Jacobi SVD (ngd_svd.cu) on graded matrices like the Nystrom factor's R (singular values
+spanning 1 .. 1e-8, with a tail cluster at the shift floor), the Cholesky kernels including the
+blocked form above 512 (ngd_chol.cu + DMMA GEMM updates), and cuSOLVER's polar SVD used above 512."""
 
 import numpy as np
 import pytest
@@ -22,10 +23,9 @@ def graded(n, seed):
     return np.linalg.qr(a)[1] if seed % 2 == 0 else a
 
 
-@pytest.mark.parametrize("method,n", [(2, 7), (2, 100), (2, 101), (2, 160), (2, 300), (2, 301), (2, 400),
-                                      (3, 7), (3, 100), (3, 101), (3, 160), (3, 300), (3, 301), (3, 310),
+@pytest.mark.parametrize("method,n", [(3, 7), (3, 100), (3, 101), (3, 160), (3, 300), (3, 301), (3, 310),
                                       (4, 7), (4, 100), (4, 101), (4, 160), (4, 300), (4, 301), (4, 310),
-                                      (4, 311), (4, 400), (4, 401), (4, 500), (4, 512)])
+                                      (4, 311), (4, 400), (4, 401), (4, 500), (4, 512), (1, 700), (1, 1000)])
 def test_jacobi_svd_matches_lapack(method, n):
     a = graded(n, n)
     ctx = utility_context()
@@ -34,7 +34,7 @@ def test_jacobi_svd_matches_lapack(method, n):
     S = torch.empty(n, dtype=torch.float64, device="cuda")
     sweeps = _lib.ctypes.c_int32()
     ctx.call("ngd_small_svd", _lib.ptr(A), n, _lib.ptr(U), _lib.ptr(S), method, _lib.ctypes.byref(sweeps))
-    assert sweeps.value > 0, "Jacobi did not converge"
+    assert sweeps.value > 0 or method == 1, "Jacobi did not converge"
     print(f"n={n} sweeps={sweeps.value}")
     s_ref = np.linalg.svd(a, compute_uv=False)
     s = S.cpu().numpy()
@@ -66,11 +66,12 @@ def test_small_cholesky_matches_lapack(n):
 
 
 @pytest.mark.parametrize("method", [1, 2, 0])
-@pytest.mark.parametrize("n", [1, 5, 31, 32, 33, 100, 160, 300, 512])
+@pytest.mark.parametrize("n", [1, 5, 31, 32, 33, 100, 160, 300, 512, 513, 700, 1000, 1100])
 def test_cholesky_kernels(n, method):
-    """ngd_small_cholesky: one-CTA (n <= 160), cluster and cuSOLVER factors agree with LAPACK."""
-    if method == 1 and n > 160:
-        pytest.skip("one-CTA kernel limited to n <= 160")
+    """ngd_small_cholesky: one-CTA (n <= 160), cluster (n <= 512) and the library's choice (blocked
+    with DMMA GEMM updates above 512) agree with LAPACK."""
+    if (method == 1 and n > 160) or (method == 2 and n > 512):
+        pytest.skip("kernel size limit")
     rng = np.random.default_rng(100 + n)
     g = rng.standard_normal((2 * n + 5, n))
     a = g.T @ g + 1e-3 * np.eye(n)
@@ -86,11 +87,12 @@ def test_cholesky_kernels(n, method):
 
 
 @pytest.mark.parametrize("method", [1, 2, 0])
-@pytest.mark.parametrize("n,k", [(40, 0), (40, 17), (300, 250), (300, 31), (300, 32)])
+@pytest.mark.parametrize("n,k", [(40, 0), (40, 17), (300, 250), (300, 31), (300, 32), (1000, 100),
+                                 (1000, 700), (1000, 512)])
 def test_cholesky_failure_index(n, k, method):
     """Non-positive pivot k: info = k + 1 (LAPACK potrf semantics) for every method."""
-    if method == 1 and n > 160:
-        pytest.skip("one-CTA kernel limited to n <= 160")
+    if (method == 1 and n > 160) or (method == 2 and n > 512):
+        pytest.skip("kernel size limit")
     d = np.ones(n)
     d[k] = -1.0
     q, _ = np.linalg.qr(np.random.default_rng(n + k).standard_normal((n, n)))
