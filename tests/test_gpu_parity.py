@@ -172,7 +172,12 @@ def test_c2_factor_preconditioner_pcg(c2):
 
 def test_c2_trajectory(c2):
     """5 fixed-rank NGD steps of the benchmarked C2 configuration (ell = 300, 50 PCG iterations)
-    with host Omega: loss within 1e-6, identical PCG iterations and matvec totals."""
+    with host Omega: loss and mu within 1e-6.  Every C2 step ends in a PCG breakdown (d.Ad <= 0 once
+    the residual reaches rounding level), and WHEN it triggers is itself a rounding event: the
+    oracle with a relative 1-ulp perturbation of each matvec stops at 23 / 25 / 28 iterations in
+    step 5 (profiles/r02_c2_pcg_breakdown_sensitivity.txt, tools/c2_pcg_sensitivity.py) while its
+    loss moves by 2e-10.  So the iteration counts are held to that measured spread (+-5), and the
+    matvec totals to ell + iterations + 2 per step (breakdown matvec + final true residual)."""
     G, prob, quad, theta = c2
     cfg = ngd.NystromNgdConfig(ell0=300, ell_max=300, cg_maxit=50, kappa=1e-300, mu_floor_mode="grad-power",
                                mu_floor_coeff=1e-6, mu_floor_exponent=1.0, iterations=5, seed=0, fixed_rank=True)
@@ -182,8 +187,12 @@ def test_c2_trajectory(c2):
     print("c2 trajectory dev", dev)
     assert np.all(dev <= 1e-6), dev
     np.testing.assert_allclose([r.mu for r in recs], G["traj_mu"], rtol=1e-6)
-    assert [r.pcg_iters for r in recs] == list(G["traj_pcg"].astype(int))
-    assert [r.matvecs for r in recs] == list(G["traj_matvecs"].astype(int))
+    its = np.array([r.pcg_iters for r in recs])
+    print("pcg iterations", its, "reference", G["traj_pcg"])
+    assert np.all(np.abs(its - G["traj_pcg"]) <= 5)
+    assert np.all(its[:2] == G["traj_pcg"][:2])  # the first steps agree exactly
+    per_step = np.diff(np.concatenate([[0], [r.matvecs for r in recs]]))
+    assert np.array_equal(per_step, 300 + its + 2)  # the breakdown iteration's matvec + the final residual
 
 
 def _omega8(p):

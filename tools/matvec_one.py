@@ -15,7 +15,7 @@ for kv in sys.argv[3:]:  # key=value library options, e.g. phb_cs=1
     _lib.set_option(k, int(v))
 side = torch.cuda.Stream()
 torch.cuda.set_stream(side)  # a non-default stream can carry the L2 access-policy window
-prob, quad, theta0, _ = bench.make_problem(ngd, cfg, 1, 0)
+prob, quad, theta0, _ = bench.make_problem(ngd, cfg)
 gop = ngd.GramianOperator.from_problem(prob, theta0, quad)
 v = torch.randn(gop.dim, dtype=torch.float64, device="cuda")
 out = torch.empty_like(v)
