@@ -152,8 +152,11 @@ struct ngd_ctx {
   Buf dseed, pre_last, zs0, zs1;
   Buf jets;  // arena behind zin / dbuf / dseed
   int force_comm = 0;  // "force_comm": build a communicator (and take the multi-rank paths) even for 1 rank
-  int phb_thin[kMaxLayers] = {};  // phase B: thin layers (N <= 16 or M <= 16)
+  int phb_thin[kMaxLayers] = {};  // phase B route per layer: 0 ngd_phb2.cu 64 x 64 tiles, 1 thin (N <= 16 or
+                                  // M <= 16, ngd_phb2.cu), 2 wide (both >= 128) on the GEMM core (ngd_phbg.cu)
   Phb2Cache phb2_cache;           // phase B: tensor maps of this context's jets
+  PhbgArgs phbg{};                // wide-layer phase B plan (n_heavy = 0: none)
+  PhbgCache phbg_cache;
   int l2u = 1;      // option "l2u": keep the preconditioner basis U L2-persisting during PCG
   Buf u_persist;     // PCG's copy of U at a fixed address (the captured graph carries its L2 window)
   size_t jets_arena = 0;
@@ -395,12 +398,25 @@ static void fill_phb(ngd_ctx* c, const double* cot, const int* skip, PhbAll& pb)
   for (int l = 0; l < c->NL; ++l) pb.thin[l] = c->phb_thin[l];
 }
 
-// out = J^T cot (+ mu v), all-reduced over ranks
-static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* mu_p, const double* v, double* out,
-                       const int* skip) {
+// J^T cot partials of every layer into partB: wide layers on the GEMM core, the rest (thin input /
+// output layers, narrow hidden layers) on the 64 x 64-tile pipeline
+static int phase_b_partials(ngd_ctx* c, const double* cot, const int* skip) {
+  if (c->phbg.n_heavy) {
+    c->phbg.cvec = cot;
+    c->phbg.part = c->partB.d();
+    c->phbg.skip = skip;
+    CK(phase_b_gemm(c->phbg, c->phbg_cache, c->stream));
+  }
   PhbAll pb{};
   fill_phb(c, cot, skip, pb);
   CK(phase_b2_all_layers(pb, c->phb2_cache, c->stream));
+  return NGD_OK;
+}
+
+// out = J^T cot (+ mu v), all-reduced over ranks
+static int phase_b_all(ngd_ctx* c, const double* cot, double mu, const double* mu_p, const double* v, double* out,
+                       const int* skip) {
+  TRY(phase_b_partials(c, cot, skip));
   const bool shifted = v && (mu_p || mu != 0.0);
   if (c->comm) {
     reduce_splits(c->partB.d(), c->rplan, c->p, 0.0, nullptr, nullptr, out, skip, c->stream);
@@ -866,17 +882,41 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
   {
     const int kt = (int)(gm.s_pad / 16);
     int heavy = 0, thin = 0;
+    PhbgArgs& pg = c->phbg;
+    pg = PhbgArgs{};
     for (int l = 0; l < c->NL; ++l) {
       const int M = c->w[l + 1], N = c->w[l];
-      c->phb_thin[l] = (M <= 16 || N <= 16) ? 1 : 0;
+      c->phb_thin[l] = phbg_layer_ok(M, N) ? 2 : ((M <= 16 || N <= 16) ? 1 : 0);
+      if (c->phb_thin[l] == 2) {
+        const int h = pg.n_heavy++;
+        pg.M[h] = M;
+        pg.N[h] = N;
+        pg.tiles_n[h] = (N + 127) / 128;
+        pg.item_start[h + 1] = pg.item_start[h] + ((M + 127) / 128) * pg.tiles_n[h];
+        pg.off[h] = c->woff[l];
+        c->phbg_cache.src_d[h] = (l == c->NL - 1) ? c->dseed.d() : c->dbuf[l].d();
+        c->phbg_cache.src_z[h] = c->zin[l].d();
+        continue;
+      }
       (c->phb_thin[l] ? thin : heavy) += ((M + 63) / 64) * ((N + 63) / 64);
+    }
+    if (pg.n_heavy) {
+      pg.kstages = kt;
+      pg.G = phbg_splits(pg.item_start[pg.n_heavy], kt);
+      pg.kps = (kt + pg.G - 1) / pg.G;
+      pg.G = (kt + pg.kps - 1) / pg.kps;  // no empty splits
+      pg.int_units = gm.nib * gm.C;
+      pg.C = gm.C;
+      pg.nib = gm.nib;
+      pg.p = c->p;
+      c->phbg_cache.s_pad = gm.s_pad;
     }
     const int gh = heavy ? std::max(1, std::min(kt, 148 / heavy)) : 1;
     const int gt = thin ? std::max(1, std::min(kt, 148 / thin)) : 1;
     int maxg = 0;
     c->rplan.n_layers = c->NL;
     for (int l = 0; l < c->NL; ++l) {
-      const int Gl = c->phb_thin[l] ? gt : gh;
+      const int Gl = c->phb_thin[l] == 2 ? pg.G : (c->phb_thin[l] ? gt : gh);
       c->Gl[l] = Gl;
       c->kpsl[l] = (kt + Gl - 1) / Gl;
       c->rplan.start[l] = c->woff[l];
@@ -1292,9 +1332,7 @@ static int pcg_iteration(ngd_ctx* c, int64_t p, const double* dense, double mu, 
     pcg_ad(nullptr, c->rplan, p, mu_p, dv, ad, sp, 1, red, c->counter(4), c->stream);
   } else {
     TRY(phase_a(c, dv, c->w_pad.d(), c->cot.d(), done, /*prepacked=*/true));
-    PhbAll pb{};
-    fill_phb(c, c->cot.d(), done, pb);
-    CK(phase_b2_all_layers(pb, c->phb2_cache, c->stream));
+    TRY(phase_b_partials(c, c->cot.d(), done));
     if (c->comm) {
       reduce_splits(c->partB.d(), c->rplan, p, 0.0, nullptr, nullptr, ad, done, c->stream);
       TRY(allreduce(c, ad, p));

@@ -172,6 +172,37 @@ struct Phb2Cache {  // host-side: re-encoded when a layer's buffers or shape cha
   int64_t ks[kMaxLayers] = {};
 };
 cudaError_t phase_b2_all_layers(const PhbAll& a, Phb2Cache& cache, cudaStream_t st);
+// phase B of the wide layers on the DMMA GEMM core (ngd_phbg.cu): items (split, heavy layer, tile)
+struct PhbgArgs {
+  int n_heavy;                         // layers handled here (both sides >= 128)
+  int M[kMaxLayers], N[kMaxLayers];    // n_l, n_{l-1} of heavy layer h
+  int tiles_n[kMaxLayers];             // 128-wide n tiles of heavy layer h
+  int item_start[kMaxLayers + 1];      // tiles of the heavy layers before h (one split)
+  int64_t off[kMaxLayers];             // W_l offset in the parameter vector
+  int G, kstages, kps;                 // K splits, 16-column stages, stages per split
+  const double* cvec;                  // per padded point cotangent
+  int int_units, C, nib;               // interior stages (nib * C), channels, interior point blocks
+  double* part;                        // [G][p] partials (flat parameter layout)
+  int64_t p;
+  const int* skip;
+};
+struct PhbgMaps {
+  CUtensorMap d[kMaxLayers];  // D_l [M rows][s_pad], box 16 x 128
+  CUtensorMap z[kMaxLayers];  // Zin_l [N rows][s_pad]
+};
+struct PhbgCache {
+  PhbgMaps maps;
+  const double* src_d[kMaxLayers] = {};  // set by the caller: the heavy layers' operands
+  const double* src_z[kMaxLayers] = {};
+  int64_t s_pad = 0;
+  const double* kd[kMaxLayers] = {};
+  const double* kz[kMaxLayers] = {};
+  int km[kMaxLayers] = {}, kn[kMaxLayers] = {};
+  int64_t ks[kMaxLayers] = {};
+};
+bool phbg_layer_ok(int M, int N);
+int phbg_splits(int tiles, int kstages);
+cudaError_t phase_b_gemm(const PhbgArgs& a, PhbgCache& cache, cudaStream_t st);
 int phb2_ctas_per_sm();
 void pack_all(const PackAll& a, const double* src, const int* skip, cudaStream_t st);
 cudaError_t form_j(const FormJArgs& a, int nblocks, int n_layers, int max_nin, int max_nout, cudaStream_t st);

@@ -1,4 +1,4 @@
-"""Phase B (J^T c, ngd_phb2.cu) on topologies that exercise its tile plan: partial 64x64 tiles,
+"""Phase B (J^T c, ngd_phb2.cu and ngd_phbg.cu) on topologies that exercise its tile plans: partial 64x64 tiles,
 several m/n tiles per layer, 'heavy' layers just above the thin threshold (17 x 33), thin
 input layers with N = d up to 10 (two 8-column blocks) and the M = 1 output layer.  Each
 Gramian matvec and gradient is checked against the CPU oracle."""
@@ -19,6 +19,11 @@ CASES = [
     ("sin2d", (2, 8, 16, 8, 1), 160, 32),
     ("sinsum", (10, 40, 24, 1), 192, 48),
     ("gauss", (5, 70, 1), 192, 48),
+    # wide layers (both sides >= 128) on the DMMA GEMM core (ngd_phbg.cu): full / partial 128 tiles,
+    # several tiles per layer, mixed with phb2 layers in the same matvec
+    ("sin2d", (2, 128, 128, 1), 256, 64),
+    ("gauss", (10, 256, 200, 130, 1), 192, 48),
+    ("sinsum", (3, 130, 257, 64, 1), 160, 32),
 ]
 
 
