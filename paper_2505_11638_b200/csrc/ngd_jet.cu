@@ -384,75 +384,100 @@ cudaError_t jet_gemm(int C, int mode, const JetArgs& a, int nblocks, int mtiles,
 // ---------------------------------------------------------------------------
 // Explicit Jacobian rows for the sketch (J-chunk formulation):
 //   Jt[pt][off_l + a*n_in + b] = sum_c D_l[a][(pt,c)] Zin_l[b][(pt,c)],  Jt[pt][off_bl + a] = D_l[a][(pt,0)]
-// One CTA per (point block of 16, layer, 32-row a-tile, 64-col b-tile): the D and Zin
-// slices of the block are staged in shared memory with coalesced 128-B reads, every
-// staged value is reused 16-64x, and the Jacobian rows are written coalesced along b.
-// Write-bound: 8 * p bytes per point.
-constexpr int FJ_A = 32, FJ_B = 64;
+// i.e. per point a rank-C outer-product sum: a 64 x 64 tile of J_r[W_l] is an (a x c) . (c x b)
+// product with K = C channels (<= 12: three DMMA k-steps of 4).  One CTA per (point block of 16,
+// layer, 64 x 64 tile): the block's D and Zin rows of the tile are staged in shared memory
+// (coalesced 128-byte channel runs), then every warp owns one 8-row band of the tile for all 16
+// points (8 DMMA blocks x k-steps per point) and stores its rows of J straight from the
+// accumulators.  Write-bound: 8 p bytes per point (the previous scalar-FMA form issued one shared
+// load per FMA and ran at 0.64 TB/s at C5, profiles/r02_launches_c5_summary.txt).
+// Shared layout: element (row, channel c, point r) at row * FJ_LD + c * 17 + r -- the channel
+// stride 17 and FJ_LD = 4 (mod 16) make every DMMA fragment load two wavefronts.
+constexpr int FJ_T = 64;                     // tile rows (a) and columns (b)
+constexpr int FJ_CS = 17;                    // channel stride in shared memory (doubles)
+constexpr int FJ_LD = 12 * FJ_CS + 8;        // 212 = 4 (mod 16)
+constexpr int FJ_THREADS = 256;
 
-__global__ void __launch_bounds__(kThreads) formj_kernel(FormJArgs a) {
-  extern __shared__ __align__(16) double sm[];
+__global__ void __launch_bounds__(FJ_THREADS, 1) formj_kernel(FormJArgs a) {
+  extern __shared__ __align__(16) double fsm[];
+  double* Ds = fsm;                 // [FJ_T][FJ_LD]
+  double* Zs = fsm + FJ_T * FJ_LD;  // [FJ_T][FJ_LD]
   const int l = blockIdx.y;
   const int nin = a.n_in[l], nout = a.n_out[l];
-  const int tiles_b = (nin + FJ_B - 1) / FJ_B;
-  const int a0 = (blockIdx.z / tiles_b) * FJ_A, b0 = (blockIdx.z % tiles_b) * FJ_B;
+  const int tiles_b = (nin + FJ_T - 1) / FJ_T;
+  const int a0 = (blockIdx.z / tiles_b) * FJ_T, b0 = (blockIdx.z % tiles_b) * FJ_T;
   if (a0 >= nout) return;
   const int blk = a.blk0 + blockIdx.x;  // global point block
   const bool interior = blk < a.nib;
   const int Cs = interior ? a.C : 1;
-  const int ncols = PB * Cs;
-  const int stride = ncols + 1;  // odd -> conflict-free column reads
+  const int nks = (Cs + 3) / 4;         // DMMA k-steps (channels padded to a multiple of 4 with zeros)
   const int64_t cbase = interior ? (int64_t)blk * PB * a.C : a.int_cols + (int64_t)(blk - a.nib) * PB;
-  double* Zs = sm;                      // [FJ_B][stride]
-  double* Ds = sm + FJ_B * stride;      // [FJ_A][stride]
   const double* Z = a.Z[l];
   const double* D = a.D[l];
-  const int nb = min(FJ_B, nin - b0), na = min(FJ_A, nout - a0);
-  for (int e = threadIdx.x; e < nb * ncols; e += blockDim.x) {
-    const int r = e / ncols, cc = e % ncols;
-    Zs[r * stride + cc] = Z[(int64_t)(b0 + r) * a.s_pad + cbase + cc];
-  }
-  for (int e = threadIdx.x; e < na * ncols; e += blockDim.x) {
-    const int r = e / ncols, cc = e % ncols;
-    Ds[r * stride + cc] = D[(int64_t)(a0 + r) * a.s_pad + cbase + cc];
+  const int nb = min(FJ_T, nin - b0), na = min(FJ_T, nout - a0);
+  const int ncols = PB * 4 * nks;  // channels 0 .. 4 nks - 1 (zero past Cs)
+  for (int e = threadIdx.x; e < FJ_T * ncols; e += FJ_THREADS) {
+    const int r = e / ncols, cc = e - r * ncols;  // cc = c * 16 + point
+    const int c = cc >> 4, pt = cc & 15;
+    const bool on = c < Cs;
+    Zs[r * FJ_LD + c * FJ_CS + pt] = (on && r < nb) ? Z[(int64_t)(b0 + r) * a.s_pad + cbase + cc] : 0.0;
+    Ds[r * FJ_LD + c * FJ_CS + pt] = (on && r < na) ? D[(int64_t)(a0 + r) * a.s_pad + cbase + cc] : 0.0;
   }
   __syncthreads();
-  const int bi = threadIdx.x % FJ_B, ar = threadIdx.x / FJ_B;  // 4 a-rows in flight
-  const int64_t prow0 = (int64_t)blockIdx.x * PB;                // chunk-local padded point row
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int64_t prow0 = (int64_t)blockIdx.x * PB;  // chunk-local padded point row
   const int64_t off = a.off[l];
+  const int arow = warp * 8 + g;  // this lane's tile row (A fragment / accumulator row)
+  const bool row_ok = arow < na;
+  const bool vec2 = ((off + (int64_t)(a0 + arow) * nin + b0) & 1) == 0 && (a.ldj & 1) == 0;
   for (int r = 0; r < PB; ++r) {
-    double* row = a.Jt + (prow0 + r) * a.ldj;
-    if (bi < nb) {
-      double z[12];
+    double acc[8][2];
 #pragma unroll
-      for (int c = 0; c < 12; ++c) z[c] = (c < Cs) ? Zs[bi * stride + c * PB + r] : 0.0;
-      for (int ai = ar; ai < na; ai += kThreads / FJ_B) {
-        const double* dr = Ds + ai * stride + r;
-        double s = 0.0;
+    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
-        for (int c = 0; c < 12; ++c)
-          if (c < Cs) s = fma(dr[c * PB], z[c], s);
-        row[off + (int64_t)(a0 + ai) * nin + b0 + bi] = s;
+    for (int ks = 0; ks < 3; ++ks) {
+      if (ks < nks) {
+        const int c = ks * 4 + t;
+        const double av = Ds[arow * FJ_LD + c * FJ_CS + r];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma884(acc[j][0], acc[j][1], av, Zs[(j * 8 + g) * FJ_LD + c * FJ_CS + r]);
       }
     }
-    if (b0 == 0)  // bias entries: value channel of D
-      for (int ai = threadIdx.x; ai < na; ai += blockDim.x) row[off + (int64_t)nout * nin + a0 + ai] = Ds[ai * stride + r];
+    double* row = a.Jt + (prow0 + r) * a.ldj + off + (int64_t)(a0 + arow) * nin + b0;
+    if (row_ok) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int col = j * 8 + 2 * t;
+        if (vec2 && col + 1 < nb) {
+          *reinterpret_cast<double2*>(row + col) = make_double2(acc[j][0], acc[j][1]);
+        } else {
+          if (col < nb) row[col] = acc[j][0];
+          if (col + 1 < nb) row[col + 1] = acc[j][1];
+        }
+      }
+    }
+    if (b0 == 0 && threadIdx.x < na)  // bias entries: value channel of D
+      a.Jt[(prow0 + r) * a.ldj + off + (int64_t)nout * nin + a0 + threadIdx.x] = Ds[threadIdx.x * FJ_LD + r];
   }
 }
 
-size_t formj_smem(int C) { return sizeof(double) * (FJ_B + FJ_A) * (PB * C + 1); }
+size_t formj_smem(int C) {
+  (void)C;
+  return sizeof(double) * 2 * FJ_T * FJ_LD;
+}
 
 cudaError_t form_j(const FormJArgs& a, int nblocks, int n_layers, int max_nin, int max_nout, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
+  if (a.C > 12) return cudaErrorInvalidValue;
   const size_t smem = formj_smem(a.C);
   static size_t attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(formj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  const int tz = ((max_nout + FJ_A - 1) / FJ_A) * ((max_nin + FJ_B - 1) / FJ_B);
+  const int tz = ((max_nout + FJ_T - 1) / FJ_T) * ((max_nin + FJ_T - 1) / FJ_T);
   probe_before(K_FORMJ, st);
-  formj_kernel<<<dim3(nblocks, n_layers, tz), kThreads, smem, st>>>(a);
+  formj_kernel<<<dim3(nblocks, n_layers, tz), FJ_THREADS, smem, st>>>(a);
   probe_after(K_FORMJ, st);
   return cudaGetLastError();
 }
