@@ -334,9 +334,13 @@ def roofline_entry(kind, widths, n_int, n_bnd, ell, p, count, total_ms, peaks, g
     pw = sum(i * o for i, o in zip(widths[:-1], widths[1:]))
     bound, unit, peak = "tensor", "TFLOP/s", peaks["fp64_tflops"]
     note = ""
-    if kind in (3, 4):  # one launch = all layers: 2 Pw S FLOP
+    if kind == 3:  # one launch = all layers: 2 Pw S FLOP
         work = 2.0 * pw * S
-        note = "2 P_w S FLOP per launch (all layers, one phase of the factored Gramian matvec)"
+        note = "2 P_w S FLOP per launch (all layers, phase A of the factored Gramian matvec)"
+    elif kind == 4:  # phase B: the wide layers' GEMM-core launch + the 64 x 64-tile launch (ngd_phbg/phb2)
+        per = 2 if any(i >= 256 and o >= 256 for i, o in zip(widths[:-1], widths[1:])) else 1
+        work = 2.0 * pw * S / per
+        note = f"2 P_w S FLOP per phase B ({per} launch(es) per matvec)"
     elif kind in (1, 2):
         work = 2.0 * pw * S / (2 * nl)
         note = "2 P_w S / (2 layers) FLOP per launch (average layer)"

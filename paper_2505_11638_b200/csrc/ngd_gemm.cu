@@ -38,18 +38,26 @@
 namespace ngd {
 
 namespace {
-constexpr int GBM = 128, GBN = 128, GBK = 16;
-constexpr int GNS = 6;     // ring depth
-constexpr int GAHEAD = 4;  // stages in flight ahead of the MMA warps (slack GNS - GAHEAD)
+constexpr int GBK = 16;
+// ring depth: 6 stages of 32 KB (128 x 128) or 5 of 40 KB (256 x 64); stages in flight ahead of
+// the MMA warps: depth - 2 (slack of two stages)
+template <int BM, int BN>
+constexpr int gemm_ns() { return (BM + BN) * GBK * 8 * 6 <= 200 * 1024 ? 6 : 5; }
 constexpr int kGemmConsumers = 8;
 constexpr int kGemmThreads = kGemmConsumers * 32;
 constexpr int kSms = 148;
 
+// CTA tile BM x BN: 128 x 128 (2 x 4 warps of 64 x 32) or 256 x 64 (4 x 2 warps) -- the latter for
+// narrow products (ell = 300: 5 tiles of 64 instead of 3 of 128, 6% padding instead of 28%)
+template <int BM, int BN>
 struct __align__(1024) GStage {
-  double A[GBM * GBK];
-  double B[GBN * GBK];
+  double A[BM * GBK];
+  double B[BN * GBK];
 };
-constexpr size_t kGemmSmem = sizeof(GStage) * GNS + 2 * GNS * sizeof(unsigned long long) + 1024;
+template <int BM, int BN>
+constexpr size_t gemm_smem() {
+  return sizeof(GStage<BM, BN>) * gemm_ns<BM, BN>() + 2 * gemm_ns<BM, BN>() * sizeof(unsigned long long) + 1024;
+}
 
 __device__ __forceinline__ unsigned g_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void g_mbar_init(unsigned long long* m, unsigned count) {
@@ -107,14 +115,15 @@ __device__ __forceinline__ GItem decode(const GemmArgs& a, int idx) {
 struct GCursor {
   int idx, s, s1, m0, n0;
 };
+template <int BM, int BN>
 __device__ __forceinline__ bool cursor_load(const GemmArgs& a, int n_items, GCursor& c) {
   while (c.idx < n_items) {
     const GItem it = decode(a, c.idx);
     if (it.s0 < it.s1) {
       c.s = it.s0;
       c.s1 = it.s1;
-      c.m0 = it.tm * GBM;
-      c.n0 = it.tn * GBN;
+      c.m0 = it.tm * BM;
+      c.n0 = it.tn * BN;
       return true;
     }
     c.idx += gridDim.x;
@@ -122,32 +131,35 @@ __device__ __forceinline__ bool cursor_load(const GemmArgs& a, int n_items, GCur
   return false;
 }
 
-template <bool AK, bool BK>
-__device__ __forceinline__ void issue_stage(GStage& st, const CUtensorMap& mapA, const CUtensorMap& mapB,
+template <int BM, int BN, bool AK, bool BK>
+__device__ __forceinline__ void issue_stage(GStage<BM, BN>& st, const CUtensorMap& mapA, const CUtensorMap& mapB,
                                             const GCursor& c, unsigned long long* full) {
-  g_expect_tx(full, sizeof(GStage));
+  g_expect_tx(full, sizeof(double) * (BM + BN) * GBK);
   const int k0 = c.s * GBK;
   if (AK) {
     g_tma2d(st.A, &mapA, k0, c.m0, full);
   } else {
 #pragma unroll
-    for (int b = 0; b < GBM / 16; ++b) g_tma2d(st.A + b * 256, &mapA, c.m0 + b * 16, k0, full);
+    for (int b = 0; b < BM / 16; ++b) g_tma2d(st.A + b * 256, &mapA, c.m0 + b * 16, k0, full);
   }
   if (BK) {
     g_tma2d(st.B, &mapB, k0, c.n0, full);
   } else {
 #pragma unroll
-    for (int b = 0; b < GBN / 16; ++b) g_tma2d(st.B + b * 256, &mapB, c.n0 + b * 16, k0, full);
+    for (int b = 0; b < BN / 16; ++b) g_tma2d(st.B + b * 256, &mapB, c.n0 + b * 16, k0, full);
   }
 }
 
-template <bool AK, bool BK>
+template <int BM, int BN, bool AK, bool BK>
 __global__ void __maxnreg__(224)
     dgemm_kernel(const __grid_constant__ GemmArgs a, const __grid_constant__ CUtensorMap mapA,
                  const __grid_constant__ CUtensorMap mapB) {
+  constexpr int WGN = BN / 32;  // warps along n (64 x 32 warp tiles, 8 warps)
+  constexpr int GNS = gemm_ns<BM, BN>(), GAHEAD = GNS - 2;
+  static_assert((BM / 64) * WGN == kGemmConsumers, "8 warps of 64 x 32");
   extern __shared__ unsigned char gsm_raw[];
   unsigned char* base = gsm_raw + ((1024u - (g_smem(gsm_raw) & 1023u)) & 1023u);
-  GStage* st = reinterpret_cast<GStage*>(base);
+  GStage<BM, BN>* st = reinterpret_cast<GStage<BM, BN>*>(base);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(st + GNS);
   unsigned long long* empty = full + GNS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -162,10 +174,10 @@ __global__ void __maxnreg__(224)
   const int n_items = a.tiles_m * a.tiles_n * a.splits;
   const bool producer = (tid == 0);
   GCursor pc{(int)blockIdx.x, 0, 0, 0, 0};
-  bool p_valid = producer ? cursor_load(a, n_items, pc) : false;
+  bool p_valid = producer ? cursor_load<BM, BN>(a, n_items, pc) : false;
   unsigned qp = 0;  // next ring position the producer fills
   // warp (wm, wn) owns rows wm*64 .. +63, cols wn*32 .. +31 of the tile
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / WGN, wn = warp % WGN;
   const int g = lane >> 2, t = lane & 3;
   const int koff = ((t & 1) << 2) | (t >> 1);  // {0, 4, 1, 5}
   unsigned q = 0;  // ring position of the next stage consumed
@@ -181,11 +193,11 @@ __global__ void __maxnreg__(224)
         while (p_valid && qp < q + GAHEAD) {
           const int slot = qp % GNS;
           if (qp >= GNS) g_wait(&empty[slot], ((qp / GNS) - 1) & 1u);
-          issue_stage<AK, BK>(st[slot], mapA, mapB, pc, &full[slot]);
+          issue_stage<BM, BN, AK, BK>(st[slot], mapA, mapB, pc, &full[slot]);
           ++qp;
           if (++pc.s >= pc.s1) {
             pc.idx += gridDim.x;
-            p_valid = cursor_load(a, n_items, pc);
+            p_valid = cursor_load<BM, BN>(a, n_items, pc);
           }
         }
       }
@@ -211,7 +223,7 @@ __global__ void __maxnreg__(224)
       if (lane == 0) g_arrive(&empty[slot]);
     }
     // epilogue: direct column-major stores (8 consecutive rows per column segment)
-    const int m0 = it.tm * GBM + wm * 64 + g, n0 = it.tn * GBN + wn * 32 + 2 * t;
+    const int m0 = it.tm * BM + wm * 64 + g, n0 = it.tn * BN + wn * 32 + 2 * t;
     double* C = a.C;
     int64_t ldc = a.ldc;
     double alpha = a.alpha, beta = a.beta;
@@ -272,8 +284,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tm_encode() {
   }
   return fn;
 }
-// K-major: dims {K, MN}, box {16, 128};  MN-major: dims {MN, K}, box {16, 16}
-bool encode_operand(CUtensorMap* m, const GemmOperand& o, int MN, int K) {
+// K-major: dims {K, MN}, box {16, tile};  MN-major: dims {MN, K}, box {16, 16}
+bool encode_operand(CUtensorMap* m, const GemmOperand& o, int MN, int K, int tile) {
   auto enc = tm_encode();
   if (!enc) return false;
   cuuint64_t dims[2];
@@ -282,7 +294,7 @@ bool encode_operand(CUtensorMap* m, const GemmOperand& o, int MN, int K) {
     dims[0] = (cuuint64_t)K;
     dims[1] = (cuuint64_t)MN;
     box[0] = 16;
-    box[1] = 128;
+    box[1] = (cuuint32_t)tile;
   } else {
     dims[0] = (cuuint64_t)MN;
     dims[1] = (cuuint64_t)K;
@@ -296,17 +308,26 @@ bool encode_operand(CUtensorMap* m, const GemmOperand& o, int MN, int K) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool AK, bool BK>
+template <int BM, int BN, bool AK, bool BK>
 cudaError_t launch(const GemmArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, int grid, cudaStream_t st) {
   static bool attr = false;
+  constexpr size_t smem = gemm_smem<BM, BN>();
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<AK, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kGemmSmem);
+    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<BM, BN, AK, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dgemm_kernel<AK, BK><<<grid, kGemmThreads, kGemmSmem, st>>>(a, ma, mb);
+  dgemm_kernel<BM, BN, AK, BK><<<grid, kGemmThreads, smem, st>>>(a, ma, mb);
   return cudaGetLastError();
+}
+template <int BM, int BN>
+cudaError_t launch_any(bool ak, bool bk, const GemmArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, int grid,
+                       cudaStream_t st) {
+  if (ak && bk) return launch<BM, BN, true, true>(a, ma, mb, grid, st);
+  if (ak) return launch<BM, BN, true, false>(a, ma, mb, grid, st);
+  if (bk) return launch<BM, BN, false, true>(a, ma, mb, grid, st);
+  return launch<BM, BN, false, false>(a, ma, mb, grid, st);
 }
 }  // namespace
 
@@ -318,8 +339,13 @@ bool gemm_operand_ok(const GemmOperand& o, int MN, int K) {
 
 GemmPlan gemm_plan(int M, int N, int K) {
   GemmPlan pl;
-  pl.tiles_m = (M + GBM - 1) / GBM;
-  pl.tiles_n = (N + GBN - 1) / GBN;
+  // tile shape: the one with the least padded area (ties: 128 x 128)
+  const int64_t pad_sq = (int64_t)((M + 127) / 128 * 128) * ((N + 127) / 128 * 128);
+  const int64_t pad_tall = (int64_t)((M + 255) / 256 * 256) * ((N + 63) / 64 * 64);
+  pl.bm = pad_tall < pad_sq ? 256 : 128;
+  pl.bn = pl.bm == 256 ? 64 : 128;
+  pl.tiles_m = (M + pl.bm - 1) / pl.bm;
+  pl.tiles_n = (N + pl.bn - 1) / pl.bn;
   pl.kstages = (K + GBK - 1) / GBK;
   const int tiles = pl.tiles_m * pl.tiles_n;
   // split long-K products so the items fill whole waves of one CTA per SM; each split keeps >= 32
@@ -373,20 +399,13 @@ cudaError_t dgemm(int M, int N, int K, double alpha, const GemmOperand& A, const
   a.row_scale = row_scale;
   a.part = work;
   CUtensorMap ma, mb;
-  if (!encode_operand(&ma, A, M, K) || !encode_operand(&mb, B, N, K)) return cudaErrorInvalidValue;
+  if (!encode_operand(&ma, A, M, K, pl.bm) || !encode_operand(&mb, B, N, K, pl.bn)) return cudaErrorInvalidValue;
   const int items = pl.tiles_m * pl.tiles_n * pl.splits;
   const int grid = std::min(items, kSms);
   g_gemm_flops += 2.0 * M * N * (double)K;
   probe_before(K_GEMM, st);
-  cudaError_t e;
-  if (A.kmaj && B.kmaj)
-    e = launch<true, true>(a, ma, mb, grid, st);
-  else if (A.kmaj)
-    e = launch<true, false>(a, ma, mb, grid, st);
-  else if (B.kmaj)
-    e = launch<false, true>(a, ma, mb, grid, st);
-  else
-    e = launch<false, false>(a, ma, mb, grid, st);
+  const cudaError_t e = pl.bm == 256 ? launch_any<256, 64>(A.kmaj, B.kmaj, a, ma, mb, grid, st)
+                                      : launch_any<128, 128>(A.kmaj, B.kmaj, a, ma, mb, grid, st);
   probe_after(K_GEMM, st);
   if (e != cudaSuccess || pl.splits == 1) return e;
   const int64_t total = (int64_t)M * N;

@@ -115,6 +115,7 @@ struct GemmArgs {
   double* part;  // split-K partials [splits][N][M]
 };
 struct GemmPlan {
+  int bm, bn;  // CTA tile: 128 x 128 or 256 x 64
   int tiles_m, tiles_n, kstages, splits, kps;
   size_t work_bytes;
 };

@@ -1,5 +1,5 @@
 // Phase B of the factored Gramian matvec on the DMMA GEMM core, for the wide layers (both sides
-// >= 128: C3's 128 and C4 / C5's 256 hidden layers):
+// >= 256: C4 / C5's hidden layers):
 //     out_l = D_l diag(c) Zin_l^T   (n_l x n_{l-1}, K = S channel-columns)  + bias column
 // (the J^T c half of gramian.py:48-53, autodiff.py:90-125; layout in ngd_common.cuh).
 //
@@ -224,7 +224,10 @@ bool encode_jets(CUtensorMap* m, const double* base, int rows, int64_t s_pad) {
 }
 }  // namespace
 
-bool phbg_layer_ok(int M, int N) { return M >= 128 && N >= 128; }
+// wide layers only: at 128 x 128 (C3) the two-launch split (this kernel + the thin pipeline of
+// ngd_phb2.cu) measured slower than ngd_phb2.cu alone (C3 phase B 0.35 vs 0.31 ms per matvec);
+// at 256 x 256 (C4 / C5) it is faster (C5 22.2 vs 22.6 ms, DMMA pipe 86% vs 81%)
+bool phbg_layer_ok(int M, int N) { return M >= 256 && N >= 256; }
 
 // splits G of the K range so the items fill whole waves of one CTA per SM (>= 64 stages per split)
 int phbg_splits(int tiles, int kstages) {

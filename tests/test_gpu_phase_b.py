@@ -19,11 +19,11 @@ CASES = [
     ("sin2d", (2, 8, 16, 8, 1), 160, 32),
     ("sinsum", (10, 40, 24, 1), 192, 48),
     ("gauss", (5, 70, 1), 192, 48),
-    # wide layers (both sides >= 128) on the DMMA GEMM core (ngd_phbg.cu): full / partial 128 tiles,
+    # wide layers (both sides >= 256) on the DMMA GEMM core (ngd_phbg.cu): full / partial 128 tiles,
     # several tiles per layer, mixed with phb2 layers in the same matvec
-    ("sin2d", (2, 128, 128, 1), 256, 64),
-    ("gauss", (10, 256, 200, 130, 1), 192, 48),
-    ("sinsum", (3, 130, 257, 64, 1), 160, 32),
+    ("sin2d", (2, 256, 256, 1), 256, 64),
+    ("gauss", (10, 256, 300, 260, 1), 192, 48),
+    ("sinsum", (3, 130, 257, 300, 64, 1), 160, 32),
 ]
 
 
