@@ -1,4 +1,5 @@
-"""Phase B (J^T c, ngd_phb2.cu and ngd_phbg.cu) on topologies that exercise its tile plans: partial 64x64 tiles,
+"""Phase A (J v, ngd_jet.cu and ngd_phag.cu) and phase B (J^T c, ngd_phb2.cu and ngd_phbg.cu) on
+topologies that exercise their tile plans: partial 64x64 tiles,
 several m/n tiles per layer, 'heavy' layers just above the thin threshold (17 x 33), thin
 input layers with N = d up to 10 (two 8-column blocks) and the M = 1 output layer.  Each
 Gramian matvec and gradient is checked against the CPU oracle."""
@@ -24,6 +25,11 @@ CASES = [
     ("sin2d", (2, 256, 256, 1), 256, 64),
     ("gauss", (10, 256, 300, 260, 1), 192, 48),
     ("sinsum", (3, 130, 257, 300, 64, 1), 160, 32),
+    # phase A of uniform wide layers on the GEMM core (ngd_phag.cu): 128-column tiles spanning
+    # several point blocks (C = 4, 7), partial m-tiles (300 rows), ragged boundary tiles
+    ("sin2d", (2, 300, 300, 1), 200, 40),
+    ("sinsum", (5, 256, 256, 256, 1), 150, 37),
+    ("gauss", (10, 256, 256, 1), 64, 16),
 ]
 
 
