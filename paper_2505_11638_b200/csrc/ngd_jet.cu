@@ -138,16 +138,33 @@ __device__ __forceinline__ void jet_tile(const JetArgs& p, const int bx, const i
     __syncthreads();
     const double* as = As + (kt & 1) * BM * ASTR + (wm * 16 + g) * ASTR + t;
     const double* bs = Bs + (kt & 1) * BK * BSTR + t * BSTR + wn * 8 + g;
+    if (m_active && kt * BK + BK <= kvalid) {
+      // full stage: no early exit inside the unrolled k-steps, so the scheduler can interleave the
+      // 2 C independent accumulator chains across k-steps (the guarded loop below serialised each
+      // chain's four DMMAs back to back: profiles/r02_phab_c5 source page)
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      if (!m_active || kt * BK + kk >= kvalid) break;
-      const double a0 = as[kk];
-      const double a1 = as[8 * ASTR + kk];
+      for (int kk = 0; kk < BK; kk += 4) {
+        const double a0 = as[kk];
+        const double a1 = as[8 * ASTR + kk];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const double b = bs[kk * BSTR + c * PB];
-        dmma884(acc[0][c][0], acc[0][c][1], a0, b);
-        dmma884(acc[1][c][0], acc[1][c][1], a1, b);
+        for (int c = 0; c < C; ++c) {
+          const double b = bs[kk * BSTR + c * PB];
+          dmma884(acc[0][c][0], acc[0][c][1], a0, b);
+          dmma884(acc[1][c][0], acc[1][c][1], a1, b);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        if (!m_active || kt * BK + kk >= kvalid) break;
+        const double a0 = as[kk];
+        const double a1 = as[8 * ASTR + kk];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double b = bs[kk * BSTR + c * PB];
+          dmma884(acc[0][c][0], acc[0][c][1], a0, b);
+          dmma884(acc[1][c][0], acc[1][c][1], a1, b);
+        }
       }
     }
     __syncthreads();
