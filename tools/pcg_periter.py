@@ -8,7 +8,7 @@ import paper_2505_11638_b200 as ngd
 from paper_2505_11638_b200 import _lib
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 opts = sys.argv[2:]
-prob, quad, theta0, c = bench.make_problem(ngd, cfg, 1, 0)
+prob, quad, theta0, c = bench.make_problem(ngd, cfg)
 gop = ngd.GramianOperator.from_problem(prob, theta0, quad)
 g = torch.as_tensor(prob.loss_grad(theta0, quad), device="cuda")
 fac = ngd.nystrom_approximate(gop, bench.CONFIGS[cfg][4], seed=1, omega_source="device")
