@@ -44,7 +44,11 @@ def test_single_rank_nccl_path_matches():
         om = np.linalg.qr(np.random.default_rng(2).standard_normal((gop.dim, 8)))[0]
         y = gop.matmat(om)
         theta, recs = ngd.nystrom_ngd_run(prob, theta0, cfg, quad, quad_eval=quad)
-        return g, mv, y, theta, recs
+        # a solve that converges long before maxit: with a communicator the host enqueues all maxit
+        # iterations (no timing-dependent early exit), the device-side stop is unchanged
+        gop = ngd.GramianOperator.from_problem(prob, theta0, quad)
+        rep = ngd.pcg(ngd.ShiftedOperator(gop, 1e-3), g, 1e-3, 40)
+        return g, mv, y, theta, recs, rep
 
     base = run(None)
     if not dist.is_initialized():
@@ -64,3 +68,8 @@ def test_single_rank_nccl_path_matches():
     np.testing.assert_allclose([r.loss for r in forced[4]], [r.loss for r in base[4]], rtol=1e-9)
     np.testing.assert_allclose([r.h1_rel_error for r in forced[4]], [r.h1_rel_error for r in base[4]], rtol=1e-9)
     assert [r.pcg_iters for r in forced[4]] == [r.pcg_iters for r in base[4]]
+    a, b = base[5], forced[5]
+    assert a.converged and a.iterations < 40
+    assert (b.iterations, b.matvecs, b.converged, b.breakdown) == (a.iterations, a.matvecs, a.converged, a.breakdown)
+    # split partials summed in a different order before the all-reduce: rounding-level differences
+    np.testing.assert_allclose(b.solution, a.solution, rtol=1e-8, atol=1e-10 * np.abs(a.solution).max())
