@@ -59,7 +59,7 @@ def test_sass_gemm_is_tma_fed_dmma():
         pytest.skip("cuobjdump unavailable")
     out = subprocess.run([exe, "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
     gemm = [s for s in out.split("Function : ") if s.split("\n", 1)[0].find("dgemm_kernel") >= 0]
-    assert len(gemm) == 4  # the four operand layouts
+    assert len(gemm) == 8  # the four operand layouts x the two CTA tile shapes (128x128, 256x64)
     for s in gemm:
         assert "DMMA.8x8x4" in s and "UTMALDG.2D" in s
     needed = subprocess.run(["readelf", "-d", _lib.LIB_PATH], capture_output=True, text=True).stdout
