@@ -45,9 +45,11 @@ def test_single_rank_nccl_path_matches():
         y = gop.matmat(om)
         theta, recs = ngd.nystrom_ngd_run(prob, theta0, cfg, quad, quad_eval=quad)
         # a solve that converges long before maxit: with a communicator the host enqueues all maxit
-        # iterations (no timing-dependent early exit), the device-side stop is unchanged
+        # iterations (no timing-dependent early exit), the device-side stop is unchanged.
+        # mu = 1 (lambda_max ~ 73) keeps CG insensitive to rounding: a 1-ulp matvec perturbation
+        # moves the 12-iteration iterate by ~4e-13 in the oracle (at mu = 1e-3, tol 1e-3: 1.3e-4)
         gop = ngd.GramianOperator.from_problem(prob, theta0, quad)
-        rep = ngd.pcg(ngd.ShiftedOperator(gop, 1e-3), g, 1e-3, 40)
+        rep = ngd.pcg(ngd.ShiftedOperator(gop, 1.0), g, 1e-8, 40)
         return g, mv, y, theta, recs, rep
 
     base = run(None)
