@@ -60,8 +60,8 @@ CONFIGS = {
 }
 KIND_NAMES = {1: "jet_fwd", 2: "jet_rev", 3: "gram_phaseA", 4: "gram_phaseB", 5: "jacobian_rows", 6: "precond",
               7: "vector", 8: "pack", 9: "jacobi_svd", 10: "cholesky", 12: "cusolver_gesvdp", 13: "trsm",
-              14: "dmma_gemm"}
-N_KINDS = 16
+              14: "dmma_gemm", 15: "int8_gemm", 16: "oz_convert", 17: "oz_crt"}
+N_KINDS = 18
 
 
 def load_peaks():

@@ -134,6 +134,13 @@ int ngd_dense_matmat(ngd_ctx* ctx, const double* d_G, int64_t p, const double* d
 int ngd_gemm(ngd_ctx* ctx, int32_t trans_a, int32_t trans_b, int32_t M, int32_t N, int32_t K, double alpha,
              const double* d_A, int64_t lda, const double* d_B, int64_t ldb, double beta, double* d_C, int64_t ldc);
 
+/* the FP64-exact GEMM on the INT8 tensor cores (Ozaki scheme II: 16 moduli, tcgen05 kind::i8,
+ * CRT) behind the large sketches' S = J_c Omega and Y += J_c^T S (gramian.py:55-61; test hook):
+ * C = alpha A B + beta C with K-major A(m, k) = d_A[m lda + k], B(k, n) = d_B[n ldb + k],
+ * C column-major.  Option "sketch_gemm" selects the sketch engine (0 DMMA, 1 INT8, 2 auto). */
+int ngd_gemm_ozaki(ngd_ctx* ctx, int32_t M, int32_t N, int32_t K, double alpha, const double* d_A, int64_t lda,
+                   const double* d_B, int64_t ldb, double beta, double* d_C, int64_t ldc);
+
 /* ---- preconditioner (NystromPreconditioner.apply, sketch.py:101-112) ---- */
 int ngd_precond_apply(ngd_ctx* ctx, const double* d_U, const double* d_eig, int32_t ell, double mu,
                       const double* d_v, double* d_out, int64_t p);
@@ -172,13 +179,16 @@ int ngd_axpy(ngd_ctx* ctx, const double* d_a, double alpha, const double* d_b, d
  * ngd_probe_start(kind, n): bracket the next n launches of kernel class `kind`
  *   (1 FWD jets, 2 REV jets, 3 phase A, 4 phase B, 5 J rows, 6 preconditioner,
  *   7 vector/scalar, 8 pack, 9 small SVD, 10 small Cholesky, 11 (unused), 12 cuSOLVER, 13 triangular
- *   solve, 14 DMMA GEMM; 0 = every class at once, read back with ngd_probe_stop_all) with CUDA events
+ *   solve, 14 DMMA GEMM, 15 INT8 tensor-core GEMM, 16 Ozaki residue conversion, 17 CRT
+ *   reconstruction; 0 = every class at once, read back with ngd_probe_stop_all) with CUDA events
  *   on their launch stream;
  *   ngd_probe_stop returns the summed device time and the launch count. */
 int ngd_stream_sync(ngd_ctx* ctx);
 int64_t ngd_launch_count(void);
 /* algorithmic FLOPs (2 M N K) of every in-house DMMA GEMM launched so far (process-wide) */
 double ngd_gemm_flops(void);
+/* INT8 tensor ops (2 M N K per modulus) of every Ozaki-scheme GEMM launched so far (process-wide) */
+double ngd_i8_ops(void);
 int ngd_probe_start(int32_t kind, int32_t max_launches);
 int ngd_probe_stop(double* h_total_ms, int64_t* h_count);
 int ngd_probe_stop_all(double* h_ms, int64_t* h_count, int32_t n_kinds);

@@ -74,6 +74,7 @@ SIGNATURES = {
     "ngd_nystrom_finish": [_P, _P, _P, _I64, _I32, _P, _P, ctypes.POINTER(_D)],
     "ngd_dense_matmat": [_P, _P, _I64, _P, _I64, _P],
     "ngd_gemm": [_P, _I32, _I32, _I32, _I32, _I32, _D, _P, _I64, _P, _I64, _D, _P, _I64],
+    "ngd_gemm_ozaki": [_P, _I32, _I32, _I32, _D, _P, _I64, _P, _I64, _D, _P, _I64],
     "ngd_precond_apply": [_P, _P, _P, _I32, _D, _P, _P, _I64],
     "ngd_pcg": [_P, _P, _I64, _P, _D, _P, _P, _I32, _D, _D, _I32, _I32, _P, ctypes.POINTER(SolveReportC)],
     "ngd_small_svd": [_P, _P, _I32, _P, _P, _I32, ctypes.POINTER(_I32)],
@@ -84,12 +85,13 @@ SIGNATURES = {
     "ngd_stream_sync": [_P],
     "ngd_launch_count": [],
     "ngd_gemm_flops": [],
+    "ngd_i8_ops": [],
     "ngd_probe_start": [_I32, _I32],
     "ngd_probe_stop": [ctypes.POINTER(_D), ctypes.POINTER(_I64)],
     "ngd_probe_stop_all": [ctypes.POINTER(_D), ctypes.POINTER(_I64), _I32],
 }
 _RESTYPE = {"ngd_last_error": ctypes.c_char_p, "ngd_param_count": _I64, "ngd_launch_count": _I64,
-            "ngd_gemm_flops": _D}
+            "ngd_gemm_flops": _D, "ngd_i8_ops": _D}
 
 _lib = None
 _contexts = []  # weak registry so option changes reach live contexts
@@ -97,7 +99,7 @@ OPTIONS = {"svd": 3}
 
 
 # library defaults of the ngd_set_option knobs (include/ngd.h), for restoring a temporary change
-DEFAULTS = {"svd": 3, "graphs": 1, "l2window": 1, "force_comm": 0, "pdl": 1, "l2u": 1}
+DEFAULTS = {"svd": 3, "graphs": 1, "l2window": 1, "force_comm": 0, "pdl": 1, "l2u": 1, "sketch_gemm": 2}
 
 
 @contextlib.contextmanager

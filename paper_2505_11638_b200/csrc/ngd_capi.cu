@@ -172,6 +172,10 @@ struct ngd_ctx {
   Buf pr, pz, pd, pad, ptmp;  // PCG vectors
   Buf ppart, pcprime;         // precond scratch
   Buf jt, smat;               // sketch scratch: Jacobian-row chunk (ld = ldp), S = J_c V
+  // INT8 tensor-core (Ozaki II) sketch: residues of the A side (J_c, then J_c^T), of Omega, of S;
+  // product residues; row / column exponents
+  Buf oz_a, oz_b, oz_s, oz_res, oz_ea, oz_eb, oz_ep, oz_ec, oz_mx;
+  int sketch_engine = 2;      // option "sketch_gemm": 0 DMMA, 1 INT8 Ozaki, 2 auto (Ozaki for large sketches)
   Buf vpad, omp, yp;          // p x ell blocks at the padded leading dimension ldp (TMA: even ld)
   Buf gwork, gscrA, gscrB;    // GEMM split-K partials; staging of operands TMA cannot address
   Buf chol_t, chol_info;      // blocked Cholesky (n > 512): off-diagonal panel, per-level status
@@ -749,7 +753,7 @@ int ngd_ctx_destroy(ngd_ctx* c) {
   for (auto& e : c->poll_ev)
     if (e) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->chol_work, &c->trsm_work, &c->jets, &c->wr_pad, &c->R_pad, &c->alpha_bar, &c->u_persist})
+  for (Buf* b : {&c->pargs, &c->px, &c->pb, &c->oz_a, &c->oz_b, &c->oz_s, &c->oz_res, &c->oz_ea, &c->oz_eb, &c->oz_ep, &c->oz_ec, &c->oz_mx, &c->chol_work, &c->trsm_work, &c->jets, &c->wr_pad, &c->R_pad, &c->alpha_bar, &c->u_persist})
     b->release();
   if (c->dn_params) cusolverDnDestroyParams(c->dn_params);
   if (c->sol) cusolverDnDestroy(c->sol);
@@ -1153,6 +1157,64 @@ int ngd_gram_dense(ngd_ctx* c, double* G, int64_t ldg) {
   return NGD_OK;
 }
 
+// The two sketch contractions on the INT8 tensor cores (ngd_ozaki.cu), per point chunk:
+//   residues of J_c (row-scaled)  ->  S = diag(w) J_c V  (16 int8 GEMMs + CRT)
+//   residues of J_c^T (column-scaled) and of S  ->  Y += J_c^T S
+// V's residues are formed once per call.
+static bool use_ozaki(ngd_ctx* c, int64_t ell) {
+  if (c->sketch_engine == 0) return false;
+  if (c->sketch_engine == 1) return true;
+  return ell >= 256 && c->p >= 16384;  // measured crossover
+}
+
+static int matmat_ozaki(ngd_ctx* c, FormJPlan& pl, const GemmOperand& vop, int ell, double* Y, int64_t ldy) {
+  const int p = (int)c->p;
+  const int64_t ldp = c->ldp;
+  const int64_t ldr = rup(pl.R, 16);
+  const int tp = oz_bits(p), tr = oz_bits(pl.R);
+  const int sp = oz_splits(p);
+  CK(c->oz_a.ensure((size_t)kOzMods * std::max<int64_t>(pl.R * ldp, (int64_t)p * ldr)));
+  CK(c->oz_b.ensure((size_t)kOzMods * ell * ldp));
+  CK(c->oz_s.ensure((size_t)kOzMods * ell * ldr));
+  CK(c->oz_res.ensure((size_t)kOzMods * ell * std::max<int64_t>(ldp, sp * ldr)));
+  CK(c->oz_ea.ensure(sizeof(int) * pl.R));
+  CK(c->oz_ec.ensure(sizeof(int) * p));
+  CK(c->oz_eb.ensure(sizeof(int) * ell));
+  CK(c->oz_ep.ensure(sizeof(int) * ell));
+  CK(c->oz_mx.ensure(sizeof(unsigned long long) * (pl.R + p)));
+  auto* A8 = static_cast<int8_t*>(c->oz_a.p);
+  auto* B8 = static_cast<int8_t*>(c->oz_b.p);
+  auto* S8 = static_cast<int8_t*>(c->oz_s.p);
+  auto* R8 = static_cast<int8_t*>(c->oz_res.p);
+  int* er = static_cast<int*>(c->oz_ea.p);  // J_c rows (points)
+  int* ec = static_cast<int*>(c->oz_ec.p);  // J_c columns (parameters)
+  int* ev = static_cast<int*>(c->oz_eb.p);  // V columns
+  int* es = static_cast<int*>(c->oz_ep.p);  // S columns
+  auto* rmax = static_cast<unsigned long long*>(c->oz_mx.p);
+  auto* cmax = rmax + pl.R;
+  pl.fa.rmax = rmax;
+  pl.fa.cmax = cmax;
+  CK(oz_rows(vop.p, vop.ld, ell, p, tp, B8, ldp, (int64_t)ell * ldp, ev, false, c->stream));
+  for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
+    const int nb = std::min(pl.bpc, pl.nblk_total - b0);
+    const int r = nb * PB;
+    const int64_t q0 = (int64_t)b0 * PB;
+    pl.fa.blk0 = b0;
+    CK(cudaMemsetAsync(rmax, 0, sizeof(unsigned long long) * (pl.R + p), c->stream));
+    CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));  // J_c + its row / column maxima
+    CK(oz_exps(rmax, r, tp, er, c->stream));
+    CK(oz_exps(cmax, p, tr, ec, c->stream));
+    CK(oz_rows(c->jt.d(), ldp, r, p, tp, A8, ldp, (int64_t)r * ldp, er, true, c->stream));
+    CK(oz_i8gemm(A8, ldp, r, B8, ldp, ell, p, R8, ldr, c->stream));
+    CK(oz_crt(R8, ldr, r, ell, sp, er, ev, c->w_pad.d() + q0, 1.0, 0.0, c->smat.d(), r, c->stream));
+    CK(oz_cols_t(c->jt.d(), ldp, r, p, ec, A8, ldr, (int64_t)p * ldr, c->stream));
+    CK(oz_rows(c->smat.d(), r, ell, r, tr, S8, ldr, (int64_t)ell * ldr, es, false, c->stream));
+    CK(oz_i8gemm(A8, ldr, p, S8, ldr, ell, r, R8, ldp, c->stream));
+    CK(oz_crt(R8, ldp, p, ell, 1, ec, es, nullptr, 1.0, q0 == 0 ? 0.0 : 1.0, Y, ldy, c->stream));
+  }
+  return NGD_OK;
+}
+
 // Y = G V by the J-chunk formulation (gramian.py:55-61 as ell matvecs): per point
 // chunk, explicit Jacobian rows J_c (formj_kernel), then on the DMMA GEMM
 //   S = J_c V  (w folded into the epilogue)   and   Y += J_c^T S.
@@ -1171,14 +1233,18 @@ int ngd_gram_matmat(ngd_ctx* c, const double* V, int64_t ell, int64_t ldv, doubl
                          cudaMemcpyDeviceToDevice, c->stream));
     vop = kmaj(c->vpad.d(), c->ldp);
   }
-  for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
-    const int nb = std::min(pl.bpc, pl.nblk_total - b0);
-    const int r = nb * PB;
-    const int64_t q0 = (int64_t)b0 * PB;
-    pl.fa.blk0 = b0;
-    CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));
-    TRY(gemm(c, r, (int)ell, p, 1.0, kmaj(c->jt.d(), c->ldp), vop, 0.0, c->smat.d(), r, c->w_pad.d() + q0));
-    TRY(gemm(c, p, (int)ell, r, 1.0, mnmaj(c->jt.d(), c->ldp), kmaj(c->smat.d(), r), q0 == 0 ? 0.0 : 1.0, Y, ldy));
+  if (use_ozaki(c, ell)) {
+    TRY(matmat_ozaki(c, pl, vop, (int)ell, Y, ldy));
+  } else {
+    for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
+      const int nb = std::min(pl.bpc, pl.nblk_total - b0);
+      const int r = nb * PB;
+      const int64_t q0 = (int64_t)b0 * PB;
+      pl.fa.blk0 = b0;
+      CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));
+      TRY(gemm(c, r, (int)ell, p, 1.0, kmaj(c->jt.d(), c->ldp), vop, 0.0, c->smat.d(), r, c->w_pad.d() + q0));
+      TRY(gemm(c, p, (int)ell, r, 1.0, mnmaj(c->jt.d(), c->ldp), kmaj(c->smat.d(), r), q0 == 0 ? 0.0 : 1.0, Y, ldy));
+    }
   }
   if (c->comm) {
     if (ldy != c->p) return fail(NGD_E_SHAPE, "multi-rank matmat needs ldy == p");
@@ -1577,6 +1643,39 @@ int ngd_gemm(ngd_ctx* c, int32_t trans_a, int32_t trans_b, int32_t M, int32_t N,
   return gemm(c, M, N, K, alpha, a, b, beta, C, ldc);
 }
 
+// C = alpha A B + beta C on the INT8 tensor cores (Ozaki II, ngd_ozaki.cu; test hook): K-major
+// operands A(m, k) = A[m lda + k], B(k, n) = B[n ldb + k] (lda, ldb multiples of 2), C column-major
+int ngd_gemm_ozaki(ngd_ctx* c, int32_t M, int32_t N, int32_t K, double alpha, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  TRY(bind(c));
+  if (M < 1 || N < 1 || K < 1 || lda < K || ldb < K || ldc < M) return fail(NGD_E_SHAPE, "bad GEMM shape");
+  const int64_t ldk = rup(K, 16), ldo = rup(M, 16);
+  const int t = oz_bits(K), sp = oz_splits(K);
+  // the residue kernels stream 16-byte chunks: operands with an odd ld / unaligned base are staged once
+  GemmOperand ao{A, lda, true}, bo{B, ldb, true};
+  if (!gemm_operand_ok(ao, M, K)) TRY(stage_operand(c, ao, M, K, c->gscrA));
+  if (!gemm_operand_ok(bo, N, K)) TRY(stage_operand(c, bo, N, K, c->gscrB));
+  A = ao.p;
+  lda = ao.ld;
+  B = bo.p;
+  ldb = bo.ld;
+  CK(c->oz_a.ensure((size_t)kOzMods * M * ldk));
+  CK(c->oz_b.ensure((size_t)kOzMods * N * ldk));
+  CK(c->oz_res.ensure((size_t)kOzMods * sp * N * ldo));
+  CK(c->oz_ea.ensure(sizeof(int) * M));
+  CK(c->oz_eb.ensure(sizeof(int) * N));
+  auto* A8 = static_cast<int8_t*>(c->oz_a.p);
+  auto* B8 = static_cast<int8_t*>(c->oz_b.p);
+  auto* R8 = static_cast<int8_t*>(c->oz_res.p);
+  int* ea = static_cast<int*>(c->oz_ea.p);
+  int* eb = static_cast<int*>(c->oz_eb.p);
+  CK(oz_rows(A, lda, M, K, t, A8, ldk, (int64_t)M * ldk, ea, false, c->stream));
+  CK(oz_rows(B, ldb, N, K, t, B8, ldk, (int64_t)N * ldk, eb, false, c->stream));
+  CK(oz_i8gemm(A8, ldk, M, B8, ldk, N, K, R8, ldo, c->stream));
+  CK(oz_crt(R8, ldo, M, N, sp, ea, eb, nullptr, alpha, beta, C, ldc, c->stream));
+  return NGD_OK;
+}
+
 int ngd_get_stat(ngd_ctx* c, const char* key, int64_t* out) {
   if (!c || !key || !out) return fail(NGD_E_SHAPE, "bad stat query");
   if (!strcmp(key, "jacobi_sweeps")) {
@@ -1617,6 +1716,11 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "l2window")) {
     c->use_l2_window = value ? 1 : 0;
     c->graph_gen++;  // the captured PCG iteration carries the stream's access-policy window
+    return NGD_OK;
+  }
+  if (!strcmp(key, "sketch_gemm")) {
+    if (value < 0 || value > 2) return fail(NGD_E_SHAPE, "sketch_gemm must be 0 (DMMA), 1 (INT8 Ozaki) or 2 (auto)");
+    c->sketch_engine = (int)value;
     return NGD_OK;
   }
   if (!strcmp(key, "svd")) {

@@ -469,6 +469,11 @@ __global__ void __launch_bounds__(FJ_THREADS, 1) formj_kernel(FormJArgs a) {
   const int arow = warp * 8 + g;  // this lane's tile row (A fragment / accumulator row)
   const bool row_ok = arow < na;
   const bool vec2 = ((off + (int64_t)(a0 + arow) * nin + b0) & 1) == 0 && (a.ldj & 1) == 0;
+  const bool track = a.rmax != nullptr;
+  unsigned long long cm[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) cm[j][0] = cm[j][1] = 0ull;
+  unsigned long long bm = 0ull;  // bias column maximum (threads < na)
   for (int r = 0; r < PB; ++r) {
     double acc[8][2];
 #pragma unroll
@@ -497,6 +502,44 @@ __global__ void __launch_bounds__(FJ_THREADS, 1) formj_kernel(FormJArgs a) {
     }
     if (b0 == 0 && threadIdx.x < na)  // bias entries: value channel of D
       a.Jt[(prow0 + r) * a.ldj + off + (int64_t)nout * nin + a0 + threadIdx.x] = Ds[threadIdx.x * FJ_LD + r];
+    if (track) {
+      unsigned long long rm = 0ull;
+      if (row_ok) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int col = j * 8 + 2 * t;
+          if (col < nb) {
+            const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(acc[j][0]));
+            cm[j][0] = max(cm[j][0], u);
+            rm = max(rm, u);
+          }
+          if (col + 1 < nb) {
+            const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(acc[j][1]));
+            cm[j][1] = max(cm[j][1], u);
+            rm = max(rm, u);
+          }
+        }
+      }
+      if (b0 == 0 && threadIdx.x < na) {
+        const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(Ds[threadIdx.x * FJ_LD + r]));
+        bm = max(bm, u);
+        rm = max(rm, u);
+      }
+      for (int o = 16; o; o >>= 1) rm = max(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+      if (lane == 0 && rm) atomicMax(a.rmax + prow0 + r, rm);
+    }
+  }
+  if (track) {
+    if (row_ok) {
+      unsigned long long* cr = a.cmax + off + (int64_t)(a0 + arow) * nin + b0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int col = j * 8 + 2 * t;
+        if (col < nb && cm[j][0]) atomicMax(cr + col, cm[j][0]);
+        if (col + 1 < nb && cm[j][1]) atomicMax(cr + col + 1, cm[j][1]);
+      }
+    }
+    if (b0 == 0 && threadIdx.x < na && bm) atomicMax(a.cmax + off + (int64_t)nout * nin + a0 + threadIdx.x, bm);
   }
 }
 

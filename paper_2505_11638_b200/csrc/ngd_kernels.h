@@ -12,7 +12,7 @@ namespace ngd {
 enum KernelKind {
   K_FWD = 1, K_REV = 2, K_PHA = 3, K_PHB = 4, K_FORMJ = 5, K_PRECOND = 6, K_VEC = 7, K_PACK = 8, K_SVD = 9, K_CHOL = 10,
   K_BLAS = 11, K_SOLVER = 12,  // library calls (cuBLAS / cuSOLVER): timed, not counted as our launches
-  K_TRSM = 13, K_GEMM = 14
+  K_TRSM = 13, K_GEMM = 14, K_I8GEMM = 15, K_OZCONV = 16, K_OZCRT = 17
 };
 void probe_before(int kind, cudaStream_t st);
 void probe_after(int kind, cudaStream_t st);
@@ -95,6 +95,10 @@ struct FormJArgs {
   int blk0;                 // first point block of this chunk (padded point order)
   double* Jt;               // [16 * blocks][ldj], row = padded point within the chunk
   int64_t ldj;
+  // optional (INT8 sketch): running maxima of |J| as ordered bit patterns (RED.MAX.U64), per chunk
+  // row (point) and per parameter (column); NaN / inf order above every finite value
+  unsigned long long* rmax;
+  unsigned long long* cmax;
 };
 
 // FP64 DMMA GEMM (ngd_gemm.cu): C(m, n) = alpha sum_k A(m, k) B(k, n) [* row_scale(m)] + beta C(m, n),
@@ -124,6 +128,25 @@ GemmPlan gemm_plan(int M, int N, int K);
 cudaError_t dgemm(int M, int N, int K, double alpha, const GemmOperand& A, const GemmOperand& B, double beta,
                   double* C, int64_t ldc, const double* row_scale, double* work, size_t work_bytes, cudaStream_t st);
 double gemm_flops_total();
+
+// FP64-exact GEMM on the INT8 tensor cores, Ozaki scheme II (ngd_ozaki.cu): residues of the
+// row / column scaled operands modulo kOzMods moduli, one tcgen05 kind::i8 GEMM per modulus,
+// CRT reconstruction.  Residue blocks are [kOzMods][rows][ld] int8 (ld a multiple of 16);
+// product residues [splits][kOzMods][N][ldo] (column-major).
+constexpr int kOzMods = 16;
+constexpr int kOzMaxKSplit = 130944;  // K per split: 128 * 128 * K < 2^31
+int oz_bits(int64_t K);               // integer width t of the scaled operands for inner length K
+int oz_splits(int64_t K);
+double oz_i8_ops_total();
+cudaError_t oz_exps(const unsigned long long* maxbits, int n, int t, int* exps, cudaStream_t st);
+cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t* out, int64_t ldo, int64_t plane,
+                    int* exps, bool have_exps, cudaStream_t st);
+cudaError_t oz_cols_t(const double* A, int64_t lda, int rows, int cols, const int* exps, int8_t* out, int64_t ldo,
+                      int64_t plane, cudaStream_t st);
+cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int M, const int8_t* B, int64_t ldb, int N, int K, int8_t* res,
+                      int64_t ldo, cudaStream_t st);
+cudaError_t oz_crt(const int8_t* res, int64_t ldo, int M, int N, int splits, const int* ea, const int* eb,
+                   const double* row_w, double alpha, double beta, double* C, int64_t ldc, cudaStream_t st);
 cudaError_t gemv_rows(const double* G, int64_t n, const double* x, double* y, const int* skip, cudaStream_t st);
 
 constexpr int kMaxLayers = 8;

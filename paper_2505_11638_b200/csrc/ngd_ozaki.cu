@@ -1,0 +1,784 @@
+// FP64-exact GEMM on the INT8 tensor cores (tcgen05.mma kind::i8, TMEM accumulators, TMA ring):
+// the Ozaki scheme II (integer modular form, CRT reconstruction) for the two dense contractions of
+// the J-chunk Nystrom sketch (gramian.py:55-61 evaluated as Y = G Omega, sketch.py:76):
+//
+//     S = diag(w) J_c Omega        (M = chunk points, N = ell, K = p)
+//     Y += J_c^T S                 (M = p,            N = ell, K = chunk points)
+//
+// FP64 has no tcgen05 kind on sm_100a; the DMMA pipe peaks at ~37 TF/s while the INT8 tensor
+// pipe runs ~3 POPS.  The product is computed exactly in integers and rounded once:
+//
+//   1. scaling (per row of A, per column of B):  A'(m,k) = rint(A(m,k) 2^alpha_m) with
+//      max_k |A'(m,k)| <= 2^t, likewise B'(k,n) = rint(B(k,n) 2^beta_n); t = 53 (the row maximum
+//      keeps its full FP64 mantissa) unless K 2^(2t+1) would reach the CRT modulus.
+//   2. residues:  A'_j = A' mod m_j for 16 pairwise-coprime moduli m_j <= 256 (symmetric, int8).
+//   3. 16 int8 GEMMs  C_j = A'_j B'_j  (exact int32: K <= 131071 per K-split), reduced mod m_j to
+//      int8 in the epilogue.
+//   4. CRT:  C' = A' B' is the unique integer in (-M/2, M/2), M = prod m_j (2^125.4), congruent to
+//      C_j mod m_j:  C'/M = sum_j r_j (y_j / m_j) mod 1, y_j = (M/m_j)^-1 mod m_j, evaluated exactly
+//      in three 41-bit slices of y_j / m_j (every partial sum is an exact FP64 integer), then one
+//      rounding: C = C' 2^-(alpha_m + beta_n).
+//
+// Accuracy: the only errors are the rounding of A, B to t-bit integers relative to their row /
+// column maxima (2^-54 relative to max_k |A(m,k)| resp. max_k |B(k,n)|) and the final rounding of
+// C' (2^-53 relative, plus an absolute 2^-83 M from the CRT slices -- 2^-64 of the largest
+// possible product term): |C - AB| <= 2^-53 (max_k|A_mk| sum_k|B_kn| + sum_k|A_mk| max_k|B_kn|)
+// + 2^-53 |AB|, the same order as FP64 GEMM's own K-dependent error bound (tests/test_gpu_ozaki.py).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "ngd_common.cuh"
+#include "ngd_kernels.h"
+
+namespace ngd {
+
+namespace {
+
+constexpr int NMOD = kOzMods;
+__host__ __device__ constexpr int mod_of(int j) {
+  return j == 0    ? 256
+         : j == 1  ? 255
+         : j == 2  ? 253
+         : j == 3  ? 251
+         : j == 4  ? 247
+         : j == 5  ? 241
+         : j == 6  ? 239
+         : j == 7  ? 233
+         : j == 8  ? 229
+         : j == 9  ? 227
+         : j == 10 ? 223
+         : j == 11 ? 217
+         : j == 12 ? 211
+         : j == 13 ? 199
+         : j == 14 ? 197
+                   : 193;
+}
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
+constexpr int kExpNonFinite = -0x40000000;     // row / column exponent of a non-finite input
+
+// per-modulus constants of the CRT and the residue generation (host-computed, passed by value)
+struct OzTab {
+  double h[NMOD], g[NMOD], l[NMOD];  // y_j / m_j = (h 2^-41 + g 2^-82 + l 2^-123) + O(2^-123)
+  double c26[NMOD];                  // 2^26 mod m_j, symmetric
+  double md;                         // M rounded to FP64
+  double log2m;
+};
+
+OzTab make_tab() {
+  OzTab t{};
+  // M = prod m_j as a 128-bit integer (2^125.4 < 2^128)
+  unsigned __int128 M = 1;
+  for (int j = 0; j < NMOD; ++j) M *= (unsigned)mod_of(j);
+  long double md = 1.0L;
+  double lg = 0.0;
+  for (int j = 0; j < NMOD; ++j) {
+    md *= (long double)mod_of(j);
+    lg += std::log2((double)mod_of(j));
+  }
+  t.md = (double)md;
+  t.log2m = lg;
+  for (int j = 0; j < NMOD; ++j) {
+    const int m = mod_of(j);
+    const unsigned __int128 Mj = M / (unsigned)m;
+    const int mjr = (int)(Mj % (unsigned)m);
+    int y = 0;
+    for (int k = 1; k < m; ++k)
+      if ((mjr * k) % m == 1) {
+        y = k;
+        break;
+      }
+    // binary expansion of y / m: 123 bits in three 41-bit slices
+    unsigned long long rem = (unsigned long long)y;
+    unsigned long long s[3] = {0, 0, 0};
+    for (int b = 0; b < 123; ++b) {
+      rem <<= 1;
+      const unsigned long long bit = rem >= (unsigned long long)m ? 1ull : 0ull;
+      if (bit) rem -= (unsigned long long)m;
+      s[b / 41] = (s[b / 41] << 1) | bit;
+    }
+    t.h[j] = (double)s[0];
+    t.g[j] = (double)s[1];
+    t.l[j] = (double)s[2];
+    int c = (int)((1ull << 26) % (unsigned long long)m);
+    if (c > m / 2) c -= m;
+    t.c26[j] = (double)c;
+  }
+  return t;
+}
+
+const OzTab& tab() {
+  static const OzTab t = make_tab();
+  return t;
+}
+
+// 2^e for |e| <= ~2100 as two exactly representable factors
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+__device__ __forceinline__ double scale2(double x, int e) {
+  const int e1 = e >> 1;
+  return (x * pow2(e1)) * pow2(e - e1);
+}
+
+// residue words of 8 elements (two groups of 4 consecutive) for every modulus: w[j][0], w[j][1].
+// The 8 elements' chains of one modulus are written as separate passes over arrays so the four
+// dependent FP64 steps of each chain interleave across the elements (the per-element form compiled
+// to back-to-back dependent DFMA / DADD pairs).
+template <int J = 0>
+__device__ __forceinline__ void residue_words8(const double (&xh)[8], const double (&xl)[8], const OzTab& tb,
+                                               unsigned (&w)[NMOD][2]) {
+  if constexpr (J < NMOD) {
+    constexpr double m = (double)mod_of(J);
+    constexpr double inv = 1.0 / (double)mod_of(J);
+    const double c = tb.c26[J];
+    double v[8], q[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = fma(xh[e], c, xl[e]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) q[e] = fma(v[e], inv, kMagic);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) q[e] -= kMagic;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = fma(-q[e], m, v[e]) + kMagic;
+    unsigned lo = 0, hi = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      lo |= ((unsigned)__double2loint(v[e]) & 0xFFu) << (8 * e);
+      hi |= ((unsigned)__double2loint(v[e + 4]) & 0xFFu) << (8 * e);
+    }
+    w[J][0] = lo;
+    w[J][1] = hi;
+    residue_words8<J + 1>(xh, xl, tb, w);
+  }
+}
+
+__device__ __forceinline__ void split26(double a, double s1, double s2, double& xh, double& xl) {
+  const double x = rint((a * s1) * s2);  // |x| <= 2^t <= 2^53
+  xh = fma(x, 1.0 / 67108864.0, kMagic) - kMagic;
+  xl = fma(-xh, 67108864.0, x);
+}
+
+__device__ __forceinline__ int exp_for_max(double mx, int t) {
+  if (!(mx <= 1.79769313486231570815e+308)) return kExpNonFinite;  // inf / nan
+  if (mx == 0.0) return 0;
+  return t - 1 - ilogb(mx);  // mx 2^alpha in [2^(t-1), 2^t)
+}
+
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sh[32] = v;
+  }
+  __syncthreads();
+  v = sh[32];
+  __syncthreads();
+  return v;
+}
+
+// Exponents from running maxima kept as ordered bit patterns of |x| (formj_kernel's RED.MAX): bit
+// patterns at or above +inf's flag a non-finite row / column.
+__global__ void oz_exps_kernel(const unsigned long long* __restrict__ mx, int n, int t, int* __restrict__ exps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long b = mx[i];
+  exps[i] = b >= 0x7ff0000000000000ull ? kExpNonFinite : exp_for_max(__longlong_as_double((long long)b), t);
+}
+
+// Row exponents of a K-major FP64 operand (standalone GEMM path): one CTA per row.
+__global__ void __launch_bounds__(256) oz_rowmax_kernel(const double* __restrict__ A, int64_t lda, int rows, int K,
+                                                        int t, int* __restrict__ exps) {
+  __shared__ double sh[33];
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const double* a = A + (int64_t)r * lda;
+  double mx = 0.0;
+  bool bad = false;  // fmax drops NaN: flagged separately
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const double v = fabs(a[k]);
+    mx = fmax(mx, v);
+    bad |= !(v <= 1.79769313486231570815e+308);
+  }
+  const bool any_bad = __syncthreads_or(bad);
+  mx = block_max(mx, sh);
+  if (threadIdx.x == 0) exps[r] = any_bad ? kExpNonFinite : exp_for_max(mx, t);
+}
+
+__device__ __forceinline__ void cp16(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Row-scaled residues of a K-major FP64 operand A(r, k) = A[r lda + k] (r < rows, k < K; lda even,
+// A 16-byte aligned) with the row exponents given: out[j][r][ldo] (int8, k contiguous, zero for
+// K <= k < ldo).  Persistent CTAs over tiles of 4 rows x 512 k: the next tile streams into shared
+// memory with cp.async while the current one is converted (the residue arithmetic is ~85 FP64
+// operations per element: without the prefetch every tile's load latency was exposed), and each
+// modulus' 4 x 512-byte output block leaves from a shared-memory stage in 16-byte stores.
+constexpr int kRowsT = 4, kRowsK = 512;
+constexpr size_t kRowsSmem = 2 * kRowsT * kRowsK * sizeof(double) + NMOD * kRowsT * kRowsK;
+__global__ void __launch_bounds__(256) oz_rows_kernel(const double* __restrict__ A, int64_t lda, int rows, int K,
+                                                      const int* __restrict__ exps, int8_t* __restrict__ out,
+                                                      int64_t ldo, int64_t plane, const OzTab tb) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  double* in = reinterpret_cast<double*>(rsm);                              // [2][4][512]
+  unsigned char* stg = rsm + 2 * kRowsT * kRowsK * sizeof(double);          // [16][4][512]
+  const int tiles_k = (int)((ldo + kRowsK - 1) / kRowsK);
+  const int ntiles = ((rows + kRowsT - 1) / kRowsT) * tiles_k;
+  const int tid = threadIdx.x;
+  auto issue = [&](int tile, int buf) {
+    if (tile < ntiles) {
+      const int r0 = (tile / tiles_k) * kRowsT, k0 = (tile % tiles_k) * kRowsK;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int ch = tid + 256 * i;  // 16-byte chunk: row ch / 256, doubles 2 (ch % 256)
+        const int q = ch >> 8, kk = k0 + 2 * (ch & 255);
+        const int r = r0 + q;
+        const bool ok = r < rows && kk < lda;
+        cp16(in + (buf * kRowsT + q) * kRowsK + 2 * (ch & 255), ok ? A + (int64_t)r * lda + kk : A, ok ? 16u : 0u);
+      }
+    }
+    cp_commit();
+  };
+  int tile = blockIdx.x;
+  issue(tile, 0);
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int buf = it & 1;
+    issue(tile + gridDim.x, buf ^ 1);
+    cp_wait<1>();
+    __syncthreads();
+    const int r0 = (tile / tiles_k) * kRowsT, k0 = (tile % tiles_k) * kRowsK;
+    const int q = tid >> 6, c = tid & 63;
+    const int r = r0 + q;
+    const int e = r < rows ? exps[r] : 0;
+    const bool dead = r >= rows || e == kExpNonFinite;
+    const int e1 = e >> 1;
+    const double s1 = pow2(e1), s2 = pow2(e - e1);
+    unsigned wd[NMOD][2];
+    {
+      double xh[8], xl[8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kl = 4 * c + 256 * h;
+        const double* src = in + (buf * kRowsT + q) * kRowsK + kl;
+        const double2 d0 = *reinterpret_cast<const double2*>(src), d1 = *reinterpret_cast<const double2*>(src + 2);
+        const double v[4] = {d0.x, d0.y, d1.x, d1.y};
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4)
+          split26(!dead && k0 + kl + e4 < K ? v[e4] : 0.0, s1, s2, xh[4 * h + e4], xl[4 * h + e4]);
+      }
+      residue_words8(xh, xl, tb, wd);
+    }
+#pragma unroll
+    for (int j = 0; j < NMOD; ++j) {
+      unsigned* o = reinterpret_cast<unsigned*>(stg + (j * kRowsT + q) * kRowsK);
+      o[c] = wd[j][0];
+      o[c + 64] = wd[j][1];
+    }
+    __syncthreads();
+    // rows past `rows` keep their previous contents; NaN-flagged rows are never read (CRT writes NaN)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int ch = tid + 256 * i;  // plane ch / 128, row (ch / 32) % 4, 16-byte column ch % 32
+      const int j = ch >> 7, qq = (ch >> 5) & 3, col = (ch & 31) * 16;
+      if (r0 + qq < rows && k0 + col < ldo)
+        *reinterpret_cast<uint4*>(out + (int64_t)j * plane + (int64_t)(r0 + qq) * ldo + k0 + col) =
+            *reinterpret_cast<const uint4*>(stg + (j * kRowsT + qq) * kRowsK + col);
+    }
+  }
+  cp_wait<0>();
+}
+
+// Column-scaled, transposed residues: out[j][k][ldo] holds (A(., k) scaled by 2^exps[k]) with the
+// rows r contiguous -- the K-major form of A^T for the product A^T B (A row-major, lda even, 16-byte
+// aligned).  Persistent CTAs over tiles of 64 rows x 32 columns, the next tile prefetched with
+// cp.async; thread (kc = tid % 32, g = tid / 32) converts rows 8 g .. 8 g + 7 of column kc, stages
+// its 8 bytes per modulus ([j][kc][64 rows], row pitch 80 B: conflict-free 8-byte stores), then
+// each modulus' 32 x 64-byte block is written in 16-byte chunks (whole 64-byte runs per row).
+constexpr int kColsPitch = 80;
+constexpr size_t kColsSmem = 2 * 64 * 32 * sizeof(double) + NMOD * 32 * kColsPitch;
+__global__ void __launch_bounds__(256) oz_cols_t_kernel(const double* __restrict__ A, int64_t lda, int rows, int cols,
+                                                        const int* __restrict__ exps, int8_t* __restrict__ out,
+                                                        int64_t ldo, int64_t plane, const OzTab tb) {
+  extern __shared__ __align__(16) unsigned char csm[];
+  double* in = reinterpret_cast<double*>(csm);                      // [2][64][32]
+  unsigned char* stg = csm + 2 * 64 * 32 * sizeof(double);          // [16][32][kColsPitch]
+  const int tiles_k = (cols + 31) / 32;
+  const int ntiles = tiles_k * ((rows + 63) / 64);
+  const int tid = threadIdx.x;
+  auto issue = [&](int tile, int buf) {
+    if (tile < ntiles) {
+      const int kb = (tile % tiles_k) * 32, rb = (tile / tiles_k) * 64;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int ch = tid + 256 * i;  // row ch / 16, doubles 2 (ch % 16)
+        const int rr = ch >> 4, kk = kb + 2 * (ch & 15);
+        const bool ok = rb + rr < rows && kk < lda;
+        cp16(in + (buf * 64 + rr) * 32 + 2 * (ch & 15), ok ? A + (int64_t)(rb + rr) * lda + kk : A, ok ? 16u : 0u);
+      }
+    }
+    cp_commit();
+  };
+  int tile = blockIdx.x;
+  issue(tile, 0);
+  const int kc = tid & 31, g = tid >> 5;
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int buf = it & 1;
+    issue(tile + gridDim.x, buf ^ 1);
+    cp_wait<1>();
+    __syncthreads();
+    const int kb = (tile % tiles_k) * 32, rb = (tile / tiles_k) * 64;
+    const int k = kb + kc;
+    const int e = k < cols ? exps[k] : 0;
+    const bool dead = (k >= cols) || e == kExpNonFinite;
+    const int e1 = e >> 1;
+    const double s1 = pow2(e1), s2 = pow2(e - e1);
+    unsigned w[NMOD][2];
+    {
+      double xh[8], xl[8];
+#pragma unroll
+      for (int e8 = 0; e8 < 8; ++e8) {
+        const int rr = 8 * g + e8;
+        split26(!dead && rb + rr < rows ? in[(buf * 64 + rr) * 32 + kc] : 0.0, s1, s2, xh[e8], xl[e8]);
+      }
+      residue_words8(xh, xl, tb, w);
+    }
+#pragma unroll
+    for (int j = 0; j < NMOD; ++j)
+      *reinterpret_cast<uint2*>(stg + (j * 32 + kc) * kColsPitch + 8 * g) = make_uint2(w[j][0], w[j][1]);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int ch = tid + 256 * i;  // plane ch / 128, row (ch / 4) % 32, 16-byte chunk ch % 4
+      const int j = ch >> 7, orow = (ch >> 2) & 31, c16 = (ch & 3) * 16;
+      const int ko = kb + orow;
+      if (ko < cols && rb + c16 < ldo)
+        *reinterpret_cast<uint4*>(out + (int64_t)j * plane + (int64_t)ko * ldo + rb + c16) =
+            *reinterpret_cast<const uint4*>(stg + (j * 32 + orow) * kColsPitch + c16);
+    }
+  }
+  cp_wait<0>();
+}
+
+// ------------------------------------------------------------------------------------------------
+// INT8 tensor-core GEMM (tcgen05.mma.cta_group::1.kind::i8): per (K-split s, modulus j, 128 x 256
+// output tile) item  C = A_j(m, k) B_j(n, k)^T  over the split's k range, both operands K-major in
+// 128-byte swizzled TMA boxes of 128 k; a 4-deep ring (48 KB stages); int32 accumulators in TMEM,
+// double-buffered (2 x 256 columns) so the epilogue of one item overlaps the next item's MMAs.
+//   warp 0: TMA producer (one lane)   warp 1: TMEM allocation + MMA issue (one lane)
+//   warps 2-5: epilogue -- tcgen05.ld 32 columns at a time, reduce mod m_j, store int8 residues
+//              res[(s NMOD + j) plane + n ldo + m]   (column-major, coalesced over m)
+// Items walk n fastest, then m, then (j, s): the CTAs that share an A panel run together and one
+// modulus' B panel stays in L2 while every m-tile reads it.
+constexpr int IBM = 128, IBN = 256, IBK = 128, INS = 4;
+constexpr int kI8Threads = 192;
+struct __align__(1024) I8Stage {
+  int8_t A[IBM * IBK];
+  int8_t B[IBN * IBK];
+};
+constexpr size_t kI8Smem = sizeof(I8Stage) * INS + 1024 + 256;
+
+struct I8Args {
+  int M, N, splits, tiles_m, tiles_n, kblocks, kb_per_split;
+  int8_t* res;
+  int64_t ldo, plane;
+};
+
+__device__ __forceinline__ unsigned sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(unsigned long long* m, unsigned c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(m)), "r"(c));
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* m, unsigned par) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0,1,0,p;\n}\n"
+        : "=r"(done)
+        : "r"(sa(m)), "r"(par)
+        : "memory");
+}
+__device__ __forceinline__ void mb_expect(unsigned long long* m, unsigned b) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(m)), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(m)) : "memory");
+}
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, unsigned long long* m) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(sa(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(sa(m))
+      : "memory");
+}
+// shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row core groups 1024 B apart
+__device__ __forceinline__ uint64_t sw128(unsigned saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ void mma_i8(unsigned tmem, uint64_t ad, uint64_t bd, unsigned idesc, unsigned acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(unsigned long long* m) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(m)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kI8Threads, 1)
+    oz_i8gemm_kernel(const __grid_constant__ I8Args a, const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapB) {
+  extern __shared__ unsigned char raw[];
+  unsigned char* base = raw + ((1024u - (sa(raw) & 1023u)) & 1023u);
+  I8Stage* st = reinterpret_cast<I8Stage*>(base);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(st + INS);
+  unsigned long long* empty = full + INS;
+  unsigned long long* tfull = empty + INS;
+  unsigned long long* tempty = tfull + 2;
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < INS; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mb_init(&tfull[b], 1);
+      mb_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sa(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tmem = *tmem_slot;
+  const int per = a.tiles_m * a.tiles_n;
+  const int n_items = per * NMOD * a.splits;
+  if (warp == 0) {
+    if (lane == 0) {
+      unsigned q = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int js = it / per, r = it % per;
+        const int j = js % NMOD, s = js / NMOD;
+        const int m0 = (r / a.tiles_n) * IBM, n0 = (r % a.tiles_n) * IBN;
+        const int kb0 = s * a.kb_per_split, kb1 = min(a.kblocks, kb0 + a.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
+          const int sl = q % INS;
+          if (q >= INS) mb_wait(&empty[sl], ((q / INS) - 1) & 1);
+          mb_expect(&full[sl], sizeof(I8Stage));
+          tma3(st[sl].A, &mapA, kb * IBK, m0, j, &full[sl]);
+          tma3(st[sl].B, &mapB, kb * IBK, n0, j, &full[sl]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // D s32, A s8, B s8, both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+      const unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(IBN >> 3) << 17) |
+                             ((unsigned)(IBM >> 4) << 24);
+      unsigned q = 0, u = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++u) {
+        const int js = it / per;
+        const int s = js / NMOD;
+        const int kb0 = s * a.kb_per_split, kb1 = min(a.kblocks, kb0 + a.kb_per_split);
+        const int buf = u & 1;
+        if (u >= 2) mb_wait(&tempty[buf], ((u >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const unsigned d = tmem + buf * IBN;
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
+          const int sl = q % INS;
+          mb_wait(&full[sl], (q / INS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t ad = sw128(sa(st[sl].A)), bd = sw128(sa(st[sl].B));
+#pragma unroll
+          for (int k = 0; k < IBK / 32; ++k) mma_i8(d, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k) ? 1u : 0u);
+          mma_commit(&empty[sl]);
+        }
+        mma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    unsigned u = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++u) {
+      const int buf = u & 1;
+      const int js = it / per, r = it % per;
+      const int j = js % NMOD;
+      const int m0 = (r / a.tiles_n) * IBM, n0 = (r % a.tiles_n) * IBN;
+      double mj = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < NMOD; ++jj)
+        if (jj == j) mj = (double)mod_of(jj);
+      const double inv = 1.0 / mj;
+      mb_wait(&tfull[buf], (u >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + row;
+      int8_t* o = a.res + (int64_t)js * a.plane + m;
+      const int ncols = min(IBN, a.N - n0);
+#pragma unroll 1
+      for (int c = 0; c < IBN; c += 32) {
+        if (c >= ncols) break;  // warp-uniform
+        int v[32];
+        tmem_ld32(tmem + ((unsigned)(quarter * 32) << 16) + buf * IBN + c, v);
+        if (m < a.M) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (c + i < ncols) {
+              const double x = (double)v[i];
+              const double qq = fma(x, inv, kMagic) - kMagic;
+              const double rr = fma(-qq, mj, x);
+              o[(int64_t)(n0 + c + i) * a.ldo] = (int8_t)(__double2loint(rr + kMagic) & 0xFF);
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mb_arrive(&tempty[buf]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ------------------------------------------------------------------------------------------------
+// CRT reconstruction + scaling: C(m, n) = alpha rw(m) 2^-(ea_m + eb_n) C'(m, n) + beta C(m, n).
+// Thread per (n, 4 consecutive m); residues summed over the K-splits.
+__global__ void __launch_bounds__(256) oz_crt_kernel(const int8_t* __restrict__ res, int64_t ldo, int64_t plane,
+                                                     int splits, int M, int N, const int* __restrict__ ea,
+                                                     const int* __restrict__ eb, const double* __restrict__ rw,
+                                                     double alpha, double beta, double* __restrict__ C, int64_t ldc,
+                                                     const OzTab tb) {
+  const int mq = (M + 3) / 4;
+  const int64_t total = (int64_t)mq * N;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(w / mq);
+    const int m0 = (int)(w % mq) * 4;
+    double T1[4] = {0, 0, 0, 0}, T2[4] = {0, 0, 0, 0}, T3[4] = {0, 0, 0, 0};
+    const int8_t* rp = res + (int64_t)n * ldo + m0;
+#pragma unroll
+    for (int j = 0; j < NMOD; ++j) {
+      int r[4] = {0, 0, 0, 0};
+      for (int s = 0; s < splits; ++s) {
+        const unsigned wv = *reinterpret_cast<const unsigned*>(rp + (int64_t)(s * NMOD + j) * plane);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) r[e] += (int)(int8_t)((wv >> (8 * e)) & 0xFF);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        int x = r[e];
+        if (splits > 1) {  // |x| <= 128 splits: bring into [-m/2, m/2]
+          const int m = mod_of(j);
+          x -= m * __float2int_rn((float)x / (float)m);
+        }
+        const double xd = (double)x;
+        T1[e] = fma(xd, tb.h[j], T1[e]);
+        T2[e] = fma(xd, tb.g[j], T2[e]);
+        T3[e] = fma(xd, tb.l[j], T3[e]);
+      }
+    }
+    const int ebn = eb[n];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int m = m0 + e;
+      if (m >= M) break;
+      const int eam = ea[m];
+      double v;
+      if (eam == kExpNonFinite || ebn == kExpNonFinite) {
+        v = __longlong_as_double(0x7ff8000000000000ll);
+      } else {
+        // C'/M = T1 2^-41 + T2 2^-82 + T3 2^-123  (mod 1, symmetric)
+        const double k1 = fma(T1[e], 1.0 / 2199023255552.0, kMagic) - kMagic;  // rint(T1 2^-41)
+        const double t1 = fma(-k1, 2199023255552.0, T1[e]);                     // exact, |t1| <= 2^40
+        const double lo = T2[e] * (1.0 / 4835703278458516698824704.0) + T3[e] * 9.4039548065783000637e-38;
+        const double f = fma(t1, 1.0 / 2199023255552.0, lo);
+        v = scale2(f * tb.md, -(eam + ebn));
+      }
+      if (rw) v *= rw[m];
+      v *= alpha;
+      double* dst = C + (int64_t)n * ldc + m;
+      if (beta != 0.0) v = fma(beta, *dst, v);
+      *dst = v;
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 oz_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// [NMOD][rows][ld] int8 residues, K = valid row length: box {128 k, box_rows, 1}
+bool encode_res(CUtensorMap* m, const int8_t* p, int K, int rows, int64_t ld, int box_rows) {
+  auto enc = oz_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)NMOD};
+  cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)ld * rows};
+  cuuint32_t box[3] = {IBK, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+static double g_oz_ops = 0.0;  // INT8 tensor ops (2 M N K per modulus) launched so far
+double oz_i8_ops_total() { return g_oz_ops; }
+
+int oz_bits(int64_t K) {
+  const double t = std::floor((tab().log2m - 1.0 - std::log2((double)std::max<int64_t>(K, 1)) - 1e-9) / 2.0);
+  return (int)std::min(53.0, t);
+}
+
+int oz_splits(int64_t K) {
+  const int64_t kb = (K + IBK - 1) / IBK;
+  const int64_t max_kb = kOzMaxKSplit / IBK;  // K-blocks per split with an exact int32 accumulator
+  return (int)((kb + max_kb - 1) / max_kb);
+}
+
+cudaError_t oz_exps(const unsigned long long* maxbits, int n, int t, int* exps, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  probe_before(K_OZCONV, st);
+  oz_exps_kernel<<<(n + 255) / 256, 256, 0, st>>>(maxbits, n, t, exps);
+  probe_after(K_OZCONV, st);
+  return cudaGetLastError();
+}
+
+// persistent grid: resident CTAs per SM x 148 (queried once per kernel; sets the smem attribute)
+template <typename Kern>
+static cudaError_t persistent_grid(Kern k, size_t smem, int& grid) {
+  if (grid > 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 256, smem);
+  if (e != cudaSuccess) return e;
+  grid = 148 * std::max(per, 1);
+  return cudaSuccess;
+}
+
+cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t* out, int64_t ldo, int64_t plane,
+                    int* exps, bool have_exps, cudaStream_t st) {
+  if (rows <= 0 || K <= 0) return cudaSuccess;
+  if ((ldo & 15) || K > ldo || K > lda || (lda & 1) || (reinterpret_cast<uintptr_t>(A) & 15))
+    return cudaErrorInvalidValue;
+  static int grid = 0;
+  const cudaError_t ea = persistent_grid(oz_rows_kernel, kRowsSmem, grid);
+  if (ea != cudaSuccess) return ea;
+  if (!have_exps) {
+    probe_before(K_OZCONV, st);
+    oz_rowmax_kernel<<<rows, 256, 0, st>>>(A, lda, rows, K, t, exps);
+    probe_after(K_OZCONV, st);
+  }
+  const int64_t tiles = (int64_t)((rows + kRowsT - 1) / kRowsT) * ((ldo + kRowsK - 1) / kRowsK);
+  probe_before(K_OZCONV, st);
+  oz_rows_kernel<<<(int)std::min<int64_t>(tiles, grid), 256, kRowsSmem, st>>>(A, lda, rows, K, exps, out, ldo,
+                                                                                   plane, tab());
+  probe_after(K_OZCONV, st);
+  return cudaGetLastError();
+}
+
+cudaError_t oz_cols_t(const double* A, int64_t lda, int rows, int cols, const int* exps, int8_t* out, int64_t ldo,
+                      int64_t plane, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if ((ldo & 15) || rows > ldo || cols > lda || (lda & 1) || (reinterpret_cast<uintptr_t>(A) & 15))
+    return cudaErrorInvalidValue;
+  static int grid = 0;
+  const cudaError_t ea = persistent_grid(oz_cols_t_kernel, kColsSmem, grid);
+  if (ea != cudaSuccess) return ea;
+  const int64_t tiles = (int64_t)((cols + 31) / 32) * ((rows + 63) / 64);
+  probe_before(K_OZCONV, st);
+  oz_cols_t_kernel<<<(int)std::min<int64_t>(tiles, grid), 256, kColsSmem, st>>>(A, lda, rows, cols, exps, out,
+                                                                                     ldo, plane, tab());
+  probe_after(K_OZCONV, st);
+  return cudaGetLastError();
+}
+
+cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int M, const int8_t* B, int64_t ldb, int N, int K, int8_t* res,
+                      int64_t ldo, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  if ((lda & 15) || (ldb & 15) || (ldo & 3) || K > lda || K > ldb || M > ldo) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(oz_i8gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kI8Smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  I8Args a{};
+  a.M = M;
+  a.N = N;
+  a.tiles_m = (M + IBM - 1) / IBM;
+  a.tiles_n = (N + IBN - 1) / IBN;
+  a.kblocks = (K + IBK - 1) / IBK;
+  a.splits = oz_splits(K);
+  a.kb_per_split = (a.kblocks + a.splits - 1) / a.splits;
+  a.res = res;
+  a.ldo = ldo;
+  a.plane = ldo * N;
+  CUtensorMap ma, mb;
+  if (!encode_res(&ma, A, K, M, lda, IBM) || !encode_res(&mb, B, K, N, ldb, IBN)) return cudaErrorInvalidValue;
+  const int items = a.tiles_m * a.tiles_n * NMOD * a.splits;
+  const int grid = std::min(items, 148);
+  g_oz_ops += 2.0 * NMOD * (double)M * N * (double)K;
+  probe_before(K_I8GEMM, st);
+  oz_i8gemm_kernel<<<grid, kI8Threads, kI8Smem, st>>>(a, ma, mb);
+  probe_after(K_I8GEMM, st);
+  return cudaGetLastError();
+}
+
+cudaError_t oz_crt(const int8_t* res, int64_t ldo, int M, int N, int splits, const int* ea, const int* eb,
+                   const double* row_w, double alpha, double beta, double* C, int64_t ldc, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (ldo & 3) return cudaErrorInvalidValue;
+  const int64_t total = (int64_t)((M + 3) / 4) * N;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  probe_before(K_OZCRT, st);
+  oz_crt_kernel<<<blocks, 256, 0, st>>>(res, ldo, ldo * N, splits, M, N, ea, eb, row_w, alpha, beta, C, ldc, tab());
+  probe_after(K_OZCRT, st);
+  return cudaGetLastError();
+}
+
+}  // namespace ngd

@@ -76,6 +76,8 @@ int64_t ngd_launch_count(void) { return (int64_t)ngd::g_launches.load(); }
 
 double ngd_gemm_flops(void) { return ngd::gemm_flops_total(); }
 
+double ngd_i8_ops(void) { return ngd::oz_i8_ops_total(); }
+
 int ngd_probe_start(int32_t kind, int32_t max_launches) {
   using ngd::g_probe;
   int dev = 0;
