@@ -76,6 +76,15 @@ def load_peaks():
     # tools/probe/fp64_peak.cu (profiles/r01_fp64_peak.txt): DMMA m16n8k16 36.99 TF/s,
     # DFMA 36.63 TF/s, cuBLAS DGEMM 8192^3 35.45 TF/s.
     peaks["fp64_tflops"] = 36.99
+    # INT8 dense tensor peak: not in MEASURED_PEAKS.json; NVIDIA's dense INT8 rate is twice the
+    # dense bf16 rate (4.5 vs 2.25 POPS nominal), applied to the measured cuBLAS bf16 burst figure
+    bf16 = None
+    if os.path.exists(path):
+        with open(path) as f:
+            bf16 = json.load(f).get("bf16_tflops")
+    peaks["int8_tops"] = 2.0 * float(bf16) if bf16 else 3180.0
+    peaks["int8_source"] = ("2 x measured bf16 burst (MEASURED_PEAKS.json bf16_tflops)" if bf16
+                            else "2 x fallback bf16 1.59 PFLOP/s (B200_PROFILING.md)")
     return peaks
 
 
@@ -326,7 +335,8 @@ def run_reference(args, rank):
 # ---------------------------------------------------------------------------
 
 
-def roofline_entry(kind, widths, n_int, n_bnd, ell, p, count, total_ms, peaks, gemm_flops=None, sweeps=(0, 0)):
+def roofline_entry(kind, widths, n_int, n_bnd, ell, p, count, total_ms, peaks, gemm_flops=None, sweeps=(0, 0),
+                   i8_ops=None, conv_elems=None):
     """Algorithmic work per launch of kernel class `kind` / average duration."""
     d = widths[0]
     S = n_int * (d + 2) + n_bnd
@@ -347,6 +357,11 @@ def roofline_entry(kind, widths, n_int, n_bnd, ell, p, count, total_ms, peaks, g
     elif kind == 14:  # DMMA GEMM: the library's running count of 2 M N K over the probed launches
         work = (gemm_flops or 0.0) / max(count, 1)
         note = "sum of 2 M N K over the GEMM launches of the timed region (split-K reductions timed too)"
+    elif kind == 15:  # INT8 tensor-core GEMM (Ozaki II): 2 M N K per modulus, library count
+        unit, peak = "TOPS", peaks["int8_tops"]
+        work = (i8_ops or 0.0) / max(count, 1)
+        note = ("sum of 2 M N K x 16 moduli (INT8 ops) over the launches of the timed region; the FP64-exact "
+                "product they make is 1/16 of that in FP64-equivalent FLOP")
     elif kind == 9:
         launches = 2 if sweeps[1] > 0 else 1
         work = 9.0 * ell * ell * (ell - 1) * (max(sweeps[0], 1) + sweeps[1]) / launches
@@ -360,7 +375,10 @@ def roofline_entry(kind, widths, n_int, n_bnd, ell, p, count, total_ms, peaks, g
         note = "nominal 22 l^3 FLOP (cuSOLVER gesvdp)"
     else:  # memory-bound classes
         bound, unit, peak = "hbm", "GB/s", peaks["hbm_gbs"]
-        if kind == 5:
+        if kind == 16:
+            work = (conv_elems or 0.0) * 24.0 / max(count, 1)
+            note = "8 B read + 16 B (residues) written per converted element (FP64-pipe bound in practice)"
+        elif kind == 5:
             work = 8.0 * p * min(n_int + n_bnd, max(1, (8 << 30) // (8 * p)))
             note = "8 p bytes per Jacobian row written"
         elif kind == 6:
@@ -369,12 +387,13 @@ def roofline_entry(kind, widths, n_int, n_bnd, ell, p, count, total_ms, peaks, g
         else:
             work = 8.0 * 3 * p
     avg_s = total_ms * 1e-3 / max(count, 1)
-    achieved = (work / max(avg_s, 1e-30)) / (1e12 if unit == "TFLOP/s" else 1e9)
+    achieved = (work / max(avg_s, 1e-30)) / (1e12 if unit in ("TFLOP/s", "TOPS") else 1e9)
     return {"bound": bound, "kernel": KIND_NAMES.get(kind, str(kind)), "achieved": achieved, "peak": peak,
             "unit": unit, "frac": achieved / peak, "traffic": None, "launches": int(count),
             "avg_launch_us": avg_s * 1e6, "algorithmic_work_per_launch": work, "work_note": note,
             "peak_source": "FP64: DMMA measured on this pool (tools/probe/fp64_peak.cu, profiles/r01_fp64_peak.txt); "
-                           f"HBM: {peaks['hbm_gbs']} GB/s from {peaks['source']}"}
+                           f"HBM: {peaks['hbm_gbs']} GB/s from {peaks['source']}; INT8: {peaks['int8_tops']:.0f} "
+                           f"TOPS = {peaks['int8_source']}"}
 
 
 def probe_all(_lib, lib, fn):
@@ -419,17 +438,20 @@ def standalone_rooflines(ngd, _lib, lib, prob, quad, theta0, widths, n_int, n_bn
     n_pts = n_int + n_bnd
     Vcm = torch.randn((ell, p), dtype=torch.float64, device="cuda")
     Ycm = torch.empty_like(Vcm)
-    f0 = lib.ngd_gemm_flops()
+    f0, i0 = lib.ngd_gemm_flops(), lib.ngd_i8_ops()
     s0.record()
     gop.matmat_colmajor(Vcm, Ycm)
     s1.record()
     s1.synchronize()
     sk_ms = s0.elapsed_time(s1)
     fl = 4.0 * n_pts * p * ell
+    i8 = lib.ngd_i8_ops() - i0
     out["sketch_block"] = {"ms": sk_ms, "tflops": fl / (sk_ms * 1e-3) / 1e12,
                            "frac_fp64": fl / (sk_ms * 1e-3) / 1e12 / peaks["fp64_tflops"],
-                           "gemm_flops": lib.ngd_gemm_flops() - f0,
-                           "note": "4 N p l FLOP (J-chunk: J rows + S = J Omega + Y = J^T(w S), in-house DMMA GEMM)"}
+                           "gemm_flops": lib.ngd_gemm_flops() - f0, "int8_ops": i8,
+                           "engine": "int8 tensor cores (Ozaki II, FP64-exact)" if i8 > 0 else "FP64 DMMA",
+                           "note": "4 N p l FP64-equivalent FLOP (J-chunk: J rows + S = J Omega + Y = J^T(w S)); "
+                                   "frac_fp64 is against the FP64 DMMA peak (the INT8 engine can exceed 1)"}
     return out
 
 
@@ -523,6 +545,8 @@ def main():
     clocks.start()
     launches0 = lib.ngd_launch_count()
     flops0 = lib.ngd_gemm_flops()
+    i80 = lib.ngd_i8_ops()
+    conv0 = lib.ngd_oz_conv_elems()
     _lib.check(lib.ngd_probe_start(probe_kind, 1 << 15))
     step_ms = []
     matvecs = sketch_cols = 0
@@ -540,6 +564,8 @@ def main():
     torch.cuda.synchronize()
     launches = lib.ngd_launch_count() - launches0
     gemm_flops = lib.ngd_gemm_flops() - flops0
+    i8_ops = lib.ngd_i8_ops() - i80
+    conv_elems = lib.ngd_oz_conv_elems() - conv0
     ktot = _lib.ctypes.c_double()
     kcnt = _lib.ctypes.c_int64()
     _lib.check(lib.ngd_probe_stop(_lib.ctypes.byref(ktot), _lib.ctypes.byref(kcnt)))
@@ -561,7 +587,8 @@ def main():
     p = len(theta0)
     if kcnt.value > 0:
         roof = roofline_entry(probe_kind, widths, n_int // world, n_bnd // world, ell, p, kcnt.value, ktot.value,
-                              peaks, gemm_flops=gemm_flops, sweeps=(abs(sweeps.value), abs(sweeps_f32.value)))
+                              peaks, gemm_flops=gemm_flops, sweeps=(abs(sweeps.value), abs(sweeps_f32.value)),
+                              i8_ops=i8_ops, conv_elems=conv_elems)
         roof["timed"] = "CUDA events around each launch of the class on its stream, inside the timed region"
     else:  # the class only runs inside the captured PCG graph: its classification-step timing
         ms_c, cnt_c = class_ms[KIND_NAMES[probe_kind]]
@@ -627,6 +654,7 @@ def main():
             "gramian_matvecs_per_sec": matvecs / (total_ms * 1e-3),
             "sketch_columns_per_sec": sketch_cols / (total_ms * 1e-3),
             "matvecs_per_step": matvecs / args.steps, "gemm_tflops_in_step": gemm_flops / (total_ms * 1e-3) / 1e12,
+            "int8_tops_in_step": i8_ops / (total_ms * 1e-3) / 1e12,
             "roofline": roof, "north_star_kernels": extra, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk,
         }

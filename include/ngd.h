@@ -189,6 +189,8 @@ int64_t ngd_launch_count(void);
 double ngd_gemm_flops(void);
 /* INT8 tensor ops (2 M N K per modulus) of every Ozaki-scheme GEMM launched so far (process-wide) */
 double ngd_i8_ops(void);
+/* FP64 elements converted to residues (Ozaki scheme) so far (process-wide) */
+double ngd_oz_conv_elems(void);
 int ngd_probe_start(int32_t kind, int32_t max_launches);
 int ngd_probe_stop(double* h_total_ms, int64_t* h_count);
 int ngd_probe_stop_all(double* h_ms, int64_t* h_count, int32_t n_kinds);

@@ -138,6 +138,7 @@ constexpr int kOzMaxKSplit = 130944;  // K per split: 128 * 128 * K < 2^31
 int oz_bits(int64_t K);               // integer width t of the scaled operands for inner length K
 int oz_splits(int64_t K);
 double oz_i8_ops_total();
+double oz_conv_elems_total();
 cudaError_t oz_exps(const unsigned long long* maxbits, int n, int t, int* exps, cudaStream_t st);
 cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t* out, int64_t ldo, int64_t plane,
                     int* exps, bool have_exps, cudaStream_t st);

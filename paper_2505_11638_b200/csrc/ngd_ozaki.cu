@@ -666,6 +666,8 @@ bool encode_res(CUtensorMap* m, const int8_t* p, int K, int rows, int64_t ld, in
 
 static double g_oz_ops = 0.0;  // INT8 tensor ops (2 M N K per modulus) launched so far
 double oz_i8_ops_total() { return g_oz_ops; }
+static double g_oz_conv = 0.0;  // FP64 elements converted to residues so far
+double oz_conv_elems_total() { return g_oz_conv; }
 
 int oz_bits(int64_t K) {
   const double t = std::floor((tab().log2m - 1.0 - std::log2((double)std::max<int64_t>(K, 1)) - 1e-9) / 2.0);
@@ -713,6 +715,7 @@ cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t
     probe_after(K_OZCONV, st);
   }
   const int64_t tiles = (int64_t)((rows + kRowsT - 1) / kRowsT) * ((ldo + kRowsK - 1) / kRowsK);
+  g_oz_conv += (double)rows * K;
   probe_before(K_OZCONV, st);
   oz_rows_kernel<<<(int)std::min<int64_t>(tiles, grid), 256, kRowsSmem, st>>>(A, lda, rows, K, exps, out, ldo,
                                                                                    plane, tab());
@@ -729,6 +732,7 @@ cudaError_t oz_cols_t(const double* A, int64_t lda, int rows, int cols, const in
   const cudaError_t ea = persistent_grid(oz_cols_t_kernel, kColsSmem, grid);
   if (ea != cudaSuccess) return ea;
   const int64_t tiles = (int64_t)((cols + 31) / 32) * ((rows + 63) / 64);
+  g_oz_conv += (double)rows * cols;
   probe_before(K_OZCONV, st);
   oz_cols_t_kernel<<<(int)std::min<int64_t>(tiles, grid), 256, kColsSmem, st>>>(A, lda, rows, cols, exps, out,
                                                                                      ldo, plane, tab());

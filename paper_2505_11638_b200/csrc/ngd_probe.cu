@@ -78,6 +78,8 @@ double ngd_gemm_flops(void) { return ngd::gemm_flops_total(); }
 
 double ngd_i8_ops(void) { return ngd::oz_i8_ops_total(); }
 
+double ngd_oz_conv_elems(void) { return ngd::oz_conv_elems_total(); }
+
 int ngd_probe_start(int32_t kind, int32_t max_launches) {
   using ngd::g_probe;
   int dev = 0;
