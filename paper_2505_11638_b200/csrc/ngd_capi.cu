@@ -1173,10 +1173,13 @@ static int matmat_ozaki(ngd_ctx* c, FormJPlan& pl, const GemmOperand& vop, int e
   const int64_t ldr = rup(pl.R, 16);
   const int tp = oz_bits(p), tr = oz_bits(pl.R);
   const int sp = oz_splits(p);
-  CK(c->oz_a.ensure((size_t)kOzMods * std::max<int64_t>(pl.R * ldp, (int64_t)p * ldr)));
-  CK(c->oz_b.ensure((size_t)kOzMods * ell * ldp));
-  CK(c->oz_s.ensure((size_t)kOzMods * ell * ldr));
-  CK(c->oz_res.ensure((size_t)kOzMods * ell * std::max<int64_t>(ldp, sp * ldr)));
+  const int64_t pl_row = oz_plane(pl.R, ldp);                             // J_c residue planes
+  const int64_t pl_v = oz_plane(ell, ldp), pl_s = oz_plane(ell, ldr);      // V, S residue planes
+  const int64_t pl_ys = oz_plane(ell, ldr), pl_yy = oz_plane(ell, ldp);    // product residues (S, Y)
+  CK(c->oz_a.ensure((size_t)kOzMods * pl_row));
+  CK(c->oz_b.ensure((size_t)kOzMods * pl_v));
+  CK(c->oz_s.ensure((size_t)kOzMods * pl_s));
+  CK(c->oz_res.ensure((size_t)kOzMods * std::max(pl_yy, sp * pl_ys)));
   CK(c->oz_ea.ensure(sizeof(int) * pl.R));
   CK(c->oz_ec.ensure(sizeof(int) * p));
   CK(c->oz_eb.ensure(sizeof(int) * ell));
@@ -1194,7 +1197,7 @@ static int matmat_ozaki(ngd_ctx* c, FormJPlan& pl, const GemmOperand& vop, int e
   auto* cmax = rmax + pl.R;
   pl.fa.rmax = rmax;
   pl.fa.cmax = cmax;
-  CK(oz_rows(vop.p, vop.ld, ell, p, tp, B8, ldp, (int64_t)ell * ldp, ev, false, c->stream));
+  CK(oz_rows(vop.p, vop.ld, ell, p, tp, B8, ldp, pl_v, ev, false, c->stream));
   for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
     const int nb = std::min(pl.bpc, pl.nblk_total - b0);
     const int r = nb * PB;
@@ -1204,13 +1207,14 @@ static int matmat_ozaki(ngd_ctx* c, FormJPlan& pl, const GemmOperand& vop, int e
     CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));  // J_c + its row / column maxima
     CK(oz_exps(rmax, r, tp, er, c->stream));
     CK(oz_exps(cmax, p, tr, ec, c->stream));
-    CK(oz_rows(c->jt.d(), ldp, r, p, tp, A8, ldp, (int64_t)r * ldp, er, true, c->stream));
-    CK(oz_i8gemm(A8, ldp, r, B8, ldp, ell, p, R8, ldr, c->stream));
-    CK(oz_crt(R8, ldr, r, ell, sp, er, ev, c->w_pad.d() + q0, 1.0, 0.0, c->smat.d(), r, c->stream));
-    CK(oz_cols_t(c->jt.d(), ldp, r, p, ec, A8, ldr, (int64_t)p * ldr, c->stream));
-    CK(oz_rows(c->smat.d(), r, ell, r, tr, S8, ldr, (int64_t)ell * ldr, es, false, c->stream));
-    CK(oz_i8gemm(A8, ldr, p, S8, ldr, ell, r, R8, ldp, c->stream));
-    CK(oz_crt(R8, ldp, p, ell, 1, ec, es, nullptr, 1.0, q0 == 0 ? 0.0 : 1.0, Y, ldy, c->stream));
+    CK(oz_rows(c->jt.d(), ldp, r, p, tp, A8, ldp, pl_row, er, true, c->stream));
+    CK(oz_i8gemm(A8, ldp, pl_row, false, r, B8, ldp, pl_v, ell, p, R8, ldr, pl_ys, c->stream));
+    CK(oz_crt(R8, ldr, pl_ys, r, ell, sp, er, ev, c->w_pad.d() + q0, 1.0, 0.0, c->smat.d(), r, c->stream));
+    // J_c^T for Y += J_c^T S: the same [points][ldp] layout, column (parameter) scaled, read MN-major
+    CK(oz_rows(c->jt.d(), ldp, r, p, tr, A8, ldp, pl_row, ec, true, c->stream, true));
+    CK(oz_rows(c->smat.d(), r, ell, r, tr, S8, ldr, pl_s, es, false, c->stream));
+    CK(oz_i8gemm(A8, ldp, pl_row, true, p, S8, ldr, pl_s, ell, r, R8, ldp, pl_yy, c->stream));
+    CK(oz_crt(R8, ldp, pl_yy, p, ell, 1, ec, es, nullptr, 1.0, q0 == 0 ? 0.0 : 1.0, Y, ldy, c->stream));
   }
   return NGD_OK;
 }
@@ -1651,6 +1655,7 @@ int ngd_gemm_ozaki(ngd_ctx* c, int32_t M, int32_t N, int32_t K, double alpha, co
   if (M < 1 || N < 1 || K < 1 || lda < K || ldb < K || ldc < M) return fail(NGD_E_SHAPE, "bad GEMM shape");
   const int64_t ldk = rup(K, 16), ldo = rup(M, 16);
   const int t = oz_bits(K), sp = oz_splits(K);
+  const int64_t pa = oz_plane(M, ldk), pb = oz_plane(N, ldk), po = oz_plane(N, ldo);
   // the residue kernels stream 16-byte chunks: operands with an odd ld / unaligned base are staged once
   GemmOperand ao{A, lda, true}, bo{B, ldb, true};
   if (!gemm_operand_ok(ao, M, K)) TRY(stage_operand(c, ao, M, K, c->gscrA));
@@ -1659,9 +1664,9 @@ int ngd_gemm_ozaki(ngd_ctx* c, int32_t M, int32_t N, int32_t K, double alpha, co
   lda = ao.ld;
   B = bo.p;
   ldb = bo.ld;
-  CK(c->oz_a.ensure((size_t)kOzMods * M * ldk));
-  CK(c->oz_b.ensure((size_t)kOzMods * N * ldk));
-  CK(c->oz_res.ensure((size_t)kOzMods * sp * N * ldo));
+  CK(c->oz_a.ensure((size_t)kOzMods * pa));
+  CK(c->oz_b.ensure((size_t)kOzMods * pb));
+  CK(c->oz_res.ensure((size_t)kOzMods * sp * po));
   CK(c->oz_ea.ensure(sizeof(int) * M));
   CK(c->oz_eb.ensure(sizeof(int) * N));
   auto* A8 = static_cast<int8_t*>(c->oz_a.p);
@@ -1669,10 +1674,10 @@ int ngd_gemm_ozaki(ngd_ctx* c, int32_t M, int32_t N, int32_t K, double alpha, co
   auto* R8 = static_cast<int8_t*>(c->oz_res.p);
   int* ea = static_cast<int*>(c->oz_ea.p);
   int* eb = static_cast<int*>(c->oz_eb.p);
-  CK(oz_rows(A, lda, M, K, t, A8, ldk, (int64_t)M * ldk, ea, false, c->stream));
-  CK(oz_rows(B, ldb, N, K, t, B8, ldk, (int64_t)N * ldk, eb, false, c->stream));
-  CK(oz_i8gemm(A8, ldk, M, B8, ldk, N, K, R8, ldo, c->stream));
-  CK(oz_crt(R8, ldo, M, N, sp, ea, eb, nullptr, alpha, beta, C, ldc, c->stream));
+  CK(oz_rows(A, lda, M, K, t, A8, ldk, pa, ea, false, c->stream));
+  CK(oz_rows(B, ldb, N, K, t, B8, ldk, pb, eb, false, c->stream));
+  CK(oz_i8gemm(A8, ldk, pa, false, M, B8, ldk, pb, N, K, R8, ldo, po, c->stream));
+  CK(oz_crt(R8, ldo, po, M, N, sp, ea, eb, nullptr, alpha, beta, C, ldc, c->stream));
   return NGD_OK;
 }
 

@@ -140,14 +140,19 @@ int oz_splits(int64_t K);
 double oz_i8_ops_total();
 double oz_conv_elems_total();
 cudaError_t oz_exps(const unsigned long long* maxbits, int n, int t, int* exps, cudaStream_t st);
+// residues of A(r, k) = A[r lda + k] scaled by 2^exps[r] (or, col_exps, by 2^exps[k]): out[j][r][ldo]
 cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t* out, int64_t ldo, int64_t plane,
-                    int* exps, bool have_exps, cudaStream_t st);
-cudaError_t oz_cols_t(const double* A, int64_t lda, int rows, int cols, const int* exps, int8_t* out, int64_t ldo,
-                      int64_t plane, cudaStream_t st);
-cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int M, const int8_t* B, int64_t ldb, int N, int K, int8_t* res,
-                      int64_t ldo, cudaStream_t st);
-cudaError_t oz_crt(const int8_t* res, int64_t ldo, int M, int N, int splits, const int* ea, const int* eb,
-                   const double* row_w, double alpha, double beta, double* C, int64_t ldc, cudaStream_t st);
+                    int* exps, bool have_exps, cudaStream_t st, bool col_exps = false);
+// plane pitch of a residue block: rounded to 256 B plus an odd multiple of 256 B, so the 16 moduli
+// planes written together do not alias onto the same memory channels (power-of-two plane strides
+// made the residue writes 4-5x slower than the HBM write bandwidth)
+inline int64_t oz_plane(int64_t rows, int64_t ld) { return (rows * ld + 255) / 256 * 256 + 37 * 256; }
+// a_mn: A stored MN-major (A(m, k) = A[k lda + m] per plane), else K-major (A[m lda + k])
+cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int64_t planeA, bool a_mn, int M, const int8_t* B, int64_t ldb,
+                      int64_t planeB, int N, int K, int8_t* res, int64_t ldo, int64_t planeO, cudaStream_t st);
+cudaError_t oz_crt(const int8_t* res, int64_t ldo, int64_t planeO, int M, int N, int splits, const int* ea,
+                   const int* eb, const double* row_w, double alpha, double beta, double* C, int64_t ldc,
+                   cudaStream_t st);
 cudaError_t gemv_rows(const double* G, int64_t n, const double* x, double* y, const int* skip, cudaStream_t st);
 
 constexpr int kMaxLayers = 8;

@@ -221,155 +221,106 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"((unsigned)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // Row-scaled residues of a K-major FP64 operand A(r, k) = A[r lda + k] (r < rows, k < K; lda even,
 // A 16-byte aligned) with the row exponents given: out[j][r][ldo] (int8, k contiguous, zero for
-// K <= k < ldo).  Persistent CTAs over tiles of 4 rows x 512 k: the next tile streams into shared
-// memory with cp.async while the current one is converted (the residue arithmetic is ~85 FP64
-// operations per element: without the prefetch every tile's load latency was exposed), and each
-// modulus' 4 x 512-byte output block leaves from a shared-memory stage in 16-byte stores.
-constexpr int kRowsT = 4, kRowsK = 512;
-constexpr size_t kRowsSmem = 2 * kRowsT * kRowsK * sizeof(double) + NMOD * kRowsT * kRowsK;
+// K <= k < ldo).  Persistent CTAs over tiles of one row x 2048 k.  Compute and memory overlap
+// (run back to back they added up: 4.2 ms of arithmetic + ~5 ms of traffic for a C3 chunk):
+//   * the next tile streams into shared memory with cp.async while this one is converted;
+//   * the 16 residue rows (2 KB each, one per modulus) leave a double-buffered shared-memory stage
+//     as asynchronous bulk copies (cp.async.bulk ... bulk_group), drained one tile later.
+constexpr int kRowsK = 2048;
+constexpr int kConvIn = 3;  // input ring depth (tiles in flight ahead of the arithmetic)
+constexpr size_t kRowsSmem = kConvIn * kRowsK * sizeof(double) + 2 * NMOD * kRowsK;
+template <bool COLS>
 __global__ void __launch_bounds__(256) oz_rows_kernel(const double* __restrict__ A, int64_t lda, int rows, int K,
                                                       const int* __restrict__ exps, int8_t* __restrict__ out,
                                                       int64_t ldo, int64_t plane, const OzTab tb) {
-  extern __shared__ __align__(16) unsigned char rsm[];
-  double* in = reinterpret_cast<double*>(rsm);                              // [2][4][512]
-  unsigned char* stg = rsm + 2 * kRowsT * kRowsK * sizeof(double);          // [16][4][512]
+  extern __shared__ __align__(128) unsigned char rsm[];
+  double* in = reinterpret_cast<double*>(rsm);                   // [kConvIn][2048]
+  unsigned char* stg = rsm + kConvIn * kRowsK * sizeof(double);  // [2][16][2048]
   const int tiles_k = (int)((ldo + kRowsK - 1) / kRowsK);
-  const int ntiles = ((rows + kRowsT - 1) / kRowsT) * tiles_k;
+  const int ntiles = rows * tiles_k;
   const int tid = threadIdx.x;
   auto issue = [&](int tile, int buf) {
     if (tile < ntiles) {
-      const int r0 = (tile / tiles_k) * kRowsT, k0 = (tile % tiles_k) * kRowsK;
+      const int r = tile / tiles_k, k0 = (tile % tiles_k) * kRowsK;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int ch = tid + 256 * i;  // 16-byte chunk: row ch / 256, doubles 2 (ch % 256)
-        const int q = ch >> 8, kk = k0 + 2 * (ch & 255);
-        const int r = r0 + q;
-        const bool ok = r < rows && kk < lda;
-        cp16(in + (buf * kRowsT + q) * kRowsK + 2 * (ch & 255), ok ? A + (int64_t)r * lda + kk : A, ok ? 16u : 0u);
+        const int kk = k0 + 2 * (tid + 256 * i);
+        const bool ok = kk < lda;
+        cp16(in + buf * kRowsK + 2 * (tid + 256 * i), ok ? A + (int64_t)r * lda + kk : A, ok ? 16u : 0u);
       }
     }
     cp_commit();
   };
+  // the row exponent is fetched one tile ahead; column exponents (COLS) are read per element (L2 / L1)
+  auto row_exp = [&](int tl) { return (!COLS && tl < ntiles) ? exps[tl / tiles_k] : 0; };
   int tile = blockIdx.x;
   issue(tile, 0);
+  issue(tile + gridDim.x, 1);
+  int e_next = row_exp(tile);
   for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    const int buf = it & 1;
-    issue(tile + gridDim.x, buf ^ 1);
-    cp_wait<1>();
+    const int buf = it & 1, ib = it % kConvIn;
+    const int e = e_next;
+    issue(tile + 2 * gridDim.x, (it + 2) % kConvIn);
+    e_next = row_exp(tile + gridDim.x);
+    if (tid == 0) bulk_wait_read<1>();  // the stage written two tiles ago has been read out
+    cp_wait<2>();
     __syncthreads();
-    const int r0 = (tile / tiles_k) * kRowsT, k0 = (tile % tiles_k) * kRowsK;
-    const int q = tid >> 6, c = tid & 63;
-    const int r = r0 + q;
-    const int e = r < rows ? exps[r] : 0;
-    const bool dead = r >= rows || e == kExpNonFinite;
-    const int e1 = e >> 1;
-    const double s1 = pow2(e1), s2 = pow2(e - e1);
+    const int r = tile / tiles_k, k0 = (tile % tiles_k) * kRowsK;
     unsigned wd[NMOD][2];
     {
       double xh[8], xl[8];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int kl = 4 * c + 256 * h;
-        const double* src = in + (buf * kRowsT + q) * kRowsK + kl;
+        const int kl = 4 * tid + (kRowsK / 2) * h;
+        const double* src = in + ib * kRowsK + kl;
         const double2 d0 = *reinterpret_cast<const double2*>(src), d1 = *reinterpret_cast<const double2*>(src + 2);
         const double v[4] = {d0.x, d0.y, d1.x, d1.y};
+        int4 ce = make_int4(e, e, e, e);
+        if (COLS && k0 + kl + 3 < K) ce = *reinterpret_cast<const int4*>(exps + k0 + kl);
+        const int ee[4] = {ce.x, ce.y, ce.z, ce.w};
 #pragma unroll
-        for (int e4 = 0; e4 < 4; ++e4)
-          split26(!dead && k0 + kl + e4 < K ? v[e4] : 0.0, s1, s2, xh[4 * h + e4], xl[4 * h + e4]);
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const int k = k0 + kl + e4;
+          const int ek = COLS ? (k < K ? (k0 + kl + 3 < K ? ee[e4] : exps[k]) : 0) : ee[e4];
+          const int e1 = ek >> 1;
+          const bool live = ek != kExpNonFinite && k < K;
+          split26(live ? v[e4] : 0.0, pow2(e1), pow2(ek - e1), xh[4 * h + e4], xl[4 * h + e4]);
+        }
       }
       residue_words8(xh, xl, tb, wd);
     }
+    unsigned* so = reinterpret_cast<unsigned*>(stg + (size_t)buf * NMOD * kRowsK);
 #pragma unroll
     for (int j = 0; j < NMOD; ++j) {
-      unsigned* o = reinterpret_cast<unsigned*>(stg + (j * kRowsT + q) * kRowsK);
-      o[c] = wd[j][0];
-      o[c + 64] = wd[j][1];
+      so[j * (kRowsK / 4) + tid] = wd[j][0];
+      so[j * (kRowsK / 4) + tid + kRowsK / 8] = wd[j][1];
     }
+    fence_async_smem();
     __syncthreads();
-    // rows past `rows` keep their previous contents; NaN-flagged rows are never read (CRT writes NaN)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int ch = tid + 256 * i;  // plane ch / 128, row (ch / 32) % 4, 16-byte column ch % 32
-      const int j = ch >> 7, qq = (ch >> 5) & 3, col = (ch & 31) * 16;
-      if (r0 + qq < rows && k0 + col < ldo)
-        *reinterpret_cast<uint4*>(out + (int64_t)j * plane + (int64_t)(r0 + qq) * ldo + k0 + col) =
-            *reinterpret_cast<const uint4*>(stg + (j * kRowsT + qq) * kRowsK + col);
+    if (tid == 0) {
+      const unsigned bytes = (unsigned)(ldo - k0 < kRowsK ? ldo - k0 : kRowsK);
+      int8_t* dst = out + (int64_t)r * ldo + k0;
+      for (int j = 0; j < NMOD; ++j)
+        bulk_store(dst + (int64_t)j * plane, stg + ((size_t)buf * NMOD + j) * kRowsK, bytes);
+      bulk_commit();
     }
   }
   cp_wait<0>();
-}
-
-// Column-scaled, transposed residues: out[j][k][ldo] holds (A(., k) scaled by 2^exps[k]) with the
-// rows r contiguous -- the K-major form of A^T for the product A^T B (A row-major, lda even, 16-byte
-// aligned).  Persistent CTAs over tiles of 64 rows x 32 columns, the next tile prefetched with
-// cp.async; thread (kc = tid % 32, g = tid / 32) converts rows 8 g .. 8 g + 7 of column kc, stages
-// its 8 bytes per modulus ([j][kc][64 rows], row pitch 80 B: conflict-free 8-byte stores), then
-// each modulus' 32 x 64-byte block is written in 16-byte chunks (whole 64-byte runs per row).
-constexpr int kColsPitch = 80;
-constexpr size_t kColsSmem = 2 * 64 * 32 * sizeof(double) + NMOD * 32 * kColsPitch;
-__global__ void __launch_bounds__(256) oz_cols_t_kernel(const double* __restrict__ A, int64_t lda, int rows, int cols,
-                                                        const int* __restrict__ exps, int8_t* __restrict__ out,
-                                                        int64_t ldo, int64_t plane, const OzTab tb) {
-  extern __shared__ __align__(16) unsigned char csm[];
-  double* in = reinterpret_cast<double*>(csm);                      // [2][64][32]
-  unsigned char* stg = csm + 2 * 64 * 32 * sizeof(double);          // [16][32][kColsPitch]
-  const int tiles_k = (cols + 31) / 32;
-  const int ntiles = tiles_k * ((rows + 63) / 64);
-  const int tid = threadIdx.x;
-  auto issue = [&](int tile, int buf) {
-    if (tile < ntiles) {
-      const int kb = (tile % tiles_k) * 32, rb = (tile / tiles_k) * 64;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int ch = tid + 256 * i;  // row ch / 16, doubles 2 (ch % 16)
-        const int rr = ch >> 4, kk = kb + 2 * (ch & 15);
-        const bool ok = rb + rr < rows && kk < lda;
-        cp16(in + (buf * 64 + rr) * 32 + 2 * (ch & 15), ok ? A + (int64_t)(rb + rr) * lda + kk : A, ok ? 16u : 0u);
-      }
-    }
-    cp_commit();
-  };
-  int tile = blockIdx.x;
-  issue(tile, 0);
-  const int kc = tid & 31, g = tid >> 5;
-  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    const int buf = it & 1;
-    issue(tile + gridDim.x, buf ^ 1);
-    cp_wait<1>();
-    __syncthreads();
-    const int kb = (tile % tiles_k) * 32, rb = (tile / tiles_k) * 64;
-    const int k = kb + kc;
-    const int e = k < cols ? exps[k] : 0;
-    const bool dead = (k >= cols) || e == kExpNonFinite;
-    const int e1 = e >> 1;
-    const double s1 = pow2(e1), s2 = pow2(e - e1);
-    unsigned w[NMOD][2];
-    {
-      double xh[8], xl[8];
-#pragma unroll
-      for (int e8 = 0; e8 < 8; ++e8) {
-        const int rr = 8 * g + e8;
-        split26(!dead && rb + rr < rows ? in[(buf * 64 + rr) * 32 + kc] : 0.0, s1, s2, xh[e8], xl[e8]);
-      }
-      residue_words8(xh, xl, tb, w);
-    }
-#pragma unroll
-    for (int j = 0; j < NMOD; ++j)
-      *reinterpret_cast<uint2*>(stg + (j * 32 + kc) * kColsPitch + 8 * g) = make_uint2(w[j][0], w[j][1]);
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int ch = tid + 256 * i;  // plane ch / 128, row (ch / 4) % 32, 16-byte chunk ch % 4
-      const int j = ch >> 7, orow = (ch >> 2) & 31, c16 = (ch & 3) * 16;
-      const int ko = kb + orow;
-      if (ko < cols && rb + c16 < ldo)
-        *reinterpret_cast<uint4*>(out + (int64_t)j * plane + (int64_t)ko * ldo + rb + c16) =
-            *reinterpret_cast<const uint4*>(stg + (j * 32 + orow) * kColsPitch + c16);
-    }
-  }
-  cp_wait<0>();
+  if (tid == 0) bulk_wait_read<0>();
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -453,6 +404,7 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+template <bool AMN>
 __global__ void __launch_bounds__(kI8Threads, 1)
     oz_i8gemm_kernel(const __grid_constant__ I8Args a, const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB) {
@@ -498,7 +450,10 @@ __global__ void __launch_bounds__(kI8Threads, 1)
           const int sl = q % INS;
           if (q >= INS) mb_wait(&empty[sl], ((q / INS) - 1) & 1);
           mb_expect(&full[sl], sizeof(I8Stage));
-          tma3(st[sl].A, &mapA, kb * IBK, m0, j, &full[sl]);
+          if constexpr (AMN)
+            tma3(st[sl].A, &mapA, m0, kb * IBK, j, &full[sl]);  // [k rows][128 m] box
+          else
+            tma3(st[sl].A, &mapA, kb * IBK, m0, j, &full[sl]);
           tma3(st[sl].B, &mapB, kb * IBK, n0, j, &full[sl]);
         }
       }
@@ -506,7 +461,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // D s32, A s8, B s8, both K-major, N >> 3 at bit 17, M >> 4 at bit 24
-      const unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(IBN >> 3) << 17) |
+      const unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | (AMN ? (1u << 15) : 0u) | ((unsigned)(IBN >> 3) << 17) |
                              ((unsigned)(IBM >> 4) << 24);
       unsigned q = 0, u = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++u) {
@@ -523,7 +478,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t ad = sw128(sa(st[sl].A)), bd = sw128(sa(st[sl].B));
 #pragma unroll
-          for (int k = 0; k < IBK / 32; ++k) mma_i8(d, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k) ? 1u : 0u);
+          for (int k = 0; k < IBK / 32; ++k)  // K-major: 32 bytes along the row; MN-major: 32 rows of 128 B
+            mma_i8(d, ad + (AMN ? 256 : 2) * k, bd + 2 * k, idesc, (kb > kb0 || k) ? 1u : 0u);
           mma_commit(&empty[sl]);
         }
         mma_commit(&tfull[buf]);
@@ -650,11 +606,11 @@ PFN_cuTensorMapEncodeTiled_v12000 oz_encode() {
 }
 
 // [NMOD][rows][ld] int8 residues, K = valid row length: box {128 k, box_rows, 1}
-bool encode_res(CUtensorMap* m, const int8_t* p, int K, int rows, int64_t ld, int box_rows) {
+bool encode_res(CUtensorMap* m, const int8_t* p, int K, int rows, int64_t ld, int64_t plane, int box_rows) {
   auto enc = oz_encode();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)NMOD};
-  cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)ld * rows};
+  cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)plane};
   cuuint32_t box[3] = {IBK, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(p), dims, strides, box, es,
@@ -702,54 +658,45 @@ static cudaError_t persistent_grid(Kern k, size_t smem, int& grid) {
 }
 
 cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t* out, int64_t ldo, int64_t plane,
-                    int* exps, bool have_exps, cudaStream_t st) {
+                    int* exps, bool have_exps, cudaStream_t st, bool col_exps) {
   if (rows <= 0 || K <= 0) return cudaSuccess;
-  if ((ldo & 15) || K > ldo || K > lda || (lda & 1) || (reinterpret_cast<uintptr_t>(A) & 15))
+  if ((ldo & 15) || K > ldo || K > lda || (lda & 1) || (reinterpret_cast<uintptr_t>(A) & 15) ||
+      (col_exps && (reinterpret_cast<uintptr_t>(exps) & 15)) || (col_exps && !have_exps))
     return cudaErrorInvalidValue;
-  static int grid = 0;
-  const cudaError_t ea = persistent_grid(oz_rows_kernel, kRowsSmem, grid);
+  static int grid[2] = {0, 0};
+  const cudaError_t ea = col_exps ? persistent_grid(oz_rows_kernel<true>, kRowsSmem, grid[1])
+                                  : persistent_grid(oz_rows_kernel<false>, kRowsSmem, grid[0]);
   if (ea != cudaSuccess) return ea;
   if (!have_exps) {
     probe_before(K_OZCONV, st);
     oz_rowmax_kernel<<<rows, 256, 0, st>>>(A, lda, rows, K, t, exps);
     probe_after(K_OZCONV, st);
   }
-  const int64_t tiles = (int64_t)((rows + kRowsT - 1) / kRowsT) * ((ldo + kRowsK - 1) / kRowsK);
+  const int64_t tiles = (int64_t)rows * ((ldo + kRowsK - 1) / kRowsK);
   g_oz_conv += (double)rows * K;
+  const int gr = (int)std::min<int64_t>(tiles, grid[col_exps]);
   probe_before(K_OZCONV, st);
-  oz_rows_kernel<<<(int)std::min<int64_t>(tiles, grid), 256, kRowsSmem, st>>>(A, lda, rows, K, exps, out, ldo,
-                                                                                   plane, tab());
+  if (col_exps)
+    oz_rows_kernel<true><<<gr, 256, kRowsSmem, st>>>(A, lda, rows, K, exps, out, ldo, plane, tab());
+  else
+    oz_rows_kernel<false><<<gr, 256, kRowsSmem, st>>>(A, lda, rows, K, exps, out, ldo, plane, tab());
   probe_after(K_OZCONV, st);
   return cudaGetLastError();
 }
 
-cudaError_t oz_cols_t(const double* A, int64_t lda, int rows, int cols, const int* exps, int8_t* out, int64_t ldo,
-                      int64_t plane, cudaStream_t st) {
-  if (rows <= 0 || cols <= 0) return cudaSuccess;
-  if ((ldo & 15) || rows > ldo || cols > lda || (lda & 1) || (reinterpret_cast<uintptr_t>(A) & 15))
-    return cudaErrorInvalidValue;
-  static int grid = 0;
-  const cudaError_t ea = persistent_grid(oz_cols_t_kernel, kColsSmem, grid);
-  if (ea != cudaSuccess) return ea;
-  const int64_t tiles = (int64_t)((cols + 31) / 32) * ((rows + 63) / 64);
-  g_oz_conv += (double)rows * cols;
-  probe_before(K_OZCONV, st);
-  oz_cols_t_kernel<<<(int)std::min<int64_t>(tiles, grid), 256, kColsSmem, st>>>(A, lda, rows, cols, exps, out,
-                                                                                     ldo, plane, tab());
-  probe_after(K_OZCONV, st);
-  return cudaGetLastError();
-}
-
-cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int M, const int8_t* B, int64_t ldb, int N, int K, int8_t* res,
-                      int64_t ldo, cudaStream_t st) {
+cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int64_t planeA, bool a_mn, int M, const int8_t* B, int64_t ldb,
+                      int64_t planeB, int N, int K, int8_t* res, int64_t ldo, int64_t planeO, cudaStream_t st) {
   if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
-  if ((lda & 15) || (ldb & 15) || (ldo & 3) || K > lda || K > ldb || M > ldo) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(oz_i8gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)kI8Smem);
+  const int64_t a_inner = a_mn ? M : K, a_outer = a_mn ? K : M;
+  if ((lda & 15) || (ldb & 15) || (ldo & 3) || a_inner > lda || K > ldb || M > ldo || (planeA & 15) ||
+      (planeB & 15) || (planeO & 3) || planeA < lda * a_outer || planeB < ldb * N || planeO < ldo * N)
+    return cudaErrorInvalidValue;
+  static bool attr[2] = {false, false};
+  if (!attr[a_mn]) {
+    const cudaError_t e = cudaFuncSetAttribute(a_mn ? oz_i8gemm_kernel<true> : oz_i8gemm_kernel<false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[a_mn] = true;
   }
   I8Args a{};
   a.M = M;
@@ -761,26 +708,32 @@ cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int M, const int8_t* B, int6
   a.kb_per_split = (a.kblocks + a.splits - 1) / a.splits;
   a.res = res;
   a.ldo = ldo;
-  a.plane = ldo * N;
+  a.plane = planeO;
   CUtensorMap ma, mb;
-  if (!encode_res(&ma, A, K, M, lda, IBM) || !encode_res(&mb, B, K, N, ldb, IBN)) return cudaErrorInvalidValue;
+  const bool ok_a = a_mn ? encode_res(&ma, A, M, K, lda, planeA, IBK)   // box {128 m, 128 k}
+                        : encode_res(&ma, A, K, M, lda, planeA, IBM);  // box {128 k, 128 m}
+  if (!ok_a || !encode_res(&mb, B, K, N, ldb, planeB, IBN)) return cudaErrorInvalidValue;
   const int items = a.tiles_m * a.tiles_n * NMOD * a.splits;
   const int grid = std::min(items, 148);
   g_oz_ops += 2.0 * NMOD * (double)M * N * (double)K;
   probe_before(K_I8GEMM, st);
-  oz_i8gemm_kernel<<<grid, kI8Threads, kI8Smem, st>>>(a, ma, mb);
+  if (a_mn)
+    oz_i8gemm_kernel<true><<<grid, kI8Threads, kI8Smem, st>>>(a, ma, mb);
+  else
+    oz_i8gemm_kernel<false><<<grid, kI8Threads, kI8Smem, st>>>(a, ma, mb);
   probe_after(K_I8GEMM, st);
   return cudaGetLastError();
 }
 
-cudaError_t oz_crt(const int8_t* res, int64_t ldo, int M, int N, int splits, const int* ea, const int* eb,
-                   const double* row_w, double alpha, double beta, double* C, int64_t ldc, cudaStream_t st) {
+cudaError_t oz_crt(const int8_t* res, int64_t ldo, int64_t planeO, int M, int N, int splits, const int* ea,
+                   const int* eb, const double* row_w, double alpha, double beta, double* C, int64_t ldc,
+                   cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  if (ldo & 3) return cudaErrorInvalidValue;
+  if ((ldo & 3) || (planeO & 3)) return cudaErrorInvalidValue;
   const int64_t total = (int64_t)((M + 3) / 4) * N;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   probe_before(K_OZCRT, st);
-  oz_crt_kernel<<<blocks, 256, 0, st>>>(res, ldo, ldo * N, splits, M, N, ea, eb, row_w, alpha, beta, C, ldc, tab());
+  oz_crt_kernel<<<blocks, 256, 0, st>>>(res, ldo, planeO, splits, M, N, ea, eb, row_w, alpha, beta, C, ldc, tab());
   probe_after(K_OZCRT, st);
   return cudaGetLastError();
 }
