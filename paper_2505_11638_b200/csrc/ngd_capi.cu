@@ -1723,6 +1723,10 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
     c->graph_gen++;  // the captured PCG iteration carries the stream's access-policy window
     return NGD_OK;
   }
+  if (!strcmp(key, "i8_pair")) {
+    g_oz_pair = value ? 1 : 0;
+    return NGD_OK;
+  }
   if (!strcmp(key, "sketch_gemm")) {
     if (value < 0 || value > 2) return fail(NGD_E_SHAPE, "sketch_gemm must be 0 (DMMA), 1 (INT8 Ozaki) or 2 (auto)");
     c->sketch_engine = (int)value;

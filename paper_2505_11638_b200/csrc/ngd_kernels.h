@@ -134,6 +134,7 @@ double gemm_flops_total();
 // CRT reconstruction.  Residue blocks are [kOzMods][rows][ld] int8 (ld a multiple of 16);
 // product residues [splits][kOzMods][N][ldo] (column-major).
 constexpr int kOzMods = 16;
+extern int g_oz_pair;  // option "i8_pair" (process-wide): CTA-pair INT8 GEMM (1) or one CTA per tile (0)
 constexpr int kOzMaxKSplit = 130944;  // K per split: 128 * 128 * K < 2^31
 int oz_bits(int64_t K);               // integer width t of the scaled operands for inner length K
 int oz_splits(int64_t K);

@@ -532,6 +532,198 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 }
 
 // ------------------------------------------------------------------------------------------------
+// CTA-pair variant (tcgen05.mma.cta_group::2): a cluster of two CTAs on one TPC computes a 256 x 512
+// item (the full TMEM of both SMs: two 128 x 256 int32 accumulators per CTA).  Per k-block of 128
+// each CTA stages its own 128 rows of A (16 KB) and its half of the item's 512 B rows (2 x 128 rows,
+// 32 KB) -- L2 traffic per MMA is half of the single-CTA 128 x 256 tile, and an A panel is read once
+// per 512 output columns instead of once per 256.  Both CTAs' TMA loads complete on the leader's
+// "full" barrier; the leader's one elected lane issues the MMAs (M = 256, N = 256, two per k-step)
+// and multicasts the completions (stage release, accumulator ready) to both CTAs; the eight epilogue
+// warps of the pair free the accumulators on the leader's barrier.  No accumulator double
+// buffering (the epilogue of an item waits for its MMAs; <= ~10% of a short-K item).
+constexpr int P_BN = 512;  // output columns per item
+struct __align__(1024) I8Stage2 {
+  int8_t A[IBM * IBK];      // this CTA's 128 rows
+  int8_t B[2][128 * IBK];   // this CTA's 128-row halves of the item's two 256-column MMAs
+};
+constexpr size_t kI8Smem2 = sizeof(I8Stage2) * INS + 1024 + 256;
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma3_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                          unsigned long long* mbar_local) {
+  const unsigned bar = sa(mbar_local) & 0xFEFFFFFFu;  // the leader CTA's barrier at the same offset
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];" ::"r"(sa(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(unsigned tmem, uint64_t ad, uint64_t bd, unsigned idesc, unsigned acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_pair(unsigned long long* m) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(sa(m)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+__device__ __forceinline__ void mb_wait_cluster(unsigned long long* m, unsigned par) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 "
+        "%0,1,0,p;\n}\n"
+        : "=r"(done)
+        : "r"(sa(m)), "r"(par)
+        : "memory");
+}
+__device__ __forceinline__ void mb_arrive_leader(unsigned long long* m) {
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(sa(m)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+template <bool AMN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
+    oz_i8gemm2_kernel(const __grid_constant__ I8Args a, const __grid_constant__ CUtensorMap mapA,
+                      const __grid_constant__ CUtensorMap mapB) {
+  extern __shared__ unsigned char raw[];
+  unsigned char* base = raw + ((1024u - (sa(raw) & 1023u)) & 1023u);
+  I8Stage2* st = reinterpret_cast<I8Stage2*>(base);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(st + INS);
+  unsigned long long* empty = full + INS;
+  unsigned long long* tfull = empty + INS;
+  unsigned long long* tempty = tfull + 1;
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned rank = cluster_rank();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < INS; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    mb_init(tfull, 1);
+    mb_init(tempty, 8);  // the pair's eight epilogue warps (leader's barrier)
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sa(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tmem = *tmem_slot;
+  const int per = a.tiles_m * a.tiles_n;  // pair m-tiles (256 rows) x n-blocks (512 columns)
+  const int n_items = per * NMOD * a.splits;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (warp == 0) {
+    if (lane == 0) {
+      unsigned q = 0;
+      for (int it = cid; it < n_items; it += ncl) {
+        const int js = it / per, r = it % per;
+        const int j = js % NMOD, s = js / NMOD;
+        const int m0 = (r / a.tiles_n) * 256 + 128 * rank, n0 = (r % a.tiles_n) * P_BN + 128 * rank;
+        const int kb0 = s * a.kb_per_split, kb1 = min(a.kblocks, kb0 + a.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
+          const int sl = q % INS;
+          if (q >= INS) mb_wait(&empty[sl], ((q / INS) - 1) & 1);
+          if (rank == 0) mb_expect(&full[sl], 2 * sizeof(I8Stage2));
+          if constexpr (AMN)
+            tma3_pair(st[sl].A, &mapA, m0, kb * IBK, j, &full[sl]);
+          else
+            tma3_pair(st[sl].A, &mapA, kb * IBK, m0, j, &full[sl]);
+          tma3_pair(st[sl].B[0], &mapB, kb * IBK, n0, j, &full[sl]);
+          tma3_pair(st[sl].B[1], &mapB, kb * IBK, n0 + 256, j, &full[sl]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // D s32, A/B s8, M = 256 (pair), N = 256 per MMA
+      const unsigned idesc =
+          (2u << 4) | (1u << 7) | (1u << 10) | (AMN ? (1u << 15) : 0u) | (256u >> 3) << 17 | (256u >> 4) << 24;
+      unsigned q = 0, u = 0;
+      for (int it = cid; it < n_items; it += ncl, ++u) {
+        const int js = it / per, r = it % per;
+        const int s = js / NMOD;
+        const int two = (r % a.tiles_n) * P_BN + 256 < a.N;  // second 256-column half present
+        const int kb0 = s * a.kb_per_split, kb1 = min(a.kblocks, kb0 + a.kb_per_split);
+        if (u >= 1) mb_wait_cluster(tempty, (u - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
+          const int sl = q % INS;
+          mb_wait(&full[sl], (q / INS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t ad = sw128(sa(st[sl].A)), bd0 = sw128(sa(st[sl].B[0])), bd1 = sw128(sa(st[sl].B[1]));
+#pragma unroll
+          for (int k = 0; k < IBK / 32; ++k) {
+            const uint64_t ak = ad + (AMN ? 256 : 2) * k;
+            const unsigned acc = (kb > kb0 || k) ? 1u : 0u;
+            mma_i8_pair(tmem, ak, bd0 + 2 * k, idesc, acc);
+            if (two) mma_i8_pair(tmem + 256, ak, bd1 + 2 * k, idesc, acc);
+          }
+          mma_commit_pair(&empty[sl]);
+        }
+        mma_commit_pair(tfull);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    unsigned u = 0;
+    for (int it = cid; it < n_items; it += ncl, ++u) {
+      const int js = it / per, r = it % per;
+      const int j = js % NMOD;
+      const int m0 = (r / a.tiles_n) * 256 + 128 * rank, n0 = (r % a.tiles_n) * P_BN;
+      double mj = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < NMOD; ++jj)
+        if (jj == j) mj = (double)mod_of(jj);
+      const double inv = 1.0 / mj;
+      mb_wait(tfull, u & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + row;
+      int8_t* o = a.res + (int64_t)js * a.plane + m;
+      const int ncols = min(P_BN, a.N - n0);
+#pragma unroll 1
+      for (int c = 0; c < P_BN; c += 32) {
+        if (c >= ncols) break;  // warp-uniform
+        int v[32];
+        tmem_ld32(tmem + ((unsigned)(quarter * 32) << 16) + c, v);
+        if (m < a.M) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (c + i < ncols) {
+              const double x = (double)v[i];
+              const double qq = fma(x, inv, kMagic) - kMagic;
+              const double rr = fma(-qq, mj, x);
+              o[(int64_t)(n0 + c + i) * a.ldo] = (int8_t)(__double2loint(rr + kMagic) & 0xFF);
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mb_arrive_leader(tempty);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ------------------------------------------------------------------------------------------------
 // CRT reconstruction + scaling: C(m, n) = alpha rw(m) 2^-(ea_m + eb_n) C'(m, n) + beta C(m, n).
 // Thread per (n, 4 consecutive m); residues summed over the K-splits.
 __global__ void __launch_bounds__(256) oz_crt_kernel(const int8_t* __restrict__ res, int64_t ldo, int64_t plane,
@@ -621,6 +813,7 @@ bool encode_res(CUtensorMap* m, const int8_t* p, int K, int rows, int64_t ld, in
 }  // namespace
 
 static double g_oz_ops = 0.0;  // INT8 tensor ops (2 M N K per modulus) launched so far
+int g_oz_pair = 1;             // option "i8_pair": CTA-pair (cta_group::2) INT8 GEMM
 double oz_i8_ops_total() { return g_oz_ops; }
 static double g_oz_conv = 0.0;  // FP64 elements converted to residues so far
 double oz_conv_elems_total() { return g_oz_conv; }
@@ -691,18 +884,23 @@ cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int64_t planeA, bool a_mn, i
   if ((lda & 15) || (ldb & 15) || (ldo & 3) || a_inner > lda || K > ldb || M > ldo || (planeA & 15) ||
       (planeB & 15) || (planeO & 3) || planeA < lda * a_outer || planeB < ldb * N || planeO < ldo * N)
     return cudaErrorInvalidValue;
-  static bool attr[2] = {false, false};
-  if (!attr[a_mn]) {
-    const cudaError_t e = cudaFuncSetAttribute(a_mn ? oz_i8gemm_kernel<true> : oz_i8gemm_kernel<false>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
+  static bool attr[4] = {false, false, false, false};
+  const bool pair = g_oz_pair != 0;
+  const int ai = (a_mn ? 1 : 0) + (pair ? 2 : 0);
+  if (!attr[ai]) {
+    const cudaError_t e =
+        pair ? cudaFuncSetAttribute(a_mn ? oz_i8gemm2_kernel<true> : oz_i8gemm2_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem2)
+             : cudaFuncSetAttribute(a_mn ? oz_i8gemm_kernel<true> : oz_i8gemm_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
     if (e != cudaSuccess) return e;
-    attr[a_mn] = true;
+    attr[ai] = true;
   }
   I8Args a{};
   a.M = M;
   a.N = N;
-  a.tiles_m = (M + IBM - 1) / IBM;
-  a.tiles_n = (N + IBN - 1) / IBN;
+  a.tiles_m = pair ? (M + 255) / 256 : (M + IBM - 1) / IBM;
+  a.tiles_n = pair ? (N + P_BN - 1) / P_BN : (N + IBN - 1) / IBN;
   a.kblocks = (K + IBK - 1) / IBK;
   a.splits = oz_splits(K);
   a.kb_per_split = (a.kblocks + a.splits - 1) / a.splits;
@@ -712,15 +910,21 @@ cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int64_t planeA, bool a_mn, i
   CUtensorMap ma, mb;
   const bool ok_a = a_mn ? encode_res(&ma, A, M, K, lda, planeA, IBK)   // box {128 m, 128 k}
                         : encode_res(&ma, A, K, M, lda, planeA, IBM);  // box {128 k, 128 m}
-  if (!ok_a || !encode_res(&mb, B, K, N, ldb, planeB, IBN)) return cudaErrorInvalidValue;
+  if (!ok_a || !encode_res(&mb, B, K, N, ldb, planeB, pair ? 128 : IBN)) return cudaErrorInvalidValue;
   const int items = a.tiles_m * a.tiles_n * NMOD * a.splits;
-  const int grid = std::min(items, 148);
+  const int grid = pair ? 2 * std::min(items, 74) : std::min(items, 148);
   g_oz_ops += 2.0 * NMOD * (double)M * N * (double)K;
   probe_before(K_I8GEMM, st);
-  if (a_mn)
+  if (pair) {
+    if (a_mn)
+      oz_i8gemm2_kernel<true><<<grid, kI8Threads, kI8Smem2, st>>>(a, ma, mb);
+    else
+      oz_i8gemm2_kernel<false><<<grid, kI8Threads, kI8Smem2, st>>>(a, ma, mb);
+  } else if (a_mn) {
     oz_i8gemm_kernel<true><<<grid, kI8Threads, kI8Smem, st>>>(a, ma, mb);
-  else
+  } else {
     oz_i8gemm_kernel<false><<<grid, kI8Threads, kI8Smem, st>>>(a, ma, mb);
+  }
   probe_after(K_I8GEMM, st);
   return cudaGetLastError();
 }

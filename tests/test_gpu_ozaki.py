@@ -55,13 +55,17 @@ def bound(a, b, ref):
         + u * np.abs(ref.astype(np.float64))
 
 
-@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (5, 7, 3), (128, 256, 128), (129, 257, 129), (300, 100, 1000)])
-def test_integer_operands_exact_crt(M, N, K):
+@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (5, 7, 3), (128, 256, 128), (129, 257, 129), (300, 100, 1000),
+                                   (600, 1030, 700)])
+def test_integer_operands_exact_crt(M, N, K, pair):
+    """Both INT8 GEMM forms: one CTA per 128 x 256 tile, and CTA pairs (cta_group::2, 256 x 512 items)."""
     rng = np.random.default_rng(M * 7 + N + K)
     a = rng.integers(-(1 << 20), 1 << 20, size=(M, K)).astype(np.float64)
     b = rng.integers(-(1 << 20), 1 << 20, size=(K, N)).astype(np.float64)
     want = (a.astype(object) @ b.astype(object)).astype(np.float64)  # |C| < 2^50: exact in FP64
-    got = oz(a, b)
+    with _lib.option("i8_pair", pair):
+        got = oz(a, b)
     assert np.all(np.abs(got - want) <= 2.0 ** -51 * np.abs(want))
 
 
@@ -124,8 +128,8 @@ def make(name):
     return prob, quad, ngd.init(top, 0).values, ell
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-def test_sketch_engines_agree_full_size(name):
+@pytest.mark.parametrize("name,pair", [("c2", 0), ("c2", 1), ("c3", 0), ("c3", 1), ("c4", 1), ("c5", 1)])
+def test_sketch_engines_agree_full_size(name, pair):
     """Y = G Omega at the config's full size and rank: INT8 (Ozaki) engine vs FP64 DMMA engine."""
     prob, quad, theta, ell = make(name)
     gop = ngd.GramianOperator.from_problem(prob, theta, quad)
@@ -134,7 +138,7 @@ def test_sketch_engines_agree_full_size(name):
     om = torch.linalg.qr(om)[0] if name != "c5" else om / np.sqrt(p)
     with _lib.option("sketch_gemm", 0):
         y0 = gop.matmat(om)
-    with _lib.option("sketch_gemm", 1):
+    with _lib.option("sketch_gemm", 1), _lib.option("i8_pair", pair):
         y1 = gop.matmat(om)
         y2 = gop.matmat(om)
     assert torch.equal(y1, y2)  # deterministic

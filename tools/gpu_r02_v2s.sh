@@ -1,0 +1,4 @@
+timeout 300 python -m pytest tests/test_gpu_ozaki.py -q -x -k "integer" > gpurun_out/v2s_oz1.log 2>&1; echo "oz int rc=$?"; tail -3 gpurun_out/v2s_oz1.log
+timeout 600 python -m pytest tests/test_gpu_ozaki.py -q -x > gpurun_out/v2s_oz.log 2>&1; echo "oz rc=$?"; tail -3 gpurun_out/v2s_oz.log
+timeout 300 python tools/sketch_engines.py c3 1 2>&1 | tail -1
+timeout 600 python tools/sketch_engines.py c5 1 2>&1 | tail -1
