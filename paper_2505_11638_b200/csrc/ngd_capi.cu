@@ -1168,54 +1168,72 @@ static bool use_ozaki(ngd_ctx* c, int64_t ell) {
 }
 
 static int matmat_ozaki(ngd_ctx* c, FormJPlan& pl, const GemmOperand& vop, int ell, double* Y, int64_t ldy) {
+  // Two-sided scaling of J (one residue conversion per chunk serves both products):
+  //   gamma_k = -floor(log2 max_all-points |J(., k)|)            (pass 0: maxima only, every chunk)
+  //   rho_r   = t - 1 - floor(log2 max_k |J(r, k)| 2^gamma_k)     (per chunk, fused into formj)
+  //   J'(r, k) = rint(J(r, k) 2^(rho_r + gamma_k))                [points][ldp], read K-major by
+  //              S = diag(w) J_c V  and MN-major (as J_c^T) by  Y += J_c^T S
+  //   V'(k, n) = rint(V(k, n) 2^(beta_n - gamma_k))   ->  S = 2^-(rho_r + beta_n) (J' V')
+  //   S'(r, n) = rint(S(r, n) 2^(sigma_n - rho_r))    ->  Y = 2^-(gamma_k + sigma_n) (J'^T S')
   const int p = (int)c->p;
   const int64_t ldp = c->ldp;
   const int64_t ldr = rup(pl.R, 16);
-  const int tp = oz_bits(p), tr = oz_bits(pl.R);
+  const int tp = std::min(oz_bits(p), oz_bits(pl.R)), tr = oz_bits(pl.R);
   const int sp = oz_splits(p);
-  const int64_t pl_row = oz_plane(pl.R, ldp);                             // J_c residue planes
-  const int64_t pl_v = oz_plane(ell, ldp), pl_s = oz_plane(ell, ldr);      // V, S residue planes
+  const int64_t pl_row = oz_plane(pl.R, ldp);                             // J' residue planes
+  const int64_t pl_v = oz_plane(ell, ldp), pl_s = oz_plane(ell, ldr);      // V', S' residue planes
   const int64_t pl_ys = oz_plane(ell, ldr), pl_yy = oz_plane(ell, ldp);    // product residues (S, Y)
   CK(c->oz_a.ensure((size_t)kOzMods * pl_row));
   CK(c->oz_b.ensure((size_t)kOzMods * pl_v));
   CK(c->oz_s.ensure((size_t)kOzMods * pl_s));
   CK(c->oz_res.ensure((size_t)kOzMods * std::max(pl_yy, sp * pl_ys)));
   CK(c->oz_ea.ensure(sizeof(int) * pl.R));
-  CK(c->oz_ec.ensure(sizeof(int) * p));
+  CK(c->oz_ec.ensure(sizeof(int) * rup(p, 4)));
   CK(c->oz_eb.ensure(sizeof(int) * ell));
   CK(c->oz_ep.ensure(sizeof(int) * ell));
-  CK(c->oz_mx.ensure(sizeof(unsigned long long) * (pl.R + p)));
+  CK(c->oz_mx.ensure(sizeof(long long) * (pl.R + p)));
   auto* A8 = static_cast<int8_t*>(c->oz_a.p);
   auto* B8 = static_cast<int8_t*>(c->oz_b.p);
   auto* S8 = static_cast<int8_t*>(c->oz_s.p);
   auto* R8 = static_cast<int8_t*>(c->oz_res.p);
-  int* er = static_cast<int*>(c->oz_ea.p);  // J_c rows (points)
-  int* ec = static_cast<int*>(c->oz_ec.p);  // J_c columns (parameters)
-  int* ev = static_cast<int*>(c->oz_eb.p);  // V columns
-  int* es = static_cast<int*>(c->oz_ep.p);  // S columns
-  auto* rmax = static_cast<unsigned long long*>(c->oz_mx.p);
-  auto* cmax = rmax + pl.R;
-  pl.fa.rmax = rmax;
+  int* rho = static_cast<int*>(c->oz_ea.p);    // J rows (points)
+  int* gam = static_cast<int*>(c->oz_ec.p);    // J columns (parameters)
+  int* beta = static_cast<int*>(c->oz_eb.p);   // V columns
+  int* sig = static_cast<int*>(c->oz_ep.p);    // S columns
+  auto* rmax = static_cast<long long*>(c->oz_mx.p);
+  auto* cmax = reinterpret_cast<unsigned long long*>(rmax + pl.R);
+  // pass 0: column maxima of J over every chunk (DMMA J tiles, no stores)
+  CK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * p, c->stream));
   pl.fa.cmax = cmax;
-  CK(oz_rows(vop.p, vop.ld, ell, p, tp, B8, ldp, pl_v, ev, false, c->stream));
+  pl.fa.rmax = nullptr;
+  pl.fa.no_store = 1;
+  for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
+    pl.fa.blk0 = b0;
+    CK(form_j(pl.fa, std::min(pl.bpc, pl.nblk_total - b0), c->NL, pl.max_nin, pl.max_nout, c->stream));
+  }
+  CK(oz_exps(cmax, p, 1, gam, c->stream));  // max |J(., k)| 2^gamma_k in [1, 2)
+  CK(oz_rows(vop.p, vop.ld, ell, p, tp, B8, ldp, pl_v, beta, false, c->stream, gam, -1));
+  pl.fa.cmax = nullptr;
+  pl.fa.rmax = rmax;
+  pl.fa.cexp = gam;
+  pl.fa.no_store = 0;
   for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
     const int nb = std::min(pl.bpc, pl.nblk_total - b0);
     const int r = nb * PB;
     const int64_t q0 = (int64_t)b0 * PB;
     pl.fa.blk0 = b0;
-    CK(cudaMemsetAsync(rmax, 0, sizeof(unsigned long long) * (pl.R + p), c->stream));
-    CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));  // J_c + its row / column maxima
-    CK(oz_exps(rmax, r, tp, er, c->stream));
-    CK(oz_exps(cmax, p, tr, ec, c->stream));
-    CK(oz_rows(c->jt.d(), ldp, r, p, tp, A8, ldp, pl_row, er, true, c->stream));
+    CK(cudaMemsetAsync(rmax, 0x80, sizeof(long long) * pl.R, c->stream));  // log-bit "empty"
+    CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));      // J_c + prescaled row maxima
+    CK(oz_exps_log(rmax, r, tp, rho, c->stream));
+    CK(oz_rows(c->jt.d(), ldp, r, p, tp, A8, ldp, pl_row, rho, true, c->stream, gam, 1));
     CK(oz_i8gemm(A8, ldp, pl_row, false, r, B8, ldp, pl_v, ell, p, R8, ldr, pl_ys, c->stream));
-    CK(oz_crt(R8, ldr, pl_ys, r, ell, sp, er, ev, c->w_pad.d() + q0, 1.0, 0.0, c->smat.d(), r, c->stream));
-    // J_c^T for Y += J_c^T S: the same [points][ldp] layout, column (parameter) scaled, read MN-major
-    CK(oz_rows(c->jt.d(), ldp, r, p, tr, A8, ldp, pl_row, ec, true, c->stream, true));
-    CK(oz_rows(c->smat.d(), r, ell, r, tr, S8, ldr, pl_s, es, false, c->stream));
+    CK(oz_crt(R8, ldr, pl_ys, r, ell, sp, rho, beta, c->w_pad.d() + q0, 1.0, 0.0, c->smat.d(), r, c->stream));
+    CK(oz_rows(c->smat.d(), r, ell, r, tr, S8, ldr, pl_s, sig, false, c->stream, rho, -1));
     CK(oz_i8gemm(A8, ldp, pl_row, true, p, S8, ldr, pl_s, ell, r, R8, ldp, pl_yy, c->stream));
-    CK(oz_crt(R8, ldp, pl_yy, p, ell, 1, ec, es, nullptr, 1.0, q0 == 0 ? 0.0 : 1.0, Y, ldy, c->stream));
+    CK(oz_crt(R8, ldp, pl_yy, p, ell, 1, gam, sig, nullptr, 1.0, q0 == 0 ? 0.0 : 1.0, Y, ldy, c->stream));
   }
+  pl.fa.rmax = nullptr;
+  pl.fa.cexp = nullptr;
   return NGD_OK;
 }
 

@@ -14,6 +14,7 @@
 // CTA tile (modes FWD/REV/PHA): 64 rows x one point block (16 points x C channels),
 // 8 warps = 4 (rows) x 2 (8-point groups).  Each lane owns 2 rows x 2 points x
 // all C channels, so the cross-channel jet nonlinearity is lane-local.
+#include <climits>
 #include "ngd_common.cuh"
 #include "ngd_kernels.h"
 
@@ -469,11 +470,24 @@ __global__ void __launch_bounds__(FJ_THREADS, 1) formj_kernel(FormJArgs a) {
   const int arow = warp * 8 + g;  // this lane's tile row (A fragment / accumulator row)
   const bool row_ok = arow < na;
   const bool vec2 = ((off + (int64_t)(a0 + arow) * nin + b0) & 1) == 0 && (a.ldj & 1) == 0;
-  const bool track = a.rmax != nullptr;
+  const bool trk_r = a.rmax != nullptr, trk_c = a.cmax != nullptr, store = !a.no_store;
   unsigned long long cm[8][2];
 #pragma unroll
   for (int j = 0; j < 8; ++j) cm[j][0] = cm[j][1] = 0ull;
   unsigned long long bm = 0ull;  // bias column maximum (threads < na)
+  // column prescale exponents of this thread's 16 weights and (threads < na) one bias
+  int gam[8][2];
+  int gamb = 0;
+  if (trk_r) {
+    const int* ce = a.cexp + off + (int64_t)(a0 + arow) * nin + b0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int col = j * 8 + 2 * t;
+      gam[j][0] = (row_ok && col < nb) ? ce[col] : 0;
+      gam[j][1] = (row_ok && col + 1 < nb) ? ce[col + 1] : 0;
+    }
+    if (b0 == 0 && threadIdx.x < na) gamb = a.cexp[off + (int64_t)nout * nin + a0 + threadIdx.x];
+  }
   for (int r = 0; r < PB; ++r) {
     double acc[8][2];
 #pragma unroll
@@ -487,49 +501,51 @@ __global__ void __launch_bounds__(FJ_THREADS, 1) formj_kernel(FormJArgs a) {
         for (int j = 0; j < 8; ++j) dmma884(acc[j][0], acc[j][1], av, Zs[(j * 8 + g) * FJ_LD + c * FJ_CS + r]);
       }
     }
-    double* row = a.Jt + (prow0 + r) * a.ldj + off + (int64_t)(a0 + arow) * nin + b0;
-    if (row_ok) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int col = j * 8 + 2 * t;
-        if (vec2 && col + 1 < nb) {
-          *reinterpret_cast<double2*>(row + col) = make_double2(acc[j][0], acc[j][1]);
-        } else {
-          if (col < nb) row[col] = acc[j][0];
-          if (col + 1 < nb) row[col + 1] = acc[j][1];
-        }
-      }
-    }
-    if (b0 == 0 && threadIdx.x < na)  // bias entries: value channel of D
-      a.Jt[(prow0 + r) * a.ldj + off + (int64_t)nout * nin + a0 + threadIdx.x] = Ds[threadIdx.x * FJ_LD + r];
-    if (track) {
-      unsigned long long rm = 0ull;
+    if (store) {
+      double* row = a.Jt + (prow0 + r) * a.ldj + off + (int64_t)(a0 + arow) * nin + b0;
       if (row_ok) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int col = j * 8 + 2 * t;
-          if (col < nb) {
-            const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(acc[j][0]));
-            cm[j][0] = max(cm[j][0], u);
-            rm = max(rm, u);
-          }
-          if (col + 1 < nb) {
-            const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(acc[j][1]));
-            cm[j][1] = max(cm[j][1], u);
-            rm = max(rm, u);
+          if (vec2 && col + 1 < nb) {
+            *reinterpret_cast<double2*>(row + col) = make_double2(acc[j][0], acc[j][1]);
+          } else {
+            if (col < nb) row[col] = acc[j][0];
+            if (col + 1 < nb) row[col + 1] = acc[j][1];
           }
         }
       }
-      if (b0 == 0 && threadIdx.x < na) {
-        const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(Ds[threadIdx.x * FJ_LD + r]));
-        bm = max(bm, u);
-        rm = max(rm, u);
+      if (b0 == 0 && threadIdx.x < na)  // bias entries: value channel of D
+        a.Jt[(prow0 + r) * a.ldj + off + (int64_t)nout * nin + a0 + threadIdx.x] = Ds[threadIdx.x * FJ_LD + r];
+    }
+    if (trk_c) {
+      if (row_ok) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int col = j * 8 + 2 * t;
+          if (col < nb) cm[j][0] = max(cm[j][0], (unsigned long long)__double_as_longlong(fabs(acc[j][0])));
+          if (col + 1 < nb) cm[j][1] = max(cm[j][1], (unsigned long long)__double_as_longlong(fabs(acc[j][1])));
+        }
       }
+      if (b0 == 0 && threadIdx.x < na)
+        bm = max(bm, (unsigned long long)__double_as_longlong(fabs(Ds[threadIdx.x * FJ_LD + r])));
+    }
+    if (trk_r) {
+      long long rm = kOzLogEmpty - 1;
+      if (row_ok) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int col = j * 8 + 2 * t;
+          if (col < nb) rm = max(rm, oz_logbits(acc[j][0], gam[j][0]));
+          if (col + 1 < nb) rm = max(rm, oz_logbits(acc[j][1], gam[j][1]));
+        }
+      }
+      if (b0 == 0 && threadIdx.x < na) rm = max(rm, oz_logbits(Ds[threadIdx.x * FJ_LD + r], gamb));
       for (int o = 16; o; o >>= 1) rm = max(rm, __shfl_xor_sync(0xffffffffu, rm, o));
-      if (lane == 0 && rm) atomicMax(a.rmax + prow0 + r, rm);
+      if (lane == 0 && rm >= kOzLogEmpty) atomicMax(a.rmax + prow0 + r, rm);
     }
   }
-  if (track) {
+  if (trk_c) {
     if (row_ok) {
       unsigned long long* cr = a.cmax + off + (int64_t)(a0 + arow) * nin + b0;
 #pragma unroll

@@ -95,10 +95,16 @@ struct FormJArgs {
   int blk0;                 // first point block of this chunk (padded point order)
   double* Jt;               // [16 * blocks][ldj], row = padded point within the chunk
   int64_t ldj;
-  // optional (INT8 sketch): running maxima of |J| as ordered bit patterns (RED.MAX.U64), per chunk
-  // row (point) and per parameter (column); NaN / inf order above every finite value
-  unsigned long long* rmax;
+  // optional (INT8 sketch, ngd_ozaki.cu two-sided scaling):
+  //   cmax: running maxima of |J| per parameter (column) as ordered bit patterns (RED.MAX.U64; NaN /
+  //         inf order above every finite value), accumulated over all chunks in a first pass;
+  //   rmax: per chunk row (point), the maximum of |J(r, k)| 2^cexp[k] as a "log-bit" pattern
+  //         bits(|J|) + cexp[k] 2^52 (signed RED.MAX; LLONG_MAX = non-finite);
+  //   no_store: the first pass computes the maxima only
   unsigned long long* cmax;
+  long long* rmax;
+  const int* cexp;
+  int no_store;
 };
 
 // FP64 DMMA GEMM (ngd_gemm.cu): C(m, n) = alpha sum_k A(m, k) B(k, n) [* row_scale(m)] + beta C(m, n),
@@ -134,6 +140,18 @@ double gemm_flops_total();
 // CRT reconstruction.  Residue blocks are [kOzMods][rows][ld] int8 (ld a multiple of 16);
 // product residues [splits][kOzMods][N][ldo] (column-major).
 constexpr int kOzMods = 16;
+constexpr int kOzNonFinite = -0x40000000;  // exponent flag of a row / column with a NaN or inf
+// "log-bit" pattern of |x| 2^g for maxima of prescaled values: (bits(|x|) >> 1) + g 2^51 -- monotone
+// in |x| 2^g, no overflow for |g| <= 2000; LLONG_MAX flags NaN / inf; values below kOzLogEmpty mean
+// "no entry" (the RED.MAX start value is memset to 0x80 bytes)
+constexpr long long kOzLogEmpty = -(3ll << 61);
+__device__ __forceinline__ long long oz_logbits(double x, int g) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(x));
+  if (b >= 0x7ff0000000000000ull || g == kOzNonFinite) return 0x7fffffffffffffffll;
+  if (b == 0) return kOzLogEmpty - 1;
+  g = g < -2000 ? -2000 : (g > 2000 ? 2000 : g);
+  return (long long)(b >> 1) + ((long long)g << 51);
+}
 extern int g_oz_pair;  // option "i8_pair" (process-wide): CTA-pair INT8 GEMM (1) or one CTA per tile (0)
 constexpr int kOzMaxKSplit = 130944;  // K per split: 128 * 128 * K < 2^31
 int oz_bits(int64_t K);               // integer width t of the scaled operands for inner length K
@@ -141,9 +159,11 @@ int oz_splits(int64_t K);
 double oz_i8_ops_total();
 double oz_conv_elems_total();
 cudaError_t oz_exps(const unsigned long long* maxbits, int n, int t, int* exps, cudaStream_t st);
-// residues of A(r, k) = A[r lda + k] scaled by 2^exps[r] (or, col_exps, by 2^exps[k]): out[j][r][ldo]
+cudaError_t oz_exps_log(const long long* logmax, int n, int t, int* exps, cudaStream_t st);
+// residues of A(r, k) = A[r lda + k] scaled by 2^(exps[r] + colsign colexp[k]) (colexp optional; with
+// have_exps false the row exponents are computed first from the column-prescaled row maxima)
 cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t* out, int64_t ldo, int64_t plane,
-                    int* exps, bool have_exps, cudaStream_t st, bool col_exps = false);
+                    int* exps, bool have_exps, cudaStream_t st, const int* colexp = nullptr, int colsign = 1);
 // plane pitch of a residue block: rounded to 256 B plus an odd multiple of 256 B, so the 16 moduli
 // planes written together do not alias onto the same memory channels (power-of-two plane strides
 // made the residue writes 4-5x slower than the HBM write bandwidth)

@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
 
@@ -58,7 +59,7 @@ __host__ __device__ constexpr int mod_of(int j) {
                    : 193;
 }
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
-constexpr int kExpNonFinite = -0x40000000;     // row / column exponent of a non-finite input
+constexpr int kExpNonFinite = kOzNonFinite;     // row / column exponent of a non-finite input
 
 // per-modulus constants of the CRT and the residue generation (host-computed, passed by value)
 struct OzTab {
@@ -166,21 +167,6 @@ __device__ __forceinline__ int exp_for_max(double mx, int t) {
   return t - 1 - ilogb(mx);  // mx 2^alpha in [2^(t-1), 2^t)
 }
 
-__device__ __forceinline__ double block_max(double v, double* sh) {
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) sh[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
-    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) sh[32] = v;
-  }
-  __syncthreads();
-  v = sh[32];
-  __syncthreads();
-  return v;
-}
 
 // Exponents from running maxima kept as ordered bit patterns of |x| (formj_kernel's RED.MAX): bit
 // patterns at or above +inf's flag a non-finite row / column.
@@ -191,23 +177,42 @@ __global__ void oz_exps_kernel(const unsigned long long* __restrict__ mx, int n,
   exps[i] = b >= 0x7ff0000000000000ull ? kExpNonFinite : exp_for_max(__longlong_as_double((long long)b), t);
 }
 
-// Row exponents of a K-major FP64 operand (standalone GEMM path): one CTA per row.
+// exponent making max |x| 2^g land in [2^(t-1), 2^t), from its log-bit pattern (oz_logbits)
+__device__ __forceinline__ int exp_from_logbits(long long v, int t) {
+  if (v == 0x7fffffffffffffffll) return kExpNonFinite;
+  if (v < kOzLogEmpty) return 0;                    // no entry (all zero)
+  return t - 1 - (int)((v >> 51) - 1023);           // floor(log2) of a normal |x| 2^g
+}
+__global__ void oz_exps_log_kernel(const long long* __restrict__ mx, int n, int t, int* __restrict__ exps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) exps[i] = exp_from_logbits(mx[i], t);
+}
+
+// Row exponents of a K-major FP64 operand, optionally of the column-prescaled |A(r, k)| 2^(sign
+// colexp[k]) (two-sided scaling): one CTA per row, log-bit maxima.
 __global__ void __launch_bounds__(256) oz_rowmax_kernel(const double* __restrict__ A, int64_t lda, int rows, int K,
-                                                        int t, int* __restrict__ exps) {
-  __shared__ double sh[33];
+                                                        int t, int* __restrict__ exps, const int* __restrict__ colexp,
+                                                        int colsign) {
+  __shared__ long long sh[8];
   const int r = blockIdx.x;
   if (r >= rows) return;
   const double* a = A + (int64_t)r * lda;
-  double mx = 0.0;
-  bool bad = false;  // fmax drops NaN: flagged separately
+  long long mx = kOzLogEmpty - 1;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    const double v = fabs(a[k]);
-    mx = fmax(mx, v);
-    bad |= !(v <= 1.79769313486231570815e+308);
+    int g = 0;
+    if (colexp) {
+      g = colexp[k];
+      if (g != kExpNonFinite) g *= colsign;
+    }
+    mx = max(mx, oz_logbits(a[k], g));
   }
-  const bool any_bad = __syncthreads_or(bad);
-  mx = block_max(mx, sh);
-  if (threadIdx.x == 0) exps[r] = any_bad ? kExpNonFinite : exp_for_max(mx, t);
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = max(mx, sh[w]);
+    exps[r] = exp_from_logbits(mx, t);
+  }
 }
 
 __device__ __forceinline__ void cp16(void* dst, const void* src, unsigned bytes) {
@@ -243,10 +248,11 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 constexpr int kRowsK = 2048;
 constexpr int kConvIn = 3;  // input ring depth (tiles in flight ahead of the arithmetic)
 constexpr size_t kRowsSmem = kConvIn * kRowsK * sizeof(double) + 2 * NMOD * kRowsK;
-template <bool COLS>
+template <bool HASCOL>
 __global__ void __launch_bounds__(256) oz_rows_kernel(const double* __restrict__ A, int64_t lda, int rows, int K,
-                                                      const int* __restrict__ exps, int8_t* __restrict__ out,
-                                                      int64_t ldo, int64_t plane, const OzTab tb) {
+                                                      const int* __restrict__ exps, const int* __restrict__ colexp,
+                                                      int colsign, int8_t* __restrict__ out, int64_t ldo,
+                                                      int64_t plane, const OzTab tb) {
   extern __shared__ __align__(128) unsigned char rsm[];
   double* in = reinterpret_cast<double*>(rsm);                   // [kConvIn][2048]
   unsigned char* stg = rsm + kConvIn * kRowsK * sizeof(double);  // [2][16][2048]
@@ -265,8 +271,8 @@ __global__ void __launch_bounds__(256) oz_rows_kernel(const double* __restrict__
     }
     cp_commit();
   };
-  // the row exponent is fetched one tile ahead; column exponents (COLS) are read per element (L2 / L1)
-  auto row_exp = [&](int tl) { return (!COLS && tl < ntiles) ? exps[tl / tiles_k] : 0; };
+  // the row exponent is fetched one tile ahead; column exponents (HASCOL) are read per element (L2 / L1)
+  auto row_exp = [&](int tl) { return tl < ntiles ? exps[tl / tiles_k] : 0; };
   int tile = blockIdx.x;
   issue(tile, 0);
   issue(tile + gridDim.x, 1);
@@ -289,15 +295,22 @@ __global__ void __launch_bounds__(256) oz_rows_kernel(const double* __restrict__
         const double* src = in + ib * kRowsK + kl;
         const double2 d0 = *reinterpret_cast<const double2*>(src), d1 = *reinterpret_cast<const double2*>(src + 2);
         const double v[4] = {d0.x, d0.y, d1.x, d1.y};
-        int4 ce = make_int4(e, e, e, e);
-        if (COLS && k0 + kl + 3 < K) ce = *reinterpret_cast<const int4*>(exps + k0 + kl);
-        const int ee[4] = {ce.x, ce.y, ce.z, ce.w};
+        int ce[4] = {0, 0, 0, 0};
+        if (HASCOL) {
+          if (k0 + kl + 3 < K) {
+            const int4 c4 = *reinterpret_cast<const int4*>(colexp + k0 + kl);
+            ce[0] = c4.x, ce[1] = c4.y, ce[2] = c4.z, ce[3] = c4.w;
+          } else {
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) ce[e4] = k0 + kl + e4 < K ? colexp[k0 + kl + e4] : 0;
+          }
+        }
 #pragma unroll
         for (int e4 = 0; e4 < 4; ++e4) {
           const int k = k0 + kl + e4;
-          const int ek = COLS ? (k < K ? (k0 + kl + 3 < K ? ee[e4] : exps[k]) : 0) : ee[e4];
+          const bool live = e != kExpNonFinite && ce[e4] != kExpNonFinite && k < K;
+          const int ek = live ? e + colsign * ce[e4] : 0;
           const int e1 = ek >> 1;
-          const bool live = ek != kExpNonFinite && k < K;
           split26(live ? v[e4] : 0.0, pow2(e1), pow2(ek - e1), xh[4 * h + e4], xl[4 * h + e4]);
         }
       }
@@ -837,6 +850,14 @@ cudaError_t oz_exps(const unsigned long long* maxbits, int n, int t, int* exps, 
   return cudaGetLastError();
 }
 
+cudaError_t oz_exps_log(const long long* logmax, int n, int t, int* exps, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  probe_before(K_OZCONV, st);
+  oz_exps_log_kernel<<<(n + 255) / 256, 256, 0, st>>>(logmax, n, t, exps);
+  probe_after(K_OZCONV, st);
+  return cudaGetLastError();
+}
+
 // persistent grid: resident CTAs per SM x 148 (queried once per kernel; sets the smem attribute)
 template <typename Kern>
 static cudaError_t persistent_grid(Kern k, size_t smem, int& grid) {
@@ -851,28 +872,29 @@ static cudaError_t persistent_grid(Kern k, size_t smem, int& grid) {
 }
 
 cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t* out, int64_t ldo, int64_t plane,
-                    int* exps, bool have_exps, cudaStream_t st, bool col_exps) {
+                    int* exps, bool have_exps, cudaStream_t st, const int* colexp, int colsign) {
   if (rows <= 0 || K <= 0) return cudaSuccess;
   if ((ldo & 15) || K > ldo || K > lda || (lda & 1) || (reinterpret_cast<uintptr_t>(A) & 15) ||
-      (col_exps && (reinterpret_cast<uintptr_t>(exps) & 15)) || (col_exps && !have_exps))
+      (colexp && (reinterpret_cast<uintptr_t>(colexp) & 15)) || (colsign != 1 && colsign != -1))
     return cudaErrorInvalidValue;
   static int grid[2] = {0, 0};
-  const cudaError_t ea = col_exps ? persistent_grid(oz_rows_kernel<true>, kRowsSmem, grid[1])
-                                  : persistent_grid(oz_rows_kernel<false>, kRowsSmem, grid[0]);
+  const bool hc = colexp != nullptr;
+  const cudaError_t ea = hc ? persistent_grid(oz_rows_kernel<true>, kRowsSmem, grid[1])
+                            : persistent_grid(oz_rows_kernel<false>, kRowsSmem, grid[0]);
   if (ea != cudaSuccess) return ea;
   if (!have_exps) {
     probe_before(K_OZCONV, st);
-    oz_rowmax_kernel<<<rows, 256, 0, st>>>(A, lda, rows, K, t, exps);
+    oz_rowmax_kernel<<<rows, 256, 0, st>>>(A, lda, rows, K, t, exps, colexp, colsign);
     probe_after(K_OZCONV, st);
   }
   const int64_t tiles = (int64_t)rows * ((ldo + kRowsK - 1) / kRowsK);
   g_oz_conv += (double)rows * K;
-  const int gr = (int)std::min<int64_t>(tiles, grid[col_exps]);
+  const int gr = (int)std::min<int64_t>(tiles, grid[hc]);
   probe_before(K_OZCONV, st);
-  if (col_exps)
-    oz_rows_kernel<true><<<gr, 256, kRowsSmem, st>>>(A, lda, rows, K, exps, out, ldo, plane, tab());
+  if (hc)
+    oz_rows_kernel<true><<<gr, 256, kRowsSmem, st>>>(A, lda, rows, K, exps, colexp, colsign, out, ldo, plane, tab());
   else
-    oz_rows_kernel<false><<<gr, 256, kRowsSmem, st>>>(A, lda, rows, K, exps, out, ldo, plane, tab());
+    oz_rows_kernel<false><<<gr, 256, kRowsSmem, st>>>(A, lda, rows, K, exps, nullptr, 1, out, ldo, plane, tab());
   probe_after(K_OZCONV, st);
   return cudaGetLastError();
 }
