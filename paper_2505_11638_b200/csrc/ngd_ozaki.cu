@@ -560,6 +560,7 @@ struct __align__(1024) I8Stage2 {
   int8_t B[2][128 * IBK];   // this CTA's 128-row halves of the item's two 256-column MMAs
 };
 constexpr size_t kI8Smem2 = sizeof(I8Stage2) * INS + 1024 + 256;
+constexpr int kI8Threads2 = 320;  // producer, MMA, eight epilogue warps
 
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
@@ -607,7 +608,7 @@ __device__ __forceinline__ void mb_arrive_leader(unsigned long long* m) {
 }
 
 template <bool AMN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads2, 1)
     oz_i8gemm2_kernel(const __grid_constant__ I8Args a, const __grid_constant__ CUtensorMap mapA,
                       const __grid_constant__ CUtensorMap mapB) {
   extern __shared__ unsigned char raw[];
@@ -626,7 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
       mb_init(&empty[s], 1);
     }
     mb_init(tfull, 1);
-    mb_init(tempty, 8);  // the pair's eight epilogue warps (leader's barrier)
+    mb_init(tempty, 16);  // the pair's sixteen epilogue warps (leader's barrier)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -692,7 +693,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
       }
     }
   } else {
-    const int quarter = warp & 3;
+    // eight epilogue warps: TMEM lane quarter (warp % 4) x column half ((warp - 2) / 4)
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     unsigned u = 0;
     for (int it = cid; it < n_items; it += ncl, ++u) {
@@ -710,7 +712,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
       int8_t* o = a.res + (int64_t)js * a.plane + m;
       const int ncols = min(P_BN, a.N - n0);
 #pragma unroll 1
-      for (int c = 0; c < P_BN; c += 32) {
+      for (int c = half * (P_BN / 2); c < (half + 1) * (P_BN / 2); c += 32) {
         if (c >= ncols) break;  // warp-uniform
         int v[32];
         tmem_ld32(tmem + ((unsigned)(quarter * 32) << 16) + c, v);
@@ -939,9 +941,9 @@ cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int64_t planeA, bool a_mn, i
   probe_before(K_I8GEMM, st);
   if (pair) {
     if (a_mn)
-      oz_i8gemm2_kernel<true><<<grid, kI8Threads, kI8Smem2, st>>>(a, ma, mb);
+      oz_i8gemm2_kernel<true><<<grid, kI8Threads2, kI8Smem2, st>>>(a, ma, mb);
     else
-      oz_i8gemm2_kernel<false><<<grid, kI8Threads, kI8Smem2, st>>>(a, ma, mb);
+      oz_i8gemm2_kernel<false><<<grid, kI8Threads2, kI8Smem2, st>>>(a, ma, mb);
   } else if (a_mn) {
     oz_i8gemm_kernel<true><<<grid, kI8Threads, kI8Smem, st>>>(a, ma, mb);
   } else {
