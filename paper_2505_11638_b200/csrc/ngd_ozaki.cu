@@ -604,7 +604,9 @@ __device__ __forceinline__ void mb_wait_cluster(unsigned long long* m, unsigned 
 __device__ __forceinline__ void mb_arrive_leader(unsigned long long* m) {
   unsigned remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(sa(m)));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  // relaxed: the TMEM reads completed (tcgen05.wait::ld) before it; a release would also wait for
+  // the item's global residue stores to drain before the MMAs of the next item may start
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
 template <bool AMN>
