@@ -1180,7 +1180,9 @@ static int matmat_ozaki(ngd_ctx* c, FormJPlan& pl, const GemmOperand& vop, int e
   const int64_t ldr = rup(pl.R, 16);
   const int tp = std::min(oz_bits(p), oz_bits(pl.R)), tr = oz_bits(pl.R);
   const int sp = oz_splits(p);
-  const int64_t pl_row = oz_plane(pl.R, ldp);                             // J' residue planes
+  const int nrb = (int)((pl.R + 127) / 128), ncb = (int)((p + 127) / 128);  // J' in 128 x 128 blocks
+  const int64_t pl_row = std::max(((int64_t)nrb * ncb * 16384 + 255) / 256 * 256 + 37 * 256,  // J' residue planes
+                                  oz_plane(pl.R, ldp));
   const int64_t pl_v = oz_plane(ell, ldp), pl_s = oz_plane(ell, ldr);      // V', S' residue planes
   const int64_t pl_ys = oz_plane(ell, ldr), pl_yy = oz_plane(ell, ldp);    // product residues (S, Y)
   CK(c->oz_a.ensure((size_t)kOzMods * pl_row));
@@ -1225,11 +1227,17 @@ static int matmat_ozaki(ngd_ctx* c, FormJPlan& pl, const GemmOperand& vop, int e
     CK(cudaMemsetAsync(rmax, 0x80, sizeof(long long) * pl.R, c->stream));  // log-bit "empty"
     CK(form_j(pl.fa, nb, c->NL, pl.max_nin, pl.max_nout, c->stream));      // J_c + prescaled row maxima
     CK(oz_exps_log(rmax, r, tp, rho, c->stream));
-    CK(oz_rows(c->jt.d(), ldp, r, p, tp, A8, ldp, pl_row, rho, true, c->stream, gam, 1));
-    CK(oz_i8gemm(A8, ldp, pl_row, false, r, B8, ldp, pl_v, ell, p, R8, ldr, pl_ys, c->stream));
+    // J' in 128 x 128 blocks for the CTA-pair GEMM (contiguous TMA boxes in both products); the
+    // one-CTA GEMM (option i8_pair = 0) reads the row-major form
+    const int rb = g_oz_pair ? (r + 127) / 128 : 0;
+    if (rb)
+      CK(oz_rows_blocked(c->jt.d(), ldp, r, p, rb, ncb, rho, gam, A8, pl_row, c->stream));
+    else
+      CK(oz_rows(c->jt.d(), ldp, r, p, tp, A8, ldp, pl_row, rho, true, c->stream, gam, 1));
+    CK(oz_i8gemm(A8, ldp, pl_row, false, r, B8, ldp, pl_v, ell, p, R8, ldr, pl_ys, c->stream, rb, ncb));
     CK(oz_crt(R8, ldr, pl_ys, r, ell, sp, rho, beta, c->w_pad.d() + q0, 1.0, 0.0, c->smat.d(), r, c->stream));
     CK(oz_rows(c->smat.d(), r, ell, r, tr, S8, ldr, pl_s, sig, false, c->stream, rho, -1));
-    CK(oz_i8gemm(A8, ldp, pl_row, true, p, S8, ldr, pl_s, ell, r, R8, ldp, pl_yy, c->stream));
+    CK(oz_i8gemm(A8, ldp, pl_row, true, p, S8, ldr, pl_s, ell, r, R8, ldp, pl_yy, c->stream, rb, ncb));
     CK(oz_crt(R8, ldp, pl_yy, p, ell, 1, gam, sig, nullptr, 1.0, q0 == 0 ? 0.0 : 1.0, Y, ldy, c->stream));
   }
   pl.fa.rmax = nullptr;

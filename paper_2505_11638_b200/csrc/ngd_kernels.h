@@ -169,8 +169,13 @@ cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t
 // made the residue writes 4-5x slower than the HBM write bandwidth)
 inline int64_t oz_plane(int64_t rows, int64_t ld) { return (rows * ld + 255) / 256 * 256 + 37 * 256; }
 // a_mn: A stored MN-major (A(m, k) = A[k lda + m] per plane), else K-major (A[m lda + k])
+// a_nrb > 0: A is blocked ([row block][column block][128][128] per plane, oz_rows_blocked; pair kernel)
 cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int64_t planeA, bool a_mn, int M, const int8_t* B, int64_t ldb,
-                      int64_t planeB, int N, int K, int8_t* res, int64_t ldo, int64_t planeO, cudaStream_t st);
+                      int64_t planeB, int N, int K, int8_t* res, int64_t ldo, int64_t planeO, cudaStream_t st,
+                      int a_nrb = 0, int a_ncb = 0);
+// residues of J'(r, k) = rint(J 2^(rexp[r] + cexp[k])) in 128 x 128 blocks (zero past rows / K)
+cudaError_t oz_rows_blocked(const double* A, int64_t lda, int rows, int K, int nrb, int ncb, const int* rexp,
+                            const int* cexp, int8_t* out, int64_t plane, cudaStream_t st);
 cudaError_t oz_crt(const int8_t* res, int64_t ldo, int64_t planeO, int M, int N, int splits, const int* ea,
                    const int* eb, const double* row_w, double alpha, double beta, double* C, int64_t ldc,
                    cudaStream_t st);

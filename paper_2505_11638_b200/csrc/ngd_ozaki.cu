@@ -336,6 +336,86 @@ __global__ void __launch_bounds__(256) oz_rows_kernel(const double* __restrict__
   if (tid == 0) bulk_wait_read<0>();
 }
 
+// Blocked residues of J' (two-sided exponents): out[j] = [row block][column block][128][128] int8,
+// each 128 x 128 block contiguous (16 KB), so the TMA boxes of BOTH products -- K-major for
+// S = J' V' and MN-major (as J'^T) for Y = J'^T S' -- are single contiguous blocks (the MN-major reads
+// of the row-major layout touched 128 rows 200 kB apart per box).  Tiles of 16 rows x 128 columns:
+// thread (q = tid / 16, c = 8 (tid % 16)) converts 8 consecutive elements of row q; the 16 residue
+// slabs (16 rows x 128 B, contiguous inside a block) leave as asynchronous bulk copies.  Rows >= rows
+// and columns >= K of the last blocks are written as zero residues.
+constexpr size_t kBlkSmem = kConvIn * 2048 * sizeof(double) + 2 * NMOD * 2048;
+__global__ void __launch_bounds__(256) oz_rows_blocked_kernel(const double* __restrict__ A, int64_t lda, int rows,
+                                                              int K, int nrb, int ncb, const int* __restrict__ rexp,
+                                                              const int* __restrict__ cexp, int8_t* __restrict__ out,
+                                                              int64_t plane, const OzTab tb) {
+  extern __shared__ __align__(128) unsigned char bsm[];
+  double* in = reinterpret_cast<double*>(bsm);                  // [kConvIn][16][128]
+  unsigned char* stg = bsm + kConvIn * 2048 * sizeof(double);   // [2][16][16 x 128]
+  const int tiles_c = ncb, ntiles = nrb * 8 * ncb;              // 8 row slabs of 16 per row block
+  const int tid = threadIdx.x;
+  const int q = tid >> 4, c = (tid & 15) * 8;
+  auto issue = [&](int tile, int buf) {
+    if (tile < ntiles) {
+      const int r0 = (tile / tiles_c) * 16, k0 = (tile % tiles_c) * 128;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int ch = tid + 256 * i;  // row ch / 64, doubles 2 (ch % 64)
+        const int rr = r0 + (ch >> 6), kk = k0 + 2 * (ch & 63);
+        const bool ok = rr < rows && kk < lda;
+        cp16(in + buf * 2048 + ch * 2, ok ? A + (int64_t)rr * lda + kk : A, ok ? 16u : 0u);
+      }
+    }
+    cp_commit();
+  };
+  auto row_exp = [&](int tl) {
+    const int rr = (tl / tiles_c) * 16 + q;
+    return (tl < ntiles && rr < rows) ? rexp[rr] : kExpNonFinite;  // rows past `rows`: zero residues
+  };
+  int tile = blockIdx.x;
+  issue(tile, 0);
+  issue(tile + gridDim.x, 1);
+  int e_next = row_exp(tile);
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int buf = it & 1, ib = it % kConvIn;
+    const int e = e_next;
+    issue(tile + 2 * gridDim.x, (it + 2) % kConvIn);
+    e_next = row_exp(tile + gridDim.x);
+    if (tid == 0) bulk_wait_read<1>();
+    cp_wait<2>();
+    __syncthreads();
+    const int r0 = (tile / tiles_c) * 16, k0 = (tile % tiles_c) * 128;
+    unsigned wd[NMOD][2];
+    {
+      double xh[8], xl[8];
+      const double* src = in + ib * 2048 + q * 128 + c;
+#pragma unroll
+      for (int e8 = 0; e8 < 8; ++e8) {
+        const int k = k0 + c + e8;
+        const int ce = k < K ? cexp[k] : kExpNonFinite;
+        const bool live = e != kExpNonFinite && ce != kExpNonFinite;
+        const int ek = live ? e + ce : 0;
+        const int e1 = ek >> 1;
+        split26(live ? src[e8] : 0.0, pow2(e1), pow2(ek - e1), xh[e8], xl[e8]);
+      }
+      residue_words8(xh, xl, tb, wd);
+    }
+    unsigned char* so = stg + (size_t)buf * NMOD * 2048;
+#pragma unroll
+    for (int j = 0; j < NMOD; ++j)
+      *reinterpret_cast<uint2*>(so + j * 2048 + q * 128 + c) = make_uint2(wd[j][0], wd[j][1]);
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const int rb = r0 >> 7, cb = k0 >> 7;
+      int8_t* dst = out + ((int64_t)rb * ncb + cb) * 16384 + (r0 & 127) * 128;
+      for (int j = 0; j < NMOD; ++j) bulk_store(dst + (int64_t)j * plane, so + j * 2048, 2048);
+      bulk_commit();
+    }
+  }
+  cp_wait<0>();
+  if (tid == 0) bulk_wait_read<0>();
+}
+
 // ------------------------------------------------------------------------------------------------
 // INT8 tensor-core GEMM (tcgen05.mma.cta_group::1.kind::i8): per (K-split s, modulus j, 128 x 256
 // output tile) item  C = A_j(m, k) B_j(n, k)^T  over the split's k range, both operands K-major in
@@ -358,6 +438,7 @@ struct I8Args {
   int M, N, splits, tiles_m, tiles_n, kblocks, kb_per_split;
   int8_t* res;
   int64_t ldo, plane;
+  int a_blocked;  // A in 128 x 128 blocks (oz_rows_blocked): 5-D boxes {128, 128, block, block, j}
 };
 
 __device__ __forceinline__ unsigned sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -579,6 +660,15 @@ __device__ __forceinline__ void tma3_pair(void* dst, const CUtensorMap* map, int
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma5_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4,
+                                          unsigned long long* mbar_local) {
+  const unsigned bar = sa(mbar_local) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5, %6}], [%7];" ::"r"(sa(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void mma_i8_pair(unsigned tmem, uint64_t ad, uint64_t bd, unsigned idesc, unsigned acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
@@ -655,7 +745,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads2, 1)
           const int sl = q % INS;
           if (q >= INS) mb_wait(&empty[sl], ((q / INS) - 1) & 1);
           if (rank == 0) mb_expect(&full[sl], 2 * sizeof(I8Stage2));
-          if constexpr (AMN)
+          if (a.a_blocked)  // K-major: block (m0 / 128, kb); MN-major (J'^T): block (kb, m0 / 128)
+            tma5_pair(st[sl].A, &mapA, 0, 0, AMN ? m0 >> 7 : kb, AMN ? kb : m0 >> 7, j, &full[sl]);
+          else if constexpr (AMN)
             tma3_pair(st[sl].A, &mapA, m0, kb * IBK, j, &full[sl]);
           else
             tma3_pair(st[sl].A, &mapA, kb * IBK, m0, j, &full[sl]);
@@ -903,12 +995,35 @@ cudaError_t oz_rows(const double* A, int64_t lda, int rows, int K, int t, int8_t
   return cudaGetLastError();
 }
 
+cudaError_t oz_rows_blocked(const double* A, int64_t lda, int rows, int K, int nrb, int ncb, const int* rexp,
+                            const int* cexp, int8_t* out, int64_t plane, cudaStream_t st) {
+  if (rows <= 0 || K <= 0) return cudaSuccess;
+  if ((lda & 1) || (reinterpret_cast<uintptr_t>(A) & 15) || (int64_t)nrb * 128 < rows || (int64_t)ncb * 128 < K ||
+      (int64_t)ncb * 128 > lda + 127 || (plane & 15) || plane < (int64_t)nrb * ncb * 16384)
+    return cudaErrorInvalidValue;
+  static int grid = 0;
+  const cudaError_t ea = persistent_grid(oz_rows_blocked_kernel, kBlkSmem, grid);
+  if (ea != cudaSuccess) return ea;
+  const int64_t tiles = (int64_t)nrb * 8 * ncb;
+  g_oz_conv += (double)rows * K;
+  probe_before(K_OZCONV, st);
+  oz_rows_blocked_kernel<<<(int)std::min<int64_t>(tiles, grid), 256, kBlkSmem, st>>>(A, lda, rows, K, nrb, ncb, rexp,
+                                                                                       cexp, out, plane, tab());
+  probe_after(K_OZCONV, st);
+  return cudaGetLastError();
+}
+
 cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int64_t planeA, bool a_mn, int M, const int8_t* B, int64_t ldb,
-                      int64_t planeB, int N, int K, int8_t* res, int64_t ldo, int64_t planeO, cudaStream_t st) {
+                      int64_t planeB, int N, int K, int8_t* res, int64_t ldo, int64_t planeO, cudaStream_t st,
+                      int a_nrb, int a_ncb) {
   if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  const bool blocked = a_nrb > 0;
   const int64_t a_inner = a_mn ? M : K, a_outer = a_mn ? K : M;
-  if ((lda & 15) || (ldb & 15) || (ldo & 3) || a_inner > lda || K > ldb || M > ldo || (planeA & 15) ||
-      (planeB & 15) || (planeO & 3) || planeA < lda * a_outer || planeB < ldb * N || planeO < ldo * N)
+  if ((lda & 15) || (ldb & 15) || (ldo & 3) || (!blocked && a_inner > lda) || K > ldb || M > ldo || (planeA & 15) ||
+      (planeB & 15) || (planeO & 3) || (!blocked && planeA < lda * a_outer) || planeB < ldb * N || planeO < ldo * N)
+    return cudaErrorInvalidValue;
+  if (blocked && (!g_oz_pair || planeA < (int64_t)a_nrb * a_ncb * 16384 ||
+                  (int64_t)(a_mn ? a_ncb : a_nrb) * 128 < M || (int64_t)(a_mn ? a_nrb : a_ncb) * 128 < K))
     return cudaErrorInvalidValue;
   static bool attr[4] = {false, false, false, false};
   const bool pair = g_oz_pair != 0;
@@ -933,9 +1048,22 @@ cudaError_t oz_i8gemm(const int8_t* A, int64_t lda, int64_t planeA, bool a_mn, i
   a.res = res;
   a.ldo = ldo;
   a.plane = planeO;
+  a.a_blocked = blocked ? 1 : 0;
   CUtensorMap ma, mb;
-  const bool ok_a = a_mn ? encode_res(&ma, A, M, K, lda, planeA, IBK)   // box {128 m, 128 k}
-                        : encode_res(&ma, A, K, M, lda, planeA, IBM);  // box {128 k, 128 m}
+  bool ok_a;
+  if (blocked) {  // [j][row block][column block][128][128]
+    auto enc = oz_encode();
+    cuuint64_t dims[5] = {128, 128, (cuuint64_t)a_ncb, (cuuint64_t)a_nrb, (cuuint64_t)NMOD};
+    cuuint64_t strides[4] = {128, 16384, (cuuint64_t)a_ncb * 16384, (cuuint64_t)planeA};
+    cuuint32_t box[5] = {128, 128, 1, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    ok_a = enc && enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<int8_t*>(A), dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  } else {
+    ok_a = a_mn ? encode_res(&ma, A, M, K, lda, planeA, IBK)   // box {128 m, 128 k}
+                : encode_res(&ma, A, K, M, lda, planeA, IBM);  // box {128 k, 128 m}
+  }
   if (!ok_a || !encode_res(&mb, B, K, N, ldb, planeB, pair ? 128 : IBN)) return cudaErrorInvalidValue;
   const int items = a.tiles_m * a.tiles_n * NMOD * a.splits;
   const int grid = pair ? 2 * std::min(items, 74) : std::min(items, 148);
