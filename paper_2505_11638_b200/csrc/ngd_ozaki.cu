@@ -835,8 +835,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads2, 1)
 // ------------------------------------------------------------------------------------------------
 // CRT reconstruction + scaling: C(m, n) = alpha rw(m) 2^-(ea_m + eb_n) C'(m, n) + beta C(m, n).
 // Thread per (n, 4 consecutive m); residues summed over the K-splits.
+template <int SPLITS>
 __global__ void __launch_bounds__(256) oz_crt_kernel(const int8_t* __restrict__ res, int64_t ldo, int64_t plane,
-                                                     int splits, int M, int N, const int* __restrict__ ea,
+                                                     int M, int N, const int* __restrict__ ea,
                                                      const int* __restrict__ eb, const double* __restrict__ rw,
                                                      double alpha, double beta, double* __restrict__ C, int64_t ldc,
                                                      const OzTab tb) {
@@ -847,18 +848,23 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const int8_t* __restrict__ 
     const int m0 = (int)(w % mq) * 4;
     double T1[4] = {0, 0, 0, 0}, T2[4] = {0, 0, 0, 0}, T3[4] = {0, 0, 0, 0};
     const int8_t* rp = res + (int64_t)n * ldo + m0;
+    // all 16 x SPLITS residue words in flight before the arithmetic
+    unsigned wv[SPLITS][NMOD];
+#pragma unroll
+    for (int sp = 0; sp < SPLITS; ++sp)
+#pragma unroll
+      for (int j = 0; j < NMOD; ++j) wv[sp][j] = *reinterpret_cast<const unsigned*>(rp + (int64_t)(sp * NMOD + j) * plane);
 #pragma unroll
     for (int j = 0; j < NMOD; ++j) {
       int r[4] = {0, 0, 0, 0};
-      for (int s = 0; s < splits; ++s) {
-        const unsigned wv = *reinterpret_cast<const unsigned*>(rp + (int64_t)(s * NMOD + j) * plane);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) r[e] += (int)(int8_t)((wv >> (8 * e)) & 0xFF);
-      }
+      for (int sp = 0; sp < SPLITS; ++sp)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) r[e] += (int)(int8_t)((wv[sp][j] >> (8 * e)) & 0xFF);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         int x = r[e];
-        if (splits > 1) {  // |x| <= 128 splits: bring into [-m/2, m/2]
+        if (SPLITS > 1) {  // |x| <= 128 splits: bring into [-m/2, m/2]
           const int m = mod_of(j);
           x -= m * __float2int_rn((float)x / (float)m);
         }
@@ -1087,11 +1093,17 @@ cudaError_t oz_crt(const int8_t* res, int64_t ldo, int64_t planeO, int M, int N,
                    const int* eb, const double* row_w, double alpha, double beta, double* C, int64_t ldc,
                    cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  if ((ldo & 3) || (planeO & 3)) return cudaErrorInvalidValue;
+  if ((ldo & 3) || (planeO & 3) || splits < 1 || splits > 4) return cudaErrorInvalidValue;
   const int64_t total = (int64_t)((M + 3) / 4) * N;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   probe_before(K_OZCRT, st);
-  oz_crt_kernel<<<blocks, 256, 0, st>>>(res, ldo, planeO, splits, M, N, ea, eb, row_w, alpha, beta, C, ldc, tab());
+  switch (splits) {
+    case 1: oz_crt_kernel<1><<<blocks, 256, 0, st>>>(res, ldo, planeO, M, N, ea, eb, row_w, alpha, beta, C, ldc, tab()); break;
+    case 2: oz_crt_kernel<2><<<blocks, 256, 0, st>>>(res, ldo, planeO, M, N, ea, eb, row_w, alpha, beta, C, ldc, tab()); break;
+    case 3: oz_crt_kernel<3><<<blocks, 256, 0, st>>>(res, ldo, planeO, M, N, ea, eb, row_w, alpha, beta, C, ldc, tab()); break;
+    case 4: oz_crt_kernel<4><<<blocks, 256, 0, st>>>(res, ldo, planeO, M, N, ea, eb, row_w, alpha, beta, C, ldc, tab()); break;
+    default: break;  // K > 4 x 130944: rejected above
+  }
   probe_after(K_OZCRT, st);
   return cudaGetLastError();
 }
