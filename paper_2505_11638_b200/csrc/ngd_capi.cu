@@ -916,7 +916,9 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
       c->phbg_cache.s_pad = gm.s_pad;
     }
     const int gh = heavy ? std::max(1, std::min(kt, 148 / heavy)) : 1;
-    const int gt = thin ? std::max(1, std::min(kt, 148 / thin)) : 1;
+    // thin tiles alone in their launch (no heavy tile left off the GEMM core): the thin-only
+    // pipeline runs several CTAs per SM, so the K splits fill all of them
+    const int gt = thin ? std::max(1, std::min(kt, (heavy ? 148 : phb2_thin_only_ctas()) / thin)) : 1;
     int maxg = 0;
     c->rplan.n_layers = c->NL;
     for (int l = 0; l < c->NL; ++l) {

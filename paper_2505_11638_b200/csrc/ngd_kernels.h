@@ -260,6 +260,7 @@ bool phbg_layer_ok(int M, int N);
 int phbg_splits(int tiles, int kstages);
 cudaError_t phase_b_gemm(const PhbgArgs& a, PhbgCache& cache, cudaStream_t st);
 int phb2_ctas_per_sm();
+int phb2_thin_only_ctas();
 void pack_all(const PackAll& a, const double* src, const int* skip, cudaStream_t st);
 cudaError_t form_j(const FormJArgs& a, int nblocks, int n_layers, int max_nin, int max_nout, cudaStream_t st);
 

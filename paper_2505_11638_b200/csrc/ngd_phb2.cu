@@ -338,10 +338,79 @@ __global__ void __maxnreg__(144) phb2_kernel(const __grid_constant__ PhbAll a,
 #undef NGD_THIN
 }
 
+// Thin-only form (no heavy tile in this launch -- every layer with both sides >= 256 runs on the GEMM
+// core, C4 / C5): five warps (four consumers + the producer) and a TO_NS-deep ring, small enough for
+// three CTAs per SM, so the memory-bound thin tiles (the input layer's D_1 and the output layer's
+// Zin_L, 2 x 3.3 GB per C5 matvec) stream with three times the bytes in flight of the paired form.
+constexpr int TO_NS = 4;
+constexpr int kThinOnlyThreads = (kThinWarps + 1) * 32;
+constexpr size_t kThinOnlySmem = sizeof(HStage) * TO_NS + 2 * TO_NS * sizeof(unsigned long long) +
+                                 sizeof(double) * HB + 1024;
+__global__ void __launch_bounds__(kThinOnlyThreads) phb2_thin_kernel(const __grid_constant__ PhbAll a,
+                                                                     const __grid_constant__ Phb2Maps maps) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
+  extern __shared__ unsigned char phb2_smem[];
+  unsigned char* base = phb2_smem + ((1024u - (smem_addr(phb2_smem) & 1023u)) & 1023u);
+  HStage* stt = reinterpret_cast<HStage*>(base);
+  unsigned long long* fullt = reinterpret_cast<unsigned long long*>(stt + TO_NS);
+  unsigned long long* emptyt = fullt + TO_NS;
+  double* redt = reinterpret_cast<double*>(emptyt + TO_NS);  // thin bias staging [HB]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Item T{};
+  const bool hasT = decode_item(a, 1, blockIdx.x, T);
+  if (a.L[0].skip && *a.L[0].skip) return;
+  if (tid == 0) {
+    for (int s = 0; s < TO_NS; ++s) {
+      mbar_init(&fullt[s], 1);
+      mbar_init(&emptyt[s], kThinWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (!hasT) return;
+  const int g = lane >> 2, t = lane & 3;
+  if (warp == kThinWarps) {
+    if (lane == 0) produce<TO_NS>(a, maps, T, stt, fullt, emptyt);
+    return;
+  }
+  const PhbArgs& p = a.L[T.l];
+  const int wm = warp >> 1, wn = warp & 1;
+  const bool do_bias = T.bx == 0 && wn == 0;
+  const int qa = blocks_of(p.M - T.by * HB, wm), ra = blocks_of(p.N - T.bx * HB, wn);
+  double acc[8][2], bs[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const int arow = (wm * 32 + g) * HK, brow = (wn * 32 + g) * HK;
+#define NGD_THIN(QA, RA)                                                                                     \
+  do {                                                                                                      \
+    consume<QA, RA, 8, 4, TO_NS>(p, T, stt, fullt, emptyt, do_bias, arow, brow, 0, g, t, lane, acc, bs);   \
+    epilogue<(QA > 0 ? QA : 1), (RA > 0 ? RA : 1), 8, 1>(p, T, acc, bs, do_bias, nullptr, redt, 0, wm, wn, g, t, \
+                                                         tid);                                              \
+  } while (0)
+  switch (qa * 8 + ra) {
+    case 4 * 8 + 1: NGD_THIN(4, 1); break;
+    case 4 * 8 + 2: NGD_THIN(4, 2); break;
+    case 3 * 8 + 1: NGD_THIN(3, 1); break;
+    case 3 * 8 + 2: NGD_THIN(3, 2); break;
+    case 2 * 8 + 1: NGD_THIN(2, 1); break;
+    case 2 * 8 + 2: NGD_THIN(2, 2); break;
+    case 1 * 8 + 1: NGD_THIN(1, 1); break;
+    case 1 * 8 + 2: NGD_THIN(1, 2); break;
+    case 1 * 8 + 3: NGD_THIN(1, 3); break;
+    case 1 * 8 + 4: NGD_THIN(1, 4); break;
+    case 2 * 8 + 3: NGD_THIN(2, 3); break;
+    case 2 * 8 + 4: NGD_THIN(2, 4); break;
+    default: NGD_THIN(0, 0); break;  // no real block: ring protocol and bias staging only
+  }
+#undef NGD_THIN
+}
+
 namespace {
 constexpr size_t kStaging = sizeof(double) * (HB * (HB + 1) + 4 * HB);
 }
 int phb2_ctas_per_sm() { return 1; }
+// thin items of a thin-only launch (every wide layer on the GEMM core): three CTAs per SM
+int phb2_thin_only_ctas() { return 3 * 148; }
 
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -383,6 +452,14 @@ cudaError_t phase_b2_all_layers(const PhbAll& a, Phb2Cache& cache, cudaStream_t 
   }
   const int ctas = std::max(nh, nt);
   if (ctas <= 0) return cudaSuccess;
+  const bool thin_only = nh == 0;
+  static bool attr_thin = false;
+  if (thin_only && !attr_thin) {
+    cudaError_t e = cudaFuncSetAttribute(phb2_thin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kThinOnlySmem);
+    if (e != cudaSuccess) return e;
+    attr_thin = true;
+  }
   // tensor maps of every layer's operands (host-side encode, cached in the context while the
   // buffers stay put)
   for (int l = 0; l < a.n_layers; ++l) {
@@ -400,7 +477,9 @@ cudaError_t phase_b2_all_layers(const PhbAll& a, Phb2Cache& cache, cudaStream_t 
     }
   }
   probe_before(K_PHB, st);
-  const cudaError_t e = launch_pdl(phb2_kernel, dim3(ctas), dim3(kPhb2Threads), smem, st, a, cache.maps);
+  const cudaError_t e = thin_only ? launch_pdl(phb2_thin_kernel, dim3(ctas), dim3(kThinOnlyThreads), kThinOnlySmem,
+                                               st, a, cache.maps)
+                                  : launch_pdl(phb2_kernel, dim3(ctas), dim3(kPhb2Threads), smem, st, a, cache.maps);
   probe_after(K_PHB, st);
   return e;
 }
