@@ -392,8 +392,9 @@ def roofline_entry(kind, widths, n_int, n_bnd, ell, p, count, total_ms, peaks, g
             "unit": unit, "frac": achieved / peak, "traffic": None, "launches": int(count),
             "avg_launch_us": avg_s * 1e6, "algorithmic_work_per_launch": work, "work_note": note,
             "peak_source": "FP64: DMMA measured on this pool (tools/probe/fp64_peak.cu, profiles/r01_fp64_peak.txt); "
-                           f"HBM: {peaks['hbm_gbs']} GB/s from {peaks['source']}; INT8: {peaks['int8_tops']:.0f} "
-                           f"TOPS = {peaks['int8_source']}"}
+                           f"HBM: {peaks['hbm_gbs']} GB/s from {peaks['source']}"
+                           + (f"; INT8: {peaks['int8_tops']:.0f} TOPS = {peaks.get('int8_source', '')}"
+                              if "int8_tops" in peaks else "")}
 
 
 def probe_all(_lib, lib, fn):

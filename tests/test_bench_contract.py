@@ -43,6 +43,10 @@ def test_roofline_work_model():
     r = bench.roofline_entry(14, widths, n_int, n_bnd, ell, 8577, 4, 2.0, peaks, gemm_flops=8e12)
     assert r["algorithmic_work_per_launch"] == pytest.approx(2e12) and r["achieved"] == pytest.approx(4000.0)
     # Jacobi SVD (mixed precision): 9 FP32 + 2 FP64 sweeps of 9 ell^2 (ell - 1) FLOP over two launches
+    r8 = bench.roofline_entry(15, widths, n_int, n_bnd, ell, 8577, 4, 2.0, {**peaks, "int8_tops": 3267.0},
+                              i8_ops=1.6e13)
+    assert r8["unit"] == "TOPS" and abs(r8["achieved"] - 1.6e13 / 4 / 0.5e-3 / 1e12) < 1e-6
+    assert abs(r8["frac"] - r8["achieved"] / 3267.0) < 1e-12
     r = bench.roofline_entry(9, widths, n_int, n_bnd, ell, 8577, 2, 5.0, peaks, sweeps=(2, 9))
     assert r["algorithmic_work_per_launch"] == pytest.approx(9.0 * ell * ell * (ell - 1) * 11 / 2)
 
