@@ -157,6 +157,14 @@ struct ngd_ctx {
   Phb2Cache phb2_cache;           // phase B: tensor maps of this context's jets
   PhbgArgs phbg{};                // wide-layer phase B plan (n_heavy = 0: none)
   PhbgCache phbg_cache;
+  PhagArgs phag{};                // wide-layer phase A plan (ngd_phag.cu; n_heavy = 0: none)
+  PhagCache phag_cache;
+  Buf colpart;                    // phase A column partials of the wide layers [slots][s_pad]
+  int pha_gemm = 2;               // option "pha_gemm": wide layers' phase A on the GEMM core (2 auto)
+  int out_pre = 2;                // option "out_pre": output layer from precontracted rows (2 auto)
+  bool pha_on = false, out_on = false;  // routes in effect (plan_routes)
+  Buf gout;                       // output layer rows G[k][pt] = sum_c dseed Zin_L (out_contract)
+  std::vector<char> wide_a;       // per layer: phase A eligible for the GEMM core (both sides >= 256)
   int l2u = 1;      // option "l2u": keep the preconditioner basis U L2-persisting during PCG
   Buf u_persist;     // PCG's copy of U at a fixed address (the captured graph carries its L2 window)
   size_t jets_arena = 0;
@@ -334,6 +342,87 @@ static PackAll vp_plan(ngd_ctx* c) {
   return pk;
 }
 
+// phase-B plan (ngd_phb2.cu), one CTA per SM: heavy tiles (both sides > 16) share 148 K-split
+// items, thin tiles (input layer N = d, output layer M = 1) another 148; CTA i streams heavy item
+// i and thin item i interleaved.  Wide layers run on the GEMM core (ngd_phbg.cu), the output layer
+// on its precontracted rows when out_on (out_phase_b, ngd_vec.cu).
+static int plan_phase_b(ngd_ctx* c) {
+  const Geom& gm = c->gm;
+  {
+    const int kt = (int)(gm.s_pad / 16);
+    int heavy = 0, thin = 0;
+    PhbgArgs& pg = c->phbg;
+    pg = PhbgArgs{};
+    for (int l = 0; l < c->NL; ++l) {
+      const int M = c->w[l + 1], N = c->w[l];
+      c->phb_thin[l] = phbg_layer_ok(M, N) ? 2 : ((M <= 16 || N <= 16) ? 1 : 0);
+      if (l == c->NL - 1 && c->out_on) {  // output layer from the precontracted rows (out_phase_b)
+        c->phb_thin[l] = 3;
+        continue;
+      }
+      if (c->phb_thin[l] == 2) {
+        const int h = pg.n_heavy++;
+        pg.M[h] = M;
+        pg.N[h] = N;
+        pg.tiles_n[h] = (N + 127) / 128;
+        pg.item_start[h + 1] = pg.item_start[h] + ((M + 127) / 128) * pg.tiles_n[h];
+        pg.off[h] = c->woff[l];
+        c->phbg_cache.src_d[h] = (l == c->NL - 1) ? c->dseed.d() : c->dbuf[l].d();
+        c->phbg_cache.src_z[h] = c->zin[l].d();
+        continue;
+      }
+      (c->phb_thin[l] ? thin : heavy) += ((M + 63) / 64) * ((N + 63) / 64);
+    }
+    if (pg.n_heavy) {
+      pg.kstages = kt;
+      pg.G = phbg_splits(pg.item_start[pg.n_heavy], kt);
+      pg.kps = (kt + pg.G - 1) / pg.G;
+      pg.G = (kt + pg.kps - 1) / pg.kps;  // no empty splits
+      pg.int_units = gm.nib * gm.C;
+      pg.C = gm.C;
+      pg.nib = gm.nib;
+      pg.p = c->p;
+      c->phbg_cache.s_pad = gm.s_pad;
+    }
+    const int gh = heavy ? std::max(1, std::min(kt, 148 / heavy)) : 1;
+    // thin tiles alone in their launch (no heavy tile left off the GEMM core): the thin-only
+    // pipeline runs several CTAs per SM, so the K splits fill all of them
+    const int gt = thin ? std::max(1, std::min(kt, (heavy ? 148 : phb2_thin_only_ctas()) / thin)) : 1;
+    int maxg = 0;
+    c->rplan.n_layers = c->NL;
+    for (int l = 0; l < c->NL; ++l) {
+      const int Gl = c->phb_thin[l] == 3 ? kOutSplits : (c->phb_thin[l] == 2 ? pg.G : (c->phb_thin[l] ? gt : gh));
+      c->Gl[l] = Gl;
+      c->kpsl[l] = (kt + Gl - 1) / Gl;
+      c->rplan.start[l] = c->woff[l];
+      c->rplan.G[l] = Gl;
+      maxg = std::max(maxg, Gl);
+    }
+    c->rplan.start[c->NL] = c->p;
+    c->G = maxg;
+  }
+  CK(c->partB.ensure(sizeof(double) * (size_t)c->G * c->p));
+  return NGD_OK;
+}
+
+// which phase-A / phase-B routes the options select for this geometry (option value 2 = auto)
+static int plan_routes(ngd_ctx* c) {
+  const Geom& gm = c->gm;
+  const bool wide = c->phag.n_heavy > 0;
+  // GEMM-core phase A: measured faster at C5 (C = 12: 43.7 vs 44.3 ms per matvec), slower at C4
+  // (C = 4: 5.02 vs 4.86 ms), where pha_all_kernel's one-point-block tile is 64 columns
+  c->pha_on = wide && (c->pha_gemm == 1 || (c->pha_gemm == 2 && gm.C >= 8));
+  // precontracted output layer: its Jacobian rows (kout per point) replace a C-times larger jet
+  // stream in both phases at the cost of one more launch per phase -- measured per C5 / C4 / C3
+  // matvec 44.3 -> 42.6, 4.86 -> 4.76, 0.665 -> 0.652 ms, but C2 (kout S = 1.1 M) 46 -> 58 us
+  const int kout = c->w[c->NL - 1];
+  c->out_on = c->out_pre == 1 || (c->out_pre == 2 && (double)kout * (double)gm.s_pad >= (double)(1 << 23));
+  if (c->out_on) CK(c->gout.ensure(sizeof(double) * (size_t)kout * gm.n_pts_pad()));
+  // partial rows a route no longer writes must read as zero (reduce_pha sums every row)
+  CK(cudaMemsetAsync(c->partA.p, 0, c->partA.bytes, c->stream));
+  return plan_phase_b(c);
+}
+
 // J v: pack v (unless prepacked: PCG's direction is packed by pcg_dir_pack), phase A, reduction
 static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double* cot_out, const int* skip,
                    bool prepacked = false) {
@@ -344,6 +433,12 @@ static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double*
   pa.nib = gm.nib;
   pa.nbb = gm.nbb;
   pa.int_cols = gm.int_cols();
+  const bool gemm_core = c->pha_on;
+  if (gemm_core) {
+    c->phag.colpart = c->colpart.d();
+    c->phag.skip = skip;
+    CK(phase_a_gemm(c->phag, c->phag_cache, c->stream));
+  }
   int tiles = 0;
   for (int l = 0; l < c->NL; ++l) {
     JetArgs& a = pa.L[l];
@@ -362,11 +457,29 @@ static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double*
     a.skip = skip;
     pa.mtiles[l] = c->mtiles[l];
     pa.tile_start[l] = tiles;
-    tiles += c->mtiles[l] * (gm.nib + gm.nbb);
+    const bool elsewhere = (gemm_core && c->wide_a[l]) || (c->out_on && l == c->NL - 1);
+    if (!elsewhere) tiles += c->mtiles[l] * (gm.nib + gm.nbb);
   }
   pa.tile_start[c->NL] = tiles;
   CK(pha_all(gm.C, pa, c->stream));
-  reduce_pha(c->partA.d(), c->rows_A, gm.n_pts_pad(), w_or_null, cot_out, skip, c->stream);
+  if (gemm_core || c->out_on) {
+    PhaCols rc{};
+    if (gemm_core) {
+      rc.colpart = c->colpart.d();
+      rc.cslots = c->phag.slot0[c->phag.n_heavy - 1] + 2 * c->phag.tiles_m[c->phag.n_heavy - 1];
+    }
+    if (c->out_on) {
+      const int l = c->NL - 1;
+      rc.gout = c->gout.d();
+      rc.kout = c->w[l];
+      rc.vout = c->vp[l].d();
+      rc.vbout = c->vp[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l];
+      rc.dseed = c->dseed.d();
+    }
+    reduce_pha_cols(c->partA.d(), c->rows_A, gm, rc, w_or_null, cot_out, skip, c->stream);
+  } else {
+    reduce_pha(c->partA.d(), c->rows_A, gm.n_pts_pad(), w_or_null, cot_out, skip, c->stream);
+  }
   CK(cudaGetLastError());
   return NGD_OK;
 }
@@ -410,6 +523,11 @@ static int phase_b_partials(ngd_ctx* c, const double* cot, const int* skip) {
     c->phbg.part = c->partB.d();
     c->phbg.skip = skip;
     CK(phase_b_gemm(c->phbg, c->phbg_cache, c->stream));
+  }
+  if (c->out_on) {
+    const int l = c->NL - 1;
+    out_phase_b(c->gout.d(), c->dseed.d(), c->w[l], c->gm, cot, c->partB.d(), c->p, c->woff[l], c->Gl[l], skip,
+                c->stream);
   }
   PhbAll pb{};
   fill_phb(c, cot, skip, pb);
@@ -681,8 +799,7 @@ int ngd_ctx_create(const int32_t* widths, int32_t n_widths, int32_t device, ngd_
     c->Mp_f.push_back((int)rup(nout, 64));
     c->Kp_f.push_back((int)rup(nin, 16));
     c->mtiles.push_back((int)rup(nout, 64) / 64);
-    c->rowbase.push_back(c->rows_A);
-    c->rows_A += c->mtiles.back();
+    c->wide_a.push_back(phbg_layer_ok(nout, nin) ? 1 : 0);
     if (l + 1 < c->NL) {
       c->Mp_r.push_back((int)rup(nout, 64));
       c->Kp_r.push_back((int)rup(c->w[l + 2], 16));
@@ -690,6 +807,10 @@ int ngd_ctx_create(const int32_t* widths, int32_t n_widths, int32_t device, ngd_
       c->Mp_r.push_back(0);
       c->Kp_r.push_back(0);
     }
+  }
+  for (int l = 0; l < c->NL; ++l) {
+    c->rowbase.push_back(c->rows_A);
+    c->rows_A += c->mtiles[l];
   }
   c->p = off;
   c->ldp = rup(off, 16);
@@ -880,60 +1001,37 @@ int ngd_set_rows(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w
   CK(cudaGetLastError());
   // phase-A partial rows and phase-B split plan
   CK(c->partA.ensure(sizeof(double) * (size_t)c->rows_A * npp));
-  // phase-B plan (ngd_phb2.cu), one CTA per SM: heavy tiles (both sides > 16) share 148 K-split
-  // items, thin tiles (input layer N = d, output layer M = 1) another 148; CTA i streams heavy item
-  // i and thin item i interleaved.
+  // phase-A plan of the wide layers (ngd_phag.cu): items (layer, n tile, m tile), two column-partial
+  // rows per 128-row m tile
   {
-    const int kt = (int)(gm.s_pad / 16);
-    int heavy = 0, thin = 0;
-    PhbgArgs& pg = c->phbg;
-    pg = PhbgArgs{};
+    PhagArgs& pa = c->phag;
+    pa = PhagArgs{};
+    pa.tiles_n = (int)((gm.s_pad + 127) / 128);
+    pa.s_pad = gm.s_pad;
+    pa.int_units = gm.nib * gm.C;
+    pa.C = gm.C;
+    int slots = 0;
     for (int l = 0; l < c->NL; ++l) {
-      const int M = c->w[l + 1], N = c->w[l];
-      c->phb_thin[l] = phbg_layer_ok(M, N) ? 2 : ((M <= 16 || N <= 16) ? 1 : 0);
-      if (c->phb_thin[l] == 2) {
-        const int h = pg.n_heavy++;
-        pg.M[h] = M;
-        pg.N[h] = N;
-        pg.tiles_n[h] = (N + 127) / 128;
-        pg.item_start[h + 1] = pg.item_start[h] + ((M + 127) / 128) * pg.tiles_n[h];
-        pg.off[h] = c->woff[l];
-        c->phbg_cache.src_d[h] = (l == c->NL - 1) ? c->dseed.d() : c->dbuf[l].d();
-        c->phbg_cache.src_z[h] = c->zin[l].d();
-        continue;
-      }
-      (c->phb_thin[l] ? thin : heavy) += ((M + 63) / 64) * ((N + 63) / 64);
+      if (!c->wide_a[l]) continue;
+      const int h = pa.n_heavy++;
+      pa.M[h] = c->w[l + 1];
+      pa.Kp[h] = c->Kp_f[l];
+      pa.tiles_m[h] = (pa.M[h] + 127) / 128;
+      pa.item_start[h + 1] = pa.item_start[h] + pa.tiles_m[h] * pa.tiles_n;
+      pa.slot0[h] = slots;
+      slots += 2 * pa.tiles_m[h];
+      pa.vbias[h] = c->vp[l].d() + (int64_t)c->Mp_f[l] * c->Kp_f[l];
+      c->phag_cache.src_v[h] = c->vp[l].d();
+      c->phag_cache.src_z[h] = c->zin[l].d();
+      c->phag_cache.src_d[h] = c->dbuf[l].d();
+      pa.dptr[h] = c->dbuf[l].d();
+      c->phag_cache.mp[h] = c->Mp_f[l];
     }
-    if (pg.n_heavy) {
-      pg.kstages = kt;
-      pg.G = phbg_splits(pg.item_start[pg.n_heavy], kt);
-      pg.kps = (kt + pg.G - 1) / pg.G;
-      pg.G = (kt + pg.kps - 1) / pg.kps;  // no empty splits
-      pg.int_units = gm.nib * gm.C;
-      pg.C = gm.C;
-      pg.nib = gm.nib;
-      pg.p = c->p;
-      c->phbg_cache.s_pad = gm.s_pad;
-    }
-    const int gh = heavy ? std::max(1, std::min(kt, 148 / heavy)) : 1;
-    // thin tiles alone in their launch (no heavy tile left off the GEMM core): the thin-only
-    // pipeline runs several CTAs per SM, so the K splits fill all of them
-    const int gt = thin ? std::max(1, std::min(kt, (heavy ? 148 : phb2_thin_only_ctas()) / thin)) : 1;
-    int maxg = 0;
-    c->rplan.n_layers = c->NL;
-    for (int l = 0; l < c->NL; ++l) {
-      const int Gl = c->phb_thin[l] == 2 ? pg.G : (c->phb_thin[l] ? gt : gh);
-      c->Gl[l] = Gl;
-      c->kpsl[l] = (kt + Gl - 1) / Gl;
-      c->rplan.start[l] = c->woff[l];
-      c->rplan.G[l] = Gl;
-      maxg = std::max(maxg, Gl);
-    }
-    c->rplan.start[c->NL] = c->p;
-    c->G = maxg;
+    c->phag_cache.s_pad = gm.s_pad;
+    if (slots) CK(c->colpart.ensure(sizeof(double) * (size_t)slots * gm.s_pad));
   }
-  CK(c->partB.ensure(sizeof(double) * (size_t)c->G * c->p));
   c->have_points = true;
+  TRY(plan_routes(c));
   c->lin_valid = false;
   c->graph_gen++;
   return NGD_OK;
@@ -1029,6 +1127,8 @@ int ngd_linearize_ex(ngd_ctx* c, const double* theta, const double* theta_bar, d
     a.lap_mask = c->lap_mask;
     CK(jet_gemm_both(gm.C, REV, a, gm.nib, gm.nbb, gm.int_cols(), c->mtiles[l], c->stream));
   }
+  // output layer precontracted once per linearisation: J_r[W_L] = sum_c dseed(r,c) Zin_L(:,(r,c))
+  if (c->out_on) out_contract(c->zin[c->NL - 1].d(), c->dseed.d(), c->w[c->NL - 1], gm, c->gout.d(), c->stream);
   if (d_metric) gather_points(c->F.d(), d_metric, gm, c->stream);
   if (d_resid) gather_points(c->R_pad.d(), d_resid, gm, c->stream);
   CK(cudaGetLastError());
@@ -1749,6 +1849,20 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "l2window")) {
     c->use_l2_window = value ? 1 : 0;
     c->graph_gen++;  // the captured PCG iteration carries the stream's access-policy window
+    return NGD_OK;
+  }
+  if (!strcmp(key, "pha_gemm") || !strcmp(key, "out_pre")) {
+    // pha_gemm: phase A of the wide layers on the GEMM core (ngd_phag.cu); out_pre: the output
+    // layer's Jacobian rows precontracted at linearisation (out_contract); 0 off, 1 on, 2 auto
+    if (value < 0 || value > 2) return fail(NGD_E_SHAPE, "%s must be 0, 1 or 2 (auto)", key);
+    (key[0] == 'p' ? c->pha_gemm : c->out_pre) = (int)value;
+    if (c->have_points) {
+      const bool had_out = c->out_on;
+      TRY(plan_routes(c));
+      // a linearisation made without the precontracted rows cannot serve the new route
+      if (c->out_on && !had_out) c->lin_valid = false;
+    }
+    c->graph_gen++;
     return NGD_OK;
   }
   if (!strcmp(key, "i8_pair")) {

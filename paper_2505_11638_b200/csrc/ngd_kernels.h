@@ -228,6 +228,60 @@ struct Phb2Cache {  // host-side: re-encoded when a layer's buffers or shape cha
   int64_t ks[kMaxLayers] = {};
 };
 cudaError_t phase_b2_all_layers(const PhbAll& a, Phb2Cache& cache, cudaStream_t st);
+// phase A of the wide layers on the DMMA GEMM core (ngd_phag.cu): items (layer, n-tile, m-tile),
+// T = V_l Zin_l on 128 x 128 tiles (K = n_{l-1}), epilogue <D_l, T + vb_l> per column and 64-row half
+struct PhagArgs {
+  int n_heavy;
+  int M[kMaxLayers], Kp[kMaxLayers];  // n_l, n_{l-1} padded to 16
+  int tiles_m[kMaxLayers];            // 128-row m tiles of heavy layer h
+  int item_start[kMaxLayers + 1];     // items of the heavy layers before h
+  int slot0[kMaxLayers];              // first column-partial row of layer h (2 per m tile)
+  int tiles_n;                        // 128-column tiles of s_pad
+  int64_t s_pad;
+  const double* vbias[kMaxLayers];    // vb_l (packed v, value channel only)
+  const double* dptr[kMaxLayers];     // D_l [M rows][s_pad]
+  double* colpart;                    // [slots][s_pad] per-column partials <D_l[rows], (V Zin)[rows]>
+  int int_units, C;                   // interior channel runs (nib * C), channels
+  const int* skip;
+};
+struct PhagMaps {
+  CUtensorMap v[kMaxLayers];  // packed V_l [Mp rows][Kp], box 16 x 128 (K-major A)
+  CUtensorMap z[kMaxLayers];  // Zin_l [Kp rows][s_pad], box 16 x 16 (MN-major B)
+  CUtensorMap d[kMaxLayers];  // D_l [M rows][s_pad], box 16 x 128 (epilogue operand)
+};
+struct PhagCache {
+  PhagMaps maps;
+  const double* src_v[kMaxLayers] = {};  // set by the caller
+  const double* src_z[kMaxLayers] = {};
+  const double* src_d[kMaxLayers] = {};
+  int mp[kMaxLayers] = {};               // packed rows of V_l
+  int64_t s_pad = 0;
+  const double* kv[kMaxLayers] = {};     // encoded keys
+  const double* kz[kMaxLayers] = {};
+  const double* kd[kMaxLayers] = {};
+  int64_t ks[kMaxLayers] = {};
+};
+cudaError_t phase_a_gemm(const PhagArgs& a, PhagCache& cache, cudaStream_t st);
+// extra phase-A terms of reduce_pha_cols: the wide layers' column partials (ngd_phag.cu) and the
+// output layer from its precontracted rows G[k][pt] (out_contract)
+struct PhaCols {
+  const double* colpart = nullptr;  // [cslots][s_pad]
+  int cslots = 0;
+  const double* gout = nullptr;     // [kout][n_pts_pad], null: output layer in the partA rows
+  int kout = 0;
+  const double* vout = nullptr;     // v of W_L (packed row 0), vbout: v of b_L
+  const double* vbout = nullptr;
+  const double* dseed = nullptr;    // D_L (value channel column per point)
+};
+// cot[pt] = w[pt] * (sum of partA rows + column partials of the point's channel columns + output layer)
+void reduce_pha_cols(const double* partA, int rows, const Geom& gm, const PhaCols& rc, const double* w, double* cot,
+                     const int* done, cudaStream_t st);
+// output layer (M = 1) precontracted: G[k][pt] = sum_c D_L(pt, c) Zin_L[k](pt, c), the W_L block of J_pt
+void out_contract(const double* zin, const double* dseed, int K, const Geom& gm, double* G, cudaStream_t st);
+// its phase B: part[g][off + k] = sum_{pt in split g} cot[pt] G[k][pt], part[g][off + K] = sum cot[pt] D_L(pt, value)
+constexpr int kOutSplits = 148;
+void out_phase_b(const double* G, const double* dseed, int K, const Geom& gm, const double* cot, double* part, int64_t p,
+                 int64_t off, int splits, const int* done, cudaStream_t st);
 // phase B of the wide layers on the DMMA GEMM core (ngd_phbg.cu): items (split, heavy layer, tile)
 struct PhbgArgs {
   int n_heavy;                         // layers handled here (both sides >= 128)

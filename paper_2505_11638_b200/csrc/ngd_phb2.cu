@@ -446,7 +446,9 @@ cudaError_t phase_b2_all_layers(const PhbAll& a, Phb2Cache& cache, cudaStream_t 
     attr_set = true;
   }
   int nh = 0, nt = 0;
-  for (int l = 0; l < a.n_layers; ++l) {  // thin[l] == 2: the layer runs on the GEMM core (ngd_phbg.cu)
+  // thin[l] == 2: the layer runs on the GEMM core (ngd_phbg.cu); 3: output layer from its precontracted
+  // rows (out_phase_b, ngd_vec.cu)
+  for (int l = 0; l < a.n_layers; ++l) {
     if (a.thin[l] == 0) nh += a.tiles_n[l] * a.tiles_m[l] * a.G[l];
     if (a.thin[l] == 1) nt += a.tiles_n[l] * a.tiles_m[l] * a.G[l];
   }
@@ -464,7 +466,7 @@ cudaError_t phase_b2_all_layers(const PhbAll& a, Phb2Cache& cache, cudaStream_t 
   // buffers stay put)
   for (int l = 0; l < a.n_layers; ++l) {
     const PhbArgs& p = a.L[l];
-    if (a.thin[l] == 2) continue;
+    if (a.thin[l] >= 2) continue;
     if (cache.kd[l] != p.D || cache.kz[l] != p.Z || cache.km[l] != p.M || cache.kn[l] != p.N ||
         cache.ks[l] != p.s_pad) {
       if (!encode_rows(&cache.maps.d[l], p.D, p.M, p.s_pad) || !encode_rows(&cache.maps.z[l], p.Z, p.N, p.s_pad))

@@ -232,6 +232,132 @@ void reduce_pha(const double* partA, int rows, int n_pts_pad, const double* w, d
   probe_after(K_VEC, st);
 }
 
+// as reduce_pha, plus (PhaCols) the wide layers' per-column partials (ngd_phag.cu: the point's C
+// channel columns -- one on the boundary -- of every column-partial row) and the output layer from its
+// precontracted rows (out_contract), all in fixed order
+__global__ void reduce_pha_cols_kernel(const double* partA, int rows, Geom gm, PhaCols rc, const double* w, double* cot,
+                                       const int* done) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
+  if (done && *done) return;
+  const int npp = gm.n_pts_pad(), int_pts = gm.nib * PB, C = gm.C;
+  for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < npp; pt += gridDim.x * blockDim.x) {
+    double s = sum_partials(partA, rows, npp, pt);
+    const bool interior = pt < int_pts;
+    const int64_t col0 = interior ? (int64_t)(pt / PB) * PB * C + (pt % PB) : (int64_t)int_pts * C + (pt - int_pts);
+    const int nch = interior ? C : 1;
+    for (int q = 0; q < rc.cslots; ++q) {
+      const double* row = rc.colpart + (int64_t)q * gm.s_pad + col0;
+      double r = 0.0;
+      for (int c = 0; c < nch; ++c) r += __ldcg(&row[(int64_t)c * PB]);
+      s += r;
+    }
+    if (rc.gout) {  // <v_{W_L}, J_pt[W_L]> + v_{b_L} D_L(pt, value)
+      double r = rc.vbout[0] * rc.dseed[col0];
+      int k = 0;
+#pragma unroll 1
+      for (; k + 8 <= rc.kout; k += 8) {
+        double g[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) g[u] = __ldcs(&rc.gout[(int64_t)(k + u) * npp + pt]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r = fma(rc.vout[k + u], g[u], r);
+      }
+      for (; k < rc.kout; ++k) r = fma(rc.vout[k], __ldcs(&rc.gout[(int64_t)k * npp + pt]), r);
+      s += r;
+    }
+    cot[pt] = w ? w[pt] * s : s;
+  }
+}
+
+void reduce_pha_cols(const double* partA, int rows, const Geom& gm, const PhaCols& rc, const double* w, double* cot,
+                     const int* done, cudaStream_t st) {
+  const int npp = gm.n_pts_pad();
+  const int grid = std::max(1, std::min((npp + 255) / 256, 148 * 8));
+  probe_before(K_VEC, st);
+  launch_pdl(reduce_pha_cols_kernel, dim3(grid), dim3(256), 0, st, partA, rows, gm, rc, w, cot, done);
+  probe_after(K_VEC, st);
+}
+
+// G[k][pt] = sum_c D_L(pt, c) Zin_L[k](pt, c): the W_L block of the Jacobian row of point pt (the output
+// layer has one unit, so its row is K numbers instead of the C K of its input jets)
+__global__ void out_contract_kernel(const double* __restrict__ zin, const double* __restrict__ dseed, Geom gm,
+                                    double* __restrict__ G) {
+  const int npp = gm.n_pts_pad(), int_pts = gm.nib * PB, C = gm.C;
+  const int k = blockIdx.y;
+  const double* zrow = zin + (int64_t)k * gm.s_pad;
+  for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < npp; pt += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    if (pt < int_pts) {
+      const int64_t col0 = (int64_t)(pt / PB) * PB * C + (pt % PB);
+      for (int c = 0; c < C; ++c) s = fma(dseed[col0 + (int64_t)c * PB], zrow[col0 + (int64_t)c * PB], s);
+    } else {
+      const int64_t col = (int64_t)int_pts * C + (pt - int_pts);
+      s = dseed[col] * zrow[col];
+    }
+    G[(int64_t)k * npp + pt] = s;
+  }
+}
+
+void out_contract(const double* zin, const double* dseed, int K, const Geom& gm, double* G, cudaStream_t st) {
+  const int npp = gm.n_pts_pad();
+  probe_before(K_PHA, st);
+  out_contract_kernel<<<dim3(std::max(1, std::min((npp + 255) / 256, 64)), K), 256, 0, st>>>(zin, dseed, gm, G);
+  probe_after(K_PHA, st);
+}
+
+// phase B of the output layer from G: block g sums its point range [g P, (g + 1) P) for every k (warp
+// w takes rows w, w + 8, ..; lanes 32 consecutive points; fixed xor tree), plus the bias entry
+__global__ void __launch_bounds__(256) out_phase_b_kernel(const double* __restrict__ G, const double* __restrict__ dseed,
+                                                          int K, Geom gm, const double* __restrict__ cot, double* part,
+                                                          int64_t p, int64_t off, int per, const int* done) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
+  if (done && *done) return;
+  const int npp = gm.n_pts_pad(), int_pts = gm.nib * PB, C = gm.C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pt0 = blockIdx.x * per, pt1 = min(npp, pt0 + per);
+  double* out = part + (int64_t)blockIdx.x * p + off;
+  for (int k0 = 0; k0 < K; k0 += 256) {
+    double acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+    double bacc = 0.0;
+    for (int pt = pt0 + lane; pt < pt1; pt += 32) {
+      const double cv = cot[pt];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int k = k0 + warp + 8 * i;
+        if (k < K) acc[i] = fma(cv, __ldcs(&G[(int64_t)k * npp + pt]), acc[i]);
+      }
+      if (k0 == 0 && warp == 0) {
+        const int64_t col0 = pt < int_pts ? (int64_t)(pt / PB) * PB * C + (pt % PB) : (int64_t)int_pts * C + (pt - int_pts);
+        bacc = fma(cv, dseed[col0], bacc);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      double v = acc[i];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      const int k = k0 + warp + 8 * i;
+      if (lane == 0 && k < K) out[k] = v;
+    }
+    if (k0 == 0 && warp == 0) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) bacc += __shfl_xor_sync(0xffffffffu, bacc, o);
+      if (lane == 0) out[K] = bacc;
+    }
+  }
+}
+
+void out_phase_b(const double* G, const double* dseed, int K, const Geom& gm, const double* cot, double* part, int64_t p,
+                 int64_t off, int splits, const int* done, cudaStream_t st) {
+  const int npp = gm.n_pts_pad();
+  const int per = ((npp + splits - 1) / splits + 31) & ~31;
+  probe_before(K_PHB, st);
+  launch_pdl(out_phase_b_kernel, dim3(splits), dim3(256), 0, st, G, dseed, K, gm, cot, part, p, off, per, done);
+  probe_after(K_PHB, st);
+}
+
 // phase B reduction: out[i] = sum_g part[g][i] (+ mu * v[i])
 __device__ __forceinline__ int plan_G(const RedPlan& rp, int64_t i) {
   int l = 0;

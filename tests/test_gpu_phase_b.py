@@ -56,3 +56,49 @@ def test_phase_b_tile_plans(kind, widths, nint, nbnd):
     assert rel(gop.matvec(v), ref) <= 1e-10
     # the gradient runs phase B with the residual cotangent
     assert rel(prob.loss_grad(theta, quad), oprob.loss_grad(theta, oq)) <= 1e-10
+
+
+# every phase-A / phase-B route on the same problems: the wide layers' phase A on the GEMM core
+# (pha_gemm, ngd_phag.cu) or on pha_all_kernel, and the output layer from its precontracted Jacobian
+# rows (out_pre: out_contract / out_phase_b / reduce_pha_cols) or from its jets (pha_all / phb2)
+ROUTE_CASES = [
+    ("gauss", (10, 256, 256, 1), 64, 16),
+    ("sin2d", (2, 300, 300, 1), 200, 40),
+    ("sin2d", (2, 50, 100, 1), 256, 64),
+    ("sinsum", (3, 17, 1), 97, 21),
+]
+
+
+@pytest.mark.parametrize("kind,widths,nint,nbnd", ROUTE_CASES)
+def test_phase_routes_agree(kind, widths, nint, nbnd):
+    from paper_2505_11638_b200 import _lib
+
+    prob, quad, theta = build(kind, widths, nint, nbnd)
+    v = np.random.default_rng(2).standard_normal(prob.topology.param_count)
+    oprob = O.PoissonProblem(widths, kind=kind)
+    oq = oprob.sample_quadrature(nint, nbnd, 0)
+    ref_mv = O.GramianOracle(oprob, theta, oq).matvec(v)
+    ref_g = oprob.loss_grad(theta, oq)
+    outs = {}
+    for pg in (0, 1):
+        for op in (0, 1):
+            with _lib.option("pha_gemm", pg), _lib.option("out_pre", op):
+                gop = ngd.GramianOperator.from_problem(prob, theta, quad)
+                mv = gop.matvec(v)
+                g = prob.loss_grad(theta, quad)
+            assert rel(mv, ref_mv) <= 1e-10, (pg, op)
+            assert rel(g, ref_g) <= 1e-10, (pg, op)
+            outs[pg, op] = mv
+    for key, mv in outs.items():
+        assert rel(mv, outs[0, 0]) <= 1e-13, key
+
+
+def test_route_options_validate():
+    from paper_2505_11638_b200 import _lib
+
+    prob, quad, theta = build("sin2d", (2, 8, 1), 32, 16)
+    prob.loss_value(theta, quad)  # a live context validates the values
+    with pytest.raises(ValueError):
+        _lib.set_option("out_pre", 3)
+    with pytest.raises(ValueError):
+        _lib.set_option("pha_gemm", -1)
