@@ -336,7 +336,7 @@ def run_reference(args, rank):
 
 
 def roofline_entry(kind, widths, n_int, n_bnd, ell, p, count, total_ms, peaks, gemm_flops=None, sweeps=(0, 0),
-                   i8_ops=None, conv_elems=None):
+                   i8_ops=None, conv_elems=None, phase_flops=None):
     """Algorithmic work per launch of kernel class `kind` / average duration."""
     d = widths[0]
     S = n_int * (d + 2) + n_bnd
@@ -344,7 +344,14 @@ def roofline_entry(kind, widths, n_int, n_bnd, ell, p, count, total_ms, peaks, g
     pw = sum(i * o for i, o in zip(widths[:-1], widths[1:]))
     bound, unit, peak = "tensor", "TFLOP/s", peaks["fp64_tflops"]
     note = ""
-    if kind == 3:  # one launch = all layers: 2 Pw S FLOP
+    if kind in (3, 4) and phase_flops:
+        # a phase is one to three launches (GEMM-core wide layers, thin-layer tiles, output-layer rows):
+        # the library counts 2 P_w S per phase invocation over the same launches the events bracket
+        work = phase_flops / max(count, 1)
+        note = (f"2 P_w S FLOP per phase {'A' if kind == 3 else 'B'} of the factored Gramian matvec "
+                f"({phase_flops / (2.0 * pw * S):.0f} phases in {int(count)} launches: library count "
+                "ngd_phase_flops / summed launch time)")
+    elif kind == 3:  # one launch = all layers: 2 Pw S FLOP
         work = 2.0 * pw * S
         note = "2 P_w S FLOP per launch (all layers, phase A of the factored Gramian matvec)"
     elif kind == 4:  # phase B: the wide layers' GEMM-core launch + the 64 x 64-tile launch (ngd_phbg/phb2)
@@ -421,11 +428,13 @@ def standalone_rooflines(ngd, _lib, lib, prob, quad, theta0, widths, n_int, n_bn
     for kind in (3, 4):
         gop.matvec_device(v)
         _lib.check(lib.ngd_probe_start(kind, 64))
+        pf0 = lib.ngd_phase_flops(kind)
         for _ in range(reps):
             gop.matvec_device(v)
         tt, cc = _lib.ctypes.c_double(), _lib.ctypes.c_int64()
         _lib.check(lib.ngd_probe_stop(_lib.ctypes.byref(tt), _lib.ctypes.byref(cc)))
-        out[KIND_NAMES[kind]] = roofline_entry(kind, widths, n_int, n_bnd, ell, p, cc.value, tt.value, peaks)
+        out[KIND_NAMES[kind]] = roofline_entry(kind, widths, n_int, n_bnd, ell, p, cc.value, tt.value, peaks,
+                                               phase_flops=lib.ngd_phase_flops(kind) - pf0)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(2):
         s0.record()
@@ -525,9 +534,11 @@ def main():
     # classification step (the last warm-up step): every kernel class timed, PCG launched directly
     # (graph replays hide their kernels from the probe); the dominant class over ALL kernels,
     # library calls included, is then timed inside the timed region
+    pfc = {k: lib.ngd_phase_flops(k) for k in (3, 4)}
     with _lib.option("graphs", 0):
         class_ms = probe_all(_lib, lib, runner.step)
     torch.cuda.synchronize()
+    pfc = {k: lib.ngd_phase_flops(k) - v for k, v in pfc.items()}
     step_class_ms = sum(v[0] for v in class_ms.values())
     if args.probe:
         probe_kind = args.probe
@@ -548,6 +559,7 @@ def main():
     flops0 = lib.ngd_gemm_flops()
     i80 = lib.ngd_i8_ops()
     conv0 = lib.ngd_oz_conv_elems()
+    phase0 = lib.ngd_phase_flops(probe_kind)
     _lib.check(lib.ngd_probe_start(probe_kind, 1 << 15))
     step_ms = []
     matvecs = sketch_cols = 0
@@ -565,6 +577,7 @@ def main():
     torch.cuda.synchronize()
     launches = lib.ngd_launch_count() - launches0
     gemm_flops = lib.ngd_gemm_flops() - flops0
+    phase_flops = lib.ngd_phase_flops(probe_kind) - phase0
     i8_ops = lib.ngd_i8_ops() - i80
     conv_elems = lib.ngd_oz_conv_elems() - conv0
     ktot = _lib.ctypes.c_double()
@@ -589,12 +602,12 @@ def main():
     if kcnt.value > 0:
         roof = roofline_entry(probe_kind, widths, n_int // world, n_bnd // world, ell, p, kcnt.value, ktot.value,
                               peaks, gemm_flops=gemm_flops, sweeps=(abs(sweeps.value), abs(sweeps_f32.value)),
-                              i8_ops=i8_ops, conv_elems=conv_elems)
+                              i8_ops=i8_ops, conv_elems=conv_elems, phase_flops=phase_flops)
         roof["timed"] = "CUDA events around each launch of the class on its stream, inside the timed region"
     else:  # the class only runs inside the captured PCG graph: its classification-step timing
         ms_c, cnt_c = class_ms[KIND_NAMES[probe_kind]]
         roof = roofline_entry(probe_kind, widths, n_int // world, n_bnd // world, ell, p, cnt_c, ms_c, peaks,
-                              sweeps=(abs(sweeps.value), abs(sweeps_f32.value)))
+                              sweeps=(abs(sweeps.value), abs(sweeps_f32.value)), phase_flops=pfc.get(probe_kind))
         roof["timed"] = "classification step (graphs off): the class runs inside the captured PCG graph"
     try:  # measured DRAM traffic of this kernel at this config (one ncu --set full capture)
         with open(os.path.join(ROOT, "profiles", "traffic_r02.json")) as fh:

@@ -191,6 +191,9 @@ double ngd_gemm_flops(void);
 double ngd_i8_ops(void);
 /* FP64 elements converted to residues (Ozaki scheme) so far (process-wide) */
 double ngd_oz_conv_elems(void);
+/* algorithmic FLOPs (2 P_w S each) of the phase A (kind 3) / phase B (kind 4) invocations launched
+ * directly so far (process-wide; graph captures excluded, like the per-launch timing) */
+double ngd_phase_flops(int32_t kind);
 int ngd_probe_start(int32_t kind, int32_t max_launches);
 int ngd_probe_stop(double* h_total_ms, int64_t* h_count);
 int ngd_probe_stop_all(double* h_ms, int64_t* h_count, int32_t n_kinds);

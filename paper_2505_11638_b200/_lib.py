@@ -87,12 +87,13 @@ SIGNATURES = {
     "ngd_gemm_flops": [],
     "ngd_i8_ops": [],
     "ngd_oz_conv_elems": [],
+    "ngd_phase_flops": [_I32],
     "ngd_probe_start": [_I32, _I32],
     "ngd_probe_stop": [ctypes.POINTER(_D), ctypes.POINTER(_I64)],
     "ngd_probe_stop_all": [ctypes.POINTER(_D), ctypes.POINTER(_I64), _I32],
 }
 _RESTYPE = {"ngd_last_error": ctypes.c_char_p, "ngd_param_count": _I64, "ngd_launch_count": _I64,
-            "ngd_gemm_flops": _D, "ngd_i8_ops": _D, "ngd_oz_conv_elems": _D}
+            "ngd_gemm_flops": _D, "ngd_i8_ops": _D, "ngd_oz_conv_elems": _D, "ngd_phase_flops": _D}
 
 _lib = None
 _contexts = []  # weak registry so option changes reach live contexts

@@ -423,10 +423,25 @@ static int plan_routes(ngd_ctx* c) {
   return plan_phase_b(c);
 }
 
+// bench evidence: algorithmic FLOPs (2 P_w S per phase) of the phase A / phase B invocations launched
+// directly (graph captures are not counted: their replays are not timed per launch either)
+static double g_phase_flops[2] = {0.0, 0.0};
+static void count_phase(ngd_ctx* c, int which) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(c->stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return;
+  }
+  double pw = 0.0;
+  for (int l = 0; l < c->NL; ++l) pw += (double)c->w[l] * c->w[l + 1];
+  g_phase_flops[which] += 2.0 * pw * ((double)c->gm.n_int * c->gm.C + c->gm.n_bnd);
+}
+
 // J v: pack v (unless prepacked: PCG's direction is packed by pcg_dir_pack), phase A, reduction
 static int phase_a(ngd_ctx* c, const double* v, const double* w_or_null, double* cot_out, const int* skip,
                    bool prepacked = false) {
   const Geom& gm = c->gm;
+  count_phase(c, 0);
   if (!prepacked) pack_all(vp_plan(c), v, skip, c->stream);
   PhaAll pa{};
   pa.n_layers = c->NL;
@@ -518,6 +533,7 @@ static void fill_phb(ngd_ctx* c, const double* cot, const int* skip, PhbAll& pb)
 // J^T cot partials of every layer into partB: wide layers on the GEMM core, the rest (thin input /
 // output layers, narrow hidden layers) on the 64 x 64-tile pipeline
 static int phase_b_partials(ngd_ctx* c, const double* cot, const int* skip) {
+  count_phase(c, 1);
   if (c->phbg.n_heavy) {
     c->phbg.cvec = cot;
     c->phbg.part = c->partB.d();
@@ -918,6 +934,8 @@ int ngd_ctx_set_comm(ngd_ctx* c, const uint8_t* h_id, int32_t rank, int32_t nran
   c->nranks = nranks;
   return NGD_OK;
 }
+
+double ngd_phase_flops(int32_t kind) { return kind == 3 ? g_phase_flops[0] : (kind == 4 ? g_phase_flops[1] : 0.0); }
 
 int ngd_set_points(ngd_ctx* c, int64_t n_int, const double* x_int, const double* w_int, const double* off_int,
                    int64_t n_bnd, const double* x_bnd, const double* w_bnd, const double* off_bnd) {

@@ -81,6 +81,193 @@ __device__ __forceinline__ AItem decode_a(const PhagArgs& a, int idx) {
 }
 }  // namespace
 
+#ifndef PHAG_KORD
+#define PHAG_KORD 2  // fragment k order (see ngd_phbg.cu)
+#endif
+#ifndef PHAG_WS
+#define PHAG_WS 1  // 1: a producer warpgroup issues the TMA ring (setmaxnreg; see ngd_phbg.cu)
+#endif
+#if PHAG_WS
+constexpr int kPhagThreads = (kPhagWarps + 4) * 32;
+static_assert(!PHAG_DG && !PHAG_PF, "the warp-specialised form streams D through the ring");
+// The producer refills a slot as soon as its eighth consumer warp has arrived, so the consumers order
+// their shared-memory reads (generic proxy) before the refill (async proxy) with fence.proxy.async ahead
+// of the arrive.  Measured without it (tools/ws_stress.py, C5): one stale 16-column box -- one point
+// block of J v off by 1e-4 .. 3e-3 -- in ~10% of the launches; with it 0 in 100 (the single-role form
+// never refilled a slot less than two stages after its release).
+__global__ void __launch_bounds__(kPhagThreads, 1) phag_kernel(const __grid_constant__ PhagArgs a,
+                                                               const __grid_constant__ PhagMaps maps) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
+  if (a.skip && *a.skip) return;
+  extern __shared__ unsigned char asm_raw[];
+  unsigned char* base = asm_raw + ((1024u - (tma::smem(asm_raw) & 1023u)) & 1023u);
+  AStage* st = reinterpret_cast<AStage*>(base);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(st + ANS);
+  unsigned long long* empty = full + ANS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < ANS; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], kPhagWarps);
+    }
+    tma::fence_init();
+  }
+  __syncthreads();
+  const int n_items = a.item_start[a.n_heavy];
+  if (warp >= kPhagWarps) {  // producer warpgroup: units 0 .. ks-1 of an item are k-stages, then its D stages
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
+    if (warp == kPhagWarps && lane == 0) {
+      unsigned qp = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const AItem it = decode_a(a, idx);
+        const int ks = a.Kp[it.h] / ABK, m0 = it.tm * ABM, n0 = it.tn * ABN;
+        for (int u = 0; u < ks + kDStages; ++u, ++qp) {
+          const int slot = qp % ANS;
+          if (qp >= ANS) tma::wait(&empty[slot], ((qp / ANS) - 1) & 1u);
+          tma::expect_tx(&full[slot], (ABM + ABN) * ABK * sizeof(double));
+          if (u < ks) {
+            const int k0 = u * ABK;
+            tma::load2d(st[slot].A, &maps.v[it.h], k0, m0, &full[slot]);
+#pragma unroll
+            for (int b = 0; b < ABN / 16; ++b)
+              tma::load2d(st[slot].B + b * 256, &maps.z[it.h], n0 + b * 16, k0, &full[slot]);
+          } else {
+            const int c0 = n0 + (u - ks) * 32;
+            tma::load2d(st[slot].A, &maps.d[it.h], c0, m0, &full[slot]);
+            tma::load2d(st[slot].B, &maps.d[it.h], c0 + 16, m0, &full[slot]);
+          }
+        }
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+#if PHAG_KORD == 2
+  const int koff = ((t & 1) * 10) ^ ((t >> 1) * 5);  // {0, 10, 5, 15}: bank-conflict-free half-warps (ngd_phbg.cu)
+#else
+  const int koff = ((t & 1) << 2) | (t >> 1);  // {0, 4, 1, 5}
+#endif
+  unsigned q = 0;
+  for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    const AItem it = decode_a(a, idx);
+    const int ks = a.Kp[it.h] / ABK;
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int s = 0; s < ks; ++s, ++q) {
+      const int slot = q % ANS;
+      tma::wait(&full[slot], (q / ANS) & 1u);
+      const double* As = st[slot].A;
+      const double* Bs = st[slot].B;
+#pragma unroll
+      for (int kq = 0; kq < 4; ++kq) {
+#if PHAG_KORD == 2
+        const int kk = (kq << 1) ^ koff;
+#else
+        const int kk = ((kq & 1) << 1) + ((kq >> 1) << 3) + koff;  // kbase {0, 2, 8, 10}
+#endif
+        double av[8], bv[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) av[i] = As[tma::kmaj_off(wm * 64 + i * 8 + g, kk)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = Bs[mn_off(wn * 32 + j * 8 + g, kk)];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+      }
+      tma::fence_proxy_async();  // generic-proxy reads of the slot before the producer's async-proxy refill
+      __syncwarp();
+      if (lane == 0) tma::arrive(&empty[slot]);
+    }
+    // epilogue: bias of the value-channel columns, dot with D over this warp's 64 rows
+    const int M = a.M[it.h];
+    const int mrow = it.tm * ABM + wm * 64 + g;
+    double vb[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) vb[i] = (mrow + i * 8 < M) ? __ldg(&a.vbias[it.h][mrow + i * 8]) : 0.0;
+    const int64_t ncol = (int64_t)it.tn * ABN + wn * 32;
+    bool val[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t run = (ncol + j * 8) >> 4;
+      val[j] = run >= a.int_units || (run % a.C) == 0;
+    }
+    double cs[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cs[j][0] = cs[j][1] = 0.0;
+    if (PHAG_DG) {
+      const int64_t s_pad = a.s_pad;
+      const double* Dg = a.dptr[it.h] + (int64_t)mrow * s_pad + ncol + 2 * t;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (ncol + j * 8 >= s_pad) break;
+        double2 dv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dv[i] = (mrow + i * 8 < M) ? __ldcg(reinterpret_cast<const double2*>(Dg + (int64_t)i * 8 * s_pad + j * 8))
+                                     : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double b = val[j] ? vb[i] : 0.0;
+          cs[j][0] = fma(dv[i].x, acc[i][j][0] + b, cs[j][0]);
+          cs[j][1] = fma(dv[i].y, acc[i][j][1] + b, cs[j][1]);
+        }
+      }
+    }
+    for (int dq = 0; dq < kDStages; ++dq, ++q) {
+      const int slot = q % ANS;
+      tma::wait(&full[slot], (q / ANS) & 1u);
+      if (dq == wn) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double* Db = (j < 2) ? st[slot].A : st[slot].B;
+          const int kin = (j & 1) * 8 + 2 * t;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const double2 dv = *reinterpret_cast<const double2*>(Db + tma::kmaj_off(wm * 64 + i * 8 + g, kin));
+            const double b = val[j] ? vb[i] : 0.0;
+            cs[j][0] = fma(dv.x, acc[i][j][0] + b, cs[j][0]);
+            cs[j][1] = fma(dv.y, acc[i][j][1] + b, cs[j][1]);
+          }
+        }
+      }
+      tma::fence_proxy_async();  // generic-proxy reads of the slot before the producer's async-proxy refill
+      __syncwarp();
+      if (lane == 0) tma::arrive(&empty[slot]);
+    }
+    // fixed xor tree over the eight row groups g, then lanes g = 0 store their two columns per j
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double v = cs[j][e];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        cs[j][e] = v;
+      }
+    if (g == 0) {
+      double* row = a.colpart + (int64_t)(a.slot0[it.h] + it.tm * 2 + wm) * a.s_pad;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t n = ncol + j * 8 + 2 * t;
+        if (n + 1 < a.s_pad) {
+          *reinterpret_cast<double2*>(row + n) = make_double2(cs[j][0], cs[j][1]);
+        } else if (n < a.s_pad) {
+          row[n] = cs[j][0];
+        }
+      }
+    }
+  }
+}
+
+#else
+constexpr int kPhagThreads = kPhagWarps * 32;
 __global__ void __maxnreg__(224) phag_kernel(const __grid_constant__ PhagArgs a, const __grid_constant__ PhagMaps maps) {
   pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (a.skip && *a.skip) return;
@@ -269,6 +456,8 @@ __global__ void __maxnreg__(224) phag_kernel(const __grid_constant__ PhagArgs a,
   }
 }
 
+#endif
+
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 enc_fn_a() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -319,7 +508,7 @@ cudaError_t phase_a_gemm(const PhagArgs& a, PhagCache& cache, cudaStream_t st) {
   if (items <= 0) return cudaSuccess;
   probe_before(K_PHA, st);
   const cudaError_t e =
-      launch_pdl(phag_kernel, dim3(std::min(items, 148)), dim3(kPhagWarps * 32), kPhagSmem, st, a, cache.maps);
+      launch_pdl(phag_kernel, dim3(std::min(items, 148)), dim3(kPhagThreads), kPhagSmem, st, a, cache.maps);
   probe_after(K_PHA, st);
   return e;
 }

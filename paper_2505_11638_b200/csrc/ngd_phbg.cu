@@ -64,12 +64,26 @@ __device__ __forceinline__ int stage_point(const PhbgArgs& a, int u) {
 __device__ __forceinline__ bool stage_is_value(const PhbgArgs& a, int u) {
   return u >= a.int_units || (u % a.C) == 0;
 }
+#ifndef PHBG_KORD
+// fragment k order: lane t of MMA ks takes column koff[t] ^ 2 ks of the 16-column stage.  A 64-bit shared load
+// is served per half-warp (rows g = 0..3 x the four t): with the 128-byte swizzle the 16 lanes cover all 32
+// banks iff the four koff differ in (parity, bit 3) -- K-major tiles -- and in bits 1..2 -- MN-major tiles
+// (ngd_phag.cu): {0, 10, 5, 15} does both.  The first order {0,4,1,5} + {0,2,8,10} (0) took two wavefronts
+// per half-warp (ncu: 2 x the ideal shared wavefronts); 1 = {0,8,1,9} + 2 ks (K-major only).
+#define PHBG_KORD 2
+#endif
 template <bool BIAS>
 __device__ __forceinline__ void stage_mma(const double* As, const double* Bs, const double* cc, int wm, int wn, int g,
                                           int koff, double (&acc)[8][4][2], double (&bsum)[8]) {
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
+#if PHBG_KORD == 2
+    const int kk = (ks << 1) ^ koff;
+#elif PHBG_KORD == 1
+    const int kk = (ks << 1) + koff;
+#else
     const int kk = ((ks & 1) << 1) + ((ks >> 1) << 3) + koff;
+#endif
     const double cv = cc[kk];
     double av[8], bv[4];
 #pragma unroll
@@ -88,6 +102,123 @@ __device__ __forceinline__ void stage_mma(const double* As, const double* Bs, co
 }
 }  // namespace
 
+#ifndef PHBG_WS
+#define PHBG_WS 1  // 1: a producer warpgroup issues the TMA ring (setmaxnreg hands its registers to the DMMA warps)
+#endif
+#if PHBG_WS
+constexpr int kPhbgThreads = (kPhbgWarps + 4) * 32;
+// Warp-specialised form.  Measured on the single-role kernel (ncu source page, C5): the ring was issued
+// by lane 0 of DMMA warp 0 -- ~135 dependent instructions per k-stage (slot wait, three bulk copies,
+// the stage -> point division), 21% of that warp's time -- and the other seven warps, limited to the
+// ring's lookahead past warp 0, spent 8.5% of theirs waiting on the full barriers (DMMA pipe 86%).
+// Here warps 8..11 are a producer warpgroup that gives its registers away (setmaxnreg: 12 warps launch
+// at 168 registers, the DMMA warps grow to 232) and one of its lanes runs the whole (item, stage)
+// sequence ahead of the consumers, bounded only by the ring depth.
+__global__ void __launch_bounds__(kPhbgThreads, 1) phbg_kernel(const __grid_constant__ PhbgArgs a,
+                                                               const __grid_constant__ PhbgMaps maps) {
+  pdl_entry();  // (PCG chain: programmatic dependent launch)
+  if (a.skip && *a.skip) return;
+  extern __shared__ unsigned char bsm_raw[];
+  unsigned char* base = bsm_raw + ((1024u - (tma::smem(bsm_raw) & 1023u)) & 1023u);
+  BStage* st = reinterpret_cast<BStage*>(base);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(st + BNS);
+  unsigned long long* empty = full + BNS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < BNS; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], kPhbgWarps);
+    }
+    tma::fence_init();
+  }
+  __syncthreads();
+  const int n_items = a.item_start[a.n_heavy] * a.G;
+  if (warp >= kPhbgWarps) {  // producer warpgroup
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
+    if (warp == kPhbgWarps && lane == 0) {
+      unsigned qp = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const BItem it = decode_b(a, idx);
+        const int m0 = it.tm * BBM, n0 = it.tn * BBN;
+        for (int s = it.s0; s < it.s1; ++s, ++qp) {
+          const int slot = qp % BNS;
+          if (qp >= BNS) tma::wait(&empty[slot], ((qp / BNS) - 1) & 1u);
+          tma::expect_tx(&full[slot], (2 * BBM * BBK + BBK) * sizeof(double));
+          tma::load2d(st[slot].A, &maps.d[it.h], s * BBK, m0, &full[slot]);
+          tma::load2d(st[slot].B, &maps.z[it.h], s * BBK, n0, &full[slot]);
+          tma::load1d(st[slot].cc, a.cvec + stage_point(a, s), BBK * sizeof(double), &full[slot]);
+        }
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+#if PHBG_KORD == 2
+  const int koff = ((t & 1) * 10) ^ ((t >> 1) * 5);  // {0, 10, 5, 15}
+#elif PHBG_KORD == 1
+  const int koff = ((t & 1) << 3) | (t >> 1);  // {0, 8, 1, 9}
+#else
+  const int koff = ((t & 1) << 2) | (t >> 1);  // {0, 4, 1, 5}: fragment k order (ngd_gemm.cu)
+#endif
+  unsigned q = 0;
+  for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    const BItem it = decode_b(a, idx);
+    const bool do_bias = it.tn == 0 && wn == 0;
+    double acc[8][4][2], bsum[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      bsum[i] = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    // value-channel stages (bias rows): every C-th interior stage, every boundary stage
+    int vc = it.s0 < a.int_units ? it.s0 % a.C : 0;
+    for (int s = it.s0; s < it.s1; ++s, ++q) {
+      const int slot = q % BNS;
+      tma::wait(&full[slot], (q / BNS) & 1u);
+      const double* As = st[slot].A;
+      const double* Bs = st[slot].B;
+      const bool value = s >= a.int_units || vc == 0;
+      vc = (vc + 1 == a.C) ? 0 : vc + 1;
+      // the n-tile-0 warps also accumulate the bias rows on value-channel stages: a uniform branch
+      // between two unrolled bodies (a predicated bias FMA would issue on every stage)
+      if (do_bias && value)
+        stage_mma<true>(As, Bs, st[slot].cc, wm, wn, g, koff, acc, bsum);
+      else
+        stage_mma<false>(As, Bs, st[slot].cc, wm, wn, g, koff, acc, bsum);
+      tma::fence_proxy_async();  // generic-proxy reads of the slot before the async-proxy refill (ngd_phag.cu)
+      __syncwarp();
+      if (lane == 0) tma::arrive(&empty[slot]);
+    }
+    // epilogue: this split's partial of W_l (rows m, cols n) and, from the n-tile 0 warps, of b_l
+    const int M = a.M[it.h], N = a.N[it.h];
+    double* out = a.part + (int64_t)it.split * a.p + a.off[it.h];
+    const int m0 = it.tm * BBM + wm * 64 + g, n0 = it.tn * BBN + wn * 32 + 2 * t;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = m0 + i * 8;
+      if (m < M) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = n0 + j * 8 + e;
+            if (n < N) out[(int64_t)m * N + n] = acc[i][j][e];
+          }
+      }
+      if (do_bias) {  // fixed xor tree over the four k-lanes
+        double b = bsum[i];
+        b += __shfl_xor_sync(0xffffffffu, b, 1);
+        b += __shfl_xor_sync(0xffffffffu, b, 2);
+        if (t == 0 && m < M) out[(int64_t)M * N + m] = b;
+      }
+    }
+  }
+}
+#else
+constexpr int kPhbgThreads = kPhbgWarps * 32;
 __global__ void __maxnreg__(224) phbg_kernel(const __grid_constant__ PhbgArgs a, const __grid_constant__ PhbgMaps maps) {
   pdl_entry();  // (PCG chain: programmatic dependent launch)
   if (a.skip && *a.skip) return;
@@ -198,6 +329,8 @@ __global__ void __maxnreg__(224) phbg_kernel(const __grid_constant__ PhbgArgs a,
   }
 }
 
+#endif
+
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 enc_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -269,7 +402,7 @@ cudaError_t phase_b_gemm(const PhbgArgs& a, PhbgCache& cache, cudaStream_t st) {
   const int items = a.item_start[a.n_heavy] * a.G;
   if (items <= 0) return cudaSuccess;
   probe_before(K_PHB, st);
-  const cudaError_t e = launch_pdl(phbg_kernel, dim3(std::min(items, 148)), dim3(kPhbgWarps * 32), kPhbgSmem, st, a,
+  const cudaError_t e = launch_pdl(phbg_kernel, dim3(std::min(items, 148)), dim3(kPhbgThreads), kPhbgSmem, st, a,
                                    cache.maps);
   probe_after(K_PHB, st);
   return e;

@@ -40,6 +40,8 @@ __device__ __forceinline__ void load1d(void* dst, const void* src, unsigned byte
                "l"(src), "r"(bytes), "r"(smem(m))
                : "memory");
 }
+// orders this thread's earlier generic-proxy accesses to shared memory before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // element (mn, k) of a 128 x 16 stage tile loaded as one K-major TMA box (128-byte swizzle)
