@@ -102,7 +102,7 @@ OPTIONS = {"svd": 3}
 
 # library defaults of the ngd_set_option knobs (include/ngd.h), for restoring a temporary change
 DEFAULTS = {"svd": 3, "graphs": 1, "l2window": 1, "force_comm": 0, "pdl": 1, "l2u": 1, "sketch_gemm": 2, "i8_pair": 1,
-            "pha_gemm": 2, "out_pre": 2}
+            "pha_gemm": 2, "out_pre": 2, "oz_max_blocks": 1024}
 
 
 @contextlib.contextmanager

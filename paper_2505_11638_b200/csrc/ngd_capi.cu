@@ -162,6 +162,8 @@ struct ngd_ctx {
   Buf colpart;                    // phase A column partials of the wide layers [slots][s_pad]
   int pha_gemm = 2;               // option "pha_gemm": wide layers' phase A on the GEMM core (2 auto)
   int out_pre = 2;                // option "out_pre": output layer from precontracted rows (2 auto)
+  int oz_max_blocks = 1024;       // option "oz_max_blocks": point blocks per row kind in the INT8 sketch's
+                                  // column-maxima pass (0 = every block)
   bool pha_on = false, out_on = false;  // routes in effect (plan_routes)
   Buf gout;                       // output layer rows G[k][pt] = sum_c dseed Zin_L (out_contract)
   std::vector<char> wide_a;       // per layer: phase A eligible for the GEMM core (both sides >= 256)
@@ -409,9 +411,9 @@ static int plan_phase_b(ngd_ctx* c) {
 static int plan_routes(ngd_ctx* c) {
   const Geom& gm = c->gm;
   const bool wide = c->phag.n_heavy > 0;
-  // GEMM-core phase A: measured faster at C5 (C = 12: 43.7 vs 44.3 ms per matvec), slower at C4
-  // (C = 4: 5.02 vs 4.86 ms), where pha_all_kernel's one-point-block tile is 64 columns
-  c->pha_on = wide && (c->pha_gemm == 1 || (c->pha_gemm == 2 && gm.C >= 8));
+  // GEMM-core phase A (producer-warpgroup form): measured faster at C5 (C = 12: 19.6 vs 23.0 ms per
+  // phase A) and at C4 (C = 4: 2.22 vs 2.27 ms; the single-role form had been slower there)
+  c->pha_on = wide && (c->pha_gemm == 1 || (c->pha_gemm == 2 && gm.C >= 4));
   // precontracted output layer: its Jacobian rows (kout per point) replace a C-times larger jet
   // stream in both phases at the cost of one more launch per phase -- measured per C5 / C4 / C3
   // matvec 44.3 -> 42.6, 4.86 -> 4.76, 0.665 -> 0.652 ms, but C2 (kout S = 1.1 M) 46 -> 58 us
@@ -1324,14 +1326,27 @@ static int matmat_ozaki(ngd_ctx* c, FormJPlan& pl, const GemmOperand& vop, int e
   int* sig = static_cast<int*>(c->oz_ep.p);    // S columns
   auto* rmax = static_cast<long long*>(c->oz_mx.p);
   auto* cmax = reinterpret_cast<unsigned long long*>(rmax + pl.R);
-  // pass 0: column maxima of J over every chunk (DMMA J tiles, no stores)
+  // pass 0: column maxima of J (DMMA J tiles, no stores) over a strided sample of the point blocks --
+  // up to kOzMaxBlocks interior and as many boundary blocks (the two row kinds differ in magnitude per
+  // column).  gamma_k only balances the precision between the columns: rho_r comes from the true row
+  // maxima of the prescaled chunk, so |J'| <= 2^t holds for any gamma; a column whose maximum the
+  // sample misses by 2^b costs the other entries of the rows it dominates b of their t bits.
   CK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * p, c->stream));
   pl.fa.cmax = cmax;
   pl.fa.rmax = nullptr;
   pl.fa.no_store = 1;
-  for (int b0 = 0; b0 < pl.nblk_total; b0 += pl.bpc) {
-    pl.fa.blk0 = b0;
-    CK(form_j(pl.fa, std::min(pl.bpc, pl.nblk_total - b0), c->NL, pl.max_nin, pl.max_nout, c->stream));
+  {
+    const Geom& gm = c->gm;
+    const int kOzMaxBlocks = c->oz_max_blocks;
+    const int si = std::max(1, kOzMaxBlocks > 0 ? gm.nib / kOzMaxBlocks : 1);
+    const int sb = std::max(1, kOzMaxBlocks > 0 ? gm.nbb / kOzMaxBlocks : 1);
+    pl.fa.blk0 = 0;
+    pl.fa.blk_stride = si;
+    CK(form_j(pl.fa, (gm.nib + si - 1) / si, c->NL, pl.max_nin, pl.max_nout, c->stream));
+    pl.fa.blk0 = gm.nib;
+    pl.fa.blk_stride = sb;
+    CK(form_j(pl.fa, (gm.nbb + sb - 1) / sb, c->NL, pl.max_nin, pl.max_nout, c->stream));
+    pl.fa.blk_stride = 1;
   }
   CK(oz_exps(cmax, p, 1, gam, c->stream));  // max |J(., k)| 2^gamma_k in [1, 2)
   CK(oz_rows(vop.p, vop.ld, ell, p, tp, B8, ldp, pl_v, beta, false, c->stream, gam, -1));
@@ -1867,6 +1882,11 @@ int ngd_set_option(ngd_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "l2window")) {
     c->use_l2_window = value ? 1 : 0;
     c->graph_gen++;  // the captured PCG iteration carries the stream's access-policy window
+    return NGD_OK;
+  }
+  if (!strcmp(key, "oz_max_blocks")) {
+    if (value < 0 || value > (1 << 30)) return fail(NGD_E_SHAPE, "oz_max_blocks must be >= 0");
+    c->oz_max_blocks = (int)value;
     return NGD_OK;
   }
   if (!strcmp(key, "pha_gemm") || !strcmp(key, "out_pre")) {

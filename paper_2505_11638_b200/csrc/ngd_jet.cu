@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(FJ_THREADS, 1) formj_kernel(FormJArgs a) {
   const int tiles_b = (nin + FJ_T - 1) / FJ_T;
   const int a0 = (blockIdx.z / tiles_b) * FJ_T, b0 = (blockIdx.z % tiles_b) * FJ_T;
   if (a0 >= nout) return;
-  const int blk = a.blk0 + blockIdx.x;  // global point block
+  const int blk = a.blk0 + blockIdx.x * max(a.blk_stride, 1);  // global point block
   const bool interior = blk < a.nib;
   const int Cs = interior ? a.C : 1;
   const int nks = (Cs + 3) / 4;         // DMMA k-steps (channels padded to a multiple of 4 with zeros)

@@ -93,6 +93,7 @@ struct FormJArgs {
   int64_t s_pad, int_cols;
   int C, nib, n_int;
   int blk0;                 // first point block of this chunk (padded point order)
+  int blk_stride;           // CTA x takes block blk0 + x * blk_stride (0 = 1; > 1 only with no_store)
   double* Jt;               // [16 * blocks][ldj], row = padded point within the chunk
   int64_t ldj;
   // optional (INT8 sketch, ngd_ozaki.cu two-sided scaling):
@@ -100,7 +101,7 @@ struct FormJArgs {
   //         inf order above every finite value), accumulated over all chunks in a first pass;
   //   rmax: per chunk row (point), the maximum of |J(r, k)| 2^cexp[k] as a "log-bit" pattern
   //         bits(|J|) + cexp[k] 2^52 (signed RED.MAX; LLONG_MAX = non-finite);
-  //   no_store: the first pass computes the maxima only
+  //   no_store: the first pass computes the maxima only (over a strided sample of the point blocks)
   unsigned long long* cmax;
   long long* rmax;
   const int* cexp;
