@@ -19,10 +19,12 @@
 //     stage four ahead: a dedicated ninth producer warp would put three warps on one SM
 //     sub-partition, whose 16K-register file then caps every warp at 168 registers (spills);
 
-//   * the four k-steps of a stage use the k order {0,4,1,5}, {2,6,3,7}, {8,12,9,13},
-//     {10,14,11,15} for lanes t = 0..3: with the 128-byte swizzle every fragment load of either
-//     layout is two wavefronts (conflict-free) -- the plain order would make MN-major loads
-//     four-way;
+//   * lane t of k-step ks takes column {0, 10, 5, 15}[t] ^ 2 ks of the 16-column stage.  A 64-bit
+//     shared load is served per half-warp (rows g = 0..3 x the four t): with the 128-byte swizzle
+//     its 16 lanes cover all 32 banks iff the four k differ in (parity, bit 3) -- K-major tiles --
+//     and in bits 1..2 -- MN-major tiles; this order does both (ncu: shared wavefronts at the
+//     ideal count; the first order {0,4,1,5} + {0,2,8,10}, checked per full warp, took twice
+//     as many, and the plain order makes MN-major loads four-way);
 //   * persistent CTAs (one per SM) walk (split, m-tile, n-tile) items n-fastest, so the CTAs
 //     sharing an A panel run together (L2 reuse); long-K products are split so the item count
 //     fills whole waves, the partials are summed in split order by a second kernel
@@ -179,7 +181,7 @@ __global__ void __maxnreg__(224)
   // warp (wm, wn) owns rows wm*64 .. +63, cols wn*32 .. +31 of the tile
   const int wm = warp / WGN, wn = warp % WGN;
   const int g = lane >> 2, t = lane & 3;
-  const int koff = ((t & 1) << 2) | (t >> 1);  // {0, 4, 1, 5}
+  const int koff = ((t & 1) * 10) ^ ((t >> 1) * 5);  // {0, 10, 5, 15}
   unsigned q = 0;  // ring position of the next stage consumed
   for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
     const GItem it = decode(a, idx);
@@ -208,7 +210,7 @@ __global__ void __maxnreg__(224)
       const double* Bs = st[slot].B;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
-        const int kk = ((ks & 1) << 1) + ((ks >> 1) << 3) + koff;  // kbase {0, 2, 8, 10}
+        const int kk = (ks << 1) ^ koff;
         double av[8], bv[4];
 #pragma unroll
         for (int i = 0; i < 8; ++i) av[i] = As[toff<AK>(wm * 64 + i * 8 + g, kk)];
