@@ -1711,6 +1711,10 @@ int ngd_pcg(ngd_ctx* c, const double* dense, int64_t p, const double* b, double 
   CK(cudaStreamSynchronize(c->stream));
   memcpy(&hs, c->h_pin + 20, sizeof(PcgState));
   CK(cudaGetLastError());
+  if (getenv("NGD_PCG_DEBUG"))
+    fprintf(stderr, "[ngd pcg] issued %d it %d iterations %d matvecs %d done %d (before final pass %d) breakdown %d rr %.3e rel %.3e dad %.3e alpha %.3e rz %.3e rz_new %.3e beta %.3e flag %d\n",
+            issued, hs.it, hs.iterations, hs.matvecs, hs.done, dn, hs.breakdown, hs.rr, hs.rel, hs.dad, hs.alpha, hs.rz,
+            hs.rz_new, hs.beta, c->h_flags[5]);
   if (rep) {
     if (dn == 2) {
       rep->iterations = 0;

@@ -181,7 +181,14 @@ __global__ void __maxnreg__(224)
   // warp (wm, wn) owns rows wm*64 .. +63, cols wn*32 .. +31 of the tile
   const int wm = warp / WGN, wn = warp % WGN;
   const int g = lane >> 2, t = lane & 3;
+#ifndef GEMM_KORD
+#define GEMM_KORD 2
+#endif
+#if GEMM_KORD == 2
   const int koff = ((t & 1) * 10) ^ ((t >> 1) * 5);  // {0, 10, 5, 15}
+#else
+  const int koff = ((t & 1) << 2) | (t >> 1);  // {0, 4, 1, 5} (first order, kept for A/B builds)
+#endif
   unsigned q = 0;  // ring position of the next stage consumed
   for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
     const GItem it = decode(a, idx);
@@ -210,7 +217,11 @@ __global__ void __maxnreg__(224)
       const double* Bs = st[slot].B;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
+#if GEMM_KORD == 2
         const int kk = (ks << 1) ^ koff;
+#else
+        const int kk = ((ks & 1) << 1) + ((ks >> 1) << 3) + koff;
+#endif
         double av[8], bv[4];
 #pragma unroll
         for (int i = 0; i < 8; ++i) av[i] = As[toff<AK>(wm * 64 + i * 8 + g, kk)];

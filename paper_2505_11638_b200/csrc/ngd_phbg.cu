@@ -360,7 +360,10 @@ bool encode_jets(CUtensorMap* m, const double* base, int rows, int64_t s_pad) {
 // wide layers only: at 128 x 128 (C3) the two-launch split (this kernel + the thin pipeline of
 // ngd_phb2.cu) measured slower than ngd_phb2.cu alone (C3 phase B 0.35 vs 0.31 ms per matvec);
 // at 256 x 256 (C4 / C5) it is faster (C5 22.2 vs 22.6 ms, DMMA pipe 86% vs 81%)
-bool phbg_layer_ok(int M, int N) { return M >= 256 && N >= 256; }
+#ifndef NGD_WIDE_MIN
+#define NGD_WIDE_MIN 256
+#endif
+bool phbg_layer_ok(int M, int N) { return M >= NGD_WIDE_MIN && N >= NGD_WIDE_MIN; }
 
 // splits G of the K range so the items fill whole waves of one CTA per SM (>= 64 stages per split)
 int phbg_splits(int tiles, int kstages) {
