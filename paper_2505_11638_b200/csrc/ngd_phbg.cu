@@ -30,7 +30,11 @@ namespace ngd {
 namespace {
 constexpr int BBM = 128, BBN = 128, BBK = 16;
 constexpr int BNS = 6, BAHEAD = 4;
-constexpr int kPhbgWarps = 8;
+#ifndef PHBG_CW
+#define PHBG_CW 8  // DMMA warps: 8 (64 x 32 warp tiles, 232 registers) or 16 (32 x 32 warp tiles, 112 registers)
+#endif
+constexpr int kPhbgWarps = PHBG_CW;
+constexpr int kMI = 16 / (PHBG_CW / 4);  // 8-row DMMA blocks per warp: 8 or 4
 
 struct __align__(1024) BStage {
   double A[BBM * BBK];  // D_l rows m0 .. m0+127, 16 columns
@@ -74,7 +78,7 @@ __device__ __forceinline__ bool stage_is_value(const PhbgArgs& a, int u) {
 #endif
 template <bool BIAS>
 __device__ __forceinline__ void stage_mma(const double* As, const double* Bs, const double* cc, int wm, int wn, int g,
-                                          int koff, double (&acc)[8][4][2], double (&bsum)[8]) {
+                                          int koff, double (&acc)[kMI][4][2], double (&bsum)[kMI]) {
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
 #if PHBG_KORD == 2
@@ -85,18 +89,18 @@ __device__ __forceinline__ void stage_mma(const double* As, const double* Bs, co
     const int kk = ((ks & 1) << 1) + ((ks >> 1) << 3) + koff;
 #endif
     const double cv = cc[kk];
-    double av[8], bv[4];
+    double av[kMI], bv[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) av[i] = As[tma::kmaj_off(wm * 64 + i * 8 + g, kk)];
+    for (int i = 0; i < kMI; ++i) av[i] = As[tma::kmaj_off(wm * (kMI * 8) + i * 8 + g, kk)];
 #pragma unroll
     for (int j = 0; j < 4; ++j) bv[j] = Bs[tma::kmaj_off(wn * 32 + j * 8 + g, kk)] * cv;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < kMI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
     if (BIAS) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) bsum[i] = fma(av[i], cv, bsum[i]);
+      for (int i = 0; i < kMI; ++i) bsum[i] = fma(av[i], cv, bsum[i]);
     }
   }
 }
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(kPhbgThreads, 1) phbg_kernel(const __grid_cons
   __syncthreads();
   const int n_items = a.item_start[a.n_heavy] * a.G;
   if (warp >= kPhbgWarps) {  // producer warpgroup
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PHBG_CW == 16 ? 32 : 40));
     if (warp == kPhbgWarps && lane == 0) {
       unsigned qp = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(kPhbgThreads, 1) phbg_kernel(const __grid_cons
     }
     return;
   }
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(PHBG_CW == 16 ? 112 : 232));
   const int wm = warp >> 2, wn = warp & 3;
   const int g = lane >> 2, t = lane & 3;
 #if PHBG_KORD == 2
@@ -166,9 +170,9 @@ __global__ void __launch_bounds__(kPhbgThreads, 1) phbg_kernel(const __grid_cons
   for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
     const BItem it = decode_b(a, idx);
     const bool do_bias = it.tn == 0 && wn == 0;
-    double acc[8][4][2], bsum[8];
+    double acc[kMI][4][2], bsum[kMI];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kMI; ++i) {
       bsum[i] = 0.0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
@@ -195,9 +199,9 @@ __global__ void __launch_bounds__(kPhbgThreads, 1) phbg_kernel(const __grid_cons
     // epilogue: this split's partial of W_l (rows m, cols n) and, from the n-tile 0 warps, of b_l
     const int M = a.M[it.h], N = a.N[it.h];
     double* out = a.part + (int64_t)it.split * a.p + a.off[it.h];
-    const int m0 = it.tm * BBM + wm * 64 + g, n0 = it.tn * BBN + wn * 32 + 2 * t;
+    const int m0 = it.tm * BBM + wm * (kMI * 8) + g, n0 = it.tn * BBN + wn * 32 + 2 * t;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kMI; ++i) {
       const int m = m0 + i * 8;
       if (m < M) {
 #pragma unroll
@@ -265,9 +269,9 @@ __global__ void __maxnreg__(224) phbg_kernel(const __grid_constant__ PhbgArgs a,
   for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
     const BItem it = decode_b(a, idx);
     const bool do_bias = it.tn == 0 && wn == 0;
-    double acc[8][4][2], bsum[8];
+    double acc[kMI][4][2], bsum[kMI];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kMI; ++i) {
       bsum[i] = 0.0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
@@ -306,9 +310,9 @@ __global__ void __maxnreg__(224) phbg_kernel(const __grid_constant__ PhbgArgs a,
     // epilogue: this split's partial of W_l (rows m, cols n) and, from the n-tile 0 warps, of b_l
     const int M = a.M[it.h], N = a.N[it.h];
     double* out = a.part + (int64_t)it.split * a.p + a.off[it.h];
-    const int m0 = it.tm * BBM + wm * 64 + g, n0 = it.tn * BBN + wn * 32 + 2 * t;
+    const int m0 = it.tm * BBM + wm * (kMI * 8) + g, n0 = it.tn * BBN + wn * 32 + 2 * t;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kMI; ++i) {
       const int m = m0 + i * 8;
       if (m < M) {
 #pragma unroll
