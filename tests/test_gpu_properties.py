@@ -62,6 +62,32 @@ def test_full_size_operator_properties(name):
     assert float(torch.linalg.norm(gop.matvec(torch.zeros_like(v)))) == 0.0
 
 
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_back_to_back_matvecs_are_bitwise_reproducible(name):
+    """Matvecs enqueued back to back (no host synchronisation in between) against results made in isolation.
+    The warp-specialised phase kernels refill a ring slot the moment its last consumer warp has released
+    it; without the consumers' fence.proxy.async ahead of the release one 16-column box of the C5 phase A
+    was stale in ~10% of the launches (tools/ws_stress.py; csrc/ngd_phag.cu)."""
+    prob, quad, theta = make(name)
+    gop = ngd.GramianOperator.from_problem(prob, theta, quad)
+    p = gop.dim
+    rng = np.random.default_rng(7)
+    u, v = dev(rng.standard_normal(p)), dev(rng.standard_normal(p))
+    torch.cuda.synchronize()
+    gu = gop.matvec(u).clone()
+    torch.cuda.synchronize()
+    gv = gop.matvec(v).clone()
+    torch.cuda.synchronize()
+    reps = 20 if name == "c5" else 40
+    outs = []
+    for _ in range(reps):
+        outs.append((gop.matvec(u), gop.matvec(v)))
+    torch.cuda.synchronize()
+    for k, (a, b) in enumerate(outs):
+        assert torch.equal(a, gu), f"repeat {k}: matvec(u) differs"
+        assert torch.equal(b, gv), f"repeat {k}: matvec(v) differs"
+
+
 @pytest.mark.parametrize("name", ["c3", "c5"])
 def test_point_subset_against_oracle(name):
     """Gv is a sum of per-point terms: a point subset is an exact oracle."""
