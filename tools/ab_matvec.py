@@ -11,7 +11,7 @@ vals = [int(x) for x in sys.argv[3:5]]
 out = []
 for v in vals:
     with _lib.option(key, v):
-        prob, quad, theta0, _ = bench.make_problem(ngd, cfg, 1, 0)
+        prob, quad, theta0, _ = bench.make_problem(ngd, cfg)
         gop = ngd.GramianOperator.from_problem(prob, theta0, quad)
         x = np.random.default_rng(0).standard_normal(gop.dim)
         out.append(gop.matvec(x))

@@ -12,7 +12,7 @@ cfg_name = sys.argv[1]
 for kv in sys.argv[2:]:
     k, v = kv.split("=")
     _lib.set_option(k, int(v))
-prob, quad, theta0, cfg = bench.make_problem(ngd, cfg_name, 1, 0)
+prob, quad, theta0, cfg = bench.make_problem(ngd, cfg_name)
 runner = NystromNgdRunner(prob, theta0, cfg, quad)
 for _ in range(3):
     runner.step()

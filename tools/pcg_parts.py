@@ -9,7 +9,7 @@ import bench
 import paper_2505_11638_b200 as ngd
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-prob, quad, theta0, c = bench.make_problem(ngd, cfg, 1, 0)
+prob, quad, theta0, c = bench.make_problem(ngd, cfg)
 gop = ngd.GramianOperator.from_problem(prob, theta0, quad)
 g = prob.loss_grad(theta0, quad)
 gop = ngd.GramianOperator.from_problem(prob, theta0, quad)

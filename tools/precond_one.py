@@ -7,7 +7,7 @@ import torch, bench
 import paper_2505_11638_b200 as ngd
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-prob, quad, theta0, c = bench.make_problem(ngd, cfg, 1, 0)
+prob, quad, theta0, c = bench.make_problem(ngd, cfg)
 gop = ngd.GramianOperator.from_problem(prob, theta0, quad)
 fac = ngd.nystrom_approximate(gop, bench.CONFIGS[cfg][4], seed=1, omega_source="device")
 pre = ngd.NystromPreconditioner(fac, 1e-4)

@@ -11,7 +11,7 @@ from paper_2505_11638_b200.optim import NystromNgdRunner, _StepTimer
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-prob, quad, theta0, c = bench.make_problem(ngd, cfg, 1, 0)
+prob, quad, theta0, c = bench.make_problem(ngd, cfg)
 runner = NystromNgdRunner(prob, theta0, c, quad)
 for _ in range(3):
     runner.step()
