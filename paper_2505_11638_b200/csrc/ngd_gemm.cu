@@ -232,6 +232,9 @@ __global__ void __maxnreg__(224)
 #pragma unroll
           for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
       }
+      // a lagging warp's release can be the one the producer is waiting on: order the shared-memory
+      // reads (generic proxy) before the TMA refill (async proxy), as in ngd_phag.cu
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) g_arrive(&empty[slot]);
     }

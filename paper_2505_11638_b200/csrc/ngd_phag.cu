@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kPhagThreads, 1) phag_kernel(const __grid_cons
           for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
       }
       tma::fence_proxy_async();  // generic-proxy reads of the slot before the producer's async-proxy refill
-      __syncwarp();
+     __syncwarp();
       if (lane == 0) tma::arrive(&empty[slot]);
     }
     // epilogue: bias of the value-channel columns, dot with D over this warp's 64 rows
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kPhagThreads, 1) phag_kernel(const __grid_cons
         }
       }
       tma::fence_proxy_async();  // generic-proxy reads of the slot before the producer's async-proxy refill
-      __syncwarp();
+     __syncwarp();
       if (lane == 0) tma::arrive(&empty[slot]);
     }
     // fixed xor tree over the eight row groups g, then lanes g = 0 store their two columns per j
@@ -370,6 +370,7 @@ __global__ void __maxnreg__(224) phag_kernel(const __grid_constant__ PhagArgs a,
 #pragma unroll
           for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
       }
+      tma::fence_proxy_async();
       __syncwarp();
       if (lane == 0) tma::arrive(&empty[slot]);
     }
@@ -427,6 +428,7 @@ __global__ void __maxnreg__(224) phag_kernel(const __grid_constant__ PhagArgs a,
           }
         }
       }
+      tma::fence_proxy_async();
       __syncwarp();
       if (lane == 0) tma::arrive(&empty[slot]);
     }

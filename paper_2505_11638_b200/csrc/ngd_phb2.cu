@@ -241,6 +241,9 @@ __device__ __forceinline__ void consume(const PhbArgs& p, const Item& it, const 
     const bool val = do_bias && (it.k0 + i >= iu || ch == 0);
     ch = (ch + 1 == p.C) ? 0 : ch + 1;
     if (QA > 0 && RA > 0) mma_unit<(QA > 0 ? QA : 1), (RA > 0 ? RA : 1), NACC, KS>(st[s], arow, brow, kg, g, t, val, acc, bs);
+    // the producer warp refills the slot as soon as the last consumer has arrived: order this warp's
+    // shared-memory reads (generic proxy) before that TMA write (async proxy) -- see ngd_phag.cu
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }

@@ -304,6 +304,7 @@ __global__ void __maxnreg__(224) phbg_kernel(const __grid_constant__ PhbgArgs a,
         stage_mma<true>(As, Bs, st[slot].cc, wm, wn, g, koff, acc, bsum);
       else
         stage_mma<false>(As, Bs, st[slot].cc, wm, wn, g, koff, acc, bsum);
+      tma::fence_proxy_async();
       __syncwarp();
       if (lane == 0) tma::arrive(&empty[slot]);
     }
